@@ -1,0 +1,221 @@
+/*
+ * tsnet.h -- C-ABI of the B200-native L-tsNET gradient hot path
+ *            (arXiv 2509.19785, "L-tsNET", Alg. 3).
+ *
+ * One shared library, libtsnet.so (paper_2509_19785_b200/), built for sm_100a.
+ * Every entry point is extern "C", takes plain pointers and sizes, returns an
+ * int status (tsnet_status) and never throws.  The library never allocates
+ * device memory on the hot path: scratch space is the caller's workspace,
+ * sized by the matching *_workspace_bytes query.  All pointers are DEVICE
+ * pointers unless marked [host].  All work is enqueued on the caller's CUDA
+ * stream `stream` (a cudaStream_t; NULL = legacy default stream); calls are
+ * asynchronous unless marked BLOCKING.  Asynchronous CUDA errors surface on a
+ * later call.  Calls are re-entrant given distinct workspaces.
+ *
+ * Notation: n vertices, X_i = (x_i, y_i) the 2-D layout,
+ * Delta_ij = X_i - X_j, r2 = |Delta_ij|^2, w_ij = 1/(1 + r2),
+ * Z = sum_{k != l} w_kl, K_e = 1/(eps + r2).
+ *
+ * Data layout:
+ *   layout Y / velocity / gains / gradient : n x 2 fp32, interleaved (x, y)
+ *   graph and P                            : CSR, int64 indptr[n+1],
+ *                                            int32 indices[nnz] (ascending per row),
+ *                                            fp32 values[nnz] (P only)
+ */
+#ifndef TSNET_H
+#define TSNET_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TSNET_API __attribute__((visibility("default")))
+#else
+#define TSNET_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* tsnet_stream_t; /* == cudaStream_t */
+
+/* Status codes.  Every call returns one of these. */
+typedef enum {
+    TSNET_OK = 0,
+    TSNET_E_ARG = 1,         /* invalid argument (message in tsnet_last_error)            */
+    TSNET_E_CAPACITY = 2,    /* P capacity too small; P->nnz holds the required nnz        */
+    TSNET_E_CUDA = 3,        /* a CUDA runtime error (message in tsnet_last_error)        */
+    TSNET_E_NCCL = 4,        /* reserved: multi-GPU collectives                             */
+    TSNET_E_NONFINITE = 5,   /* returned by tsnet_read_stats when a non-finite value was seen */
+    TSNET_W_PERPLEXITY = 6   /* warning from tsnet_build_P: some rows could not reach the
+                                perplexity (c_min >= u, reading R6); P is still valid       */
+} tsnet_status;
+
+/* Undirected input graph G = (V, E) ("Input: Graph G=(V,E)"):
+ * symmetric adjacency, no self loops, no duplicates, rows ascending.
+ * Connectivity is NOT required (rows of small components are short). */
+typedef struct {
+    int64_t n;
+    const int64_t* indptr;   /* device, n+1 */
+    const int32_t* indices;  /* device, indptr[n] */
+} tsnet_graph;
+
+/* Sparse symmetric affinity matrix P (Eq. 2) in CSR.
+ * `capacity` = allocated length of indices/values (input to tsnet_build_P),
+ * `nnz` = stored entries (output of tsnet_build_P, input elsewhere). */
+typedef struct {
+    int64_t n;
+    int64_t nnz;
+    int64_t capacity;
+    int64_t* indptr;         /* device, n+1 */
+    int32_t* indices;        /* device, capacity */
+    float* values;           /* device, capacity */
+} tsnet_csr;
+
+/* Cost multipliers and interpolation grid policy.
+ *   lambda_kl, lambda_c, lambda_r : Eq. 1 multipliers
+ *   eps                           : entropy regulariser, 1/20 in the paper
+ *   interp_P                      : interpolation points per interval ("P");
+ *                                   only 3 is supported (TSNET_E_ARG otherwise)
+ *   h_max, I_min, I_max           : grid policy of reading R9: per axis
+ *                                   I = clamp(ceil(S/h_max), I_min, I_max) intervals over
+ *                                   the bounding-box span S, rounded up to 2^a 3^b 5^c
+ *                                   ("# of intervals I"); 1 <= I_min <= I_max
+ *                                   <= TSNET_I_MAX_LIMIT. */
+typedef struct {
+    float lambda_kl, lambda_c, lambda_r, eps;
+    int32_t interp_P;
+    float h_max;
+    int32_t I_min, I_max;
+} tsnet_grad_params;
+
+#define TSNET_I_MAX_LIMIT 256
+
+/* Momentum/gains update (reading R12; the paper only says "Move each vertex v
+ * in the direction of dC/dv"):
+ *   gains <- max(gain_min, sign(g) != sign(v) ? gains + gain_inc : gain_dec * gains)
+ *   v     <- momentum * v - eta * gains * g ;   Y <- Y + v ;   if recenter: Y <- Y - mean(Y) */
+typedef struct {
+    float eta, momentum, gain_inc, gain_dec, gain_min;
+    int32_t recenter;
+} tsnet_step_params;
+
+/* Row shard for multi-GPU runs.  NULL (or world == 1, rows [0, n)) = one GPU.
+ * Round 1 supports only the single-GPU case (TSNET_E_ARG otherwise). */
+typedef struct {
+    int32_t rank, world;
+    int64_t row_begin, row_end;
+} tsnet_shard;
+
+/* Per-call statistics kept in the workspace (read with tsnet_read_stats). */
+typedef struct {
+    double Z;                /* normaliser of the last gradient evaluation              */
+    double lo_x, lo_y, S;    /* bounding box origin and span of the last evaluation     */
+    double h_b;              /* interval (box) width                                    */
+    int32_t I, N, M;         /* intervals per axis, nodes per axis (3I), FFT size (6I)   */
+    int32_t nonfinite;       /* 1 if a non-finite coordinate/gradient was produced       */
+} tsnet_stats;
+
+/* ---------------------------------------------------------------- C0 (set-up) */
+
+/* k = round(3u) ("k = 3u"; half rounds up) when k_req <= 0, else
+ * k_req; capped at n-1 (reading R5).  [host, pure] */
+TSNET_API int32_t tsnet_resolve_k(int64_t n, double perplexity_u, int32_t k_req);
+
+/* Device scratch bytes tsnet_build_P needs for n vertices and k neighbours. [host] */
+TSNET_API size_t tsnet_build_P_workspace_bytes(int64_t n, int32_t k);
+
+/*
+ * C0: build P from G (Alg. 3 l.385-394), on the GPU.
+ *  (1) partial BFS from every v until k vertices are visited (PAPER.md:388,
+ *      §3.1 l.270): whole BFS levels while the count stays <= k; at the first
+ *      overflowing level the k - taken vertices with the smallest
+ *      (SplitMix64(seed ^ (v<<32 | w)), w) are taken (reading R4: "ties are
+ *      broken randomly" made reproducible);
+ *  (2) per row, beta_i = 1/(2 sigma_i^2) so that the perplexity of
+ *      p_j|i ∝ exp(-beta_i d_ij^2) equals u (Eq. 3), d_ij =
+ *      hop distance; bisection to |H - ln u| <= 1e-13 (R7); beta = 0 when the
+ *      row has <= u entries, beta = inf (uniform on the nearest hop level)
+ *      when that level alone has >= u entries (R6, counted -> TSNET_W_PERPLEXITY);
+ *  (3) p_ij = (p_j|i + p_i|j) / (2n) (Eq. 2), computed in fp64, exact zeros
+ *      dropped, rounded to fp32, columns ascending.
+ * Outputs: knn_idx / knn_hop [n * k] (row v = its kNN sorted by (hop, w),
+ * entries >= knn_len[v] are -1), knn_len [n], beta [n] (fp64; may be NULL),
+ * P (indptr/indices/values, P->nnz).  If P->capacity < nnz the call returns
+ * TSNET_E_CAPACITY with P->nnz = the required nnz (2 n k always suffices).
+ * BLOCKING: synchronises `stream` (it returns nnz on the host).
+ */
+TSNET_API int tsnet_build_P(const tsnet_graph* g, double perplexity_u, int32_t k, uint64_t seed,
+                  tsnet_csr* P, int32_t* knn_idx, int32_t* knn_hop, int32_t* knn_len, double* beta,
+                  void* ws, size_t ws_bytes, tsnet_stream_t stream);
+
+/* ------------------------------------------------------- the per-iteration path */
+
+/* Device workspace bytes for tsnet_grad / tsnet_grad_parts / tsnet_step /
+ * tsnet_cost on n vertices and nnz entries of P. [host] */
+TSNET_API size_t tsnet_workspace_bytes(int64_t n, int64_t nnz, const tsnet_grad_params* gp, const tsnet_shard* shard);
+
+/*
+ * Gradient of C = C_KL + C_CMP + C_ENT at layout Y (one L-tsNET iteration,
+ * Alg. 3 l.396-404):
+ *   grad_i = 4 lambda_kl (F_attr,i - F_rep,i) + (lambda_c / n) X_i + lambda_r g_ent,i
+ *   F_attr,i = sum_j p_ij w_ij Delta_ij                (Eq. 6 term 1, exact sparse SpMV)
+ *   F_rep,i  ~ sum_j w_ij^2 Delta_ij / Z,  Z ~ sum_{k!=l} w_kl   (Eq. 6 term 2, FIt-SNE
+ *              interpolation)
+ *   g_ent,i  ~ -(1/n^2) sum_j Delta_ij / (eps + r2)    (Eq. 8)
+ * The two interpolated sums use P=3 Lagrange nodes per interval on an
+ * I x I-interval grid, convolved by FFT (local-moment form).
+ * grad: n x 2 fp32 (device).  Z: device fp64 scalar (may be NULL).
+ */
+TSNET_API int tsnet_grad(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, const tsnet_shard* shard,
+               float* grad, double* Z, void* ws, size_t ws_bytes, tsnet_stream_t stream);
+
+/* Same evaluation, returning the parts separately (diagnostics / parity):
+ *   f_attr  = F_attr (n x 2), f_field = -4 lambda_kl F_rep + lambda_r g_ent (n x 2),
+ * so that grad = 4 lambda_kl f_attr + f_field + (lambda_c / n) Y.  Any output may be NULL. */
+TSNET_API int tsnet_grad_parts(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp,
+                     const tsnet_shard* shard, float* f_attr, float* f_field, double* Z,
+                     void* ws, size_t ws_bytes, tsnet_stream_t stream);
+
+/*
+ * One full iteration: gradient at Y (as tsnet_grad) followed by the
+ * momentum/gains move ("Move each vertex v in the direction of
+ * dC/dv"; reading R12), in place on Y, vel, gains (n x 2 fp32 each).
+ */
+TSNET_API int tsnet_step(const tsnet_csr* P, float* Y, float* vel, float* gains, const tsnet_grad_params* gp,
+               const tsnet_step_params* sp, const tsnet_shard* shard, void* ws, size_t ws_bytes,
+               tsnet_stream_t stream);
+
+/*
+ * Same as tsnet_step with HOST state buffers (pinned host memory recommended):
+ * copies Y, vel, gains host -> device into the workspace, runs one iteration
+ * and copies them back device -> host, all on `stream`.  P stays on the device.
+ * BLOCKING (synchronises `stream` before returning).  Used for the end-to-end
+ * measurement of the host-facing API.
+ */
+TSNET_API int tsnet_step_host(const tsnet_csr* P, float* Y_host, float* vel_host, float* gains_host,
+                    const tsnet_grad_params* gp, const tsnet_step_params* sp, const tsnet_shard* shard,
+                    void* ws, size_t ws_bytes, tsnet_stream_t stream);
+
+/*
+ * Cost C = (C_KL, C_CMP, C_ENT*) written to out3 (device, 3 doubles):
+ *   C_KL  = lambda_kl sum_{p_ij > 0} p_ij ln(p_ij Z / w_ij)    (Eq. 1/4, natural log, R14)
+ *   C_CMP = lambda_c / (2n) sum_i |X_i|^2                       (Eq. 1)
+ *   C_ENT* = -lambda_r / (4 n^2) sum_{i != j} ln(eps + r2_ij)   (reading R1 of PAPER.md:90)
+ * mode 0: exact (Z and C_ENT* by O(n^2) tiles, fp64 accumulation);
+ * mode 1: Z from the interpolation grid, C_ENT* = NaN (not computed; NEXT).
+ */
+TSNET_API int tsnet_cost(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, int32_t mode,
+               const tsnet_shard* shard, double* out3, void* ws, size_t ws_bytes, tsnet_stream_t stream);
+
+/* Copy the statistics of the last evaluation from the workspace. BLOCKING. [host out] */
+TSNET_API int tsnet_read_stats(const void* ws, tsnet_stats* out, tsnet_stream_t stream);
+
+/* Thread-local message describing the last error of this thread. [host] */
+TSNET_API const char* tsnet_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSNET_H */

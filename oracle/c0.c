@@ -99,15 +99,34 @@ static int64_t partial_bfs(int64_t n, const int64_t* indptr, const int32_t* indi
             int64_t tc = cap_f; cap_f = cap_n; cap_n = tc;
             nf = nn;
         } else {
-            cand_t* lev = (cand_t*)malloc(sizeof(cand_t) * nn);
+            /* the cap = k - taken smallest (key, w) of the level: a bounded
+             * max-heap of size cap over the level, then sorted */
+            const int64_t cap = k - taken;
+            cand_t* heap = (cand_t*)malloc(sizeof(cand_t) * cap);
+            int64_t hs = 0;
             for (int64_t a = 0; a < nn; ++a) {
-                lev[a].w = next[a];
-                lev[a].hop = d;
-                lev[a].key = oracle_tie_key(seed, v, next[a]);
+                cand_t c = {next[a], d, oracle_tie_key(seed, v, next[a])};
+                if (hs < cap) {                       /* push, sift up */
+                    int64_t i = hs++;
+                    while (i > 0 && cmp_key_w(&heap[(i - 1) / 2], &c) < 0) { heap[i] = heap[(i - 1) / 2]; i = (i - 1) / 2; }
+                    heap[i] = c;
+                } else if (cmp_key_w(&c, &heap[0]) < 0) { /* replace the max, sift down */
+                    int64_t i = 0;
+                    for (;;) {
+                        int64_t l = 2 * i + 1, r = l + 1, m = i;
+                        const cand_t* big = &c;
+                        if (l < hs && cmp_key_w(&heap[l], big) > 0) { m = l; big = &heap[l]; }
+                        if (r < hs && cmp_key_w(&heap[r], big) > 0) { m = r; }
+                        if (m == i) break;
+                        heap[i] = heap[m];
+                        i = m;
+                    }
+                    heap[i] = c;
+                }
             }
-            qsort(lev, (size_t)nn, sizeof(cand_t), cmp_key_w);
-            for (int64_t a = 0; taken < k; ++a) row[taken++] = lev[a];
-            free(lev);
+            qsort(heap, (size_t)hs, sizeof(cand_t), cmp_key_w);
+            for (int64_t a = 0; a < hs; ++a) row[taken++] = heap[a];
+            free(heap);
             break;
         }
     }

@@ -1,0 +1,155 @@
+// common.cuh -- internal helpers of libtsnet (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstddef>
+
+#include "../../include/tsnet.h"
+
+namespace tsnet {
+
+constexpr int kWarp = 32;
+constexpr int kNumSMs = 148;     // B200; launch geometry only, never correctness
+
+// ------------------------------------------------------------------ errors
+void set_error(const char* fmt, ...);
+
+#define TSNET_CUDA(call)                                                                  \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) {                                                          \
+            ::tsnet::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+            return TSNET_E_CUDA;                                                          \
+        }                                                                                 \
+    } while (0)
+
+#define TSNET_LAUNCH_CHECK()                                                              \
+    do {                                                                                  \
+        cudaError_t e_ = cudaGetLastError();                                              \
+        if (e_ != cudaSuccess) {                                                          \
+            ::tsnet::set_error("%s:%d kernel launch: %s", __FILE__, __LINE__, cudaGetErrorString(e_)); \
+            return TSNET_E_CUDA;                                                          \
+        }                                                                                 \
+    } while (0)
+
+#define TSNET_ARG(cond, ...)                                                              \
+    do {                                                                                  \
+        if (!(cond)) {                                                                    \
+            ::tsnet::set_error(__VA_ARGS__);                                              \
+            return TSNET_E_ARG;                                                           \
+        }                                                                                 \
+    } while (0)
+
+// ------------------------------------------------------- per-iteration geometry
+// Lives in the workspace header; written by the bbox kernel's last block,
+// read by every later kernel of the iteration (no host round trip).
+struct Geo {
+    double lo_x, lo_y, S, h_b, delta;  // fp64: box assignment matches the fp64 definition (R16)
+    double zacc;                       // Parseval accumulator  <W1, K1 * W1> * M^2
+    double Z;                          // Z = zacc / M^2 - n
+    int I, N, M, nrad;
+    unsigned long long plan;           // FFT plan for length M: stage s radix = ((plan >> 2s) & 3) + 2
+    int nitems;                        // spread work items
+    int nonfinite;
+    unsigned int ticket;               // last-block-done counter of the bbox kernel
+    int bbox[4];                       // ordered-int encodings: min x, min y, max x, max y
+    double sum_x, sum_y;               // centroid accumulation (recenter)
+    unsigned int ticket2;
+    int pad;
+};
+
+// Ordered float <-> int (monotone), for atomicMin/atomicMax on floats.
+__device__ __forceinline__ int f2o(float f) {
+    int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float o2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
+
+// ------------------------------------------------------------ workspace map
+struct Ws {
+    Geo* geo;
+    float2* f_attr;      // n
+    float2* f_field;     // n (grad_parts only)
+    int* box;            // n   box id of each point
+    int* rank;           // n   rank of the point inside its box
+    float2* uv;          // n   in-box coordinates (u_x, u_y) in [0,1]
+    float2* sorted_uv;   // n   uv in box order
+    int* box_cnt;        // I_max^2 + 1
+    int* box_start;      // I_max^2 + 1
+    int2* items;         // max_items (box, first point)
+    float4* wgrid;       // N_max^2 spread charges (W1, Mx, My, 0), row-major [gy][gx]
+    float2* tw;          // M_max twiddles exp(-2 pi i k / M)
+    float2* spec;        // 10 * (M_max/2+1) * M_max : forward row spectra, [a][kx][y]
+    float2* colout;      // 6 * (M_max/2+1) * N_max  : after column pass, [b][kx][y]
+    float4* fgrid;       // N_max^2 fields (P0, Qx, Qy, 0), row-major [gy][gx]
+    float2* state;       // 3 n : host-facing step staging (Y, vel, gains)
+    double* cost;        // scratch for tsnet_cost (4 doubles)
+    int64_t n, nnz;
+    int I_max, N_max, M_max, max_items;
+    size_t bytes;
+};
+
+constexpr int kSpreadChunk = 256;   // points per spread work item
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Computes the map; base == nullptr only sizes it.
+inline Ws ws_map(void* base, int64_t n, int64_t nnz, int I_max) {
+    Ws w{};
+    w.n = n;
+    w.nnz = nnz;
+    w.I_max = I_max;
+    w.N_max = 3 * I_max;
+    w.M_max = 6 * I_max;
+    w.max_items = (int)((n + kSpreadChunk - 1) / kSpreadChunk + (int64_t)I_max * I_max + 1);
+    const int64_t nb = (int64_t)I_max * I_max + 1;
+    const int64_t half = w.M_max / 2 + 1;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off = align_up(off + bytes, 256);
+        return (char*)base + o;
+    };
+    w.geo = (Geo*)take(sizeof(Geo));
+    w.f_attr = (float2*)take(sizeof(float2) * n);
+    w.f_field = (float2*)take(sizeof(float2) * n);
+    w.box = (int*)take(sizeof(int) * n);
+    w.rank = (int*)take(sizeof(int) * n);
+    w.uv = (float2*)take(sizeof(float2) * n);
+    w.sorted_uv = (float2*)take(sizeof(float2) * n);
+    w.box_cnt = (int*)take(sizeof(int) * nb);
+    w.box_start = (int*)take(sizeof(int) * nb);
+    w.items = (int2*)take(sizeof(int2) * w.max_items);
+    w.wgrid = (float4*)take(sizeof(float4) * (size_t)w.N_max * w.N_max);
+    w.tw = (float2*)take(sizeof(float2) * w.M_max);
+    w.spec = (float2*)take(sizeof(float2) * 10 * half * (size_t)w.M_max);
+    w.colout = (float2*)take(sizeof(float2) * 6 * half * (size_t)w.N_max);
+    w.fgrid = (float4*)take(sizeof(float4) * (size_t)w.N_max * w.N_max);
+    w.state = (float2*)take(sizeof(float2) * 3 * n);
+    w.cost = (double*)take(sizeof(double) * 8);
+    w.bytes = off;
+    return w;
+}
+
+// ------------------------------------------------------------ launchers
+// (defined in the .cu files; all enqueue on `s`, return cudaError_t of launch)
+struct GradArgs {
+    int64_t n, nnz;
+    const int64_t* indptr;
+    const int32_t* indices;
+    const float* values;
+    const float2* Y;
+    float lambda_kl, lambda_c, lambda_r, eps, h_max;
+    int I_min, I_max;
+};
+
+cudaError_t launch_field_phase(const Ws& w, const GradArgs& a, cudaStream_t s);
+cudaError_t launch_spmv(const Ws& w, const GradArgs& a, cudaStream_t s);
+cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2* f_field, double* Z,
+                            cudaStream_t s);
+cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,
+                          const tsnet_step_params& sp, cudaStream_t s);
+cudaError_t launch_cost(const Ws& w, const GradArgs& a, int mode, double* out3, cudaStream_t s);
+
+}  // namespace tsnet

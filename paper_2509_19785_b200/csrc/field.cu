@@ -1,0 +1,502 @@
+// field.cu -- the FFT-accelerated interpolation phase of one L-tsNET iteration
+// (FIt-SNE interpolation; Alg. 3 l.397-400 and l.403,
+// PAPER.md:397-403; entropy kernel K_e = 1/(eps + r^2)).
+//
+// Steps, all device-driven (no host round trip):
+//   a0 k_iter_init + k_bbox   bounding box -> grid geometry (I, h_b, N = 3I, M = 6I, FFT plan)
+//   .. k_prep                 zero box counters and charge grid, twiddles of length M
+//   a1 k_box_count/k_box_scan/k_box_scatter  counting sort of points by box
+//   a2 k_spread               box-local charges W1 and local moments M_x, M_y (warp per
+//                             box chunk, register accumulation, 9 vector reds per warp)
+//   a3/a4 k_row_fwd, k_col, k_row_inv   kernel tabulation + 2-D FFT convolution
+//                             (rows -> columns with products -> inverse rows)
+//   a5 Z by Parseval inside k_col (fp64 accumulation)
+// Output: fgrid[gy][gx] = (P0, Qx, Qy) with the combined kernel
+//   C = alpha K2 + beta K_e,  alpha = -4 lambda_kl / Z,  beta = -lambda_r / n^2,
+//   P0 = C * W1,  Qx = (D_x C) * W1 + C * M_x,  Qy = (D_y C) * W1 + C * M_y,
+// so that for a point in box (bx, by) with in-box coordinates (u_x, u_y):
+//   f_field = sum_{a,b} L_a(u_x) L_b(u_y) [ (X - t_ab) P0 + Q ]
+//           = -4 lambda_kl F_rep + lambda_r g_ent   (local-moment form).
+#include "common.cuh"
+#include "fft.cuh"
+
+namespace tsnet {
+
+// Lagrange basis on the nodes s_t = (t + 1/2)/3 of one interval.
+__device__ __forceinline__ void lagrange3(float u, float (&L)[3]) {
+    const float s0 = 1.0f / 6.0f, s1 = 0.5f, s2 = 5.0f / 6.0f;
+    L[0] = 4.5f * (u - s1) * (u - s2);
+    L[1] = -9.0f * (u - s0) * (u - s2);
+    L[2] = 4.5f * (u - s0) * (u - s1);
+}
+
+__device__ __forceinline__ bool is5smooth(int m) {
+    while (m % 2 == 0) m /= 2;
+    while (m % 3 == 0) m /= 3;
+    while (m % 5 == 0) m /= 5;
+    return m == 1;
+}
+
+__global__ void k_iter_init(Geo* g) {
+    g->bbox[0] = 0x7FFFFFFF;
+    g->bbox[1] = 0x7FFFFFFF;
+    g->bbox[2] = (int)0x80000000;
+    g->bbox[3] = (int)0x80000000;
+    g->ticket = 0u;
+    g->ticket2 = 0u;
+    g->zacc = 0.0;
+    g->sum_x = 0.0;
+    g->sum_y = 0.0;
+}
+
+// a0: bounding box of Y and, in the last block, the grid geometry (R9).
+__global__ void __launch_bounds__(256) k_bbox(const float2* __restrict__ Y, int64_t n, Geo* g, float h_max,
+                                              int I_min, int I_max) {
+    float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float2 y = Y[i];
+        bad |= !(isfinite(y.x) && isfinite(y.y));
+        mnx = fminf(mnx, y.x);
+        mny = fminf(mny, y.y);
+        mxx = fmaxf(mxx, y.x);
+        mxy = fmaxf(mxy, y.y);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+        mny = fminf(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+        mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+        mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    __shared__ float s[4][8];
+    __shared__ int sbad;
+    __shared__ bool last;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (threadIdx.x == 0) sbad = 0;
+    __syncthreads();
+    if (l == 0) {
+        s[0][w] = mnx; s[1][w] = mny; s[2][w] = mxx; s[3][w] = mxy;
+        if (bad) atomicOr(&sbad, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+            mnx = fminf(mnx, s[0][k]); mny = fminf(mny, s[1][k]);
+            mxx = fmaxf(mxx, s[2][k]); mxy = fmaxf(mxy, s[3][k]);
+        }
+        if (n > 0) {
+            atomicMin(&g->bbox[0], f2o(mnx));
+            atomicMin(&g->bbox[1], f2o(mny));
+            atomicMax(&g->bbox[2], f2o(mxx));
+            atomicMax(&g->bbox[3], f2o(mxy));
+        }
+        if (sbad) atomicOr(&g->nonfinite, 1);
+        __threadfence();
+        unsigned int t = atomicAdd(&g->ticket, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    // ---- geometry (fp64, identical to the oracle's definition) ----
+    volatile int* bb = g->bbox;
+    double lo_x = (double)o2f(bb[0]), lo_y = (double)o2f(bb[1]);
+    double hi_x = (double)o2f(bb[2]), hi_y = (double)o2f(bb[3]);
+    double S = fmax(hi_x - lo_x, hi_y - lo_y);
+    if (!(S >= 1e-12)) S = 1e-12;            // also catches NaN (non-finite layouts)
+    if (!isfinite(S) || !isfinite(lo_x) || !isfinite(lo_y)) {
+        g->nonfinite = 1;
+        S = 1.0; lo_x = 0.0; lo_y = 0.0;
+    }
+    double q = ceil(S / (double)h_max);
+    double qc = fmin(fmax(q, (double)I_min), (double)I_max);
+    int I = (int)qc;
+    int Iu = I;
+    while (!is5smooth(Iu)) ++Iu;
+    if (Iu > I_max) {
+        Iu = I_max;
+        while (!is5smooth(Iu)) --Iu;
+    }
+    I = Iu;
+    g->lo_x = lo_x;
+    g->lo_y = lo_y;
+    g->S = S;
+    g->I = I;
+    g->h_b = S / (double)I;
+    g->delta = g->h_b / 3.0;
+    g->N = 3 * I;
+    g->M = 6 * I;
+    int m = 6 * I, nr = 0;
+    unsigned long long plan = 0ull;
+    const int rads[4] = {4, 2, 3, 5};
+    for (int q = 0; q < 4; ++q)
+        while (m % rads[q] == 0) {
+            plan |= (unsigned long long)(rads[q] - 2) << (2 * nr++);
+            m /= rads[q];
+        }
+    g->plan = plan;
+    g->nrad = nr;
+}
+
+// Zero the box counters and the charge grid; twiddles w_M^k = exp(-2 pi i k / M).
+__global__ void k_prep(Geo* g, int* box_cnt, float4* wgrid, float2* tw) {
+    const int I = g->I, N = g->N, M = g->M;
+    const int64_t nb = (int64_t)I * I + 1, nn = (int64_t)N * N;
+    const int64_t tot = nb + nn + M;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        if (t < nb) {
+            box_cnt[t] = 0;
+        } else if (t < nb + nn) {
+            wgrid[t - nb] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            int k = (int)(t - nb - nn);
+            double s, c;
+            sincospi(-2.0 * (double)k / (double)M, &s, &c);
+            tw[k] = make_float2((float)c, (float)s);
+        }
+    }
+}
+
+// a1: box of every point (fp64 arithmetic, R16) and its rank inside the box.
+__global__ void __launch_bounds__(256) k_box_count(const float2* __restrict__ Y, int64_t n, const Geo* __restrict__ g,
+                                                   int* __restrict__ box_cnt, int* __restrict__ box,
+                                                   int* __restrict__ rank, float2* __restrict__ uv) {
+    const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b;
+    const int I = g->I;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        const bool act = i < n;
+        int b = -1;
+        float ux = 0.f, uy = 0.f;
+        if (act) {
+            float2 y = Y[i];
+            double rx = ((double)y.x - lo_x) / h_b;
+            double ry = ((double)y.y - lo_y) / h_b;
+            double fx = floor(rx), fy = floor(ry);
+            int bx = (int)fmin(fmax(fx, 0.0), (double)(I - 1));
+            int by = (int)fmin(fmax(fy, 0.0), (double)(I - 1));
+            ux = (float)(rx - (double)bx);
+            uy = (float)(ry - (double)by);
+            b = by * I + bx;
+        }
+        // warp-aggregated atomic: one atomicAdd per distinct box in the warp
+        const unsigned act_mask = __ballot_sync(0xffffffffu, act);
+        if (act) {
+            const unsigned peers = __match_any_sync(act_mask, b);
+            const int leader = __ffs(peers) - 1;
+            const int lane = threadIdx.x & 31;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(&box_cnt[b], __popc(peers));
+            base = __shfl_sync(peers, base, leader);
+            const int r = base + __popc(peers & ((1u << lane) - 1u));
+            box[i] = b;
+            rank[i] = r;
+            uv[i] = make_float2(ux, uy);
+        }
+    }
+}
+
+// a1: exclusive scan of box counts -> box_start, and the spread work list
+// (one item per kSpreadChunk points of a box).  Single CTA of 1024 threads.
+__global__ void __launch_bounds__(1024) k_box_scan(Geo* g, const int* __restrict__ box_cnt, int* __restrict__ box_start,
+                                                   int2* __restrict__ items, int64_t n) {
+    const int nb = g->I * g->I;
+    const int T = blockDim.x;
+    const int per = (nb + T - 1) / T;
+    const int b0 = threadIdx.x * per, b1 = min(nb, b0 + per);
+    int cs = 0, is = 0;
+    for (int b = b0; b < b1; ++b) {
+        int c = box_cnt[b];
+        cs += c;
+        is += (c + kSpreadChunk - 1) / kSpreadChunk;
+    }
+    __shared__ int sc[1024], si[1024];
+    sc[threadIdx.x] = cs;
+    si[threadIdx.x] = is;
+    __syncthreads();
+    for (int o = 1; o < T; o <<= 1) {            // Hillis-Steele inclusive scan
+        int a = threadIdx.x >= o ? sc[threadIdx.x - o] : 0;
+        int c = threadIdx.x >= o ? si[threadIdx.x - o] : 0;
+        __syncthreads();
+        sc[threadIdx.x] += a;
+        si[threadIdx.x] += c;
+        __syncthreads();
+    }
+    int run = sc[threadIdx.x] - cs, irun = si[threadIdx.x] - is;
+    for (int b = b0; b < b1; ++b) {
+        int c = box_cnt[b];
+        box_start[b] = run;
+        int ni = (c + kSpreadChunk - 1) / kSpreadChunk;
+        for (int q = 0; q < ni; ++q) items[irun + q] = make_int2(b, run + q * kSpreadChunk);
+        run += c;
+        irun += ni;
+    }
+    if (threadIdx.x == T - 1) {
+        box_start[nb] = (int)n;
+        g->nitems = si[T - 1];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_box_scatter(int64_t n, const int* __restrict__ box, const int* __restrict__ rank,
+                                                     const int* __restrict__ box_start, const float2* __restrict__ uv,
+                                                     float2* __restrict__ sorted_uv) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        sorted_uv[box_start[box[i]] + rank[i]] = uv[i];
+}
+
+__device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float c) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(0.0f)
+                 : "memory");
+}
+
+// a2: spread.  One warp per item = up to kSpreadChunk points of one box.
+//   W1[g]  = sum_i L_g(X_i)
+//   M_x[g] = sum_i L_g(X_i) (t_gx - x_i) = h_b sum_i L_g (s_a - u_x)   (local moments)
+__global__ void __launch_bounds__(256) k_spread(const Geo* __restrict__ g, const int2* __restrict__ items,
+                                                const int* __restrict__ box_start,
+                                                const float2* __restrict__ sorted_uv, float4* __restrict__ wgrid) {
+    const int nitems = g->nitems, I = g->I, N = g->N;
+    const float h_b = (float)g->h_b;
+    const float s[3] = {1.0f / 6.0f, 0.5f, 5.0f / 6.0f};
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    for (int it = blockIdx.x * wpb + (threadIdx.x >> 5); it < nitems; it += gridDim.x * wpb) {
+        const int2 item = items[it];
+        const int b = item.x;
+        const int end = min(item.y + kSpreadChunk, box_start[b + 1]);
+        float acc[27];
+#pragma unroll
+        for (int q = 0; q < 27; ++q) acc[q] = 0.f;
+        for (int p = item.y + lane; p < end; p += 32) {
+            const float2 u = sorted_uv[p];
+            float Lx[3], Ly[3];
+            lagrange3(u.x, Lx);
+            lagrange3(u.y, Ly);
+#pragma unroll
+            for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const float w = Lx[a] * Ly[bb];
+                    const int q = 3 * (3 * bb + a);
+                    acc[q] += w;
+                    acc[q + 1] += w * (s[a] - u.x);
+                    acc[q + 2] += w * (s[bb] - u.y);
+                }
+        }
+#pragma unroll
+        for (int q = 0; q < 27; ++q)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+        if (lane < 9) {
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+#pragma unroll
+            for (int q = 0; q < 9; ++q)
+                if (q == lane) { a0 = acc[3 * q]; a1 = acc[3 * q + 1]; a2 = acc[3 * q + 2]; }
+            const int bx = b % I, by = b / I;
+            const int gx = 3 * bx + lane % 3, gy = 3 * by + lane / 3;
+            red_add_v4(&wgrid[(int64_t)gy * N + gx], a0, a1 * h_b, a2 * h_b);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- FFT passes
+constexpr int kRowThreads = 512;
+constexpr int kInvThreads = 256;
+constexpr int kColThreads = 512;
+constexpr int kMmax = 6 * TSNET_I_MAX_LIMIT;   // 1536
+// spectra layout: array a, column kx, row y  ->  spec[(a * half_max + kx) * M_max + y]
+
+// a3 + first half of a4: per row y of the M x M circulant grid, build the 10
+// real arrays (3 charges, 7 kernel tables), FFT them along x in 5 packed
+// complex transforms, unpack to half spectra and store transposed.
+//   arrays: 0 W1, 1 Mx, 2 My, 3 K1, 4 K2, 5 Ke, 6 DxK2, 7 DxKe, 8 DyK2, 9 DyKe
+__global__ void __launch_bounds__(kRowThreads, 1) k_row_fwd(const Geo* __restrict__ gp, const float4* __restrict__ wgrid,
+                                                         const float2* __restrict__ twg, float2* __restrict__ spec,
+                                                         int M_max, float eps) {
+    extern __shared__ float2 sm[];
+    float2* tw = sm;                      // M
+    float2* buf = sm + M_max;             // 5 * M
+    float2* scr = buf + 5 * M_max;        // 5 * M
+    const int M = gp->M, N = gp->N, half = M / 2 + 1, nrad = gp->nrad;
+    const unsigned long long plan = gp->plan;
+    const int half_max = M_max / 2 + 1;
+    const double dlt = gp->delta;
+    for (int k = threadIdx.x; k < M; k += blockDim.x) tw[k] = twg[k];
+    for (int y = blockIdx.x; y < M; y += gridDim.x) {
+        const int dy = (y <= M / 2) ? y : y - M;
+        const bool ky = (dy < N) && (-dy < N);       // |dy| <= N - 1
+        for (int x = threadIdx.x; x < M; x += blockDim.x) {
+            const int dx = (x <= M / 2) ? x : x - M;
+            float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (y < N && x < N) wv = wgrid[(int64_t)y * N + x];
+            float k1 = 0.f, k2 = 0.f, ke = 0.f, dxk2 = 0.f, dxke = 0.f, dyk2 = 0.f, dyke = 0.f;
+            if (ky && dx < N && -dx < N) {
+                const double ox = dx * dlt, oy = dy * dlt;
+                const double r2 = ox * ox + oy * oy;
+                const double K1 = 1.0 / (1.0 + r2), K2 = K1 * K1, Ke = 1.0 / ((double)eps + r2);
+                k1 = (float)K1; k2 = (float)K2; ke = (float)Ke;
+                dxk2 = (float)(ox * K2); dxke = (float)(ox * Ke);
+                dyk2 = (float)(oy * K2); dyke = (float)(oy * Ke);
+            }
+            buf[0 * M + x] = make_float2(wv.x, wv.y);
+            buf[1 * M + x] = make_float2(wv.z, k1);
+            buf[2 * M + x] = make_float2(k2, ke);
+            buf[3 * M + x] = make_float2(dxk2, dxke);
+            buf[4 * M + x] = make_float2(dyk2, dyke);
+        }
+        __syncthreads();
+        fft_block(buf, scr, M, 5, M, plan, nrad, tw, false);
+        // unpack z = A + iB:  A_k = (Z_k + conj Z_{M-k}) / 2,  B_k = -i (Z_k - conj Z_{M-k}) / 2
+        for (int t = threadIdx.x; t < 5 * half; t += blockDim.x) {
+            const int p = t / half, k = t - p * half;
+            const float2 Zk = buf[p * M + k];
+            const float2 Zm = cconj(buf[p * M + (k == 0 ? 0 : M - k)]);
+            const float2 A = make_float2(0.5f * (Zk.x + Zm.x), 0.5f * (Zk.y + Zm.y));
+            const float2 D = make_float2(0.5f * (Zk.x - Zm.x), 0.5f * (Zk.y - Zm.y));
+            const float2 B = mul_mi(D);
+            spec[((int64_t)(2 * p) * half_max + k) * M_max + y] = A;
+            spec[((int64_t)(2 * p + 1) * half_max + k) * M_max + y] = B;
+        }
+        __syncthreads();
+    }
+}
+
+// Second half of a4 + a5: per column kx, forward FFT along y of the 10
+// arrays, Parseval partial of Z, the kernel-charge products, inverse FFT of
+// the 6 products along y; rows y < N are stored.
+//   A0 = K2 W1, Ax = DxK2 W1 + K2 Mx, Ay = DyK2 W1 + K2 My   (alpha part)
+//   B0 = Ke W1, Bx = DxKe W1 + Ke Mx, By = DyKe W1 + Ke My   (beta part)
+__global__ void __launch_bounds__(kColThreads, 1) k_col(Geo* __restrict__ gp, const float2* __restrict__ spec,
+                                                        const float2* __restrict__ twg, float2* __restrict__ colout,
+                                                        int M_max, int N_max) {
+    extern __shared__ float2 sm[];
+    float2* tw = sm;                      // M
+    float2* buf = sm + M_max;             // 10 * M
+    float2* scr = buf + 10 * M_max;       // 6 * M
+    __shared__ double zred[kColThreads / 32];
+    const int M = gp->M, N = gp->N, half = M / 2 + 1, nrad = gp->nrad;
+    const unsigned long long plan = gp->plan;
+    const int half_max = M_max / 2 + 1;
+    for (int k = threadIdx.x; k < M; k += blockDim.x) tw[k] = twg[k];
+    double zpart = 0.0;
+    for (int kx = blockIdx.x; kx < half; kx += gridDim.x) {
+        for (int t = threadIdx.x; t < 10 * M; t += blockDim.x) {
+            const int a = t / M, y = t - a * M;
+            buf[t] = spec[((int64_t)a * half_max + kx) * M_max + y];
+        }
+        __syncthreads();
+        fft_block(buf, scr, M, 5, M, plan, nrad, tw, false);
+        fft_block(buf + 5 * M, scr, M, 5, M, plan, nrad, tw, false);
+        const double wt = (kx == 0 || 2 * kx == M) ? 1.0 : 2.0;
+        for (int k = threadIdx.x; k < M; k += blockDim.x) {
+            const float2 W1 = buf[k], Mx = buf[M + k], My = buf[2 * M + k];
+            const float2 K1 = buf[3 * M + k], K2 = buf[4 * M + k], Ke = buf[5 * M + k];
+            const float2 DxK2 = buf[6 * M + k], DxKe = buf[7 * M + k];
+            const float2 DyK2 = buf[8 * M + k], DyKe = buf[9 * M + k];
+            zpart += wt * (double)K1.x * ((double)W1.x * W1.x + (double)W1.y * W1.y);
+            buf[k] = cmul(K2, W1);
+            buf[M + k] = cadd(cmul(DxK2, W1), cmul(K2, Mx));
+            buf[2 * M + k] = cadd(cmul(DyK2, W1), cmul(K2, My));
+            buf[3 * M + k] = cmul(Ke, W1);
+            buf[4 * M + k] = cadd(cmul(DxKe, W1), cmul(Ke, Mx));
+            buf[5 * M + k] = cadd(cmul(DyKe, W1), cmul(Ke, My));
+        }
+        __syncthreads();
+        fft_block(buf, scr, M, 6, M, plan, nrad, tw, true);
+        for (int t = threadIdx.x; t < 6 * N; t += blockDim.x) {
+            const int b = t / N, y = t - b * N;
+            colout[((int64_t)b * half_max + kx) * N_max + y] = buf[b * M + y];
+        }
+        __syncthreads();
+    }
+    for (int o = 16; o > 0; o >>= 1) zpart += __shfl_xor_sync(0xffffffffu, zpart, o);
+    if ((threadIdx.x & 31) == 0) zred[threadIdx.x >> 5] = zpart;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double z = 0.0;
+        for (int k = 0; k < kColThreads / 32; ++k) z += zred[k];
+        atomicAdd(&gp->zacc, z);
+    }
+}
+
+// Last part of a4: per row y < N, combine with alpha/beta (Z is complete now),
+// inverse FFT along x (P0 + i Qx packed, Qy alone), scale 1/M^2, keep x < N.
+__global__ void __launch_bounds__(kInvThreads) k_row_inv(Geo* __restrict__ gp, const float2* __restrict__ colout,
+                                                         const float2* __restrict__ twg, float4* __restrict__ fgrid,
+                                                         int M_max, int N_max, int64_t n, float lambda_kl,
+                                                         float lambda_r) {
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* buf = sm + M_max;             // 2 * M
+    float2* scr = buf + 2 * M_max;        // 2 * M
+    const int M = gp->M, N = gp->N, nrad = gp->nrad;
+    const unsigned long long plan = gp->plan;
+    const int half_max = M_max / 2 + 1;
+    const double M2 = (double)M * (double)M;
+    const double Z = gp->zacc / M2 - (double)n;
+    // n < 2: there are no pairs, the repulsion sum and Z are both empty (alpha = 0)
+    const float alpha = (n >= 2 && Z > 0.0) ? (float)(-4.0 * (double)lambda_kl / Z) : 0.0f;
+    const float beta = (float)(-(double)lambda_r / ((double)n * (double)n));
+    if (blockIdx.x == 0 && threadIdx.x == 0) gp->Z = Z;
+    const float sc = (float)(1.0 / M2);
+    for (int k = threadIdx.x; k < M; k += blockDim.x) tw[k] = twg[k];
+    for (int y = blockIdx.x; y < N; y += gridDim.x) {
+        for (int k = threadIdx.x; k < M; k += blockDim.x) {
+            const bool lo = (k <= M / 2);
+            const int kk = lo ? k : M - k;
+            float2 c[6];
+#pragma unroll
+            for (int b = 0; b < 6; ++b) {
+                c[b] = colout[((int64_t)b * half_max + kk) * N_max + y];
+                if (!lo) c[b] = cconj(c[b]);
+            }
+            const float2 C0 = make_float2(alpha * c[0].x + beta * c[3].x, alpha * c[0].y + beta * c[3].y);
+            const float2 Cx = make_float2(alpha * c[1].x + beta * c[4].x, alpha * c[1].y + beta * c[4].y);
+            const float2 Cy = make_float2(alpha * c[2].x + beta * c[5].x, alpha * c[2].y + beta * c[5].y);
+            buf[k] = cadd(C0, mul_pi(Cx));
+            buf[M + k] = Cy;
+        }
+        __syncthreads();
+        fft_block(buf, scr, M, 2, M, plan, nrad, tw, true);
+        for (int x = threadIdx.x; x < N; x += blockDim.x) {
+            const float2 a = buf[x], b = buf[M + x];
+            fgrid[(int64_t)y * N + x] = make_float4(a.x * sc, a.y * sc, b.x * sc, 0.f);
+        }
+        __syncthreads();
+    }
+}
+
+size_t field_smem_row(int M_max) { return sizeof(float2) * (size_t)M_max * 11; }
+size_t field_smem_col(int M_max) { return sizeof(float2) * (size_t)M_max * 17; }
+size_t field_smem_inv(int M_max) { return sizeof(float2) * (size_t)M_max * 5; }
+
+cudaError_t field_set_attrs(int M_max) {
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_row_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem_row(M_max))) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_col, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem_col(M_max))) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(k_row_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem_inv(M_max))) != cudaSuccess) return e;
+    return cudaSuccess;
+}
+
+cudaError_t launch_field_phase(const Ws& w, const GradArgs& a, cudaStream_t s) {
+    cudaError_t e;
+    if ((e = field_set_attrs(w.M_max)) != cudaSuccess) return e;
+    const int64_t n = a.n;
+    const int pts_blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)kNumSMs * 8);
+    const int pb = pts_blocks > 0 ? pts_blocks : 1;
+    k_iter_init<<<1, 1, 0, s>>>(w.geo);
+    k_bbox<<<pb, 256, 0, s>>>(a.Y, n, w.geo, a.h_max, a.I_min, a.I_max);
+    k_prep<<<kNumSMs * 4, 256, 0, s>>>(w.geo, w.box_cnt, w.wgrid, w.tw);
+    k_box_count<<<pb, 256, 0, s>>>(a.Y, n, w.geo, w.box_cnt, w.box, w.rank, w.uv);
+    k_box_scan<<<1, 1024, 0, s>>>(w.geo, w.box_cnt, w.box_start, w.items, n);
+    k_box_scatter<<<pb, 256, 0, s>>>(n, w.box, w.rank, w.box_start, w.uv, w.sorted_uv);
+    k_spread<<<kNumSMs * 8, 256, 0, s>>>(w.geo, w.items, w.box_start, w.sorted_uv, w.wgrid);
+    k_row_fwd<<<kNumSMs * 2, kRowThreads, field_smem_row(w.M_max), s>>>(w.geo, w.wgrid, w.tw, w.spec, w.M_max, a.eps);
+    k_col<<<kNumSMs, kColThreads, field_smem_col(w.M_max), s>>>(w.geo, w.spec, w.tw, w.colout, w.M_max, w.N_max);
+    k_row_inv<<<kNumSMs * 2, kInvThreads, field_smem_inv(w.M_max), s>>>(w.geo, w.colout, w.tw, w.fgrid, w.M_max,
+                                                                        w.N_max, n, a.lambda_kl, a.lambda_r);
+    return cudaGetLastError();
+}
+
+}  // namespace tsnet

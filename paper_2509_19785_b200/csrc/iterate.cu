@@ -1,0 +1,245 @@
+// iterate.cu -- the attractive SpMV (a6) and the gather/assemble/update (a7)
+// of one L-tsNET iteration.
+//
+// a6  F_attr,i = sum_{j in row i} p_ij w_ij (X_i - X_j),  w = 1/(1 + r^2)
+//     (Eq. 6 first term, "analogous to attraction forces"; the
+//     sparse P of C0).  HBM-bound: 8 B per stored entry.
+// a7  grad_i = 4 lambda_kl F_attr,i + f_field,i + (lambda_c / n) X_i  with
+//     f_field gathered from the convolved grid (field.cu), followed by the
+//     momentum/gains move (reading R12).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace tsnet {
+
+constexpr int kSpmvChunk = 2048;   // stored entries of P per warp work item
+constexpr int kSpmvUnroll = 4;
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ int ld_stream_i32(const int32_t* a, uint64_t pol) {
+    int v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ld_stream_f32(const float* a, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+    return v;
+}
+
+// Largest r in [0, n) with indptr[r] <= e (indptr[0] = 0 <= e < indptr[n]),
+// 32-ary search by one warp.
+__device__ __forceinline__ int64_t warp_row_of(const int64_t* __restrict__ indptr, int64_t n, int64_t e) {
+    const int lane = threadIdx.x & 31;
+    int64_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const int64_t step = (hi - lo + 31) / 32;
+        const int64_t p = lo + lane * step;
+        const bool pred = (p < hi) && (__ldg(indptr + p) <= e);
+        const unsigned m = __ballot_sync(0xffffffffu, pred);
+        const int L = 31 - __clz(m);
+        lo = lo + L * step;
+        hi = std::min(lo + step, hi);
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256) k_spmv(int64_t n, int64_t nnz, const int64_t* __restrict__ indptr,
+                                              const int32_t* __restrict__ indices, const float* __restrict__ values,
+                                              const float2* __restrict__ Y, float2* __restrict__ F) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nchunks = (nnz + kSpmvChunk - 1) / kSpmvChunk;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t pol = policy_evict_first();
+    for (int64_t c = wid; c < nchunks; c += nw) {
+        const int64_t cs = c * kSpmvChunk, ce = std::min(cs + kSpmvChunk, nnz);
+        int64_t r = warp_row_of(indptr, n, cs);
+        while (true) {
+            const int64_t rs = __ldg(indptr + r), re = __ldg(indptr + r + 1);
+            const int64_t s0 = std::max(rs, cs), s1 = std::min(re, ce);
+            if (s0 < s1) {
+                const float2 yi = __ldg(Y + r);
+                float fx = 0.f, fy = 0.f;
+                for (int64_t base = s0; base < s1; base += 32 * kSpmvUnroll) {
+                    int col[kSpmvUnroll];
+                    float val[kSpmvUnroll];
+#pragma unroll
+                    for (int q = 0; q < kSpmvUnroll; ++q) {
+                        const int64_t e = base + lane + 32 * q;
+                        const bool ok = e < s1;
+                        col[q] = ok ? ld_stream_i32(indices + e, pol) : (int)r;
+                        val[q] = ok ? ld_stream_f32(values + e, pol) : 0.f;
+                    }
+                    float2 yj[kSpmvUnroll];
+#pragma unroll
+                    for (int q = 0; q < kSpmvUnroll; ++q) yj[q] = __ldg(Y + col[q]);
+#pragma unroll
+                    for (int q = 0; q < kSpmvUnroll; ++q) {
+                        const float dx = yi.x - yj[q].x, dy = yi.y - yj[q].y;
+                        const float w = __frcp_rn(1.0f + dx * dx + dy * dy);
+                        const float pw = val[q] * w;
+                        fx = fmaf(pw, dx, fx);
+                        fy = fmaf(pw, dy, fy);
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    fx += __shfl_xor_sync(0xffffffffu, fx, o);
+                    fy += __shfl_xor_sync(0xffffffffu, fy, o);
+                }
+                if (lane == 0) atomicAdd(F + r, make_float2(fx, fy));
+            }
+            if (re >= ce) break;
+            ++r;
+        }
+    }
+}
+
+cudaError_t launch_spmv(const Ws& w, const GradArgs& a, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(w.f_attr, 0, sizeof(float2) * (size_t)a.n, s);
+    if (e != cudaSuccess || a.nnz == 0) return e;
+    const int64_t nchunks = (a.nnz + kSpmvChunk - 1) / kSpmvChunk;
+    const int blocks = (int)std::min<int64_t>((nchunks + 7) / 8, (int64_t)kNumSMs * 8);
+    k_spmv<<<blocks, 256, 0, s>>>(a.n, a.nnz, a.indptr, a.indices, a.values, a.Y, w.f_attr);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- gather (a7)
+__device__ __forceinline__ void lagrange3u(float u, float (&L)[3]) {
+    const float s0 = 1.0f / 6.0f, s1 = 0.5f, s2 = 5.0f / 6.0f;
+    L[0] = 4.5f * (u - s1) * (u - s2);
+    L[1] = -9.0f * (u - s0) * (u - s2);
+    L[2] = 4.5f * (u - s0) * (u - s1);
+}
+
+// f_field_i = sum_{a,b} L_a(u_x) L_b(u_y) [ (X_i - t_ab) P0 + Q ],  X_i - t_ab = (u - s) h_b
+__device__ __forceinline__ float2 gather_field(const Geo& g, const float4* __restrict__ fgrid, int b, float2 u) {
+    const int I = g.I, N = g.N;
+    const float h_b = (float)g.h_b;
+    const int bx = b % I, by = b / I;
+    float Lx[3], Ly[3];
+    lagrange3u(u.x, Lx);
+    lagrange3u(u.y, Ly);
+    const float s[3] = {1.0f / 6.0f, 0.5f, 5.0f / 6.0f};
+    float fx = 0.f, fy = 0.f;
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) {
+        const float4* row = fgrid + (int64_t)(3 * by + bb) * N + 3 * bx;
+        const float ey = (u.y - s[bb]) * h_b;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float4 f = __ldg(row + a);
+            const float wgt = Lx[a] * Ly[bb];
+            const float ex = (u.x - s[a]) * h_b;
+            fx = fmaf(wgt, fmaf(ex, f.x, f.y), fx);
+            fy = fmaf(wgt, fmaf(ey, f.x, f.z), fy);
+        }
+    }
+    return make_float2(fx, fy);
+}
+
+// mode 0: write grad; mode 1: write f_field (and F_attr stays in ws)
+__global__ void __launch_bounds__(256) k_grad_out(int64_t n, const Geo* __restrict__ gp, const float4* __restrict__ fgrid,
+                                                  const int* __restrict__ box, const float2* __restrict__ uv,
+                                                  const float2* __restrict__ Y, const float2* __restrict__ Fa,
+                                                  float lambda_kl, float lambda_c, float2* __restrict__ grad,
+                                                  float2* __restrict__ f_field) {
+    const Geo g = *gp;
+    const float cn = (float)((double)lambda_c / (double)n);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float2 ff = gather_field(g, fgrid, box[i], uv[i]);
+        if (f_field) f_field[i] = ff;
+        if (grad) {
+            const float2 y = Y[i], fa = Fa[i];
+            grad[i] = make_float2(fmaf(4.0f * lambda_kl, fa.x, ff.x) + cn * y.x,
+                                  fmaf(4.0f * lambda_kl, fa.y, ff.y) + cn * y.y);
+        }
+    }
+}
+
+__device__ __forceinline__ float sgnf(float x) { return (float)((x > 0.f) - (x < 0.f)); }
+
+__device__ __forceinline__ void gains_move(float gr, float& v, float& gn, float& y, const tsnet_step_params& sp) {
+    gn = (sgnf(gr) != sgnf(v)) ? gn + sp.gain_inc : gn * sp.gain_dec;
+    gn = fmaxf(gn, sp.gain_min);
+    v = sp.momentum * v - sp.eta * gn * gr;
+    y = y + v;
+}
+
+__global__ void __launch_bounds__(256) k_update(int64_t n, Geo* __restrict__ gp, const float4* __restrict__ fgrid,
+                                                const int* __restrict__ box, const float2* __restrict__ uv,
+                                                float2* __restrict__ Y, const float2* __restrict__ Fa,
+                                                float2* __restrict__ vel, float2* __restrict__ gains, float lambda_kl,
+                                                float lambda_c, tsnet_step_params sp) {
+    const Geo g = *gp;
+    const float cn = (float)((double)lambda_c / (double)n);
+    double sx = 0.0, sy = 0.0;
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float2 ff = gather_field(g, fgrid, box[i], uv[i]);
+        float2 y = Y[i];
+        const float2 fa = Fa[i];
+        const float gx = fmaf(4.0f * lambda_kl, fa.x, ff.x) + cn * y.x;
+        const float gy = fmaf(4.0f * lambda_kl, fa.y, ff.y) + cn * y.y;
+        float2 v = vel[i], gn = gains[i];
+        gains_move(gx, v.x, gn.x, y.x, sp);
+        gains_move(gy, v.y, gn.y, y.y, sp);
+        bad |= !(isfinite(y.x) && isfinite(y.y));
+        Y[i] = y;
+        vel[i] = v;
+        gains[i] = gn;
+        sx += y.x;
+        sy += y.y;
+    }
+    if (sp.recenter) {
+        for (int o = 16; o > 0; o >>= 1) {
+            sx += __shfl_xor_sync(0xffffffffu, sx, o);
+            sy += __shfl_xor_sync(0xffffffffu, sy, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(&gp->sum_x, sx);
+            atomicAdd(&gp->sum_y, sy);
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&gp->nonfinite, 1);
+}
+
+__global__ void k_recenter(int64_t n, const Geo* __restrict__ gp, float2* __restrict__ Y) {
+    const float mx = (float)(gp->sum_x / (double)n), my = (float)(gp->sum_y / (double)n);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float2 y = Y[i];
+        Y[i] = make_float2(y.x - mx, y.y - my);
+    }
+}
+
+static int pts_blocks(int64_t n) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)kNumSMs * 8));
+}
+
+cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2* f_field, double* Z,
+                            cudaStream_t s) {
+    k_grad_out<<<pts_blocks(a.n), 256, 0, s>>>(a.n, w.geo, w.fgrid, w.box, w.uv, a.Y, w.f_attr, a.lambda_kl,
+                                               a.lambda_c, grad, f_field);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (Z) e = cudaMemcpyAsync(Z, &w.geo->Z, sizeof(double), cudaMemcpyDeviceToDevice, s);
+    return e;
+}
+
+cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,
+                          const tsnet_step_params& sp, cudaStream_t s) {
+    k_update<<<pts_blocks(a.n), 256, 0, s>>>(a.n, w.geo, w.fgrid, w.box, w.uv, Y, w.f_attr, vel, gains, a.lambda_kl,
+                                             a.lambda_c, sp);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || !sp.recenter) return e;
+    k_recenter<<<pts_blocks(a.n), 256, 0, s>>>(a.n, w.geo, Y);
+    return cudaGetLastError();
+}
+
+}  // namespace tsnet

@@ -1,0 +1,225 @@
+// tsnet.cu -- the C-ABI entry points of libtsnet (declared in include/tsnet.h).
+// Argument checking, workspace map, orchestration of the kernels of
+// field.cu / iterate.cu / cost.cu / knn.cu on the caller's stream.
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace tsnet {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+size_t build_P_ws_bytes(int64_t n, int k);
+int build_P_impl(const tsnet_graph* g, double u, int k, uint64_t seed, tsnet_csr* P, int32_t* knn_idx,
+                 int32_t* knn_hop, int32_t* knn_len, double* beta, void* ws, size_t ws_bytes, cudaStream_t s);
+
+static int check_grad_params(const tsnet_grad_params* gp) {
+    TSNET_ARG(gp != nullptr, "grad params are NULL");
+    TSNET_ARG(gp->interp_P == 3, "interp_P = %d: only 3 interpolation points per interval are implemented",
+              gp->interp_P);
+    TSNET_ARG(gp->I_min >= 1 && gp->I_min <= gp->I_max && gp->I_max <= TSNET_I_MAX_LIMIT,
+              "need 1 <= I_min (%d) <= I_max (%d) <= %d", gp->I_min, gp->I_max, TSNET_I_MAX_LIMIT);
+    TSNET_ARG(gp->h_max > 0.f && std::isfinite(gp->h_max), "h_max must be > 0");
+    TSNET_ARG(gp->eps > 0.f, "eps must be > 0");
+    return TSNET_OK;
+}
+
+static int check_shard(const tsnet_shard* sh, int64_t n) {
+    if (sh == nullptr) return TSNET_OK;
+    TSNET_ARG(sh->world == 1 && sh->rank == 0 && sh->row_begin == 0 && sh->row_end == n,
+              "multi-GPU shards are not implemented in this build (world=%d)", sh->world);
+    return TSNET_OK;
+}
+
+static int check_csr(const tsnet_csr* P) {
+    TSNET_ARG(P != nullptr, "P is NULL");
+    TSNET_ARG(P->n >= 0 && P->nnz >= 0, "P has negative sizes");
+    TSNET_ARG(P->n == 0 || P->indptr != nullptr, "P->indptr is NULL");
+    TSNET_ARG(P->nnz == 0 || (P->indices != nullptr && P->values != nullptr), "P arrays are NULL");
+    return TSNET_OK;
+}
+
+static int prepare(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, const tsnet_shard* sh, void* ws,
+                   size_t ws_bytes, Ws& w, GradArgs& a) {
+    int st;
+    if ((st = check_csr(P)) != TSNET_OK) return st;
+    if ((st = check_grad_params(gp)) != TSNET_OK) return st;
+    if ((st = check_shard(sh, P->n)) != TSNET_OK) return st;
+    TSNET_ARG(P->n == 0 || Y != nullptr, "Y is NULL");
+    w = ws_map(ws, P->n, P->nnz, gp->I_max);
+    TSNET_ARG(ws != nullptr && ws_bytes >= w.bytes, "workspace too small (%zu < %zu bytes)", ws_bytes, w.bytes);
+    a.n = P->n;
+    a.nnz = P->nnz;
+    a.indptr = P->indptr;
+    a.indices = P->indices;
+    a.values = P->values;
+    a.Y = reinterpret_cast<const float2*>(Y);
+    a.lambda_kl = gp->lambda_kl;
+    a.lambda_c = gp->lambda_c;
+    a.lambda_r = gp->lambda_r;
+    a.eps = gp->eps;
+    a.h_max = gp->h_max;
+    a.I_min = gp->I_min;
+    a.I_max = gp->I_max;
+    return TSNET_OK;
+}
+
+static int eval_gradient_parts(const Ws& w, const GradArgs& a, cudaStream_t s) {
+    TSNET_CUDA(launch_field_phase(w, a, s));
+    TSNET_CUDA(launch_spmv(w, a, s));
+    return TSNET_OK;
+}
+
+}  // namespace tsnet
+
+using namespace tsnet;
+
+extern "C" {
+
+const char* tsnet_last_error(void) { return g_err; }
+
+int32_t tsnet_resolve_k(int64_t n, double u, int32_t k_req) {
+    int64_t k = k_req > 0 ? k_req : (int64_t)std::floor(3.0 * u + 0.5);
+    if (k > n - 1) k = n - 1;
+    if (k < 0) k = 0;
+    return (int32_t)k;
+}
+
+size_t tsnet_build_P_workspace_bytes(int64_t n, int32_t k) { return build_P_ws_bytes(n, k); }
+
+int tsnet_build_P(const tsnet_graph* g, double u, int32_t k, uint64_t seed, tsnet_csr* P, int32_t* knn_idx,
+                  int32_t* knn_hop, int32_t* knn_len, double* beta, void* ws, size_t ws_bytes, tsnet_stream_t stream) {
+    TSNET_ARG(g != nullptr && P != nullptr, "graph or P is NULL");
+    TSNET_ARG(g->n >= 0, "negative n");
+    TSNET_ARG(u >= 1.0 && std::isfinite(u), "perplexity u = %g must be >= 1", u);
+    TSNET_ARG(k >= 0 && k <= 256, "k = %d outside [0, 256] (resolve it with tsnet_resolve_k)", k);
+    TSNET_ARG(k <= (g->n > 0 ? g->n - 1 : 0), "k = %d > n - 1", k);
+    TSNET_ARG(g->n == 0 || (g->indptr && g->indices), "graph arrays are NULL");
+    TSNET_ARG(g->n == 0 || k == 0 || (knn_idx && knn_hop && knn_len), "kNN output arrays are NULL");
+    TSNET_ARG(P->indptr != nullptr, "P->indptr is NULL");
+    return build_P_impl(g, u, k, seed, P, knn_idx, knn_hop, knn_len, beta, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t tsnet_workspace_bytes(int64_t n, int64_t nnz, const tsnet_grad_params* gp, const tsnet_shard*) {
+    const int I_max = (gp && gp->I_max >= 1 && gp->I_max <= TSNET_I_MAX_LIMIT) ? gp->I_max : TSNET_I_MAX_LIMIT;
+    return ws_map(nullptr, n, nnz, I_max).bytes;
+}
+
+int tsnet_grad_parts(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, const tsnet_shard* shard,
+                     float* f_attr, float* f_field, double* Z, void* ws, size_t ws_bytes, tsnet_stream_t stream) {
+    Ws w;
+    GradArgs a;
+    int st = prepare(P, Y, gp, shard, ws, ws_bytes, w, a);
+    if (st != TSNET_OK) return st;
+    if (a.n == 0) return TSNET_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((st = eval_gradient_parts(w, a, s)) != TSNET_OK) return st;
+    TSNET_CUDA(launch_grad_out(w, a, nullptr, reinterpret_cast<float2*>(f_field), Z, s));
+    if (f_attr) TSNET_CUDA(cudaMemcpyAsync(f_attr, w.f_attr, sizeof(float2) * a.n, cudaMemcpyDeviceToDevice, s));
+    return TSNET_OK;
+}
+
+int tsnet_grad(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, const tsnet_shard* shard, float* grad,
+               double* Z, void* ws, size_t ws_bytes, tsnet_stream_t stream) {
+    Ws w;
+    GradArgs a;
+    int st = prepare(P, Y, gp, shard, ws, ws_bytes, w, a);
+    if (st != TSNET_OK) return st;
+    TSNET_ARG(a.n == 0 || grad != nullptr, "grad is NULL");
+    if (a.n == 0) return TSNET_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((st = eval_gradient_parts(w, a, s)) != TSNET_OK) return st;
+    TSNET_CUDA(launch_grad_out(w, a, reinterpret_cast<float2*>(grad), nullptr, Z, s));
+    return TSNET_OK;
+}
+
+int tsnet_step(const tsnet_csr* P, float* Y, float* vel, float* gains, const tsnet_grad_params* gp,
+               const tsnet_step_params* sp, const tsnet_shard* shard, void* ws, size_t ws_bytes,
+               tsnet_stream_t stream) {
+    Ws w;
+    GradArgs a;
+    int st = prepare(P, Y, gp, shard, ws, ws_bytes, w, a);
+    if (st != TSNET_OK) return st;
+    TSNET_ARG(sp != nullptr, "step params are NULL");
+    TSNET_ARG(a.n == 0 || (vel && gains), "vel or gains is NULL");
+    if (a.n == 0) return TSNET_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((st = eval_gradient_parts(w, a, s)) != TSNET_OK) return st;
+    TSNET_CUDA(launch_update(w, a, reinterpret_cast<float2*>(Y), reinterpret_cast<float2*>(vel),
+                             reinterpret_cast<float2*>(gains), *sp, s));
+    return TSNET_OK;
+}
+
+int tsnet_step_host(const tsnet_csr* P, float* Y_host, float* vel_host, float* gains_host,
+                    const tsnet_grad_params* gp, const tsnet_step_params* sp, const tsnet_shard* shard, void* ws,
+                    size_t ws_bytes, tsnet_stream_t stream) {
+    TSNET_ARG(P != nullptr && gp != nullptr, "P or params NULL");
+    Ws w0 = ws_map(ws, P->n, P->nnz, (gp->I_max >= 1 && gp->I_max <= TSNET_I_MAX_LIMIT) ? gp->I_max : 1);
+    TSNET_ARG(ws != nullptr && ws_bytes >= w0.bytes, "workspace too small");
+    const int64_t n = P->n;
+    if (n == 0) return TSNET_OK;
+    TSNET_ARG(Y_host && vel_host && gains_host, "host state arrays are NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    float2* dY = w0.state;
+    float2* dV = w0.state + n;
+    float2* dG = w0.state + 2 * n;
+    const size_t b = sizeof(float2) * (size_t)n;
+    TSNET_CUDA(cudaMemcpyAsync(dY, Y_host, b, cudaMemcpyHostToDevice, s));
+    TSNET_CUDA(cudaMemcpyAsync(dV, vel_host, b, cudaMemcpyHostToDevice, s));
+    TSNET_CUDA(cudaMemcpyAsync(dG, gains_host, b, cudaMemcpyHostToDevice, s));
+    int st = tsnet_step(P, reinterpret_cast<float*>(dY), reinterpret_cast<float*>(dV), reinterpret_cast<float*>(dG),
+                        gp, sp, shard, ws, ws_bytes, stream);
+    if (st != TSNET_OK) return st;
+    TSNET_CUDA(cudaMemcpyAsync(Y_host, dY, b, cudaMemcpyDeviceToHost, s));
+    TSNET_CUDA(cudaMemcpyAsync(vel_host, dV, b, cudaMemcpyDeviceToHost, s));
+    TSNET_CUDA(cudaMemcpyAsync(gains_host, dG, b, cudaMemcpyDeviceToHost, s));
+    TSNET_CUDA(cudaStreamSynchronize(s));
+    return TSNET_OK;
+}
+
+int tsnet_cost(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, int32_t mode, const tsnet_shard* shard,
+               double* out3, void* ws, size_t ws_bytes, tsnet_stream_t stream) {
+    Ws w;
+    GradArgs a;
+    int st = prepare(P, Y, gp, shard, ws, ws_bytes, w, a);
+    if (st != TSNET_OK) return st;
+    TSNET_ARG(mode == 0 || mode == 1, "cost mode must be 0 (exact) or 1 (interpolated Z)");
+    TSNET_ARG(out3 != nullptr, "out3 is NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (a.n == 0) {
+        TSNET_CUDA(cudaMemsetAsync(out3, 0, 3 * sizeof(double), s));
+        return TSNET_OK;
+    }
+    if (mode == 1) TSNET_CUDA(launch_field_phase(w, a, s));
+    TSNET_CUDA(launch_cost(w, a, mode, out3, s));
+    return TSNET_OK;
+}
+
+int tsnet_read_stats(const void* ws, tsnet_stats* out, tsnet_stream_t stream) {
+    TSNET_ARG(ws != nullptr && out != nullptr, "NULL argument");
+    Geo g;
+    cudaStream_t s = (cudaStream_t)stream;
+    TSNET_CUDA(cudaMemcpyAsync(&g, ws, sizeof(Geo), cudaMemcpyDeviceToHost, s));
+    TSNET_CUDA(cudaStreamSynchronize(s));
+    out->Z = g.Z;
+    out->lo_x = g.lo_x;
+    out->lo_y = g.lo_y;
+    out->S = g.S;
+    out->h_b = g.h_b;
+    out->I = g.I;
+    out->N = g.N;
+    out->M = g.M;
+    out->nonfinite = g.nonfinite;
+    return g.nonfinite ? TSNET_E_NONFINITE : TSNET_OK;
+}
+
+}  // extern "C"

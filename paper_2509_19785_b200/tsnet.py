@@ -1,0 +1,287 @@
+"""Thin ctypes binding of libtsnet.so (include/tsnet.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels behind the C-ABI.  PyTorch provides device memory and the stream.
+Names follow the C-ABI (tsnet_build_P, tsnet_grad, tsnet_grad_parts,
+tsnet_step, tsnet_step_host, tsnet_cost, tsnet_workspace_bytes,
+tsnet_read_stats, tsnet_last_error).  There is no CPU fallback: if the
+library is missing or fails, these functions raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtsnet.so")
+
+c_i32, c_i64, c_f32, c_f64, c_sz, c_vp, c_u64 = (ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_double,
+                                                 ctypes.c_size_t, ctypes.c_void_p, ctypes.c_uint64)
+
+TSNET_OK, TSNET_E_ARG, TSNET_E_CAPACITY, TSNET_E_CUDA, TSNET_E_NCCL, TSNET_E_NONFINITE, TSNET_W_PERPLEXITY = range(7)
+TSNET_I_MAX_LIMIT = 256
+
+
+class tsnet_graph(ctypes.Structure):
+    _fields_ = [("n", c_i64), ("indptr", c_vp), ("indices", c_vp)]
+
+
+class tsnet_csr(ctypes.Structure):
+    _fields_ = [("n", c_i64), ("nnz", c_i64), ("capacity", c_i64), ("indptr", c_vp), ("indices", c_vp),
+                ("values", c_vp)]
+
+
+class tsnet_grad_params(ctypes.Structure):
+    _fields_ = [("lambda_kl", c_f32), ("lambda_c", c_f32), ("lambda_r", c_f32), ("eps", c_f32),
+                ("interp_P", c_i32), ("h_max", c_f32), ("I_min", c_i32), ("I_max", c_i32)]
+
+
+class tsnet_step_params(ctypes.Structure):
+    _fields_ = [("eta", c_f32), ("momentum", c_f32), ("gain_inc", c_f32), ("gain_dec", c_f32),
+                ("gain_min", c_f32), ("recenter", c_i32)]
+
+
+class tsnet_shard(ctypes.Structure):
+    _fields_ = [("rank", c_i32), ("world", c_i32), ("row_begin", c_i64), ("row_end", c_i64)]
+
+
+class tsnet_stats(ctypes.Structure):
+    _fields_ = [("Z", c_f64), ("lo_x", c_f64), ("lo_y", c_f64), ("S", c_f64), ("h_b", c_f64), ("I", c_i32),
+                ("N", c_i32), ("M", c_i32), ("nonfinite", c_i32)]
+
+
+_lib = None
+
+# (name, restype, argtypes) of every C-ABI entry point
+SIGNATURES = [
+    ("tsnet_resolve_k", c_i32, [c_i64, c_f64, c_i32]),
+    ("tsnet_build_P_workspace_bytes", c_sz, [c_i64, c_i32]),
+    ("tsnet_build_P", ctypes.c_int, [ctypes.POINTER(tsnet_graph), c_f64, c_i32, c_u64, ctypes.POINTER(tsnet_csr),
+                                     c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    ("tsnet_workspace_bytes", c_sz, [c_i64, c_i64, ctypes.POINTER(tsnet_grad_params), ctypes.POINTER(tsnet_shard)]),
+    ("tsnet_grad", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, ctypes.POINTER(tsnet_grad_params),
+                                  ctypes.POINTER(tsnet_shard), c_vp, c_vp, c_vp, c_sz, c_vp]),
+    ("tsnet_grad_parts", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, ctypes.POINTER(tsnet_grad_params),
+                                        ctypes.POINTER(tsnet_shard), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    ("tsnet_step", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, c_vp, c_vp, ctypes.POINTER(tsnet_grad_params),
+                                  ctypes.POINTER(tsnet_step_params), ctypes.POINTER(tsnet_shard), c_vp, c_sz, c_vp]),
+    ("tsnet_step_host", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, c_vp, c_vp,
+                                       ctypes.POINTER(tsnet_grad_params), ctypes.POINTER(tsnet_step_params),
+                                       ctypes.POINTER(tsnet_shard), c_vp, c_sz, c_vp]),
+    ("tsnet_cost", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, ctypes.POINTER(tsnet_grad_params), c_i32,
+                                  ctypes.POINTER(tsnet_shard), c_vp, c_vp, c_sz, c_vp]),
+    ("tsnet_read_stats", ctypes.c_int, [c_vp, ctypes.POINTER(tsnet_stats), c_vp]),
+    ("tsnet_last_error", ctypes.c_char_p, []),
+]
+
+
+def lib():
+    """Load libtsnet.so (fails loudly if it is not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2509_19785_b200.build` "
+                               "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+class TsnetError(RuntimeError):
+    def __init__(self, fn, status):
+        msg = lib().tsnet_last_error().decode(errors="replace")
+        super().__init__(f"{fn} failed with status {status}: {msg}")
+        self.status = status
+
+
+def _check(fn, st, ok=(TSNET_OK,)):
+    if st not in ok:
+        raise TsnetError(fn, st)
+    return st
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("tensor must be on the CUDA device (no CPU fallback)")
+
+
+# ----------------------------------------------------------------- params
+@dataclass
+class GradParams:
+    lambda_kl: float = 1.0
+    lambda_c: float = 0.01
+    lambda_r: float = 0.6
+    eps: float = 0.05
+    interp_P: int = 3
+    h_max: float = 0.25
+    I_min: int = 20
+    I_max: int = TSNET_I_MAX_LIMIT
+
+    def c(self):
+        return tsnet_grad_params(self.lambda_kl, self.lambda_c, self.lambda_r, self.eps, self.interp_P, self.h_max,
+                                 self.I_min, self.I_max)
+
+
+@dataclass
+class StepParams:
+    eta: float = 50.0
+    momentum: float = 0.8
+    gain_inc: float = 0.2
+    gain_dec: float = 0.8
+    gain_min: float = 0.01
+    recenter: int = 0
+
+    def c(self):
+        return tsnet_step_params(self.eta, self.momentum, self.gain_inc, self.gain_dec, self.gain_min,
+                                 int(self.recenter))
+
+
+class CSR:
+    """Device CSR matrix P (int64 indptr, int32 indices, fp32 values)."""
+
+    def __init__(self, indptr: torch.Tensor, indices: torch.Tensor, values: torch.Tensor, nnz: int | None = None):
+        _require_cuda(indptr, indices, values)
+        assert indptr.dtype == torch.int64 and indices.dtype == torch.int32 and values.dtype == torch.float32
+        self.indptr, self.indices, self.values = indptr, indices, values
+        self.n = indptr.numel() - 1
+        self.nnz = int(indices.numel()) if nnz is None else int(nnz)
+
+    def c(self):
+        return tsnet_csr(self.n, self.nnz, int(self.indices.numel()), self.indptr.data_ptr(),
+                         self.indices.data_ptr() if self.indices.numel() else None,
+                         self.values.data_ptr() if self.values.numel() else None)
+
+
+def _shard(shard):
+    return None if shard is None else ctypes.byref(shard)
+
+
+# ------------------------------------------------------------------ C0
+def tsnet_resolve_k(n: int, u: float, k: int = 0) -> int:
+    return int(lib().tsnet_resolve_k(n, u, k))
+
+
+def tsnet_build_P_workspace_bytes(n: int, k: int) -> int:
+    return int(lib().tsnet_build_P_workspace_bytes(n, k))
+
+
+def tsnet_build_P(indptr: torch.Tensor, indices: torch.Tensor, u: float = 40.0, k: int = 0, seed: int = 0,
+                  capacity: int | None = None, stream=None):
+    """C0 on the GPU.  Returns dict(P=CSR, knn_idx, knn_hop, knn_len, beta, k, status)."""
+    _require_cuda(indptr, indices)
+    dev = indptr.device
+    n = indptr.numel() - 1
+    k = tsnet_resolve_k(n, u, k)
+    ws_bytes = tsnet_build_P_workspace_bytes(n, k)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    knn_idx = torch.empty((n, max(k, 1)), dtype=torch.int32, device=dev)
+    knn_hop = torch.empty((n, max(k, 1)), dtype=torch.int32, device=dev)
+    knn_len = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    beta = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    cap = 2 * n * k if capacity is None else capacity
+    P_ip = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    P_ix = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    P_v = torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
+    g = tsnet_graph(n, indptr.data_ptr(), indices.data_ptr() if indices.numel() else None)
+    P = tsnet_csr(n, 0, cap, P_ip.data_ptr(), P_ix.data_ptr(), P_v.data_ptr())
+    st = lib().tsnet_build_P(ctypes.byref(g), float(u), k, seed & 0xFFFFFFFFFFFFFFFF, ctypes.byref(P),
+                             _ptr(knn_idx), _ptr(knn_hop), _ptr(knn_len), _ptr(beta), _ptr(ws), ws_bytes,
+                             _stream(stream))
+    if st == TSNET_E_CAPACITY:
+        return dict(status=st, required_nnz=int(P.nnz))
+    _check("tsnet_build_P", st, ok=(TSNET_OK, TSNET_W_PERPLEXITY))
+    nnz = int(P.nnz)
+    del ws
+    return dict(P=CSR(P_ip, P_ix[:nnz].clone(), P_v[:nnz].clone()), knn_idx=knn_idx[:, :k], knn_hop=knn_hop[:, :k],
+                knn_len=knn_len[:n], beta=beta[:n], k=k, status=st)
+
+
+# ------------------------------------------------------ per-iteration path
+def tsnet_workspace_bytes(n: int, nnz: int, gp: GradParams, shard=None) -> int:
+    g = gp.c()
+    return int(lib().tsnet_workspace_bytes(n, nnz, ctypes.byref(g), _shard(shard)))
+
+
+def alloc_workspace(n: int, nnz: int, gp: GradParams, device="cuda") -> torch.Tensor:
+    """Zero-initialised workspace (the header must start zeroed)."""
+    return torch.zeros(max(tsnet_workspace_bytes(n, nnz, gp), 1), dtype=torch.uint8, device=device)
+
+
+def tsnet_grad(P: CSR, Y: torch.Tensor, gp: GradParams, ws: torch.Tensor, grad=None, Z=None, shard=None,
+               stream=None):
+    _require_cuda(Y, ws)
+    grad = torch.empty_like(Y) if grad is None else grad
+    Z = torch.empty(1, dtype=torch.float64, device=Y.device) if Z is None else Z
+    Pc, g = P.c(), gp.c()
+    _check("tsnet_grad", lib().tsnet_grad(ctypes.byref(Pc), _ptr(Y), ctypes.byref(g), _shard(shard), _ptr(grad),
+                                          _ptr(Z), _ptr(ws), ws.numel(), _stream(stream)))
+    return grad, Z
+
+
+def tsnet_grad_parts(P: CSR, Y: torch.Tensor, gp: GradParams, ws: torch.Tensor, shard=None, stream=None):
+    _require_cuda(Y, ws)
+    f_attr = torch.empty_like(Y)
+    f_field = torch.empty_like(Y)
+    Z = torch.empty(1, dtype=torch.float64, device=Y.device)
+    Pc, g = P.c(), gp.c()
+    _check("tsnet_grad_parts", lib().tsnet_grad_parts(ctypes.byref(Pc), _ptr(Y), ctypes.byref(g), _shard(shard),
+                                                      _ptr(f_attr), _ptr(f_field), _ptr(Z), _ptr(ws), ws.numel(),
+                                                      _stream(stream)))
+    return f_attr, f_field, Z
+
+
+def tsnet_step(P: CSR, Y, vel, gains, gp: GradParams, sp: StepParams, ws, shard=None, stream=None):
+    _require_cuda(Y, vel, gains, ws)
+    Pc, g, s = P.c(), gp.c(), sp.c()
+    _check("tsnet_step", lib().tsnet_step(ctypes.byref(Pc), _ptr(Y), _ptr(vel), _ptr(gains), ctypes.byref(g),
+                                          ctypes.byref(s), _shard(shard), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def tsnet_step_host(P: CSR, Y_host, vel_host, gains_host, gp: GradParams, sp: StepParams, ws, shard=None,
+                    stream=None):
+    """One iteration with HOST state tensors (pinned CPU memory), H2D + D2H inside."""
+    for t in (Y_host, vel_host, gains_host):
+        assert not t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
+    Pc, g, s = P.c(), gp.c(), sp.c()
+    _check("tsnet_step_host", lib().tsnet_step_host(ctypes.byref(Pc), _ptr(Y_host), _ptr(vel_host),
+                                                    _ptr(gains_host), ctypes.byref(g), ctypes.byref(s),
+                                                    _shard(shard), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def tsnet_cost(P: CSR, Y, gp: GradParams, ws, mode: int = 0, shard=None, stream=None):
+    _require_cuda(Y, ws)
+    out = torch.empty(3, dtype=torch.float64, device=Y.device)
+    Pc, g = P.c(), gp.c()
+    _check("tsnet_cost", lib().tsnet_cost(ctypes.byref(Pc), _ptr(Y), ctypes.byref(g), mode, _shard(shard),
+                                          _ptr(out), _ptr(ws), ws.numel(), _stream(stream)))
+    return out
+
+
+def tsnet_read_stats(ws, stream=None) -> dict:
+    st = tsnet_stats()
+    rc = lib().tsnet_read_stats(_ptr(ws), ctypes.byref(st), _stream(stream))
+    _check("tsnet_read_stats", rc, ok=(TSNET_OK, TSNET_E_NONFINITE))
+    return {f: getattr(st, f) for f, _ in tsnet_stats._fields_}
+
+
+def tsnet_last_error() -> str:
+    return lib().tsnet_last_error().decode(errors="replace")

@@ -1,0 +1,380 @@
+"""GPU <-> oracle parity through the C-ABI (run on a B200: pytest -m gpu).
+
+Bars (BASELINE.json north star):
+  * BFS neighbour sets and hop distances: bit-exact
+  * P: identical sparsity, <= 1e-6 relative per entry
+  * interpolated gradient (fp32 GPU) vs the fp64 interpolation oracle O5: <= 1e-4 relL2
+  * interpolated gradient vs the exact O(n^2) gradient O4a (n <= 20k): <= 2e-2 relL2
+  * one step from a common state: <= 1e-4 relL2 on the move
+Inputs are seeded and synthetic (workloads/); layouts past iteration 0 come from
+the oracle's own iterations (oracle.run_layout), never from the CUDA path.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2509_19785_b200 import (CSR, GradParams, StepParams, TsnetError, alloc_workspace, tsnet_build_P,
+                                   tsnet_cost, tsnet_grad, tsnet_grad_parts, tsnet_read_stats, tsnet_step)
+from paper_2509_19785_b200 import tsnet as T
+from workloads import (clustered_layout, config_graph, erdos_renyi, grid2d, init_layout, path_graph, random_state,
+                       star_graph, uniform_layout)
+
+pytestmark = pytest.mark.gpu
+
+GRAD_TOL = 1e-4
+EXACT_TOL = 2e-2
+
+
+def relL2(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    T.lib()   # fail loudly if the library is missing
+
+
+def dev_graph(ip, ix):
+    return torch.from_numpy(np.asarray(ip, np.int64)).cuda(), torch.from_numpy(np.asarray(ix, np.int32)).cuda()
+
+
+def dev_P(P):
+    """Oracle P rounded to fp32 -> device CSR (a common input for both sides)."""
+    return CSR(torch.from_numpy(P["indptr"]).cuda(), torch.from_numpy(P["indices"]).cuda(),
+               torch.from_numpy(P["values"].astype(np.float32)).cuda())
+
+
+def p32(P):
+    return P["values"].astype(np.float32).astype(np.float64)
+
+
+_CACHE = {}
+
+
+def oracle_P(cfg):
+    if cfg not in _CACHE:
+        ip, ix = config_graph(cfg)
+        _CACHE[cfg] = oracle.build_P(ip, ix, 40.0, seed=0)
+    return _CACHE[cfg]
+
+
+# ------------------------------------------------------------------ C0
+def check_build(ip, ix, u=40.0, k=0, seed=0):
+    got = tsnet_build_P(*dev_graph(ip, ix), u=u, k=k, seed=seed)
+    want = oracle.build_P(ip, ix, u, k=k, seed=seed)
+    kk = want["k"]
+    assert got["k"] == kk
+    assert np.array_equal(got["knn_len"].cpu().numpy(), want["knn_len"])
+    if kk > 0:
+        assert np.array_equal(got["knn_idx"].cpu().numpy(), want["knn_idx"])
+        assert np.array_equal(got["knn_hop"].cpu().numpy(), want["knn_hop"])
+    gb = got["beta"].cpu().numpy()
+    wb = want["beta"]
+    fin = np.isfinite(wb)
+    assert np.array_equal(np.isfinite(gb), fin)
+    assert np.allclose(gb[fin], wb[fin], rtol=1e-9, atol=0)
+    P = got["P"]
+    assert np.array_equal(P.indptr.cpu().numpy(), want["indptr"])
+    assert np.array_equal(P.indices.cpu().numpy(), want["indices"])
+    gv = P.values.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(gv - want["values"]) <= 1e-6 * np.abs(want["values"]))
+    return got, want
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_build_P_bitexact_configs(cfg):
+    ip, ix = config_graph(cfg)
+    got, want = check_build(ip, ix)
+    assert abs(want["values"].sum() - 1.0) < 1e-9
+
+
+@pytest.mark.parametrize("make,u,seed", [
+    (lambda: path_graph(9), 2.0, 0), (lambda: star_graph(300), 40.0, 3),      # ties at the cut-off, unreachable u
+    (lambda: erdos_renyi(300, 0.01, 4), 5.0, 1),                                # disconnected, short rows
+    (lambda: grid2d(7, 5), 40.0, 9),                                             # k capped at n-1
+    (lambda: erdos_renyi(400, 0.3, 2), 40.0, 11),                                # dense: overflow at level 1
+])
+def test_build_P_bitexact_edge_graphs(make, u, seed):
+    ip, ix = make()
+    check_build(ip, ix, u=u, seed=seed)
+
+
+def test_build_P_k_override_and_capacity():
+    ip, ix = grid2d(12, 12)
+    check_build(ip, ix, u=3.0, k=17, seed=5)
+    r = tsnet_build_P(*dev_graph(ip, ix), u=40.0, capacity=10)
+    assert r["status"] == T.TSNET_E_CAPACITY and r["required_nnz"] > 10
+
+
+def test_build_P_config4_sampled_rows():
+    """Full size (n ~ 0.95M Chung-Lu): kNN rows of sampled sources bit-exact,
+    P values of sampled rows == (p_j|i + p_i|j)/2n from oracle rows, global
+    invariants (symmetry, mass 1)."""
+    ip, ix = config_graph(4)
+    n = len(ip) - 1
+    got = tsnet_build_P(*dev_graph(ip, ix), u=40.0, seed=0)
+    assert got["status"] == T.TSNET_W_PERPLEXITY          # hubs with degree >= 40 (R6)
+    rng = np.random.default_rng(0)
+    hub = np.argsort(np.diff(ip))[-20:]
+    src = np.unique(np.concatenate([rng.choice(n, 2000, replace=False), hub]))
+    oi, oh, ol = oracle.knn(ip, ix, 120, 0, src=src)
+    gi = got["knn_idx"].cpu().numpy()[src]
+    gh = got["knn_hop"].cpu().numpy()[src]
+    assert np.array_equal(got["knn_len"].cpu().numpy()[src], ol)
+    assert np.array_equal(gi, oi) and np.array_equal(gh, oh)
+    P = got["P"]
+    pip, pix, pv = P.indptr.cpu().numpy(), P.indices.cpu().numpy(), P.values.cpu().numpy().astype(np.float64)
+    assert abs(pv.sum() - 1.0) < 1e-5
+    import scipy.sparse as sp
+    A = sp.csr_matrix((pv, pix, pip), shape=(n, n))
+    assert (A != A.T).nnz == 0
+    rows = src[:200]
+    for i in rows:
+        cols = pix[pip[i]:pip[i + 1]]
+        _, hop_i, _ = oracle.knn(ip, ix, 120, 0, src=[i])
+        idx_i, _, len_i = oracle.knn(ip, ix, 120, 0, src=[i])
+        pc_i, _ = oracle.calibrate(hop_i, len_i, 40.0)
+        jdx, jhop, jlen = oracle.knn(ip, ix, 120, 0, src=cols)
+        jpc, _ = oracle.calibrate(jhop, jlen, 40.0)
+        want = np.zeros(len(cols))
+        own = dict(zip(idx_i[0, :len_i[0]].tolist(), pc_i[0, :len_i[0]].tolist()))
+        for t, j in enumerate(cols):
+            row = jdx[t, :jlen[t]]
+            back = pc_i = jpc[t, np.flatnonzero(row == i)]
+            want[t] = (own.get(int(j), 0.0) + (back[0] if back.size else 0.0)) / (2.0 * n)
+        assert np.all(np.abs(pv[pip[i]:pip[i + 1]] - want) <= 1e-6 * want)
+        # every neighbour of i's own kNN list is present
+        assert set(own) <= set(cols.tolist())
+
+
+# ------------------------------------------------------------- gradient
+def gpu_grad(P_dev, Y32, gp):
+    ws = alloc_workspace(P_dev.n, P_dev.nnz, gp)
+    Yd = torch.from_numpy(Y32).cuda()
+    g, Z = tsnet_grad(P_dev, Yd, gp, ws)
+    fa, ff, Z2 = tsnet_grad_parts(P_dev, Yd, gp, ws)
+    torch.cuda.synchronize()
+    st = tsnet_read_stats(ws)
+    return g.cpu().numpy(), float(Z.item()), fa.cpu().numpy(), ff.cpu().numpy(), st
+
+
+def oracle_grad(P, Y32, lam, h_max=0.25, I_min=20, I_max=256):
+    return oracle.interp_gradient(Y32.astype(np.float64), P["indptr"], P["indices"], p32(P), *lam, eps=0.05,
+                                  h_max=h_max, I_min=I_min, I_max=I_max)
+
+
+_LAYOUTS = {}
+
+
+def oracle_layouts(cfg, iters=(249, 499)):
+    """Layouts of the oracle's own L-tsNET run (O5 + O6/O7) from the seeded init."""
+    key = (cfg, iters)
+    if key not in _LAYOUTS:
+        P = oracle_P(cfg)
+        n = P["n"]
+        out = {}
+
+        def cb(it, Y, vel, gains):
+            if it in iters:
+                out[it] = (Y.astype(np.float32), vel.astype(np.float32), gains.astype(np.float32))
+        oracle.run_layout(init_layout(n, 0), P["indptr"], P["indices"], p32(P), max(iters) + 1, callback=cb)
+        _LAYOUTS[key] = out
+    return _LAYOUTS[key]
+
+
+STAGE_A = (1.0, 1.2, 0.0)
+STAGE_B = (1.0, 0.01, 0.6)
+
+
+def layouts_for(cfg):
+    n = oracle_P(cfg)["n"]
+    L = {
+        "init": init_layout(n, 0),
+        "uniform30": uniform_layout(n, 30.0, 1),
+        "clustered": clustered_layout(n, 25.0, 7, 1.2, 2),
+        "offset": uniform_layout(n, 12.0, 3, offset=(-250.0, 400.0)),
+    }
+    return L
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+@pytest.mark.parametrize("lay", ["init", "uniform30", "clustered", "offset"])
+@pytest.mark.parametrize("lam", [STAGE_A, STAGE_B], ids=["stageA", "stageB"])
+def test_grad_parity_synthetic_layouts(cfg, lay, lam):
+    P = oracle_P(cfg)
+    Y = layouts_for(cfg)[lay]
+    gp = GradParams(*lam)
+    g, Z, fa, ff, st = gpu_grad(dev_P(P), Y, gp)
+    r = oracle_grad(P, Y, lam)
+    assert st["I"] == r["geo"]["I"] and st["N"] == r["geo"]["N"]
+    assert abs(Z - r["Z"]) <= 1e-5 * r["Z"]
+    assert relL2(fa, r["F_attr"]) <= 1e-5
+    assert relL2(g, r["g"]) <= GRAD_TOL, relL2(g, r["g"])
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_grad_parity_oracle_trajectory(cfg):
+    """Stage-A end and converged stage-B layouts of the oracle's own run."""
+    if cfg == 2:
+        pytest.importorskip("scipy")
+    P = oracle_P(cfg)
+    for it, (Y, _, _) in oracle_layouts(cfg).items():
+        lam = STAGE_A if it < 250 else STAGE_B
+        g, Z, _, _, st = gpu_grad(dev_P(P), Y, GradParams(*lam))
+        r = oracle_grad(P, Y, lam)
+        assert relL2(g, r["g"]) <= GRAD_TOL, (it, relL2(g, r["g"]))
+        # interpolation vs the exact O(n^2) gradient (n <= 20k)
+        ge, _ = oracle.exact_grad(Y.astype(np.float64), P["indptr"], P["indices"], p32(P), *lam)
+        assert relL2(g, ge) <= EXACT_TOL, (it, relL2(g, ge))
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+@pytest.mark.parametrize("lay", ["uniform30", "clustered"])
+def test_grad_vs_exact(cfg, lay):
+    P = oracle_P(cfg)
+    Y = layouts_for(cfg)[lay]
+    g, _, _, _, _ = gpu_grad(dev_P(P), Y, GradParams(*STAGE_B))
+    ge, _ = oracle.exact_grad(Y.astype(np.float64), P["indptr"], P["indices"], p32(P), *STAGE_B)
+    assert relL2(g, ge) <= EXACT_TOL
+
+
+def test_grad_parity_full_size_config4():
+    """n ~ 0.95M (bench workload), full gradient vs the oracle at a synthetic layout."""
+    ip, ix = config_graph(4)
+    got = tsnet_build_P(*dev_graph(ip, ix), u=40.0, seed=0)
+    Pd = got["P"]
+    n = Pd.n
+    Pnp = dict(indptr=Pd.indptr.cpu().numpy(), indices=Pd.indices.cpu().numpy(),
+               values=Pd.values.cpu().numpy().astype(np.float64))
+    Y = clustered_layout(n, 30.0, 40, 2.0, 5)
+    g, Z, fa, ff, st = gpu_grad(Pd, Y, GradParams(*STAGE_B))
+    r = oracle_grad(Pnp, Y, STAGE_B)
+    assert st["I"] == r["geo"]["I"]
+    assert relL2(g, r["g"]) <= GRAD_TOL
+
+
+# ---------------------------------------------------------------- steps
+@pytest.mark.parametrize("stage", [0, 1])
+def test_step_parity_common_state(stage):
+    P = oracle_P(2)
+    n = P["n"]
+    Y = clustered_layout(n, 20.0, 5, 1.5, 7)
+    vel, gains = random_state(n, 3)
+    lam = STAGE_A if stage == 0 else STAGE_B
+    mu = 0.5 if stage == 0 else 0.8
+    gp, sp = GradParams(*lam), StepParams(eta=50.0, momentum=mu)
+    Pd = dev_P(P)
+    ws = alloc_workspace(n, Pd.nnz, gp)
+    Yd, Vd, Gd = (torch.from_numpy(a.copy()).cuda() for a in (Y, vel, gains))
+    tsnet_step(Pd, Yd, Vd, Gd, gp, sp, ws)
+    torch.cuda.synchronize()
+    r = oracle_grad(P, Y, lam)
+    Yo, Vo, Go = oracle.update_step(Y, vel, gains, r["g"], eta=50.0, mu=mu)
+    assert relL2(Vd.cpu().numpy(), Vo) <= GRAD_TOL
+    assert relL2(Yd.cpu().numpy() - Y, Yo - Y) <= GRAD_TOL
+    small = np.abs(r["g"]) < 1e-6 * np.abs(r["g"]).max()
+    assert np.array_equal(np.isclose(Gd.cpu().numpy(), Go, rtol=1e-5)[~small], np.ones((~small).sum(), bool))
+
+
+def test_ten_iterations_config1():
+    """Free-running 10 iterations (config 1: stage-B multipliers, momentum 0.5)."""
+    P = oracle_P(1)
+    n = P["n"]
+    Y0 = init_layout(n, 0)
+    gp, sp = GradParams(*STAGE_B), StepParams(eta=50.0, momentum=0.5)
+    Pd = dev_P(P)
+    ws = alloc_workspace(n, Pd.nnz, gp)
+    Yd = torch.from_numpy(Y0.copy()).cuda()
+    Vd, Gd = torch.zeros_like(Yd), torch.ones_like(Yd)
+    Y, V, G = Y0.astype(np.float64), np.zeros((n, 2)), np.ones((n, 2))
+    for _ in range(10):
+        tsnet_step(Pd, Yd, Vd, Gd, gp, sp, ws)
+        g = oracle.interp_gradient(Y, P["indptr"], P["indices"], p32(P), *STAGE_B)["g"]
+        Y, V, G = oracle.update_step(Y, V, G, g, eta=50.0, mu=0.5)
+        Y, V, G = (a.astype(np.float32).astype(np.float64) for a in (Y, V, G))
+    torch.cuda.synchronize()
+    assert relL2(Yd.cpu().numpy(), Y) <= 1e-3
+
+
+def test_runner_graphs_match_eager():
+    from paper_2509_19785_b200 import Layout
+    P = oracle_P(1)
+    Pd = dev_P(P)
+    Y0 = torch.from_numpy(init_layout(P["n"], 0)).cuda()
+    a = Layout(Pd, Y0, use_graphs=True).run(260)
+    b = Layout(Pd, Y0, use_graphs=False).run(260)
+    a.sync(), b.sync()
+    assert relL2(a.Y.cpu().numpy(), b.Y.cpu().numpy()) <= 1e-3
+    assert a.stats()["nonfinite"] == 0
+
+
+# ----------------------------------------------------------------- cost
+def test_cost_exact_and_interpolated():
+    P = oracle_P(1)
+    Y = uniform_layout(P["n"], 20.0, 4)
+    gp = GradParams(*STAGE_B)
+    Pd = dev_P(P)
+    ws = alloc_workspace(Pd.n, Pd.nnz, gp)
+    Yd = torch.from_numpy(Y).cuda()
+    c0 = tsnet_cost(Pd, Yd, gp, ws, mode=0).cpu().numpy()
+    c1 = tsnet_cost(Pd, Yd, gp, ws, mode=1).cpu().numpy()
+    want = oracle.exact_cost(Y.astype(np.float64), P["indptr"], P["indices"], p32(P), *STAGE_B)
+    assert np.allclose(c0, want, rtol=2e-5)
+    assert abs(c1[0] - want[0]) <= 1e-3 * abs(want[0]) and abs(c1[1] - want[1]) <= 1e-6 * abs(want[1])
+    assert np.isnan(c1[2])
+
+
+# ----------------------------------------------------------------- edges
+def test_edge_cases():
+    gp = GradParams(*STAGE_B)
+    # n = 2, one pair
+    P = dict(indptr=np.array([0, 1, 2], np.int64), indices=np.array([1, 0], np.int32), values=np.array([0.5, 0.5]))
+    Y = np.array([[0.0, 0.0], [1.0, 0.0]], np.float32)
+    g, Z, _, _, _ = gpu_grad(dev_P(P), Y, gp)
+    r = oracle_grad(P, Y, STAGE_B)
+    assert relL2(g, r["g"]) <= GRAD_TOL
+    # coincident points (span floor 1e-12) and an empty P row
+    P = dict(indptr=np.array([0, 1, 2, 2], np.int64), indices=np.array([1, 0], np.int32),
+             values=np.array([0.5, 0.5]))
+    Y = np.zeros((3, 2), np.float32)
+    g, Z, _, _, st = gpu_grad(dev_P(P), Y, gp)
+    assert np.all(np.isfinite(g)) and st["nonfinite"] == 0
+    # huge span -> I clamped at I_max (box width > h_max)
+    Pc = oracle_P(1)
+    Y = uniform_layout(Pc["n"], 400.0, 9)
+    g, Z, _, _, st = gpu_grad(dev_P(Pc), Y, gp)
+    r = oracle_grad(Pc, Y, STAGE_B)
+    assert st["I"] == 256 and relL2(g, r["g"]) <= GRAD_TOL
+    # non-finite input is flagged
+    Yn = Y.copy()
+    Yn[5, 0] = np.nan
+    _, _, _, _, st = gpu_grad(dev_P(Pc), Yn, gp)
+    assert st["nonfinite"] == 1
+    # invalid parameters fail loudly
+    bad = GradParams(*STAGE_B, interp_P=4)
+    with pytest.raises(TsnetError):
+        ws = alloc_workspace(Pc["n"], len(Pc["values"]), GradParams())
+        tsnet_grad(dev_P(Pc), torch.from_numpy(Y).cuda(), bad, ws)
+
+
+@pytest.mark.parametrize("n", [1, 33, 1000, 4099])
+def test_ragged_sizes(n):
+    ip, ix = erdos_renyi(n, min(1.0, 6.0 / max(n, 2)), 1) if n > 1 else (np.array([0, 0], np.int64),
+                                                                         np.zeros(0, np.int32))
+    u = 3.0
+    if n > 1:
+        got, want = check_build(ip, ix, u=u)
+        P = dict(indptr=want["indptr"], indices=want["indices"], values=want["values"])
+    else:
+        P = dict(indptr=ip, indices=ix, values=np.zeros(0))
+    Y = clustered_layout(n, 8.0, 3, 1.0, n)
+    g, Z, _, _, _ = gpu_grad(dev_P(P), Y, GradParams(*STAGE_B))
+    if n > 1:
+        r = oracle_grad(P, Y, STAGE_B)
+        assert relL2(g, r["g"]) <= GRAD_TOL
+    else:
+        assert np.allclose(g, (0.01 / 1) * Y, atol=1e-7)

@@ -131,5 +131,5 @@ def test_geometry_policy():
     g = interp.geometry(np.array([[0.0, 0.0], [33.1, 1.0]]))
     assert g["I"] == 135                                  # ceil(132.4)=133 -> 5-smooth 135
     g = interp.geometry(np.array([[0.0, 0.0], [1000.0, 1.0]]))
-    assert g["I"] == 384                                  # I_max clamp
+    assert g["I"] == 256                                  # I_max clamp
     assert interp.five_smooth_at_least(97) == 100 and interp.five_smooth_at_most(97) == 96
