@@ -171,6 +171,11 @@ TSNET_API size_t tsnet_workspace_bytes(int64_t n, int64_t nnz, const tsnet_grad_
 TSNET_API int tsnet_grad(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, const tsnet_shard* shard,
                float* grad, double* Z, void* ws, size_t ws_bytes, tsnet_stream_t stream);
 
+/* The attractive term alone (step a6, Eq. 6 first term):
+ *   f_attr,i = sum_{j in row i} p_ij w_ij Delta_ij   (n x 2 fp32, device)
+ * Needs no workspace.  Async.  (Also the kernel bench.py times for the roofline.) */
+TSNET_API int tsnet_attr(const tsnet_csr* P, const float* Y, float* f_attr, tsnet_stream_t stream);
+
 /* Same evaluation, returning the parts separately (diagnostics / parity):
  *   f_attr  = F_attr (n x 2), f_field = -4 lambda_kl F_rep + lambda_r g_ent (n x 2),
  * so that grad = 4 lambda_kl f_attr + f_field + (lambda_c / n) Y.  Any output may be NULL. */

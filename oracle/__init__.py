@@ -64,6 +64,8 @@ def lib():
         _lib.oracle_symmetrize.argtypes = [i64, i64, P, P, P, P, P, P]
         _lib.oracle_attr_sparse.restype = None
         _lib.oracle_attr_sparse.argtypes = [i64, P, P, P, P, P]
+        _lib.oracle_attr_sparse_rows.restype = None
+        _lib.oracle_attr_sparse_rows.argtypes = [i64, i64, P, P, P, P, P]
         _lib.oracle_exact_Z.restype = f64
         _lib.oracle_exact_Z.argtypes = [i64, P]
         _lib.oracle_exact_grad.restype = f64
@@ -170,6 +172,15 @@ def attr_sparse(X, indptr, indices, pval):
     ip, ix, pv = _c(indptr, np.int64), _c(indices, np.int32), _c(pval, np.float64)
     F = np.zeros_like(X)
     lib().oracle_attr_sparse(X.shape[0], _p(X), _p(ip), _p(ix), _p(pv), _p(F))
+    return F
+
+
+def attr_sparse_rows(X, indptr, indices, pval, row0: int, nrows: int):
+    """attr_sparse for the rows [row0, row0 + nrows) only."""
+    X = _c(X, np.float64)
+    ip, ix, pv = _c(indptr, np.int64), _c(indices, np.int32), _c(pval, np.float64)
+    F = np.zeros((nrows, 2))
+    lib().oracle_attr_sparse_rows(row0, nrows, _p(X), _p(ip), _p(ix), _p(pv), _p(F))
     return F
 
 

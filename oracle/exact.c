@@ -13,7 +13,27 @@
 #include <math.h>
 
 /* Eq. 6 first term ("analogous to attraction forces") without
- * the factor 4 lambda_KL: F_i = sum_{j in row i} p_ij w_ij Delta_ij. */
+ * the factor 4 lambda_KL: F_i = sum_{j in row i} p_ij w_ij Delta_ij, for the
+ * rows i in [row0, row0 + nrows) (F holds those rows only). */
+void oracle_attr_sparse_rows(int64_t row0, int64_t nrows, const double* X, const int64_t* indptr,
+                             const int32_t* indices, const double* pval, double* F)
+{
+#pragma omp parallel for schedule(dynamic, 1024) if (nrows > 4096)
+    for (int64_t r = 0; r < nrows; ++r) {
+        const int64_t i = row0 + r;
+        double fx = 0.0, fy = 0.0;
+        for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+            int64_t j = indices[e];
+            double dx = X[2 * i] - X[2 * j], dy = X[2 * i + 1] - X[2 * j + 1];
+            double w = 1.0 / (1.0 + dx * dx + dy * dy);
+            fx += pval[e] * w * dx;
+            fy += pval[e] * w * dy;
+        }
+        F[2 * r] = fx;
+        F[2 * r + 1] = fy;
+    }
+}
+
 void oracle_attr_sparse(int64_t n, const double* X, const int64_t* indptr, const int32_t* indices,
                         const double* pval, double* F)
 {

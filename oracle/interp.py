@@ -268,3 +268,48 @@ def interp_gradient(Y, indptr, indices, pval, lkl, lc, lr, eps=0.05, h_max=0.25,
     F_attr = attr_sparse(Y, indptr, indices, pval)
     g = 4.0 * lkl * (F_attr - F_rep) + (lc / n) * Y + lr * g_ent
     return dict(g=g, Z=Z, F_attr=F_attr, F_rep=F_rep, g_ent=g_ent, geo=geo)
+
+
+# ------------------------------------------- the same plain form, in row blocks
+# Used only by the bounded-sample CPU timing legs of bench.py: one iteration of
+# O5 is split into the layout-wide part (geometry, spread, 7 convolutions, Z)
+# and per-row-block parts (gather, sparse attraction, assembly).  Same
+# arithmetic as interp_gradient(form="plain"); pinned equal to it by
+# tests/test_oracle_interp.py::test_row_blocks_equal_full_gradient.
+def field_state(Y, eps=0.05, h_max=0.25, I_min=20, I_max=256, p=3, method="auto"):
+    Y = np.asarray(Y, dtype=np.float64)
+    n = Y.shape[0]
+    geo = geometry(Y, h_max, I_min, I_max, p)
+    it = _Interp(Y, geo)
+    delta = geo["delta"]
+    tab = lambda kern: (lambda dx, dy: kern(dx * dx + dy * dy))  # noqa: E731
+    cx = geo["lo_x"] + geo["N"] * delta / 2.0
+    cy = geo["lo_y"] + geo["N"] * delta / 2.0
+    W1 = it.spread(np.ones(n))
+    Wx, Wy = it.spread(Y[:, 0] - cx), it.spread(Y[:, 1] - cy)
+    Phi = {}
+    for name, kern in (("K2", k2), ("Ke", ke_factory(eps))):
+        Phi[name] = (convolve(W1, tab(kern), delta, method), convolve(Wx, tab(kern), delta, method),
+                     convolve(Wy, tab(kern), delta, method))
+    Z = float(it.gather(convolve(W1, tab(k1), delta, method)).sum()) - n
+    return dict(geo=geo, Phi=Phi, Z=Z, cx=cx, cy=cy, n=n)
+
+
+def gradient_rows(state, Y, indptr, indices, pval, lkl, lc, lr, row0, nrows):
+    """O5 gradient of the rows [row0, row0 + nrows) from a field_state of Y."""
+    from . import attr_sparse_rows
+
+    Y = np.asarray(Y, dtype=np.float64)
+    n = state["n"]
+    Yr = Y[row0:row0 + nrows]
+    it = _Interp(Yr, state["geo"])
+    xt, yt = Yr[:, 0] - state["cx"], Yr[:, 1] - state["cy"]
+
+    def pair_sum(name):
+        f1, fx, fy = (it.gather(F) for F in state["Phi"][name])
+        return np.stack([xt * f1 - fx, yt * f1 - fy], axis=1)
+
+    F_rep = pair_sum("K2") / state["Z"]
+    g_ent = -pair_sum("Ke") / (float(n) * float(n))
+    F_attr = attr_sparse_rows(Y, indptr, indices, pval, row0, nrows)
+    return 4.0 * lkl * (F_attr - F_rep) + (lc / n) * Yr + lr * g_ent

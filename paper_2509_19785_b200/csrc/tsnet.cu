@@ -114,6 +114,24 @@ size_t tsnet_workspace_bytes(int64_t n, int64_t nnz, const tsnet_grad_params* gp
     return ws_map(nullptr, n, nnz, I_max).bytes;
 }
 
+int tsnet_attr(const tsnet_csr* P, const float* Y, float* f_attr, tsnet_stream_t stream) {
+    int st;
+    if ((st = check_csr(P)) != TSNET_OK) return st;
+    TSNET_ARG(P->n == 0 || (Y != nullptr && f_attr != nullptr), "Y or f_attr is NULL");
+    if (P->n == 0) return TSNET_OK;
+    Ws w{};
+    w.f_attr = reinterpret_cast<float2*>(f_attr);
+    GradArgs a{};
+    a.n = P->n;
+    a.nnz = P->nnz;
+    a.indptr = P->indptr;
+    a.indices = P->indices;
+    a.values = P->values;
+    a.Y = reinterpret_cast<const float2*>(Y);
+    TSNET_CUDA(launch_spmv(w, a, (cudaStream_t)stream));
+    return TSNET_OK;
+}
+
 int tsnet_grad_parts(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, const tsnet_shard* shard,
                      float* f_attr, float* f_field, double* Z, void* ws, size_t ws_bytes, tsnet_stream_t stream) {
     Ws w;

@@ -64,6 +64,7 @@ SIGNATURES = [
     ("tsnet_workspace_bytes", c_sz, [c_i64, c_i64, ctypes.POINTER(tsnet_grad_params), ctypes.POINTER(tsnet_shard)]),
     ("tsnet_grad", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, ctypes.POINTER(tsnet_grad_params),
                                   ctypes.POINTER(tsnet_shard), c_vp, c_vp, c_vp, c_sz, c_vp]),
+    ("tsnet_attr", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, c_vp, c_vp]),
     ("tsnet_grad_parts", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, ctypes.POINTER(tsnet_grad_params),
                                         ctypes.POINTER(tsnet_shard), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     ("tsnet_step", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, c_vp, c_vp, ctypes.POINTER(tsnet_grad_params),
@@ -235,6 +236,15 @@ def tsnet_grad(P: CSR, Y: torch.Tensor, gp: GradParams, ws: torch.Tensor, grad=N
     _check("tsnet_grad", lib().tsnet_grad(ctypes.byref(Pc), _ptr(Y), ctypes.byref(g), _shard(shard), _ptr(grad),
                                           _ptr(Z), _ptr(ws), ws.numel(), _stream(stream)))
     return grad, Z
+
+
+def tsnet_attr(P: CSR, Y: torch.Tensor, f_attr=None, stream=None):
+    """Attractive SpMV alone (a6)."""
+    _require_cuda(Y)
+    f_attr = torch.empty_like(Y) if f_attr is None else f_attr
+    Pc = P.c()
+    _check("tsnet_attr", lib().tsnet_attr(ctypes.byref(Pc), _ptr(Y), _ptr(f_attr), _stream(stream)))
+    return f_attr
 
 
 def tsnet_grad_parts(P: CSR, Y: torch.Tensor, gp: GradParams, ws: torch.Tensor, shard=None, stream=None):

@@ -123,6 +123,18 @@ def test_interp_vs_exact_on_config1_layouts():
         assert np.linalg.norm(r["g"] - ge) / np.linalg.norm(ge) < 2e-2
 
 
+def test_row_blocks_equal_full_gradient(grid_P):
+    """The block split used by the CPU timing legs is the same computation."""
+    n = grid_P["n"]
+    Y = clustered_layout(n, 15.0, 5, 1.0, 3).astype(np.float64)
+    lam = (1.0, 0.01, 0.6)
+    full = _grad_parts(Y, grid_P, lam, 0.25)["g"]
+    st = interp.field_state(Y)
+    parts = [interp.gradient_rows(st, Y, grid_P["indptr"], grid_P["indices"], grid_P["values"], *lam, r0,
+                                  min(100, n - r0)) for r0 in range(0, n, 100)]
+    assert np.abs(np.concatenate(parts) - full).max() <= 1e-13 * np.abs(full).max()
+
+
 def test_geometry_policy():
     g = interp.geometry(np.array([[0.0, 0.0], [1.0, 0.5]]))
     assert g["I"] == 20 and g["N"] == 60                 # I_min clamp, span < 5

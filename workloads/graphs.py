@@ -235,7 +235,7 @@ def _build_config(i: int):
 
 
 def cache_dir() -> str:
-    d = os.environ.get("TSNET_CACHE", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), ".cache"))
+    d = os.environ.get("TSNET_CACHE", "/tmp/tsnet_cache")
     os.makedirs(d, exist_ok=True)
     return d
 
