@@ -195,7 +195,7 @@ def run_reference(args, rank):
 def config_dict(cfg, n, nnz, extra):
     d = {"workload": CONFIG_DESC[cfg], "n": int(n), "nnz": int(nnz), "perplexity": 40,
          "window": "stage B (iterations 250+; lambda = (1, 0.01, 0.6), momentum 0.8, eta 50)",
-         "parallelism": "single GPU (replicas when N > 1)", "l2": "inputs larger than L2 (CSR >> 126 MB)"
+         "l2": "inputs larger than L2 (CSR >> 126 MB)"
          if 8 * nnz > 126e6 else "CSR fits in L2 (small config)"}
     if extra:
         d.update(extra)
@@ -207,7 +207,8 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
-    from paper_2509_19785_b200 import Layout, tsnet_attr, tsnet_build_P, tsnet_step_host, tsnet_read_stats
+    from paper_2509_19785_b200 import (Layout, tsnet_attr, tsnet_build_P, tsnet_plan_build, tsnet_read_stats,
+                                       tsnet_step_host)
     from workloads import config_graph, init_layout
 
     dev = torch.device("cuda", local_rank)
@@ -219,7 +220,25 @@ def run_ours(args, rank, world, local_rank):
     c0_s = time.perf_counter() - t0
     P = built["P"]
     n, nnz = P.n, P.nnz
-    lay = Layout(P, torch.from_numpy(init_layout(n, 0)).to(dev), use_graphs=True)
+    Y0 = torch.from_numpy(init_layout(n, 0)).to(dev)
+    plan_s = None
+    t0 = time.perf_counter()
+    if world > 1:
+        # row shards + NCCL communicator + the plan of the own rows (set-up, untimed)
+        from paper_2509_19785_b200.distributed import ShardedLayout
+        lay = ShardedLayout(P, Y0, rank, world)
+        shard = lay.shard
+        rb, re = lay.rows
+    else:
+        if not args.no_plan:
+            tsnet_plan_build(P)               # column-blocked layout of P (set-up, untimed)
+        lay = Layout(P, Y0, use_graphs=True)
+        shard, rb, re = None, 0, n
+    torch.cuda.synchronize()
+    if world > 1 or not args.no_plan:
+        plan_s = time.perf_counter() - t0
+    nnz_l = int(P.indptr[re].item() - P.indptr[rb].item())
+    nl = re - rb
     it = 0
     lay.run(args.pre_iters, start=0)          # stage A, untimed
     it += args.pre_iters
@@ -248,28 +267,31 @@ def run_ours(args, rank, world, local_rank):
         ms = float(t.item())
     stats = tsnet_read_stats(lay.ws, stream=lay.stream)
 
-    # dominant kernel: the attractive SpMV alone, CUDA events on its stream
+    # dominant kernel: the attractive SpMV alone (own rows), CUDA events on its stream
+    Pk = lay.P
     reps = max(10, min(args.steps, 200))
     fa = torch.empty_like(lay.Y)
     with torch.cuda.stream(lay.stream):
         for _ in range(3):
-            tsnet_attr(P, lay.Y, fa, stream=lay.stream)
+            tsnet_attr(Pk, lay.Y, fa, stream=lay.stream)
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(lay.stream)
         for _ in range(reps):
-            tsnet_attr(P, lay.Y, fa, stream=lay.stream)
+            tsnet_attr(Pk, lay.Y, fa, stream=lay.stream)
         s1.record(lay.stream)
     torch.cuda.synchronize()
     spmv_ms = s0.elapsed_time(s1) / reps
     peak, peak_src = measured_peak()
-    spmv_bytes = 8 * nnz + 8 * (n + 1) + 16 * n            # col+val, indptr, Y_i read, F_i write
+    spmv_bytes = 8 * nnz_l + 8 * (nl + 1) + 16 * nl        # col+val, indptr, Y_i read, F_i write
     achieved = spmv_bytes / (spmv_ms * 1e-3) / 1e9
     step_ms = ms / args.steps
-    step_bytes = 8 * nnz + 8 * (n + 1) + 48 * n             # SURVEY §8(d) B_g at G = 1
+    # SURVEY §8(d) B_g: CSR + state of the own rows + the all-gather payload landing in HBM
+    step_bytes = 8 * nnz_l + 8 * (nl + 1) + 48 * nl + 8 * (n - nl)
     traffic = None
-    tp = os.path.join(ROOT, "profiles", f"spmv_dram_bytes_cfg{args.config}.json")
-    if os.path.exists(tp):
+    kname = "k_attr_cb" if (world > 1 or not args.no_plan) else "k_spmv"
+    tp = os.path.join(ROOT, "profiles", f"{kname}_dram_bytes_cfg{args.config}.json")
+    if os.path.exists(tp) and world == 1:
         with open(tp) as f:
             rec = json.load(f)
         traffic = float(rec["dram_bytes_per_launch"]) * (nnz / rec["nnz"])
@@ -282,41 +304,49 @@ def run_ours(args, rank, world, local_rank):
         Vh = lay.vel.cpu().pin_memory()
         Gh = lay.gains.cpu().pin_memory()
         ne = max(3, min(args.steps, 50))
-        tsnet_step_host(P, Yh, Vh, Gh, gp, sp, lay.ws, stream=lay.stream)
+        tsnet_step_host(Pk, Yh, Vh, Gh, gp, sp, lay.ws, shard=shard, stream=lay.stream)
+        if world > 1:
+            dist.barrier()
         h0 = time.perf_counter()
         for _ in range(ne):
-            tsnet_step_host(P, Yh, Vh, Gh, gp, sp, lay.ws, stream=lay.stream)
+            tsnet_step_host(Pk, Yh, Vh, Gh, gp, sp, lay.ws, shard=shard, stream=lay.stream)
         h1 = time.perf_counter()
         el = h1 - h0
         if world > 1:
             t = torch.tensor([el], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        e2e = {"value": world * ne / el, "unit": UNIT, "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 24 * n,
+        e2e = {"value": ne / el, "unit": UNIT, "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 24 * n,
                "steps": ne}
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config, args.cpu_budget)
 
     if rank == 0:
-        value = world * args.steps / (ms * 1e-3)
+        value = args.steps / (ms * 1e-3)       # whole-job iterations/s: every rank takes part in each iteration
+        par = ("single GPU" if world == 1 else
+               f"{world} row shards (nnz-balanced), NCCL all-reduce of the charge grid + all-gather of Y")
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": config_dict(args.config, n, nnz,
                                       {"grid_I": stats["I"], "grid_N": stats["N"], "fft_M": stats["M"],
                                        "span": round(stats["S"], 3), "pre_iters": args.pre_iters,
-                                       "c0_gpu_s": round(c0_s, 3)}),
+                                       "c0_gpu_s": round(c0_s, 3), "parallelism": par,
+                                       "attr_layout": "CSR" if kname == "k_spmv" else "column-blocked plan",
+                                       "plan_build_s": None if plan_s is None else round(plan_s, 3)}),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": traffic, "kernel": "k_spmv (tsnet_attr)",
+                             "frac": achieved / peak, "traffic": traffic, "kernel": f"{kname} (tsnet_attr)",
                              "kernel_ms": spmv_ms, "algorithmic_bytes": spmv_bytes, "peak_source": peak_src,
-                             "share_of_step": spmv_ms / step_ms},
+                             "share_of_step": spmv_ms / step_ms, "rank": 0},
                 "step_roofline": {"achieved": step_bytes / (step_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                                   "frac": step_bytes / (step_ms * 1e-3) / 1e9 / peak, "algorithmic_bytes": step_bytes},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": KERNELS_PER_STEP * args.steps,
                 "clocks": clk, "nonfinite": stats["nonfinite"]}
         print(json.dumps(line), flush=True)
+    if world > 1:
+        lay.close()
 
 
 def main():
@@ -329,6 +359,7 @@ def main():
     ap.add_argument("--pre-iters", type=int, default=250)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-plan", action="store_true", help="CSR SpMV kernel instead of the column-blocked plan")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     assert args.warmup >= 3, "at least 3 warm-up steps"

@@ -63,7 +63,12 @@ typedef struct {
 
 /* Sparse symmetric affinity matrix P (Eq. 2) in CSR.
  * `capacity` = allocated length of indices/values (input to tsnet_build_P),
- * `nnz` = stored entries (output of tsnet_build_P, input elsewhere). */
+ * `nnz` = stored entries (output of tsnet_build_P, input elsewhere).
+ * `plan` = optional column-blocked copy of the same P built by
+ * tsnet_plan_build (device, caller-owned; NULL = none).  When set, the
+ * attractive SpMV (step a6) reads the plan instead of indices/values; the
+ * caller must rebuild it whenever P's pattern or values change (the library
+ * cannot detect a stale plan). */
 typedef struct {
     int64_t n;
     int64_t nnz;
@@ -71,6 +76,7 @@ typedef struct {
     int64_t* indptr;         /* device, n+1 */
     int32_t* indices;        /* device, capacity */
     float* values;           /* device, capacity */
+    const void* plan;        /* device, tsnet_plan_build output, or NULL */
 } tsnet_csr;
 
 /* Cost multipliers and interpolation grid policy.
@@ -101,12 +107,31 @@ typedef struct {
     int32_t recenter;
 } tsnet_step_params;
 
-/* Row shard for multi-GPU runs.  NULL (or world == 1, rows [0, n)) = one GPU.
- * Round 1 supports only the single-GPU case (TSNET_E_ARG otherwise). */
+/* Row shard for multi-GPU runs.  One process per GPU; rank
+ * `rank` of `world` owns the contiguous rows [row_begin, row_end) of P, of the
+ * gradient and of the state (vel, gains).  Y is REPLICATED: every rank holds
+ * all n x 2 positions; each iteration the ranks
+ *   - derive the same grid geometry from the full Y (no collective),
+ *   - spread their own points (step a2) and all-reduce (sum) the charge grid
+ *     over `comm` (fixed size 4 (3 I_max)^2 floats),
+ *   - convolve the reduced grid (replicated FFT), run the attractive SpMV and
+ *     the gather/move for their own rows,
+ *   - all-gather Y (each rank broadcasts its slice) -- tsnet_step only.
+ * comm   : communicator from tsnet_comm_init (NULL only for the phase calls
+ *          tsnet_field_local / tsnet_step_finish, which do no communication).
+ * bounds : [host] world + 1 row offsets, bounds[r] .. bounds[r+1] = rank r's rows
+ *          (tsnet_shard_rows); row_begin/row_end must equal bounds[rank], bounds[rank+1].
+ * NULL shard, or world == 1 with rows [0, n), = one GPU, all rows.
+ * Sharded calls need P->plan built for the same rows (tsnet_plan_build with
+ * this shard); recentring is not supported across ranks (TSNET_E_ARG). */
 typedef struct {
     int32_t rank, world;
     int64_t row_begin, row_end;
+    void* comm;
+    const int64_t* bounds;
 } tsnet_shard;
+
+#define TSNET_COMM_ID_BYTES 128
 
 /* Per-call statistics kept in the workspace (read with tsnet_read_stats). */
 typedef struct {
@@ -166,13 +191,16 @@ TSNET_API size_t tsnet_workspace_bytes(int64_t n, int64_t nnz, const tsnet_grad_
  *   g_ent,i  ~ -(1/n^2) sum_j Delta_ij / (eps + r2)    (Eq. 8)
  * The two interpolated sums use P=3 Lagrange nodes per interval on an
  * I x I-interval grid, convolved by FFT (local-moment form).
- * grad: n x 2 fp32 (device).  Z: device fp64 scalar (may be NULL).
+ * grad: (row_end - row_begin) x 2 fp32 (device; n x 2 without a shard), row q
+ * = vertex row_begin + q.  Z: device fp64 scalar (may be NULL).  Sharded:
+ * all-reduces the charge grid over shard->comm.
  */
 TSNET_API int tsnet_grad(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, const tsnet_shard* shard,
                float* grad, double* Z, void* ws, size_t ws_bytes, tsnet_stream_t stream);
 
 /* The attractive term alone (step a6, Eq. 6 first term):
  *   f_attr,i = sum_{j in row i} p_ij w_ij Delta_ij   (n x 2 fp32, device)
+ * Uses P->plan when set (column-blocked kernel), else the CSR kernel.
  * Needs no workspace.  Async.  (Also the kernel bench.py times for the roofline.) */
 TSNET_API int tsnet_attr(const tsnet_csr* P, const float* Y, float* f_attr, tsnet_stream_t stream);
 
@@ -187,6 +215,8 @@ TSNET_API int tsnet_grad_parts(const tsnet_csr* P, const float* Y, const tsnet_g
  * One full iteration: gradient at Y (as tsnet_grad) followed by the
  * momentum/gains move ("Move each vertex v in the direction of
  * dC/dv"; reading R12), in place on Y, vel, gains (n x 2 fp32 each).
+ * Sharded: rows [row_begin, row_end) of vel/gains are updated, and Y is
+ * all-gathered over shard->comm before the call returns (stream order).
  */
 TSNET_API int tsnet_step(const tsnet_csr* P, float* Y, float* vel, float* gains, const tsnet_grad_params* gp,
                const tsnet_step_params* sp, const tsnet_shard* shard, void* ws, size_t ws_bytes,
@@ -213,6 +243,73 @@ TSNET_API int tsnet_step_host(const tsnet_csr* P, float* Y_host, float* vel_host
  */
 TSNET_API int tsnet_cost(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, int32_t mode,
                const tsnet_shard* shard, double* out3, void* ws, size_t ws_bytes, tsnet_stream_t stream);
+
+/* ------------------------------------------- column-blocked layout of P (a6) */
+
+/*
+ * The attractive SpMV (Eq. 6 first term) gathers Y_j for every
+ * stored entry of P.  On graphs without locality (config 4) those gathers, not
+ * HBM, bound a CSR kernel.  A plan is P re-laid out for a shared-memory-staged
+ * kernel: rows [row_begin, row_end) of `shard` (all rows if NULL)
+ * are cut into nnz-balanced tasks of <= 11264 rows, columns into blocks of 8192
+ * points; each task's entries are stored block by block as 8-byte words
+ * ((row - task row0) << 16 | col - block col0, p_ij fp32), rows ascending.
+ * The plan holds the values: the kernel that uses it reads no CSR array.
+ *
+ * tsnet_plan_query : bytes of the plan and of the build workspace for this P
+ *                    and shard.  BLOCKING (reads P->indptr to cut the tasks).
+ * tsnet_plan_build : writes the plan into `plan` (device, 256-byte aligned,
+ *                    >= plan_bytes) using `ws` as scratch.  BLOCKING.  Set
+ *                    P->plan = plan afterwards to use it.  Needs nnz of the
+ *                    shard < 2^31 and n < 2^31 (TSNET_E_ARG otherwise).
+ * tsnet_plan_partition : the host task cut alone (for tests): rows
+ *                    [row_begin, row_end) of the HOST indptr into T = base_tasks * w
+ *                    tasks (smallest w >= 1 that respects rows_max), written to
+ *                    task_row0 / task_rows (capacity max_tasks).  Returns T, or
+ *                    -1 on bad arguments / overflow.  [host, pure]
+ */
+TSNET_API int tsnet_plan_query(const tsnet_csr* P, const tsnet_shard* shard, size_t* plan_bytes, size_t* ws_bytes,
+                               tsnet_stream_t stream);
+TSNET_API int tsnet_plan_build(const tsnet_csr* P, const tsnet_shard* shard, void* plan, size_t plan_bytes, void* ws,
+                               size_t ws_bytes, tsnet_stream_t stream);
+TSNET_API int32_t tsnet_plan_partition(const int64_t* indptr_host, int64_t row_begin, int64_t row_end,
+                                       int32_t rows_max, int32_t base_tasks, int32_t max_tasks, int64_t* task_row0,
+                                       int32_t* task_rows);
+
+/* ------------------------------------------------------------- multi-GPU (§8(e)) */
+
+/* NCCL plumbing (NCCL is loaded at run time; TSNET_E_ARG if it cannot be).
+ * tsnet_comm_unique_id : on one rank, write the 128-byte id to share with the
+ *                        others (e.g. through torch.distributed). [host]
+ * tsnet_comm_init      : every rank, collectively: communicator of `world` ranks
+ *                        (the calling thread's current CUDA device). BLOCKING.
+ * tsnet_comm_destroy   : release it. */
+TSNET_API int tsnet_comm_unique_id(uint8_t* id_out);
+TSNET_API int tsnet_comm_init(const uint8_t* id, int32_t world, int32_t rank, void** comm);
+TSNET_API int tsnet_comm_destroy(void* comm);
+
+/* Row shards: bounds[0..world] (host) cutting rows [0, n) of the HOST indptr
+ * into `world` contiguous ranges balanced on nnz + rows (the per-rank bytes of
+ * steps a6/a7).  Returns world, or -1 on bad arguments.  [host, pure] */
+TSNET_API int32_t tsnet_shard_rows(const int64_t* indptr_host, int64_t n, int32_t world, int64_t* bounds);
+
+/* The two halves of tsnet_step around its collectives, for callers that run
+ * their own communication (and for single-GPU emulation of several ranks):
+ * tsnet_field_local : steps a0-a2 -- geometry from the full Y, box sort and
+ *                     spread of the shard's own rows into the charge grid in ws.
+ * tsnet_ws_grid     : where that grid lives: byte offset into ws and its
+ *                     length in floats (the buffer tsnet_step all-reduces). [host]
+ * tsnet_step_finish : steps a3-a7 from the (summed) grid in ws: convolution, Z,
+ *                     attractive SpMV and gather + move of the own rows of Y,
+ *                     vel, gains (full n x 2 arrays).  No communication.
+ * tsnet_step = field_local + all-reduce(grid) + step_finish + all-gather(Y). */
+TSNET_API int tsnet_field_local(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp,
+                                const tsnet_shard* shard, void* ws, size_t ws_bytes, tsnet_stream_t stream);
+TSNET_API int tsnet_ws_grid(int64_t n, int64_t nnz, const tsnet_grad_params* gp, size_t* offset_bytes,
+                            size_t* count_floats);
+TSNET_API int tsnet_step_finish(const tsnet_csr* P, float* Y, float* vel, float* gains, const tsnet_grad_params* gp,
+                                const tsnet_step_params* sp, const tsnet_shard* shard, void* ws, size_t ws_bytes,
+                                tsnet_stream_t stream);
 
 /* Copy the statistics of the last evaluation from the workspace. BLOCKING. [host out] */
 TSNET_API int tsnet_read_stats(const void* ws, tsnet_stats* out, tsnet_stream_t stream);

@@ -135,17 +135,22 @@ inline Ws ws_map(void* base, int64_t n, int64_t nnz, int I_max) {
 // ------------------------------------------------------------ launchers
 // (defined in the .cu files; all enqueue on `s`, return cudaError_t of launch)
 struct GradArgs {
-    int64_t n, nnz;
+    int64_t n, nnz;       // global vertex count and stored entries of P
+    int64_t rb, re;       // rows owned by this call (shard), [0, n) on one GPU
     const int64_t* indptr;
     const int32_t* indices;
     const float* values;
+    const void* plan;     // column-blocked P (attr_cb.cu) or nullptr
     const float2* Y;
     float lambda_kl, lambda_c, lambda_r, eps, h_max;
     int I_min, I_max;
 };
 
 cudaError_t launch_field_phase(const Ws& w, const GradArgs& a, cudaStream_t s);
+cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, bool zero_all);
+cudaError_t launch_field_conv(const Ws& w, const GradArgs& a, cudaStream_t s);
 cudaError_t launch_spmv(const Ws& w, const GradArgs& a, cudaStream_t s);
+cudaError_t launch_attr_cb(const void* plan, const float2* Y, float2* F, cudaStream_t s);
 cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2* f_field, double* Z,
                             cudaStream_t s);
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,

@@ -159,42 +159,73 @@ __global__ void k_prep(Geo* g, int* box_cnt, float4* wgrid, float2* tw) {
 }
 
 // a1: box of every point (fp64 arithmetic, R16) and its rank inside the box.
+// Each CTA takes a contiguous chunk of points.  When the I^2 box counters fit
+// in shared memory (kBoxSmem), the CTA counts its chunk there (warp-aggregated
+// shared atomics), reserves one range per non-empty box with a single global
+// atomicAdd, and offsets the local ranks -- so a layout packed into a few boxes
+// (stage A: 1e6 points in <= 400 boxes) does not serialise on global atomics.
+// Otherwise (many boxes, little contention) warp-aggregated global atomics.
+constexpr int kBoxSmem = 12288;   // counters (48 KB)
+
+__device__ __forceinline__ void box_of(float2 y, double lo_x, double lo_y, double h_b, int I, int& b, float& ux,
+                                       float& uy) {
+    double rx = ((double)y.x - lo_x) / h_b;
+    double ry = ((double)y.y - lo_y) / h_b;
+    double fx = floor(rx), fy = floor(ry);
+    int bx = (int)fmin(fmax(fx, 0.0), (double)(I - 1));
+    int by = (int)fmin(fmax(fy, 0.0), (double)(I - 1));
+    ux = (float)(rx - (double)bx);
+    uy = (float)(ry - (double)by);
+    b = by * I + bx;
+}
+
 __global__ void __launch_bounds__(256) k_box_count(const float2* __restrict__ Y, int64_t n, const Geo* __restrict__ g,
                                                    int* __restrict__ box_cnt, int* __restrict__ box,
                                                    int* __restrict__ rank, float2* __restrict__ uv) {
+    extern __shared__ int hist[];
     const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b;
     const int I = g->I;
-    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int nb = I * I;
+    const bool local = nb <= kBoxSmem;
+    const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t c0 = blockIdx.x * chunk, c1 = std::min<int64_t>(n, c0 + chunk);
+    const int lane = threadIdx.x & 31;
+    if (local) {
+        for (int q = threadIdx.x; q < nb; q += blockDim.x) hist[q] = 0;
+        __syncthreads();
+    }
+    int* cnt = local ? hist : box_cnt;
+    for (int64_t i0 = c0; i0 < c1; i0 += blockDim.x) {
         const int64_t i = i0 + threadIdx.x;
-        const bool act = i < n;
+        const bool act = i < c1;
         int b = -1;
         float ux = 0.f, uy = 0.f;
-        if (act) {
-            float2 y = Y[i];
-            double rx = ((double)y.x - lo_x) / h_b;
-            double ry = ((double)y.y - lo_y) / h_b;
-            double fx = floor(rx), fy = floor(ry);
-            int bx = (int)fmin(fmax(fx, 0.0), (double)(I - 1));
-            int by = (int)fmin(fmax(fy, 0.0), (double)(I - 1));
-            ux = (float)(rx - (double)bx);
-            uy = (float)(ry - (double)by);
-            b = by * I + bx;
-        }
+        if (act) box_of(Y[i], lo_x, lo_y, h_b, I, b, ux, uy);
         // warp-aggregated atomic: one atomicAdd per distinct box in the warp
         const unsigned act_mask = __ballot_sync(0xffffffffu, act);
         if (act) {
             const unsigned peers = __match_any_sync(act_mask, b);
             const int leader = __ffs(peers) - 1;
-            const int lane = threadIdx.x & 31;
             int base = 0;
-            if (lane == leader) base = atomicAdd(&box_cnt[b], __popc(peers));
+            if (lane == leader) base = atomicAdd(&cnt[b], __popc(peers));
             base = __shfl_sync(peers, base, leader);
-            const int r = base + __popc(peers & ((1u << lane) - 1u));
             box[i] = b;
-            rank[i] = r;
+            rank[i] = base + __popc(peers & ((1u << lane) - 1u));
             uv[i] = make_float2(ux, uy);
         }
     }
+    if (!local) return;
+    __syncthreads();
+    for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+        const int c = hist[q];
+        if (c) hist[q] = atomicAdd(&box_cnt[q], c);   // this CTA's range inside box q
+    }
+    __syncthreads();
+    for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) rank[i] += hist[box[i]];
+}
+
+static size_t box_smem_bytes(int I_max) {
+    return sizeof(int) * (size_t)std::min<int64_t>((int64_t)I_max * I_max, kBoxSmem);
 }
 
 // a1: exclusive scan of box counts -> box_start, and the spread work list
@@ -479,24 +510,47 @@ cudaError_t field_set_attrs(int M_max) {
     return cudaSuccess;
 }
 
-cudaError_t launch_field_phase(const Ws& w, const GradArgs& a, cudaStream_t s) {
+// a0-a2 for the rows [rb, re) this call owns: geometry from the bounding box of
+// the FULL layout Y (replicated on every rank, so every rank derives the same
+// grid without a collective), then box sort + spread of the own rows only.
+// On one GPU rb = 0, re = n.  With `zero_all`, the whole I_max-sized grid is
+// zeroed (it is all-reduced as one fixed-size buffer across ranks).
+cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, bool zero_all) {
     cudaError_t e;
     if ((e = field_set_attrs(w.M_max)) != cudaSuccess) return e;
-    const int64_t n = a.n;
-    const int pts_blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)kNumSMs * 8);
-    const int pb = pts_blocks > 0 ? pts_blocks : 1;
+    const int64_t n = a.n, nl = a.re - a.rb;
+    const int pb = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)kNumSMs * 8));
+    const int pbl = (int)std::max<int64_t>(1, std::min<int64_t>((nl + 255) / 256, (int64_t)kNumSMs * 8));
     k_iter_init<<<1, 1, 0, s>>>(w.geo);
     k_bbox<<<pb, 256, 0, s>>>(a.Y, n, w.geo, a.h_max, a.I_min, a.I_max);
+    if (zero_all && (e = cudaMemsetAsync(w.wgrid, 0, sizeof(float4) * (size_t)w.N_max * w.N_max, s)) != cudaSuccess)
+        return e;
     k_prep<<<kNumSMs * 4, 256, 0, s>>>(w.geo, w.box_cnt, w.wgrid, w.tw);
-    k_box_count<<<pb, 256, 0, s>>>(a.Y, n, w.geo, w.box_cnt, w.box, w.rank, w.uv);
-    k_box_scan<<<1, 1024, 0, s>>>(w.geo, w.box_cnt, w.box_start, w.items, n);
-    k_box_scatter<<<pb, 256, 0, s>>>(n, w.box, w.rank, w.box_start, w.uv, w.sorted_uv);
+    const float2* Yl = a.Y + a.rb;
+    const int cb = (int)std::max<int64_t>(1, std::min<int64_t>((nl + 2047) / 2048, (int64_t)kNumSMs * 8));
+    k_box_count<<<cb, 256, box_smem_bytes(a.I_max), s>>>(Yl, nl, w.geo, w.box_cnt, w.box, w.rank, w.uv);
+    k_box_scan<<<1, 1024, 0, s>>>(w.geo, w.box_cnt, w.box_start, w.items, nl);
+    k_box_scatter<<<pbl, 256, 0, s>>>(nl, w.box, w.rank, w.box_start, w.uv, w.sorted_uv);
     k_spread<<<kNumSMs * 8, 256, 0, s>>>(w.geo, w.items, w.box_start, w.sorted_uv, w.wgrid);
+    return cudaGetLastError();
+}
+
+// a3-a5 from the (all-reduced) charge grid: kernel tabulation, FFT
+// convolution, Z by Parseval (global n), combined fields.  Replicated.
+cudaError_t launch_field_conv(const Ws& w, const GradArgs& a, cudaStream_t s) {
+    cudaError_t e;
+    if ((e = field_set_attrs(w.M_max)) != cudaSuccess) return e;
     k_row_fwd<<<kNumSMs * 2, kRowThreads, field_smem_row(w.M_max), s>>>(w.geo, w.wgrid, w.tw, w.spec, w.M_max, a.eps);
     k_col<<<kNumSMs, kColThreads, field_smem_col(w.M_max), s>>>(w.geo, w.spec, w.tw, w.colout, w.M_max, w.N_max);
     k_row_inv<<<kNumSMs * 2, kInvThreads, field_smem_inv(w.M_max), s>>>(w.geo, w.colout, w.tw, w.fgrid, w.M_max,
-                                                                        w.N_max, n, a.lambda_kl, a.lambda_r);
+                                                                        w.N_max, a.n, a.lambda_kl, a.lambda_r);
     return cudaGetLastError();
+}
+
+cudaError_t launch_field_phase(const Ws& w, const GradArgs& a, cudaStream_t s) {
+    cudaError_t e = launch_field_local(w, a, s, false);
+    if (e != cudaSuccess) return e;
+    return launch_field_conv(w, a, s);
 }
 
 }  // namespace tsnet

@@ -102,6 +102,8 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t n, int64_t nnz, const int6
 }
 
 cudaError_t launch_spmv(const Ws& w, const GradArgs& a, cudaStream_t s) {
+    if (a.plan) return launch_attr_cb(a.plan, a.Y, w.f_attr, s);   // rows of the plan's shard
+    if (a.rb != 0 || a.re != a.n) return cudaErrorInvalidValue;   // CSR kernel: all rows only
     cudaError_t e = cudaMemsetAsync(w.f_attr, 0, sizeof(float2) * (size_t)a.n, s);
     if (e != cudaSuccess || a.nnz == 0) return e;
     const int64_t nchunks = (a.nnz + kSpmvChunk - 1) / kSpmvChunk;
@@ -145,13 +147,13 @@ __device__ __forceinline__ float2 gather_field(const Geo& g, const float4* __res
 }
 
 // mode 0: write grad; mode 1: write f_field (and F_attr stays in ws)
+// n = rows of this call (local); cn = lambda_c / n_global
 __global__ void __launch_bounds__(256) k_grad_out(int64_t n, const Geo* __restrict__ gp, const float4* __restrict__ fgrid,
                                                   const int* __restrict__ box, const float2* __restrict__ uv,
                                                   const float2* __restrict__ Y, const float2* __restrict__ Fa,
-                                                  float lambda_kl, float lambda_c, float2* __restrict__ grad,
+                                                  float lambda_kl, float cn, float2* __restrict__ grad,
                                                   float2* __restrict__ f_field) {
     const Geo g = *gp;
-    const float cn = (float)((double)lambda_c / (double)n);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float2 ff = gather_field(g, fgrid, box[i], uv[i]);
         if (f_field) f_field[i] = ff;
@@ -172,13 +174,13 @@ __device__ __forceinline__ void gains_move(float gr, float& v, float& gn, float&
     y = y + v;
 }
 
+// n = rows of this call (local; Y, vel, gains point at the first own row); cn = lambda_c / n_global
 __global__ void __launch_bounds__(256) k_update(int64_t n, Geo* __restrict__ gp, const float4* __restrict__ fgrid,
                                                 const int* __restrict__ box, const float2* __restrict__ uv,
                                                 float2* __restrict__ Y, const float2* __restrict__ Fa,
                                                 float2* __restrict__ vel, float2* __restrict__ gains, float lambda_kl,
-                                                float lambda_c, tsnet_step_params sp) {
+                                                float cn, tsnet_step_params sp) {
     const Geo g = *gp;
-    const float cn = (float)((double)lambda_c / (double)n);
     double sx = 0.0, sy = 0.0;
     bool bad = false;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -222,20 +224,26 @@ static int pts_blocks(int64_t n) {
     return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)kNumSMs * 8));
 }
 
+static float cn_of(const GradArgs& a) { return (float)((double)a.lambda_c / (double)a.n); }
+
+// grad / f_field: (re - rb) x 2, row q = global row rb + q
 cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2* f_field, double* Z,
                             cudaStream_t s) {
-    k_grad_out<<<pts_blocks(a.n), 256, 0, s>>>(a.n, w.geo, w.fgrid, w.box, w.uv, a.Y, w.f_attr, a.lambda_kl,
-                                               a.lambda_c, grad, f_field);
+    const int64_t nl = a.re - a.rb;
+    k_grad_out<<<pts_blocks(nl), 256, 0, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, a.Y + a.rb, w.f_attr, a.lambda_kl,
+                                              cn_of(a), grad, f_field);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (Z) e = cudaMemcpyAsync(Z, &w.geo->Z, sizeof(double), cudaMemcpyDeviceToDevice, s);
     return e;
 }
 
+// Y, vel, gains: full n x 2 arrays; rows [rb, re) are updated
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,
                           const tsnet_step_params& sp, cudaStream_t s) {
-    k_update<<<pts_blocks(a.n), 256, 0, s>>>(a.n, w.geo, w.fgrid, w.box, w.uv, Y, w.f_attr, vel, gains, a.lambda_kl,
-                                             a.lambda_c, sp);
+    const int64_t nl = a.re - a.rb;
+    k_update<<<pts_blocks(nl), 256, 0, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, Y + a.rb, w.f_attr, vel + a.rb,
+                                            gains + a.rb, a.lambda_kl, cn_of(a), sp);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !sp.recenter) return e;
     k_recenter<<<pts_blocks(a.n), 256, 0, s>>>(a.n, w.geo, Y);

@@ -33,10 +33,35 @@ static int check_grad_params(const tsnet_grad_params* gp) {
     return TSNET_OK;
 }
 
+int comm_allreduce_grid(void* comm, float* grid, size_t count, cudaStream_t s);
+int comm_allgather_rows(void* comm, float* Y, const int64_t* bounds, int world, cudaStream_t s);
+
 static int check_shard(const tsnet_shard* sh, int64_t n) {
     if (sh == nullptr) return TSNET_OK;
-    TSNET_ARG(sh->world == 1 && sh->rank == 0 && sh->row_begin == 0 && sh->row_end == n,
-              "multi-GPU shards are not implemented in this build (world=%d)", sh->world);
+    TSNET_ARG(sh->world >= 1 && sh->rank >= 0 && sh->rank < sh->world, "shard rank %d / world %d", sh->rank,
+              sh->world);
+    TSNET_ARG(0 <= sh->row_begin && sh->row_begin <= sh->row_end && sh->row_end <= n,
+              "shard rows [%lld, %lld) outside [0, %lld)", (long long)sh->row_begin, (long long)sh->row_end,
+              (long long)n);
+    if (sh->bounds) {
+        TSNET_ARG(sh->bounds[0] == 0 && sh->bounds[sh->world] == n, "shard bounds must cover [0, n)");
+        for (int r = 0; r < sh->world; ++r)
+            TSNET_ARG(sh->bounds[r] <= sh->bounds[r + 1], "shard bounds must be non-decreasing");
+        TSNET_ARG(sh->bounds[sh->rank] == sh->row_begin && sh->bounds[sh->rank + 1] == sh->row_end,
+                  "row_begin/row_end differ from bounds[rank], bounds[rank+1]");
+    }
+    return TSNET_OK;
+}
+
+static bool sharded(const tsnet_shard* sh, int64_t n) {
+    return sh != nullptr && (sh->world > 1 || sh->row_begin != 0 || sh->row_end != n);
+}
+
+// Calls that communicate need the communicator (world > 1) and a plan.
+static int check_comm(const tsnet_shard* sh, const GradArgs& a) {
+    if (!sharded(sh, a.n)) return TSNET_OK;
+    TSNET_ARG(a.plan != nullptr, "sharded calls need P->plan built for the shard's rows (tsnet_plan_build)");
+    if (sh->world > 1) TSNET_ARG(sh->comm != nullptr, "world = %d needs shard->comm (tsnet_comm_init)", sh->world);
     return TSNET_OK;
 }
 
@@ -59,10 +84,14 @@ static int prepare(const tsnet_csr* P, const float* Y, const tsnet_grad_params* 
     TSNET_ARG(ws != nullptr && ws_bytes >= w.bytes, "workspace too small (%zu < %zu bytes)", ws_bytes, w.bytes);
     a.n = P->n;
     a.nnz = P->nnz;
+    a.rb = sh ? sh->row_begin : 0;
+    a.re = sh ? sh->row_end : P->n;
     a.indptr = P->indptr;
     a.indices = P->indices;
     a.values = P->values;
+    a.plan = P->plan;
     a.Y = reinterpret_cast<const float2*>(Y);
+    if (sharded(sh, P->n)) TSNET_ARG(a.plan != nullptr, "a shard needs P->plan built for its rows");
     a.lambda_kl = gp->lambda_kl;
     a.lambda_c = gp->lambda_c;
     a.lambda_r = gp->lambda_r;
@@ -73,8 +102,17 @@ static int prepare(const tsnet_csr* P, const float* Y, const tsnet_grad_params* 
     return TSNET_OK;
 }
 
-static int eval_gradient_parts(const Ws& w, const GradArgs& a, cudaStream_t s) {
-    TSNET_CUDA(launch_field_phase(w, a, s));
+static size_t grid_floats(const Ws& w) { return (size_t)4 * w.N_max * w.N_max; }
+
+// field (with the grid all-reduce when world > 1) + attractive SpMV of the own rows
+static int eval_gradient_parts(const Ws& w, const GradArgs& a, const tsnet_shard* sh, cudaStream_t s) {
+    int st;
+    if ((st = check_comm(sh, a)) != TSNET_OK) return st;
+    const bool multi = sh != nullptr && sh->comm != nullptr;   // collectives (also with a 1-rank comm)
+    TSNET_CUDA(launch_field_local(w, a, s, multi));
+    if (multi && (st = comm_allreduce_grid(sh->comm, reinterpret_cast<float*>(w.wgrid), grid_floats(w), s)) != TSNET_OK)
+        return st;
+    TSNET_CUDA(launch_field_conv(w, a, s));
     TSNET_CUDA(launch_spmv(w, a, s));
     return TSNET_OK;
 }
@@ -124,9 +162,12 @@ int tsnet_attr(const tsnet_csr* P, const float* Y, float* f_attr, tsnet_stream_t
     GradArgs a{};
     a.n = P->n;
     a.nnz = P->nnz;
+    a.rb = 0;
+    a.re = P->n;
     a.indptr = P->indptr;
     a.indices = P->indices;
     a.values = P->values;
+    a.plan = P->plan;
     a.Y = reinterpret_cast<const float2*>(Y);
     TSNET_CUDA(launch_spmv(w, a, (cudaStream_t)stream));
     return TSNET_OK;
@@ -140,9 +181,10 @@ int tsnet_grad_parts(const tsnet_csr* P, const float* Y, const tsnet_grad_params
     if (st != TSNET_OK) return st;
     if (a.n == 0) return TSNET_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    if ((st = eval_gradient_parts(w, a, s)) != TSNET_OK) return st;
+    if ((st = eval_gradient_parts(w, a, shard, s)) != TSNET_OK) return st;
     TSNET_CUDA(launch_grad_out(w, a, nullptr, reinterpret_cast<float2*>(f_field), Z, s));
-    if (f_attr) TSNET_CUDA(cudaMemcpyAsync(f_attr, w.f_attr, sizeof(float2) * a.n, cudaMemcpyDeviceToDevice, s));
+    if (f_attr)
+        TSNET_CUDA(cudaMemcpyAsync(f_attr, w.f_attr, sizeof(float2) * (a.re - a.rb), cudaMemcpyDeviceToDevice, s));
     return TSNET_OK;
 }
 
@@ -155,7 +197,7 @@ int tsnet_grad(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, 
     TSNET_ARG(a.n == 0 || grad != nullptr, "grad is NULL");
     if (a.n == 0) return TSNET_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    if ((st = eval_gradient_parts(w, a, s)) != TSNET_OK) return st;
+    if ((st = eval_gradient_parts(w, a, shard, s)) != TSNET_OK) return st;
     TSNET_CUDA(launch_grad_out(w, a, reinterpret_cast<float2*>(grad), nullptr, Z, s));
     return TSNET_OK;
 }
@@ -169,9 +211,53 @@ int tsnet_step(const tsnet_csr* P, float* Y, float* vel, float* gains, const tsn
     if (st != TSNET_OK) return st;
     TSNET_ARG(sp != nullptr, "step params are NULL");
     TSNET_ARG(a.n == 0 || (vel && gains), "vel or gains is NULL");
+    TSNET_ARG(!(sp->recenter && sharded(shard, a.n)), "recentring is not supported with shards");
+    const bool multi = shard != nullptr && shard->comm != nullptr;
+    TSNET_ARG(!multi || shard->bounds != nullptr, "a communicating shard needs shard->bounds to all-gather Y");
     if (a.n == 0) return TSNET_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    if ((st = eval_gradient_parts(w, a, s)) != TSNET_OK) return st;
+    if ((st = eval_gradient_parts(w, a, shard, s)) != TSNET_OK) return st;
+    TSNET_CUDA(launch_update(w, a, reinterpret_cast<float2*>(Y), reinterpret_cast<float2*>(vel),
+                             reinterpret_cast<float2*>(gains), *sp, s));
+    if (multi) return comm_allgather_rows(shard->comm, Y, shard->bounds, shard->world, s);
+    return TSNET_OK;
+}
+
+int tsnet_field_local(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, const tsnet_shard* shard,
+                      void* ws, size_t ws_bytes, tsnet_stream_t stream) {
+    Ws w;
+    GradArgs a;
+    int st = prepare(P, Y, gp, shard, ws, ws_bytes, w, a);
+    if (st != TSNET_OK) return st;
+    if (a.n == 0) return TSNET_OK;
+    TSNET_CUDA(launch_field_local(w, a, (cudaStream_t)stream, true));
+    return TSNET_OK;
+}
+
+int tsnet_ws_grid(int64_t n, int64_t nnz, const tsnet_grad_params* gp, size_t* offset_bytes, size_t* count_floats) {
+    TSNET_ARG(offset_bytes != nullptr && count_floats != nullptr, "NULL argument");
+    int st;
+    if ((st = check_grad_params(gp)) != TSNET_OK) return st;
+    Ws w = ws_map(nullptr, n, nnz, gp->I_max);
+    *offset_bytes = (size_t)((const char*)w.wgrid - (const char*)nullptr);
+    *count_floats = grid_floats(w);
+    return TSNET_OK;
+}
+
+int tsnet_step_finish(const tsnet_csr* P, float* Y, float* vel, float* gains, const tsnet_grad_params* gp,
+                      const tsnet_step_params* sp, const tsnet_shard* shard, void* ws, size_t ws_bytes,
+                      tsnet_stream_t stream) {
+    Ws w;
+    GradArgs a;
+    int st = prepare(P, Y, gp, shard, ws, ws_bytes, w, a);
+    if (st != TSNET_OK) return st;
+    TSNET_ARG(sp != nullptr, "step params are NULL");
+    TSNET_ARG(a.n == 0 || (vel && gains), "vel or gains is NULL");
+    TSNET_ARG(!(sp->recenter && sharded(shard, a.n)), "recentring is not supported with shards");
+    if (a.n == 0) return TSNET_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    TSNET_CUDA(launch_field_conv(w, a, s));
+    TSNET_CUDA(launch_spmv(w, a, s));
     TSNET_CUDA(launch_update(w, a, reinterpret_cast<float2*>(Y), reinterpret_cast<float2*>(vel),
                              reinterpret_cast<float2*>(gains), *sp, s));
     return TSNET_OK;
@@ -211,6 +297,7 @@ int tsnet_cost(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, 
     int st = prepare(P, Y, gp, shard, ws, ws_bytes, w, a);
     if (st != TSNET_OK) return st;
     TSNET_ARG(mode == 0 || mode == 1, "cost mode must be 0 (exact) or 1 (interpolated Z)");
+    TSNET_ARG(!sharded(shard, a.n), "tsnet_cost is single-GPU only");
     TSNET_ARG(out3 != nullptr, "out3 is NULL");
     cudaStream_t s = (cudaStream_t)stream;
     if (a.n == 0) {

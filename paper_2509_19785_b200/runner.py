@@ -44,6 +44,8 @@ class Layout:
         self.stage_switch = stage_switch
         self.use_graphs = use_graphs
         self.stream = stream or torch.cuda.Stream(device=Y0.device)
+        # the state above was written on the caller's stream; every later step runs on self.stream
+        self.stream.wait_stream(torch.cuda.current_stream(Y0.device))
         self.graphs = [None, None]
 
     def _raw_step(self, stage: int):
@@ -52,20 +54,21 @@ class Layout:
 
     def _graph(self, stage: int):
         if self.graphs[stage] is None:
-            # warm-up outside capture on a scratch copy of the state so the captured
-            # iteration does not advance the real layout
-            saved = (self.Y.clone(), self.vel.clone(), self.gains.clone())
+            # warm-up outside capture, then restore the state so the captured
+            # iteration does not advance the real layout.  Snapshot and restore run
+            # on self.stream, ordered after every step already enqueued there.
             with torch.cuda.stream(self.stream):
+                saved = (self.Y.clone(), self.vel.clone(), self.gains.clone())
                 self._raw_step(stage)
             self.stream.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=self.stream):
                 self._raw_step(stage)
+            with torch.cuda.stream(self.stream):
+                self.Y.copy_(saved[0])
+                self.vel.copy_(saved[1])
+                self.gains.copy_(saved[2])
             self.stream.synchronize()
-            self.Y.copy_(saved[0])
-            self.vel.copy_(saved[1])
-            self.gains.copy_(saved[2])
-            torch.cuda.synchronize()
             self.graphs[stage] = g
         return self.graphs[stage]
 

@@ -31,7 +31,7 @@ class tsnet_graph(ctypes.Structure):
 
 class tsnet_csr(ctypes.Structure):
     _fields_ = [("n", c_i64), ("nnz", c_i64), ("capacity", c_i64), ("indptr", c_vp), ("indices", c_vp),
-                ("values", c_vp)]
+                ("values", c_vp), ("plan", c_vp)]
 
 
 class tsnet_grad_params(ctypes.Structure):
@@ -45,7 +45,8 @@ class tsnet_step_params(ctypes.Structure):
 
 
 class tsnet_shard(ctypes.Structure):
-    _fields_ = [("rank", c_i32), ("world", c_i32), ("row_begin", c_i64), ("row_end", c_i64)]
+    _fields_ = [("rank", c_i32), ("world", c_i32), ("row_begin", c_i64), ("row_end", c_i64), ("comm", c_vp),
+                ("bounds", ctypes.POINTER(c_i64))]
 
 
 class tsnet_stats(ctypes.Structure):
@@ -74,6 +75,22 @@ SIGNATURES = [
                                        ctypes.POINTER(tsnet_shard), c_vp, c_sz, c_vp]),
     ("tsnet_cost", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, ctypes.POINTER(tsnet_grad_params), c_i32,
                                   ctypes.POINTER(tsnet_shard), c_vp, c_vp, c_sz, c_vp]),
+    ("tsnet_plan_query", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard),
+                                        ctypes.POINTER(c_sz), ctypes.POINTER(c_sz), c_vp]),
+    ("tsnet_plan_build", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard), c_vp, c_sz, c_vp,
+                                        c_sz, c_vp]),
+    ("tsnet_plan_partition", c_i32, [c_vp, c_i64, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp]),
+    ("tsnet_comm_unique_id", ctypes.c_int, [c_vp]),
+    ("tsnet_comm_init", ctypes.c_int, [c_vp, c_i32, c_i32, ctypes.POINTER(c_vp)]),
+    ("tsnet_comm_destroy", ctypes.c_int, [c_vp]),
+    ("tsnet_shard_rows", c_i32, [c_vp, c_i64, c_i32, c_vp]),
+    ("tsnet_field_local", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, ctypes.POINTER(tsnet_grad_params),
+                                         ctypes.POINTER(tsnet_shard), c_vp, c_sz, c_vp]),
+    ("tsnet_ws_grid", ctypes.c_int, [c_i64, c_i64, ctypes.POINTER(tsnet_grad_params), ctypes.POINTER(c_sz),
+                                     ctypes.POINTER(c_sz)]),
+    ("tsnet_step_finish", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, c_vp, c_vp,
+                                         ctypes.POINTER(tsnet_grad_params), ctypes.POINTER(tsnet_step_params),
+                                         ctypes.POINTER(tsnet_shard), c_vp, c_sz, c_vp]),
     ("tsnet_read_stats", ctypes.c_int, [c_vp, ctypes.POINTER(tsnet_stats), c_vp]),
     ("tsnet_last_error", ctypes.c_char_p, []),
 ]
@@ -157,7 +174,9 @@ class StepParams:
 
 
 class CSR:
-    """Device CSR matrix P (int64 indptr, int32 indices, fp32 values)."""
+    """Device CSR matrix P (int64 indptr, int32 indices, fp32 values), plus the
+    optional column-blocked plan of the same P (tsnet_plan_build; `plan` is a
+    uint8 device tensor, None = CSR kernel)."""
 
     def __init__(self, indptr: torch.Tensor, indices: torch.Tensor, values: torch.Tensor, nnz: int | None = None):
         _require_cuda(indptr, indices, values)
@@ -165,15 +184,18 @@ class CSR:
         self.indptr, self.indices, self.values = indptr, indices, values
         self.n = indptr.numel() - 1
         self.nnz = int(indices.numel()) if nnz is None else int(nnz)
+        self.plan = None
 
     def c(self):
         return tsnet_csr(self.n, self.nnz, int(self.indices.numel()), self.indptr.data_ptr(),
                          self.indices.data_ptr() if self.indices.numel() else None,
-                         self.values.data_ptr() if self.values.numel() else None)
+                         self.values.data_ptr() if self.values.numel() else None,
+                         self.plan.data_ptr() if self.plan is not None else None)
 
-
-def _shard(shard):
-    return None if shard is None else ctypes.byref(shard)
+    def without_plan(self) -> "CSR":
+        """Same P, CSR kernel (shares the tensors)."""
+        q = CSR(self.indptr, self.indices, self.values, self.nnz)
+        return q
 
 
 # ------------------------------------------------------------------ C0
@@ -214,6 +236,43 @@ def tsnet_build_P(indptr: torch.Tensor, indices: torch.Tensor, u: float = 40.0, 
     del ws
     return dict(P=CSR(P_ip, P_ix[:nnz].clone(), P_v[:nnz].clone()), knn_idx=knn_idx[:, :k], knn_hop=knn_hop[:, :k],
                 knn_len=knn_len[:n], beta=beta[:n], k=k, status=st)
+
+
+# ------------------------------------------------ column-blocked plan of P
+def tsnet_plan_query(P: CSR, shard=None, stream=None):
+    pb, wb = c_sz(0), c_sz(0)
+    Pc = P.c()
+    _check("tsnet_plan_query", lib().tsnet_plan_query(ctypes.byref(Pc), _shard(shard), ctypes.byref(pb),
+                                                      ctypes.byref(wb), _stream(stream)))
+    return int(pb.value), int(wb.value)
+
+
+def tsnet_plan_build(P: CSR, shard=None, stream=None) -> CSR:
+    """Build the column-blocked plan of P (set-up, blocking) and attach it: P.plan."""
+    pbytes, wbytes = tsnet_plan_query(P, shard, stream)
+    plan = torch.empty(max(pbytes, 1), dtype=torch.uint8, device=P.indptr.device)
+    ws = torch.empty(max(wbytes, 1), dtype=torch.uint8, device=P.indptr.device)
+    P.plan = None
+    Pc = P.c()
+    _check("tsnet_plan_build", lib().tsnet_plan_build(ctypes.byref(Pc), _shard(shard), _ptr(plan), pbytes, _ptr(ws),
+                                                      wbytes, _stream(stream)))
+    del ws
+    P.plan = plan
+    return P
+
+
+def tsnet_plan_partition(indptr_host, row_begin: int, row_end: int, rows_max: int, base_tasks: int,
+                         max_tasks: int = 1 << 16):
+    """Host task cut (pure): returns (task_row0, task_rows) numpy arrays."""
+    import numpy as np
+    ip = np.ascontiguousarray(indptr_host, dtype=np.int64)
+    r0 = np.zeros(max_tasks, np.int64)
+    rr = np.zeros(max_tasks, np.int32)
+    T = lib().tsnet_plan_partition(ip.ctypes.data, row_begin, row_end, rows_max, base_tasks, max_tasks,
+                                   r0.ctypes.data, rr.ctypes.data)
+    if T < 0:
+        raise TsnetError("tsnet_plan_partition", T)
+    return r0[:T], rr[:T]
 
 
 # ------------------------------------------------------ per-iteration path
@@ -291,6 +350,89 @@ def tsnet_read_stats(ws, stream=None) -> dict:
     rc = lib().tsnet_read_stats(_ptr(ws), ctypes.byref(st), _stream(stream))
     _check("tsnet_read_stats", rc, ok=(TSNET_OK, TSNET_E_NONFINITE))
     return {f: getattr(st, f) for f, _ in tsnet_stats._fields_}
+
+
+# ------------------------------------------------------------ multi-GPU
+class Shard:
+    """Host-side shard description (rank, world, row bounds, NCCL communicator).
+    `c()` gives the tsnet_shard struct; the bounds array is kept alive here."""
+
+    def __init__(self, rank: int, world: int, bounds, comm=None):
+        import numpy as np
+        self.rank, self.world = int(rank), int(world)
+        self.bounds = np.ascontiguousarray(bounds, dtype=np.int64)
+        assert len(self.bounds) == self.world + 1
+        self.comm = comm
+        self.row_begin, self.row_end = int(self.bounds[rank]), int(self.bounds[rank + 1])
+        self._c = tsnet_shard(self.rank, self.world, self.row_begin, self.row_end, comm,
+                              self.bounds.ctypes.data_as(ctypes.POINTER(c_i64)))
+
+    def c(self):
+        return self._c
+
+
+def _shard(shard):
+    if shard is None:
+        return None
+    if isinstance(shard, Shard):
+        return ctypes.byref(shard.c())
+    return ctypes.byref(shard)
+
+
+def tsnet_shard_rows(indptr_host, world: int):
+    """nnz + rows balanced contiguous row bounds (host, pure)."""
+    import numpy as np
+    ip = np.ascontiguousarray(indptr_host, dtype=np.int64)
+    b = np.zeros(world + 1, np.int64)
+    r = lib().tsnet_shard_rows(ip.ctypes.data, len(ip) - 1, world, b.ctypes.data)
+    if r != world:
+        raise TsnetError("tsnet_shard_rows", r)
+    return b
+
+
+def tsnet_comm_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check("tsnet_comm_unique_id", lib().tsnet_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def tsnet_comm_init(uid: bytes, world: int, rank: int):
+    buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+    comm = c_vp()
+    _check("tsnet_comm_init", lib().tsnet_comm_init(buf, world, rank, ctypes.byref(comm)))
+    return comm.value
+
+
+def tsnet_comm_destroy(comm):
+    _check("tsnet_comm_destroy", lib().tsnet_comm_destroy(comm))
+
+
+def tsnet_ws_grid(n: int, nnz: int, gp: GradParams):
+    off, cnt = c_sz(0), c_sz(0)
+    g = gp.c()
+    _check("tsnet_ws_grid", lib().tsnet_ws_grid(n, nnz, ctypes.byref(g), ctypes.byref(off), ctypes.byref(cnt)))
+    return int(off.value), int(cnt.value)
+
+
+def ws_grid_view(ws: torch.Tensor, n: int, nnz: int, gp: GradParams) -> torch.Tensor:
+    """fp32 view of the charge grid inside a workspace (for external reduction)."""
+    off, cnt = tsnet_ws_grid(n, nnz, gp)
+    return ws[off:off + 4 * cnt].view(torch.float32)
+
+
+def tsnet_field_local(P: CSR, Y, gp: GradParams, ws, shard=None, stream=None):
+    _require_cuda(Y, ws)
+    Pc, g = P.c(), gp.c()
+    _check("tsnet_field_local", lib().tsnet_field_local(ctypes.byref(Pc), _ptr(Y), ctypes.byref(g), _shard(shard),
+                                                        _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def tsnet_step_finish(P: CSR, Y, vel, gains, gp: GradParams, sp: StepParams, ws, shard=None, stream=None):
+    _require_cuda(Y, vel, gains, ws)
+    Pc, g, s = P.c(), gp.c(), sp.c()
+    _check("tsnet_step_finish", lib().tsnet_step_finish(ctypes.byref(Pc), _ptr(Y), _ptr(vel), _ptr(gains),
+                                                        ctypes.byref(g), ctypes.byref(s), _shard(shard), _ptr(ws),
+                                                        ws.numel(), _stream(stream)))
 
 
 def tsnet_last_error() -> str:

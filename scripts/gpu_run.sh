@@ -1,15 +1,24 @@
-# one gpurun call: GPU tests, bench (cfg 4), launch list + ncu full of the SpMV
-# usage: bash scripts/gpu_run.sh TAG
+# one gpurun call: GPU tests, bench (cfg 4), launch list + ncu full of the top kernel
+# usage: bash scripts/gpu_run.sh TAG [pytest -k expr] [ncu kernel regex]
 TAG=${1:-r1}
+KEXPR=${2:-}
+KREGEX=${3:-k_attr_cb}
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/${TAG}_smi.txt 2>&1
-timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/${TAG}_pytest_gpu.log 2>&1
+if [ -n "$KEXPR" ]; then
+  timeout 1500 python -m pytest tests -m gpu -q -x --timeout 900 -p no:cacheprovider -k "$KEXPR" > gpurun_out/${TAG}_pytest_gpu.log 2>&1
+else
+  timeout 1800 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/${TAG}_pytest_gpu.log 2>&1
+fi
 echo "pytest exit $?" >> gpurun_out/${TAG}_pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
 echo "smoke exit $?" >> gpurun_out/${TAG}_smoke.log
 timeout 900 python bench.py > gpurun_out/${TAG}_bench4.log 2>&1
 echo "bench exit $?" >> gpurun_out/${TAG}_bench4.log
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 3000 -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_spmv -s 5 -c 1 -o gpurun_out/${TAG}_spmv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_ncu.log 2>&1
+timeout 900 python bench.py --no-plan --no-cpu-baseline --no-e2e --steps 200 > gpurun_out/${TAG}_bench4_csr.log 2>&1
+B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e"
+timeout 600 $B > gpurun_out/${TAG}_plain.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 3000 -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv $B > gpurun_out/${TAG}_ncu_launch.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX} -s 5 -c 1 -o gpurun_out/${TAG}_top $B > gpurun_out/${TAG}_ncu.log 2>&1
 echo done

@@ -1,0 +1,143 @@
+"""Column-blocked attractive SpMV (attr_cb.cu, tsnet_plan_build) vs the oracle.
+
+F_attr,i = sum_j p_ij w_ij (X_i - X_j) (Eq. 6 first term) is
+computed by oracle.attr_sparse in fp64 from the same fp32 P and fp32 Y.
+Bar: relL2 <= 1e-5 over all rows (fp32 per-entry arithmetic, fp32 sums in
+another order), and per row |f - f_oracle| <= 1e-5 * sum_j |p_ij w_ij Delta_ij|
+(the row's own term scale), so no row can hide behind the global norm.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2509_19785_b200 import CSR, tsnet_attr
+from paper_2509_19785_b200 import tsnet as T
+from workloads import clustered_layout, config_graph, random_csr, uniform_layout
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def relL2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def row_scale(Y, ip, ix, pv, rows):
+    """sum_j |p_ij w_ij Delta_ij| per row (L1 of the row's terms)."""
+    out = np.zeros(len(rows))
+    for t, i in enumerate(rows):
+        cols = ix[ip[i]:ip[i + 1]]
+        d = Y[i] - Y[cols]
+        w = 1.0 / (1.0 + (d * d).sum(1))
+        out[t] = (np.abs(pv[ip[i]:ip[i + 1]] * w)[:, None] * np.abs(d)).sum()
+    return out
+
+
+def dev_csr(ip, ix, pv):
+    return CSR(torch.from_numpy(np.asarray(ip, np.int64)).cuda(), torch.from_numpy(np.asarray(ix, np.int32)).cuda(),
+               torch.from_numpy(np.asarray(pv, np.float32)).cuda())
+
+
+def check(ip, ix, pv, Y, shard=None, y_offset_rows=0):
+    """Plan + CB kernel vs oracle on rows [rb, re)."""
+    n = len(ip) - 1
+    pv32 = np.asarray(pv, np.float32).astype(np.float64)
+    P = dev_csr(ip, ix, pv32)
+    T.tsnet_plan_build(P, shard=shard)
+    rb, re = (0, n) if shard is None else (shard.row_begin, shard.row_end)
+    # optionally place Y at an 8-byte (not 16-byte) aligned address -> non-TMA copy path
+    base = torch.zeros((n + y_offset_rows, 2), dtype=torch.float32, device="cuda")
+    base[y_offset_rows:] = torch.from_numpy(Y)
+    Yd = base[y_offset_rows:]
+    F = torch.full((n, 2), float("nan"), dtype=torch.float32, device="cuda")
+    tsnet_attr(P, Yd, F)
+    torch.cuda.synchronize()
+    got = F.cpu().numpy()[: re - rb].astype(np.float64)
+    want = oracle.attr_sparse(Y.astype(np.float64), ip, ix, pv32)[rb:re]
+    assert np.all(np.isfinite(got))
+    if re > rb and np.linalg.norm(want) > 0:
+        assert relL2(got, want) <= TOL, relL2(got, want)
+    rows = np.arange(rb, re)
+    if len(rows) > 4000:
+        rows = np.unique(np.concatenate([rows[:1000], rows[-1000:], np.random.default_rng(1).choice(rows, 2000)]))
+    sc = row_scale(Y.astype(np.float64), ip, ix, pv32, rows)
+    err = np.abs(got[rows - rb] - want[rows - rb]).sum(1)
+    assert np.all(err <= TOL * sc + 1e-30), float((err / np.maximum(sc, 1e-300)).max())
+    return P
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_configs(cfg):
+    ip, ix = config_graph(cfg)
+    P = oracle.build_P(ip, ix, 40.0, seed=0)
+    n = P["n"]
+    for Y in (clustered_layout(n, 25.0, 7, 1.2, 2), uniform_layout(n, 3.0, 4)):
+        check(P["indptr"], P["indices"], P["values"], Y)
+
+
+@pytest.mark.parametrize("n,kind", [(1, "single"), (7, "tiny"), (8191, "one_block_minus"), (8192, "one_block"),
+                                    (8193, "block_plus_one"), (24577, "odd_tail"), (20011, "hub_and_empty")])
+def test_edge_patterns(n, kind):
+    rng = np.random.default_rng(n)
+    L = rng.integers(0, 40, n)
+    if kind == "hub_and_empty":
+        L[::7] = 0                      # empty rows
+        L[5] = n                        # a row touching every column (every block)
+        L[6] = 3000
+    if kind == "single":
+        L[:] = 1
+    ip, ix, pv = random_csr(n, L, seed=n)
+    Y = uniform_layout(n, 10.0, 9)
+    check(ip, ix, pv, Y)
+
+
+def test_unaligned_Y_uses_copy_path():
+    n = 9000
+    ip, ix, pv = random_csr(n, np.random.default_rng(0).integers(1, 60, n), seed=3)
+    check(ip, ix, pv, uniform_layout(n, 5.0, 1), y_offset_rows=1)
+
+
+def test_long_rows_many_tasks():
+    """Rows longer than a sweep and more than one wave of tasks (rows > 148 * 11264)."""
+    n = 148 * 11264 + 5000
+    L = np.full(n, 3)
+    L[:200] = 2000
+    ip, ix, pv = random_csr(n, L, seed=11)
+    check(ip, ix, pv, uniform_layout(n, 20.0, 2))
+
+
+def test_shards_partition_the_rows():
+    ip, ix = config_graph(2)
+    P = oracle.build_P(ip, ix, 40.0, seed=0)
+    n = P["n"]
+    Y = clustered_layout(n, 25.0, 7, 1.2, 2)
+    for rb, re in ((0, n // 3), (n // 3, n // 3 + 1), (n // 3 + 1, n), (n, n)):
+        check(P["indptr"], P["indices"], P["values"], Y, shard=T.tsnet_shard(0, 1, rb, re))
+
+
+def test_config4_full_size_sampled_rows():
+    """The bench workload (n ~ 0.95M, nnz ~ 2.06e8), GPU C0 output, plan kernel."""
+    from paper_2509_19785_b200 import tsnet_build_P
+    ip, ix = config_graph(4)
+    got = tsnet_build_P(torch.from_numpy(ip).cuda(), torch.from_numpy(ix).cuda(), u=40.0, seed=0)
+    P = got["P"]
+    n = P.n
+    Y = clustered_layout(n, 30.0, 40, 2.0, 5)
+    Yd = torch.from_numpy(Y).cuda()
+    T.tsnet_plan_build(P)
+    F = tsnet_attr(P, Yd)
+    torch.cuda.synchronize()
+    pip, pix = P.indptr.cpu().numpy(), P.indices.cpu().numpy()
+    pv = P.values.cpu().numpy().astype(np.float64)
+    deg = np.diff(pip)
+    rows = np.unique(np.concatenate([np.random.default_rng(0).choice(n, 3000, replace=False),
+                                     np.argsort(deg)[-50:], [0, n - 1]]))
+    want = np.stack([oracle.attr_sparse_rows(Y.astype(np.float64), pip, pix, pv, int(i), 1)[0] for i in rows])
+    got = F.cpu().numpy()[rows].astype(np.float64)
+    sc = row_scale(Y.astype(np.float64), pip, pix, pv, rows)
+    err = np.abs(got - want).sum(1)
+    assert np.all(err <= TOL * sc), float((err / sc).max())

@@ -194,7 +194,10 @@ def oracle_grad(P, Y32, lam, h_max=0.25, I_min=20, I_max=256):
 _LAYOUTS = {}
 
 
-def oracle_layouts(cfg, iters=(249, 499)):
+TRAJ_ITERS = (249, 260, 499)
+
+
+def oracle_layouts(cfg, iters=TRAJ_ITERS):
     """Layouts of the oracle's own L-tsNET run (O5 + O6/O7) from the seeded init."""
     key = (cfg, iters)
     if key not in _LAYOUTS:
@@ -242,20 +245,27 @@ def test_grad_parity_synthetic_layouts(cfg, lay, lam):
 
 @pytest.mark.parametrize("cfg", [1, 2])
 def test_grad_parity_oracle_trajectory(cfg):
-    """Stage-A end and converged stage-B layouts of the oracle's own run."""
+    """Stage-A end (249), mid stage-B expansion (260) and converged stage-B (499)
+    layouts of the oracle's own run."""
     if cfg == 2:
         pytest.importorskip("scipy")
     P = oracle_P(cfg)
-    for it, (Y, _, _) in sorted(oracle_layouts(cfg).items()):
+    for it, (Y, _, _) in sorted(oracle_layouts(cfg, TRAJ_ITERS).items()):
         for lam in (STAGE_A, STAGE_B):
             g, Z, _, _, st = gpu_grad(dev_P(P), Y, GradParams(*lam))
             r = oracle_grad(P, Y, lam)
             assert_grad_close(g, r, Y, lam)
-            # interpolation vs the exact O(n^2) gradient (n <= 20k), stage-B multipliers
-            # (all terms active; the stage-A equilibrium is a residual below the
-            # interpolation error of its terms, SURVEY.md A.7)
-            if lam == STAGE_B:
-                ge, _ = oracle.exact_grad(Y.astype(np.float64), P["indptr"], P["indices"], p32(P), *lam)
+            if lam != STAGE_B:
+                continue
+            # interpolation vs the exact O(n^2) gradient (n <= 20k), stage-B multipliers.
+            ge, _ = oracle.exact_grad(Y.astype(np.float64), P["indptr"], P["indices"], p32(P), *lam)
+            if it == 499:
+                # 499 is an equilibrium of the INTERPOLATED dynamics: there g_interp ~ 0 by
+                # construction and relL2 vs exact is ~1 whatever h is (DESIGN.md §2, R18).
+                # The interpolation error is graded against the size of the terms instead.
+                err = np.linalg.norm(np.asarray(g, np.float64) - ge)
+                assert err <= EXACT_TOL * term_scale(r, Y, lam), (it, err / term_scale(r, Y, lam))
+            else:
                 assert relL2(g, ge) <= EXACT_TOL, (it, relL2(g, ge))
 
 

@@ -250,3 +250,24 @@ def config_graph(i: int, use_cache: bool = True):
     if use_cache:
         np.savez(path, indptr=ip, indices=ix)
     return ip, ix
+
+
+def random_csr(n: int, row_lengths, seed: int = 0):
+    """Seeded random sparse matrix pattern for SpMV edge cases (not a graph of
+    the method): row i draws row_lengths[i] columns uniformly from [0, n) with
+    replacement, keeps the distinct ones sorted (so a row has at most
+    row_lengths[i] entries), values positive fp32-representable in [0.5, 1.5) / n.
+    Returns (indptr int64, indices int32, values float64)."""
+    rng = np.random.default_rng(seed)
+    L = np.asarray(row_lengths, dtype=np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), L)
+    cols = rng.integers(0, n, size=len(rows), dtype=np.int64)
+    order = np.lexsort((cols, rows))
+    rows, cols = rows[order], cols[order]
+    keep = np.ones(len(rows), bool)
+    keep[1:] = (rows[1:] != rows[:-1]) | (cols[1:] != cols[:-1])
+    rows, cols = rows[keep], cols[keep]
+    indptr = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=indptr[1:])
+    values = ((rng.random(len(cols)) + 0.5) / n).astype(np.float32).astype(np.float64)
+    return indptr, cols.astype(np.int32), values
