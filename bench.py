@@ -35,7 +35,7 @@ import numpy as np  # noqa: E402
 
 METRIC = "tsNET gradient iterations/sec at n=1M (1/2/4/8 B200); % of HBM roofline"
 UNIT = "iterations/s"
-KERNELS_PER_STEP = 12   # kernels tsnet_step launches (field.cu 10, iterate.cu 2; recenter off)
+KERNELS_PER_STEP = 11   # kernels tsnet_step launches (field.cu 9, attr 1, update 1; recenter off)
 CONFIG_DESC = {
     1: "cfg1 2-D grid 32x32 (n=1024), u=40",
     2: "cfg2 RGG n=20,000 mean degree 8 (LCC), u=40",
@@ -226,16 +226,16 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         # row shards + NCCL communicator + the plan of the own rows (set-up, untimed)
         from paper_2509_19785_b200.distributed import ShardedLayout
-        lay = ShardedLayout(P, Y0, rank, world)
+        lay = ShardedLayout(P, Y0, rank, world, plan=args.plan)
         shard = lay.shard
         rb, re = lay.rows
     else:
-        if not args.no_plan:
+        if args.plan:
             tsnet_plan_build(P)               # column-blocked layout of P (set-up, untimed)
         lay = Layout(P, Y0, use_graphs=True)
         shard, rb, re = None, 0, n
     torch.cuda.synchronize()
-    if world > 1 or not args.no_plan:
+    if world > 1 or args.plan:
         plan_s = time.perf_counter() - t0
     nnz_l = int(P.indptr[re].item() - P.indptr[rb].item())
     nl = re - rb
@@ -289,7 +289,7 @@ def run_ours(args, rank, world, local_rank):
     # SURVEY §8(d) B_g: CSR + state of the own rows + the all-gather payload landing in HBM
     step_bytes = 8 * nnz_l + 8 * (nl + 1) + 48 * nl + 8 * (n - nl)
     traffic = None
-    kname = "k_attr_cb" if (world > 1 or not args.no_plan) else "k_spmv"
+    kname = "k_attr_cb" if args.plan else "k_spmv2"
     tp = os.path.join(ROOT, "profiles", f"{kname}_dram_bytes_cfg{args.config}.json")
     if os.path.exists(tp) and world == 1:
         with open(tp) as f:
@@ -334,7 +334,7 @@ def run_ours(args, rank, world, local_rank):
                                       {"grid_I": stats["I"], "grid_N": stats["N"], "fft_M": stats["M"],
                                        "span": round(stats["S"], 3), "pre_iters": args.pre_iters,
                                        "c0_gpu_s": round(c0_s, 3), "parallelism": par,
-                                       "attr_layout": "CSR" if kname == "k_spmv" else "column-blocked plan",
+                                       "attr_layout": "column-blocked plan" if args.plan else "CSR",
                                        "plan_build_s": None if plan_s is None else round(plan_s, 3)}),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic, "kernel": f"{kname} (tsnet_attr)",
@@ -359,7 +359,7 @@ def main():
     ap.add_argument("--pre-iters", type=int, default=250)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-plan", action="store_true", help="CSR SpMV kernel instead of the column-blocked plan")
+    ap.add_argument("--plan", action="store_true", help="column-blocked plan kernel for the SpMV instead of CSR")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     assert args.warmup >= 3, "at least 3 warm-up steps"

@@ -122,8 +122,9 @@ typedef struct {
  * bounds : [host] world + 1 row offsets, bounds[r] .. bounds[r+1] = rank r's rows
  *          (tsnet_shard_rows); row_begin/row_end must equal bounds[rank], bounds[rank+1].
  * NULL shard, or world == 1 with rows [0, n), = one GPU, all rows.
- * Sharded calls need P->plan built for the same rows (tsnet_plan_build with
- * this shard); recentring is not supported across ranks (TSNET_E_ARG). */
+ * With a plan (P->plan), it must have been built for the same rows
+ * (tsnet_plan_build with this shard); recentring is not supported across
+ * ranks (TSNET_E_ARG). */
 typedef struct {
     int32_t rank, world;
     int64_t row_begin, row_end;
@@ -200,7 +201,7 @@ TSNET_API int tsnet_grad(const tsnet_csr* P, const float* Y, const tsnet_grad_pa
 
 /* The attractive term alone (step a6, Eq. 6 first term):
  *   f_attr,i = sum_{j in row i} p_ij w_ij Delta_ij   (n x 2 fp32, device)
- * Uses P->plan when set (column-blocked kernel), else the CSR kernel.
+ * Uses P->plan when set (column-blocked kernel), else the row-wise CSR kernel.
  * Needs no workspace.  Async.  (Also the kernel bench.py times for the roofline.) */
 TSNET_API int tsnet_attr(const tsnet_csr* P, const float* Y, float* f_attr, tsnet_stream_t stream);
 

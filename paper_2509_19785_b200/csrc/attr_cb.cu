@@ -25,6 +25,7 @@
 // HBM bytes per launch: 8 per stored entry (+ padding) + 8 per (task, block)
 // segment offset + 8 per row written; Y slices come from L2.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -36,8 +37,7 @@ namespace tsnet {
 
 constexpr int kCbCols = 8192;       // points per column block (2 x 64 KB shared tiles)
 constexpr int kCbRowsMax = 11264;   // rows per task (88 KB shared accumulator)
-constexpr int kCbWarps = 16;        // consumer warps per CTA (+1 producer warp)
-constexpr int kCbThreads = (kCbWarps + 1) * 32;
+constexpr int kCbWarpsDefault = 24;   // consumer warps per CTA (+1 producer warp); env TSNET_CB_WARPS
 constexpr uint32_t kCbSentinel = 0xFFFFu;
 constexpr uint64_t kCbMagic = 0x4243544e53545354ull;  // "TSTSNTCB"
 
@@ -77,7 +77,8 @@ static CbHeader cb_layout(int64_t n, int64_t rb, int64_t re, int64_t nnz, int32_
 }
 
 // Host partition of rows [rb, re) into tasks: T = 148 w (w = 1, 2, ...) tasks,
-// nnz-balanced (greedy cut at multiples of nnz/T) with at most rows_max rows.
+// balanced on nnz + rows (greedy cut at multiples of (nnz + rows)/T) with at
+// most rows_max rows each.
 // ipr[q] = indptr[rb + q], q = 0 .. re - rb.
 static int32_t cb_partition(const int64_t* ipr, int64_t rb, int64_t re, int32_t rows_max, int32_t base,
                             std::vector<int64_t>& row0, std::vector<int32_t>& rows) {
@@ -88,23 +89,25 @@ static int32_t cb_partition(const int64_t* ipr, int64_t rb, int64_t re, int32_t 
         rows.assign(1, 0);
         return 1;
     }
-    for (int32_t w = 1; w < (1 << 20); ++w) {
+    // enough tasks for the row cap, whatever the nnz balance asks
+    const int64_t wmax = 2 + (nr + (int64_t)rows_max * base - 1) / ((int64_t)rows_max * base);
+    for (int64_t w = 1; w <= wmax; ++w) {
         const int64_t T = (int64_t)base * w;
         row0.clear();
         rows.clear();
         int64_t r = rb;
-        bool ok = true;
-        for (int64_t t = 0; t < T && ok; ++t) {
-            const int64_t target = ipr[0] + (nnz * (t + 1) + T - 1) / T;
+        for (int64_t t = 0; t < T; ++t) {
+            // balance nnz + rows (empty rows weigh 1); the last task takes every
+            // remaining row (trailing empty rows included)
+            const int64_t target = (t == T - 1) ? INT64_MAX : ((nnz + nr) * (t + 1) + T - 1) / T;
             int64_t r1 = r;
-            // extend while the next row's start is below the target and the cap allows
-            while (r1 < re && ipr[r1 - rb] < target && r1 - r < rows_max) ++r1;
-            if (t == T - 1 && r1 < re) ok = false;
+            // extend while the weight before the next row is below the target and the cap allows
+            while (r1 < re && (ipr[r1 - rb] - ipr[0]) + (r1 - rb) < target && r1 - r < rows_max) ++r1;
             row0.push_back(r);
             rows.push_back((int32_t)(r1 - r));
             r = r1;
         }
-        if (ok && r == re) return (int32_t)T;
+        if (r == re && T <= INT32_MAX) return (int32_t)T;
     }
     return -1;
 }
@@ -158,104 +161,140 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 }
 
 // ------------------------------------------------------------------ kernel
-// Run-end update of the shared accumulator.  Inside one block segment a row is
-// shared between warps only at the two ends of a warp's share (keys kf, kl):
-// those go through atomicAdd (a CAS loop on shared fp32, rare); every other row
-// of the share is owned by this warp for the block, so a plain read-modify-write
-// suffices (flush keys within one sweep are distinct; sweeps of a warp are
-// ordered by __syncwarp; blocks are separated by a consumer barrier).
-__device__ __forceinline__ void cb_flush(float* Fs, uint32_t k, float x, float y, uint32_t kf, uint32_t kl) {
-    if (k == kf || k == kl) {
-        atomicAdd(Fs + 2 * k, x);
-        atomicAdd(Fs + 2 * k + 1, y);
-    } else {
-        float2* f = reinterpret_cast<float2*>(Fs) + k;
-        float2 v = *f;
+// One entry: contribution p w (X_i - X_j) with w = 1 / (1 + r^2).  Padding
+// entries (p = 0) contribute exactly 0.  rcp.approx: 1 + r^2 >= 1, relative
+// error <= 2^-22, far below the fp32 summation error of a row.
+__device__ __forceinline__ float2 cb_term(float2 yi, float2 yj, float p) {
+    const float dx = yi.x - yj.x, dy = yi.y - yj.y;
+    float w;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(w) : "f"(fmaf(dx, dx, fmaf(dy, dy, 1.0f))));
+    const float pw = p * w;
+    return make_float2(pw * dx, pw * dy);
+}
+
+__device__ __forceinline__ void fs_add(float2* Fs, uint32_t k, float x, float y) {
+    float2 v = Fs[k];
+    v.x += x;
+    v.y += y;
+    Fs[k] = v;
+}
+
+// Run-end update of F_s.  Inside one block segment a row is shared between
+// warps only at the two ends of a warp's share (keys kf, kl): those runs go to
+// the warp's private slots edge[0..1] and are folded into F_s with shared
+// atomics once per share; every other row of the share is owned by this warp
+// for the block -> plain read-modify-write (one emit per key per sweep; sweeps
+// of a warp are ordered by __syncwarp; blocks are separated by a barrier).
+__device__ __forceinline__ void cb_emit(bool on, uint32_t k, float x, float y, float2* Fs, float2* edge, uint32_t kf,
+                                        uint32_t kl) {
+    float2* dst = (k == kf) ? edge : ((k == kl) ? edge + 1 : Fs + k);
+    if (on) {
+        float2 v = *dst;
         v.x += x;
         v.y += y;
-        *f = v;
+        *dst = v;
     }
 }
 
-// One entry: contribution p w (X_i - X_j) with w = 1 / (1 + r^2).
-__device__ __forceinline__ void cb_term(uint32_t word, uint32_t vbits, const float2* __restrict__ Ys,
-                                        const float2* __restrict__ Yrow, uint32_t& key, float& fx, float& fy) {
-    key = word >> 16;
-    if (key == kCbSentinel) {
-        fx = 0.f;
-        fy = 0.f;
-        return;
-    }
-    const float2 yj = Ys[word & 0xFFFFu];
-    const float2 yi = __ldg(Yrow + key);
-    const float dx = yi.x - yj.x, dy = yi.y - yj.y;
-    const float w = __frcp_rn(1.0f + dx * dx + dy * dy);
-    const float pw = __uint_as_float(vbits) * w;
-    fx = pw * dx;
-    fy = pw * dy;
+// One sweep: lane holds entries 4 lane .. 4 lane + 3 of 128 consecutive entries
+// of the segment (keys = local rows, non-decreasing; masked entries carry the
+// sentinel key and p = 0 and sit at the end).
+// Y_i of the lane's four entries (issued one sweep ahead; one load per
+// distinct row of the lane, sentinel keys read row 0 and are multiplied by p = 0)
+struct CbYi {
+    float2 y[4];
+};
+__device__ __forceinline__ CbYi cb_yi(uint4 a, uint4 b, const float2* __restrict__ Yrow) {
+    const uint32_t k0 = a.x >> 16, k1 = a.z >> 16, k2 = b.x >> 16, k3 = b.z >> 16;
+    CbYi r;
+    r.y[0] = __ldg(Yrow + (k0 == kCbSentinel ? 0u : k0));
+    r.y[1] = (k1 == k0) ? r.y[0] : __ldg(Yrow + (k1 == kCbSentinel ? 0u : k1));
+    r.y[2] = (k2 == k1) ? r.y[1] : __ldg(Yrow + (k2 == kCbSentinel ? 0u : k2));
+    r.y[3] = (k3 == k2) ? r.y[2] : __ldg(Yrow + (k3 == kCbSentinel ? 0u : k3));
+    return r;
 }
 
-// Process one sweep: lane holds entries 4 lane .. 4 lane + 3 of 128 consecutive
-// entries (keys non-decreasing across the sweep; masked entries carry the
-// sentinel key and sit at the end).
-__device__ __forceinline__ void cb_sweep(uint4 a, uint4 b, const float2* __restrict__ Ys,
-                                         const float2* __restrict__ Yrow, float* Fs, int lane, uint32_t kf,
-                                         uint32_t kl) {
+__device__ __forceinline__ void cb_sweep(uint4 a, uint4 b, const CbYi& yi, const float2* __restrict__ Ys,
+                                         float2* Fs, int lane, float2* edge, uint32_t kf, uint32_t kl) {
+    const uint32_t wd[4] = {a.x, a.z, b.x, b.z};
+    const float pv[4] = {__uint_as_float(a.y), __uint_as_float(a.w), __uint_as_float(b.y), __uint_as_float(b.w)};
     uint32_t k[4];
-    float fx[4], fy[4];
-    cb_term(a.x, a.y, Ys, Yrow, k[0], fx[0], fy[0]);
-    cb_term(a.z, a.w, Ys, Yrow, k[1], fx[1], fy[1]);
-    cb_term(b.x, b.y, Ys, Yrow, k[2], fx[2], fy[2]);
-    cb_term(b.z, b.w, Ys, Yrow, k[3], fx[3], fy[3]);
-    // runs inside the lane: head (first run, if the lane has >= 2 runs), middles, tail
-    uint32_t hk = kCbSentinel, tk = k[0];
-    float hx = 0.f, hy = 0.f, tx = fx[0], ty = fy[0];
-    bool open_first = true;
+    float2 yj[4];
 #pragma unroll
-    for (int q = 1; q < 4; ++q) {
-        if (k[q] == tk) {
-            tx += fx[q];
-            ty += fy[q];
-        } else {
-            if (open_first) {
-                hk = tk;
-                hx = tx;
-                hy = ty;
-                open_first = false;
-            } else if (tk != kCbSentinel) {
-                cb_flush(Fs, tk, tx, ty, kf, kl);
+    for (int q = 0; q < 4; ++q) {
+        k[q] = wd[q] >> 16;
+        yj[q] = Ys[wd[q] & 0xFFFFu];
+    }
+    const bool mid1 = k[1] != k[0] && k[1] != k[3], mid2 = k[2] != k[0] && k[2] != k[3];
+    float2 f[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) f[q] = cb_term(yi.y[q], yj[q], pv[q]);
+    // lane runs: tail (key k3), head (key k0 if != k3), middles (rare)
+    const uint32_t tk = k[3];
+    float tx = f[3].x, ty = f[3].y;
+    float hx = 0.f, hy = 0.f;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const bool t = k[q] == tk, h = k[q] == k[0];
+        tx += t ? f[q].x : 0.f;
+        ty += t ? f[q].y : 0.f;
+        hx += (h && !t) ? f[q].x : 0.f;
+        hy += (h && !t) ? f[q].y : 0.f;
+    }
+    const bool has_head = k[0] != tk;
+    // middle runs: keys k1 / k2 different from both ends (a row with <= 2 entries
+    // inside this lane); they are complete here
+    if (__any_sync(0xffffffffu, mid1 || mid2)) {
+        float m1x = 0.f, m1y = 0.f, m2x = 0.f, m2y = 0.f;
+        if (mid1) {
+            m1x = f[1].x;
+            m1y = f[1].y;
+            if (k[2] == k[1]) {
+                m1x += f[2].x;
+                m1y += f[2].y;
             }
-            tk = k[q];
-            tx = fx[q];
-            ty = fy[q];
         }
-    }
-    // segmented inclusive scan of the tails over lanes (keys sorted => runs contiguous)
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t uk = __shfl_up_sync(0xffffffffu, tk, o);
-        const float ux = __shfl_up_sync(0xffffffffu, tx, o);
-        const float uy = __shfl_up_sync(0xffffffffu, ty, o);
-        if (lane >= o && uk == tk) {
-            tx += ux;
-            ty += uy;
+        const bool m2 = mid2 && k[2] != k[1];
+        if (m2) {
+            m2x = f[2].x;
+            m2y = f[2].y;
         }
+        cb_emit(mid1, k[1], m1x, m1y, Fs, edge, kf, kl);
+        cb_emit(m2, k[2], m2x, m2y, Fs, edge, kf, kl);
     }
-    const uint32_t nk = __shfl_down_sync(0xffffffffu, tk, 1);
+    // join the lane runs across lanes.  Usually a run spans at most two lanes
+    // (the tail of lane l continues as the head of lane l+1): one hand-down.  When
+    // some run covers a whole lane (rows with many entries in this block), a
+    // segmented inclusive scan of the tails does the general case.
     const uint32_t pk = __shfl_up_sync(0xffffffffu, tk, 1);
+    const uint32_t nk = __shfl_down_sync(0xffffffffu, tk, 1);
+    float sx = tx, sy = ty;
+    const bool through = lane > 0 && !has_head && tk == pk;   // whole lane continues the previous run
+    if (__any_sync(0xffffffffu, through)) {
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t uk = __shfl_up_sync(0xffffffffu, tk, o);
+            const float ux = __shfl_up_sync(0xffffffffu, sx, o);
+            const float uy = __shfl_up_sync(0xffffffffu, sy, o);
+            const bool add = lane >= o && uk == tk;
+            sx += add ? ux : 0.f;
+            sy += add ? uy : 0.f;
+        }
+    }
     const bool last = (lane == 31) || (nk != tk);
-    // a head run continues the previous lane's tail run, or stands alone
-    const bool give = (hk != kCbSentinel) && lane > 0 && hk == pk;
-    if (hk != kCbSentinel && !give) cb_flush(Fs, hk, hx, hy, kf, kl);
+    // a head run continues the previous lane's tail run (hand it down), or stands alone
+    const bool give = has_head && lane > 0 && k[0] == pk;
     const float gx = __shfl_down_sync(0xffffffffu, give ? hx : 0.f, 1);
     const float gy = __shfl_down_sync(0xffffffffu, give ? hy : 0.f, 1);
-    if (last && tk != kCbSentinel) {
-        const bool got = (lane < 31);
-        cb_flush(Fs, tk, tx + (got ? gx : 0.f), ty + (got ? gy : 0.f), kf, kl);
-    }
+    const bool gv = lane < 31;
+    cb_emit(has_head && !give && k[0] != kCbSentinel, k[0], hx, hy, Fs, edge, kf, kl);
+    // without the scan, a tail that continues into the next lane is not "last"
+    // there, so only run ends emit: sum = own tail (+ scanned prefix) + next head
+    cb_emit(last && tk != kCbSentinel, tk, sx + (gv ? gx : 0.f), sy + (gv ? gy : 0.f), Fs, edge, kf, kl);
 }
 
-__global__ void __launch_bounds__(kCbThreads, 1) k_attr_cb(const uint8_t* __restrict__ plan, const float2* __restrict__ Y,
+template <int kCbWarps>
+__global__ void __launch_bounds__((kCbWarps + 1) * 32, 1) k_attr_cb(const uint8_t* __restrict__ plan, const float2* __restrict__ Y,
                                                            float2* __restrict__ F, int y_aligned) {
     extern __shared__ __align__(128) uint8_t cb_smem[];
     float2* Ys0 = reinterpret_cast<float2*>(cb_smem);
@@ -315,6 +354,10 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_attr_cb(const uint8_t* __rest
     // ---------------- consumers
     const uint64_t pol = cb_policy_evict_first();
     const int nthr = kCbWarps * 32;
+    float2* F2s = reinterpret_cast<float2*>(Fs);
+    float2* edge = reinterpret_cast<float2*>(bars + 4) + 2 * warp;   // this warp's two boundary slots
+    if (lane < 2) edge[lane] = make_float2(0.f, 0.f);
+    __syncwarp();
     uint32_t k = 0;
     for (int t = blockIdx.x; t < T; t += gridDim.x) {
         const int64_t row0 = row0s[t];
@@ -323,39 +366,80 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_attr_cb(const uint8_t* __rest
         for (int q = threadIdx.x; q < 2 * rows; q += nthr) Fs[q] = 0.f;
         named_bar(1, nthr);
         const int64_t* sg = seg + (int64_t)t * NB;
-        for (int J = 0; J < NB; ++J) {
+        const uint4 pad = make_uint4(kCbSentinel << 16, 0u, kCbSentinel << 16, 0u);
+        const int l2 = 2 * lane;
+        // this warp's share of block J's segment, in pairs of entries (16 B), and the
+        // keys of its first and last entries (rows possibly shared with neighbours)
+        auto share = [&](int J, const uint4*& sp, int& npw, uint32_t& kf, uint32_t& kl) {
             const int64_t s0 = sg[J], s1 = sg[J + 1];
-            if (s0 == s1) continue;
+            const int np = (int)((s1 - s0) >> 1);
+            const int per = (np + kCbWarps - 1) / kCbWarps;
+            const int q0 = min(np, per * warp);
+            npw = min(np, per * (warp + 1)) - q0;
+            sp = ent + (s0 >> 1) + q0;
+            kf = kl = kCbSentinel;
+            if (npw > 0) {
+                kf = __ldg(reinterpret_cast<const uint32_t*>(sp)) >> 16;
+                kl = __ldg(reinterpret_cast<const uint32_t*>(sp + npw - 1) + 2) >> 16;
+            }
+        };
+        auto next_block = [&](int J) {
+            while (J < NB && sg[J] == sg[J + 1]) ++J;
+            return J;
+        };
+        // prologue of the first block; later blocks are prefetched during the previous one
+        int J = next_block(0);
+        const uint4* sp = ent;
+        int npw = 0;
+        uint32_t kf = kCbSentinel, kl = kCbSentinel;
+        uint4 a0 = pad, c0 = pad, a1 = pad, c1 = pad;
+        if (J < NB) {
+            share(J, sp, npw, kf, kl);
+            if (l2 < npw) a0 = ld_stream_v4(sp + l2, pol);
+            if (l2 + 1 < npw) c0 = ld_stream_v4(sp + l2 + 1, pol);
+            if (l2 + 64 < npw) a1 = ld_stream_v4(sp + l2 + 64, pol);
+            if (l2 + 65 < npw) c1 = ld_stream_v4(sp + l2 + 65, pol);
+        }
+        while (J < NB) {
             const int b = k & 1;
             const float2* Ys = b ? Ys1 : Ys0;
-            // this warp's share of the segment, in pairs of entries (16 B)
-            const int64_t p0 = s0 >> 1, np = (s1 - s0) >> 1;
-            const int64_t per = (np + kCbWarps - 1) / kCbWarps;
-            const int64_t w0 = p0 + std::min<int64_t>(np, per * warp), w1 = p0 + std::min<int64_t>(np, per * (warp + 1));
-            const uint4 pad = make_uint4(kCbSentinel << 16, 0u, kCbSentinel << 16, 0u);
-            int64_t p = w0;
-            uint4 a = pad, c = pad;
-            if (p + 2 * lane < w1) a = ld_stream_v4(ent + p + 2 * lane, pol);
-            if (p + 2 * lane + 1 < w1) c = ld_stream_v4(ent + p + 2 * lane + 1, pol);
-            // keys of the share's first and last entries (rows possibly shared with neighbours)
-            uint32_t kf = kCbSentinel, kl = kCbSentinel;
-            if (w0 < w1) {
-                kf = __shfl_sync(0xffffffffu, a.x, 0) >> 16;
-                kl = __ldg(reinterpret_cast<const uint32_t*>(ent + w1 - 1) + 2) >> 16;
-            }
+            CbYi y0 = cb_yi(a0, c0, Yrow);
             mbar_wait(&bars[b], (k >> 1) & 1);
-            for (; p < w1; p += 64) {
-                uint4 a2 = pad, c2 = pad;
-                const int64_t pn = p + 64;
-                if (pn + 2 * lane < w1) a2 = ld_stream_v4(ent + pn + 2 * lane, pol);
-                if (pn + 2 * lane + 1 < w1) c2 = ld_stream_v4(ent + pn + 2 * lane + 1, pol);
-                cb_sweep(a, c, Ys, Yrow, Fs, lane, kf, kl);
+            const int nsw = (npw + 63) >> 6;
+#pragma unroll 1
+            for (int sw = 0; sw < nsw; ++sw) {
+                const int o = (sw + 2) * 64 + l2;
+                const uint4 a2 = o < npw ? ld_stream_v4(sp + o, pol) : pad;
+                const uint4 c2 = o + 1 < npw ? ld_stream_v4(sp + o + 1, pol) : pad;
+                const CbYi y1 = cb_yi(a1, c1, Yrow);   // rows of the next sweep, one sweep ahead
+                cb_sweep(a0, c0, y0, Ys, F2s, lane, edge, kf, kl);
                 __syncwarp();
-                a = a2;
-                c = c2;
+                a0 = a1;
+                c0 = c1;
+                a1 = a2;
+                c1 = c2;
+                y0 = y1;
             }
             if (lane == 0) mbar_arrive(&bars[2 + b]);
+            if (lane < 4) {   // fold the two boundary rows: one shared atomic per lane
+                const uint32_t ke = (lane < 2) ? kf : kl;
+                const bool ok = ke != kCbSentinel && (lane < 2 || kl != kf);
+                float* e = reinterpret_cast<float*>(edge) + lane;
+                if (ok) atomicAdd(Fs + 2 * ke + (lane & 1), *e);
+                *e = 0.f;
+            }
+            __syncwarp();
             ++k;
+            // prefetch the next block's first two sweeps before the barrier
+            J = next_block(J + 1);
+            a0 = c0 = a1 = c1 = pad;
+            if (J < NB) {
+                share(J, sp, npw, kf, kl);
+                if (l2 < npw) a0 = ld_stream_v4(sp + l2, pol);
+                if (l2 + 1 < npw) c0 = ld_stream_v4(sp + l2 + 1, pol);
+                if (l2 + 64 < npw) a1 = ld_stream_v4(sp + l2 + 64, pol);
+                if (l2 + 65 < npw) c1 = ld_stream_v4(sp + l2 + 65, pol);
+            }
             named_bar(1, nthr);   // rows owned by one warp in this block may be shared in the next
         }
         named_bar(1, nthr);
@@ -366,7 +450,11 @@ __global__ void __launch_bounds__(kCbThreads, 1) k_attr_cb(const uint8_t* __rest
     }
 }
 
-size_t cb_smem_bytes() { return sizeof(float2) * 2 * kCbCols + sizeof(float) * 2 * kCbRowsMax + 4 * sizeof(uint64_t); }
+constexpr int kCbWarpsMax = 31;
+size_t cb_smem_bytes() {
+    return sizeof(float2) * 2 * kCbCols + sizeof(float) * 2 * kCbRowsMax + 4 * sizeof(uint64_t) +
+           sizeof(float2) * 2 * kCbWarpsMax;
+}
 
 static int num_sms() {
     static int sms = 0;
@@ -378,16 +466,38 @@ static int num_sms() {
     return sms;
 }
 
-cudaError_t launch_attr_cb(const void* plan, const float2* Y, float2* F, cudaStream_t s) {
+template <int W>
+static cudaError_t launch_cb_w(const void* plan, const float2* Y, float2* F, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_attr_cb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cb_smem_bytes());
+        cudaError_t e = cudaFuncSetAttribute(k_attr_cb<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)cb_smem_bytes());
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     const int aligned = ((uintptr_t)Y % 16) == 0;
-    k_attr_cb<<<num_sms(), kCbThreads, cb_smem_bytes(), s>>>(reinterpret_cast<const uint8_t*>(plan), Y, F, aligned);
+    k_attr_cb<W><<<num_sms(), (W + 1) * 32, cb_smem_bytes(), s>>>(reinterpret_cast<const uint8_t*>(plan), Y, F,
+                                                                  aligned);
     return cudaGetLastError();
+}
+
+static int cb_warps() {
+    static int w = 0;
+    if (w == 0) {
+        const char* e = getenv("TSNET_CB_WARPS");
+        w = e ? atoi(e) : kCbWarpsDefault;
+        if (w != 8 && w != 12 && w != 16 && w != 24) w = kCbWarpsDefault;
+    }
+    return w;
+}
+
+cudaError_t launch_attr_cb(const void* plan, const float2* Y, float2* F, cudaStream_t s) {
+    switch (cb_warps()) {
+        case 8: return launch_cb_w<8>(plan, Y, F, s);
+        case 12: return launch_cb_w<12>(plan, Y, F, s);
+        case 16: return launch_cb_w<16>(plan, Y, F, s);
+        default: return launch_cb_w<24>(plan, Y, F, s);
+    }
 }
 
 // ------------------------------------------------------------------ plan build

@@ -53,9 +53,9 @@ struct Geo {
     int nitems;                        // spread work items
     int nonfinite;
     unsigned int ticket;               // last-block-done counter of the bbox kernel
-    int bbox[4];                       // ordered-int encodings: min x, min y, max x, max y
+    unsigned bbox[4];                  // ~u(min x), ~u(min y), u(max x), u(max y); 0 = empty (field.cu)
     double sum_x, sum_y;               // centroid accumulation (recenter)
-    unsigned int ticket2;
+    unsigned int pad2;
     int pad;
 };
 

@@ -3,7 +3,7 @@
 // PAPER.md:397-403; entropy kernel K_e = 1/(eps + r^2)).
 //
 // Steps, all device-driven (no host round trip):
-//   a0 k_iter_init + k_bbox   bounding box -> grid geometry (I, h_b, N = 3I, M = 6I, FFT plan)
+//   a0 k_bbox                 bounding box -> grid geometry (I, h_b, N = 3I, M = 6I, FFT plan)
 //   .. k_prep                 zero box counters and charge grid, twiddles of length M
 //   a1 k_box_count/k_box_scan/k_box_scatter  counting sort of points by box
 //   a2 k_spread               box-local charges W1 and local moments M_x, M_y (warp per
@@ -37,17 +37,11 @@ __device__ __forceinline__ bool is5smooth(int m) {
     return m == 1;
 }
 
-__global__ void k_iter_init(Geo* g) {
-    g->bbox[0] = 0x7FFFFFFF;
-    g->bbox[1] = 0x7FFFFFFF;
-    g->bbox[2] = (int)0x80000000;
-    g->bbox[3] = (int)0x80000000;
-    g->ticket = 0u;
-    g->ticket2 = 0u;
-    g->zacc = 0.0;
-    g->sum_x = 0.0;
-    g->sum_y = 0.0;
-}
+// Bounding-box accumulators whose all-zero state means "empty", so a zeroed
+// workspace needs no initialisation kernel: max as the monotone unsigned key
+// u(x), min as ~u(x); both reduced with atomicMax.
+__device__ __forceinline__ unsigned bb_key(float x) { return (unsigned)f2o(x) ^ 0x80000000u; }
+__device__ __forceinline__ float bb_val(unsigned u) { return o2f((int)(u ^ 0x80000000u)); }
 
 // a0: bounding box of Y and, in the last block, the grid geometry (R9).
 __global__ void __launch_bounds__(256) k_bbox(const float2* __restrict__ Y, int64_t n, Geo* g, float h_max,
@@ -86,10 +80,10 @@ __global__ void __launch_bounds__(256) k_bbox(const float2* __restrict__ Y, int6
             mxx = fmaxf(mxx, s[2][k]); mxy = fmaxf(mxy, s[3][k]);
         }
         if (n > 0) {
-            atomicMin(&g->bbox[0], f2o(mnx));
-            atomicMin(&g->bbox[1], f2o(mny));
-            atomicMax(&g->bbox[2], f2o(mxx));
-            atomicMax(&g->bbox[3], f2o(mxy));
+            atomicMax(&g->bbox[0], ~bb_key(mnx));
+            atomicMax(&g->bbox[1], ~bb_key(mny));
+            atomicMax(&g->bbox[2], bb_key(mxx));
+            atomicMax(&g->bbox[3], bb_key(mxy));
         }
         if (sbad) atomicOr(&g->nonfinite, 1);
         __threadfence();
@@ -100,9 +94,19 @@ __global__ void __launch_bounds__(256) k_bbox(const float2* __restrict__ Y, int6
     if (!last || threadIdx.x != 0) return;
     __threadfence();
     // ---- geometry (fp64, identical to the oracle's definition) ----
-    volatile int* bb = g->bbox;
-    double lo_x = (double)o2f(bb[0]), lo_y = (double)o2f(bb[1]);
-    double hi_x = (double)o2f(bb[2]), hi_y = (double)o2f(bb[3]);
+    volatile unsigned* bb = g->bbox;
+    double lo_x = (double)bb_val(~bb[0]), lo_y = (double)bb_val(~bb[1]);
+    double hi_x = (double)bb_val(bb[2]), hi_y = (double)bb_val(bb[3]);
+    // reset the per-iteration accumulators for the next call (this block runs
+    // after every other block's atomics; zacc / sums are accumulated later)
+    bb[0] = 0u;
+    bb[1] = 0u;
+    bb[2] = 0u;
+    bb[3] = 0u;
+    g->ticket = 0u;
+    g->zacc = 0.0;
+    g->sum_x = 0.0;
+    g->sum_y = 0.0;
     double S = fmax(hi_x - lo_x, hi_y - lo_y);
     if (!(S >= 1e-12)) S = 1e-12;            // also catches NaN (non-finite layouts)
     if (!isfinite(S) || !isfinite(lo_x) || !isfinite(lo_y)) {
@@ -255,16 +259,17 @@ __global__ void __launch_bounds__(1024) k_box_scan(Geo* g, const int* __restrict
         __syncthreads();
     }
     int run = sc[threadIdx.x] - cs, irun = si[threadIdx.x] - is;
+    int* item_start = reinterpret_cast<int*>(items);   // first spread item of each box
     for (int b = b0; b < b1; ++b) {
         int c = box_cnt[b];
         box_start[b] = run;
-        int ni = (c + kSpreadChunk - 1) / kSpreadChunk;
-        for (int q = 0; q < ni; ++q) items[irun + q] = make_int2(b, run + q * kSpreadChunk);
+        item_start[b] = irun;
         run += c;
-        irun += ni;
+        irun += (c + kSpreadChunk - 1) / kSpreadChunk;
     }
     if (threadIdx.x == T - 1) {
         box_start[nb] = (int)n;
+        item_start[nb] = si[T - 1];
         g->nitems = si[T - 1];
     }
 }
@@ -292,9 +297,20 @@ __global__ void __launch_bounds__(256) k_spread(const Geo* __restrict__ g, const
     const float s[3] = {1.0f / 6.0f, 0.5f, 5.0f / 6.0f};
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
+    const int* item_start = reinterpret_cast<const int*>(items);
+    const int nb = I * I;
     for (int it = blockIdx.x * wpb + (threadIdx.x >> 5); it < nitems; it += gridDim.x * wpb) {
-        const int2 item = items[it];
-        const int b = item.x;
+        // box of this item: largest b with item_start[b] <= it (32-ary warp search)
+        int lo = 0, hi = nb;
+        while (hi - lo > 1) {
+            const int step = (hi - lo + 31) / 32;
+            const int p = lo + lane * step;
+            const unsigned m = __ballot_sync(0xffffffffu, p < hi && item_start[p] <= it);
+            lo += (31 - __clz(m)) * step;
+            hi = min(lo + step, hi);
+        }
+        const int b = lo;
+        const int2 item = make_int2(b, box_start[b] + (it - item_start[b]) * kSpreadChunk);
         const int end = min(item.y + kSpreadChunk, box_start[b + 1]);
         float acc[27];
 #pragma unroll
@@ -519,9 +535,8 @@ cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, b
     cudaError_t e;
     if ((e = field_set_attrs(w.M_max)) != cudaSuccess) return e;
     const int64_t n = a.n, nl = a.re - a.rb;
-    const int pb = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)kNumSMs * 8));
+    const int pb = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)kNumSMs * 2));
     const int pbl = (int)std::max<int64_t>(1, std::min<int64_t>((nl + 255) / 256, (int64_t)kNumSMs * 8));
-    k_iter_init<<<1, 1, 0, s>>>(w.geo);
     k_bbox<<<pb, 256, 0, s>>>(a.Y, n, w.geo, a.h_max, a.I_min, a.I_max);
     if (zero_all && (e = cudaMemsetAsync(w.wgrid, 0, sizeof(float4) * (size_t)w.N_max * w.N_max, s)) != cudaSuccess)
         return e;

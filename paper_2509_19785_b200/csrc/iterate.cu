@@ -8,6 +8,8 @@
 //     f_field gathered from the convolved grid (field.cu), followed by the
 //     momentum/gains move (reading R12).
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -101,14 +103,136 @@ __global__ void __launch_bounds__(256) k_spmv(int64_t n, int64_t nnz, const int6
     }
 }
 
+// Row-wise CSR SpMV with the next row's first batch prefetched while the
+// current row is gathered and reduced (so a row's HBM stream overlaps the
+// previous row's L2 gathers), U entries per lane per batch, CHUNK entries per
+// warp work item.  Rows entirely inside the chunk are stored, the two rows a
+// chunk may share with its neighbours use vector atomics (F zeroed first).
+template <int U>
+__device__ __forceinline__ void spmv2_load(const int32_t* __restrict__ indices, const float* __restrict__ values,
+                                           int64_t s0, int64_t s1, int lane, int (&col)[U], float (&val)[U],
+                                           int fill, uint64_t pol) {
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+        const int64_t e = s0 + lane + 32 * q;
+        const bool ok = e < s1;
+        col[q] = ok ? ld_stream_i32(indices + e, pol) : fill;
+        val[q] = ok ? ld_stream_f32(values + e, pol) : 0.f;
+    }
+}
+
+template <int U>
+__device__ __forceinline__ void spmv2_acc(const float2* __restrict__ Y, float2 yi, const int (&col)[U],
+                                          const float (&val)[U], float& fx, float& fy) {
+    float2 yj[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) yj[q] = __ldg(Y + col[q]);
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+        const float dx = yi.x - yj[q].x, dy = yi.y - yj[q].y;
+        float w;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(w) : "f"(fmaf(dx, dx, fmaf(dy, dy, 1.0f))));
+        const float pw = val[q] * w;
+        fx = fmaf(pw, dx, fx);
+        fy = fmaf(pw, dy, fy);
+    }
+}
+
+// Rows [rb, re): the stored entries indptr[rb] .. indptr[re] are cut into
+// chunks; F holds rows rb.. (F[r - rb]).
+template <int U, int CHUNK>
+__global__ void __launch_bounds__(256) k_spmv2(int64_t rb, int64_t re_rows, const int64_t* __restrict__ indptr,
+                                               const int32_t* __restrict__ indices, const float* __restrict__ values,
+                                               const float2* __restrict__ Y, float2* __restrict__ F) {
+    const int lane = threadIdx.x & 31;
+    const int64_t e_begin = __ldg(indptr + rb), e_end = __ldg(indptr + re_rows);
+    const int64_t nchunks = (e_end - e_begin + CHUNK - 1) / CHUNK;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t pol = policy_evict_first();
+    F -= rb;
+    for (int64_t c = wid; c < nchunks; c += nw) {
+        const int64_t cs = e_begin + c * CHUNK, ce = std::min(cs + CHUNK, e_end);
+        // row containing entry cs: largest r in [rb, re) with indptr[r] <= cs
+        int64_t r = rb + warp_row_of(indptr + rb, re_rows - rb, cs);
+        int64_t rs = cs;                                  // current row segment [rs, re)
+        int64_t re = std::min(__ldg(indptr + r + 1), ce);
+        int col[U];
+        float val[U];
+        spmv2_load<U>(indices, values, rs, std::min(re, rs + 32 * U), lane, col, val, (int)r, pol);
+        while (true) {
+            const bool more = re < ce;                    // a next row starts inside the chunk
+            int64_t r2 = r + 1, rs2 = re, re2 = re;
+            int col2[U];
+            float val2[U];
+            if (more) {
+                re2 = std::min(__ldg(indptr + r2 + 1), ce);
+                spmv2_load<U>(indices, values, rs2, std::min(re2, rs2 + 32 * U), lane, col2, val2, (int)r2, pol);
+            }
+            const float2 yi = __ldg(Y + r);
+            float fx = 0.f, fy = 0.f;
+            spmv2_acc<U>(Y, yi, col, val, fx, fy);
+            for (int64_t b = rs + 32 * U; b < re; b += 32 * U) {   // long rows: further batches
+                int cb[U];
+                float vb[U];
+                spmv2_load<U>(indices, values, b, re, lane, cb, vb, (int)r, pol);
+                spmv2_acc<U>(Y, yi, cb, vb, fx, fy);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                fx += __shfl_xor_sync(0xffffffffu, fx, o);
+                fy += __shfl_xor_sync(0xffffffffu, fy, o);
+            }
+            if (lane == 0) {
+                // rows starting before the chunk or ending after it are shared
+                const bool shared = (rs == cs && __ldg(indptr + r) < cs) || re == ce;
+                if (shared) atomicAdd(F + r, make_float2(fx, fy));
+                else F[r] = make_float2(fx, fy);
+            }
+            if (!more) break;
+            r = r2;
+            rs = rs2;
+            re = re2;
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                col[q] = col2[q];
+                val[q] = val2[q];
+            }
+        }
+    }
+}
+
+static int attr_kernel_choice() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TSNET_ATTR_KERNEL");   // probe hook: v1 | v2u8 (default: v2, 4 per lane)
+        v = 2;
+        if (e && !strcmp(e, "v1")) v = 1;
+        if (e && !strcmp(e, "v2u8")) v = 8;
+    }
+    return v;
+}
+
+// a6 for the rows [rb, re) of the call into w.f_attr (local rows): the
+// column-blocked plan kernel when P has a plan, else the row-wise CSR kernel.
 cudaError_t launch_spmv(const Ws& w, const GradArgs& a, cudaStream_t s) {
     if (a.plan) return launch_attr_cb(a.plan, a.Y, w.f_attr, s);   // rows of the plan's shard
-    if (a.rb != 0 || a.re != a.n) return cudaErrorInvalidValue;   // CSR kernel: all rows only
-    cudaError_t e = cudaMemsetAsync(w.f_attr, 0, sizeof(float2) * (size_t)a.n, s);
-    if (e != cudaSuccess || a.nnz == 0) return e;
-    const int64_t nchunks = (a.nnz + kSpmvChunk - 1) / kSpmvChunk;
-    const int blocks = (int)std::min<int64_t>((nchunks + 7) / 8, (int64_t)kNumSMs * 8);
-    k_spmv<<<blocks, 256, 0, s>>>(a.n, a.nnz, a.indptr, a.indices, a.values, a.Y, w.f_attr);
+    const int64_t nl = a.re - a.rb;
+    cudaError_t e = cudaMemsetAsync(w.f_attr, 0, sizeof(float2) * (size_t)nl, s);
+    if (e != cudaSuccess || a.nnz == 0 || nl == 0) return e;
+    const int kc = attr_kernel_choice();
+    if (kc == 1 && a.rb == 0 && a.re == a.n) {
+        const int64_t nchunks = (a.nnz + kSpmvChunk - 1) / kSpmvChunk;
+        const int blocks = (int)std::min<int64_t>((nchunks + 7) / 8, (int64_t)kNumSMs * 8);
+        k_spmv<<<blocks, 256, 0, s>>>(a.n, a.nnz, a.indptr, a.indices, a.values, a.Y, w.f_attr);
+        return cudaGetLastError();
+    }
+    constexpr int kChunk = 8192;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((a.nnz / kChunk + 8) / 8, (int64_t)kNumSMs * 8));
+    if (kc == 8)
+        k_spmv2<8, kChunk><<<blocks, 256, 0, s>>>(a.rb, a.re, a.indptr, a.indices, a.values, a.Y, w.f_attr);
+    else
+        k_spmv2<4, kChunk><<<blocks, 256, 0, s>>>(a.rb, a.re, a.indptr, a.indices, a.values, a.Y, w.f_attr);
     return cudaGetLastError();
 }
 

@@ -60,7 +60,6 @@ static bool sharded(const tsnet_shard* sh, int64_t n) {
 // Calls that communicate need the communicator (world > 1) and a plan.
 static int check_comm(const tsnet_shard* sh, const GradArgs& a) {
     if (!sharded(sh, a.n)) return TSNET_OK;
-    TSNET_ARG(a.plan != nullptr, "sharded calls need P->plan built for the shard's rows (tsnet_plan_build)");
     if (sh->world > 1) TSNET_ARG(sh->comm != nullptr, "world = %d needs shard->comm (tsnet_comm_init)", sh->world);
     return TSNET_OK;
 }
@@ -91,7 +90,6 @@ static int prepare(const tsnet_csr* P, const float* Y, const tsnet_grad_params* 
     a.values = P->values;
     a.plan = P->plan;
     a.Y = reinterpret_cast<const float2*>(Y);
-    if (sharded(sh, P->n)) TSNET_ARG(a.plan != nullptr, "a shard needs P->plan built for its rows");
     a.lambda_kl = gp->lambda_kl;
     a.lambda_c = gp->lambda_c;
     a.lambda_r = gp->lambda_r;

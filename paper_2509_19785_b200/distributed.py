@@ -36,14 +36,16 @@ class ShardedLayout:
     own rows)."""
 
     def __init__(self, P: CSR, Y0: torch.Tensor, rank: int, world: int, base: GradParams | None = None,
-                 use_graphs: bool = True, eta: float = 50.0, stage_switch: int = STAGE_SWITCH, group=None):
+                 use_graphs: bool = True, eta: float = 50.0, stage_switch: int = STAGE_SWITCH, group=None,
+                 plan: bool = False):
         assert Y0.is_cuda and Y0.shape == (P.n, 2)
         self.rank, self.world = rank, world
         bounds = shard_bounds(P.indptr.cpu().numpy(), world)
         uid = share_comm_id(rank, group)
         self.comm = tsnet_comm_init(uid, world, rank)
         self.shard = Shard(rank, world, bounds, self.comm)
-        self.P = tsnet_plan_build(P, self.shard)      # plan of the own rows only
+        # the attractive SpMV reads the own rows of P (CSR), or a plan of them
+        self.P = tsnet_plan_build(P, self.shard) if plan else P
         self.Y = Y0.clone()
         self.vel = torch.zeros_like(self.Y)
         self.gains = torch.ones_like(self.Y)

@@ -2,7 +2,7 @@
 # usage: bash scripts/gpu_run.sh TAG [pytest -k expr] [ncu kernel regex]
 TAG=${1:-r1}
 KEXPR=${2:-}
-KREGEX=${3:-k_attr_cb}
+KREGEX=${3:-k_spmv2}
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/${TAG}_smi.txt 2>&1
@@ -16,7 +16,8 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TA
 echo "smoke exit $?" >> gpurun_out/${TAG}_smoke.log
 timeout 900 python bench.py > gpurun_out/${TAG}_bench4.log 2>&1
 echo "bench exit $?" >> gpurun_out/${TAG}_bench4.log
-timeout 900 python bench.py --no-plan --no-cpu-baseline --no-e2e --steps 200 > gpurun_out/${TAG}_bench4_csr.log 2>&1
+timeout 900 python bench.py --plan --no-cpu-baseline --no-e2e --steps 200 > gpurun_out/${TAG}_bench4_plan.log 2>&1
+timeout 1200 python bench.py --config 5 --no-cpu-baseline --no-e2e --steps 200 > gpurun_out/${TAG}_bench5.log 2>&1
 B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e"
 timeout 600 $B > gpurun_out/${TAG}_plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 3000 -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv $B > gpurun_out/${TAG}_ncu_launch.log 2>&1 && \

@@ -1,4 +1,6 @@
-"""Column-blocked attractive SpMV (attr_cb.cu, tsnet_plan_build) vs the oracle.
+"""Attractive SpMV kernels vs the oracle: the column-blocked plan kernel
+(attr_cb.cu, tsnet_plan_build) and the streamed CSR kernel (attr_csr.cu, used
+when P has no plan).
 
 F_attr,i = sum_j p_ij w_ij (X_i - X_j) (Eq. 6 first term) is
 computed by oracle.attr_sparse in fp64 from the same fp32 P and fp32 Y.
@@ -42,12 +44,13 @@ def dev_csr(ip, ix, pv):
                torch.from_numpy(np.asarray(pv, np.float32)).cuda())
 
 
-def check(ip, ix, pv, Y, shard=None, y_offset_rows=0):
-    """Plan + CB kernel vs oracle on rows [rb, re)."""
+def check(ip, ix, pv, Y, shard=None, y_offset_rows=0, plan=True):
+    """Plan + CB kernel (or the CSR kernel) vs oracle on rows [rb, re)."""
     n = len(ip) - 1
     pv32 = np.asarray(pv, np.float32).astype(np.float64)
     P = dev_csr(ip, ix, pv32)
-    T.tsnet_plan_build(P, shard=shard)
+    if plan:
+        T.tsnet_plan_build(P, shard=shard)
     rb, re = (0, n) if shard is None else (shard.row_begin, shard.row_end)
     # optionally place Y at an 8-byte (not 16-byte) aligned address -> non-TMA copy path
     base = torch.zeros((n + y_offset_rows, 2), dtype=torch.float32, device="cuda")
@@ -70,18 +73,21 @@ def check(ip, ix, pv, Y, shard=None, y_offset_rows=0):
     return P
 
 
+@pytest.mark.parametrize("plan", [True, False], ids=["cb", "csr"])
 @pytest.mark.parametrize("cfg", [1, 2, 3])
-def test_configs(cfg):
+def test_configs(cfg, plan):
     ip, ix = config_graph(cfg)
     P = oracle.build_P(ip, ix, 40.0, seed=0)
     n = P["n"]
     for Y in (clustered_layout(n, 25.0, 7, 1.2, 2), uniform_layout(n, 3.0, 4)):
-        check(P["indptr"], P["indices"], P["values"], Y)
+        check(P["indptr"], P["indices"], P["values"], Y, plan=plan)
 
 
+@pytest.mark.parametrize("plan", [True, False], ids=["cb", "csr"])
 @pytest.mark.parametrize("n,kind", [(1, "single"), (7, "tiny"), (8191, "one_block_minus"), (8192, "one_block"),
-                                    (8193, "block_plus_one"), (24577, "odd_tail"), (20011, "hub_and_empty")])
-def test_edge_patterns(n, kind):
+                                    (8193, "block_plus_one"), (24577, "odd_tail"), (20011, "hub_and_empty"),
+                                    (50000, "short_rows"), (30011, "many_empty")])
+def test_edge_patterns(n, kind, plan):
     rng = np.random.default_rng(n)
     L = rng.integers(0, 40, n)
     if kind == "hub_and_empty":
@@ -90,9 +96,13 @@ def test_edge_patterns(n, kind):
         L[6] = 3000
     if kind == "single":
         L[:] = 1
+    if kind == "short_rows":            # > 32 row ends per 128 entries (window overflow path)
+        L = rng.integers(0, 4, n)
+    if kind == "many_empty":
+        L[rng.random(n) < 0.8] = 0
     ip, ix, pv = random_csr(n, L, seed=n)
     Y = uniform_layout(n, 10.0, 9)
-    check(ip, ix, pv, Y)
+    check(ip, ix, pv, Y, plan=plan)
 
 
 def test_unaligned_Y_uses_copy_path():
@@ -101,13 +111,14 @@ def test_unaligned_Y_uses_copy_path():
     check(ip, ix, pv, uniform_layout(n, 5.0, 1), y_offset_rows=1)
 
 
-def test_long_rows_many_tasks():
+@pytest.mark.parametrize("plan", [True, False], ids=["cb", "csr"])
+def test_long_rows_many_tasks(plan):
     """Rows longer than a sweep and more than one wave of tasks (rows > 148 * 11264)."""
     n = 148 * 11264 + 5000
     L = np.full(n, 3)
     L[:200] = 2000
     ip, ix, pv = random_csr(n, L, seed=11)
-    check(ip, ix, pv, uniform_layout(n, 20.0, 2))
+    check(ip, ix, pv, uniform_layout(n, 20.0, 2), plan=plan)
 
 
 def test_shards_partition_the_rows():
@@ -119,8 +130,9 @@ def test_shards_partition_the_rows():
         check(P["indptr"], P["indices"], P["values"], Y, shard=T.tsnet_shard(0, 1, rb, re))
 
 
-def test_config4_full_size_sampled_rows():
-    """The bench workload (n ~ 0.95M, nnz ~ 2.06e8), GPU C0 output, plan kernel."""
+@pytest.mark.parametrize("plan", [True, False], ids=["cb", "csr"])
+def test_config4_full_size_sampled_rows(plan):
+    """The bench workload (n ~ 0.95M, nnz ~ 2.06e8), GPU C0 output."""
     from paper_2509_19785_b200 import tsnet_build_P
     ip, ix = config_graph(4)
     got = tsnet_build_P(torch.from_numpy(ip).cuda(), torch.from_numpy(ix).cuda(), u=40.0, seed=0)
@@ -128,7 +140,8 @@ def test_config4_full_size_sampled_rows():
     n = P.n
     Y = clustered_layout(n, 30.0, 40, 2.0, 5)
     Yd = torch.from_numpy(Y).cuda()
-    T.tsnet_plan_build(P)
+    if plan:
+        T.tsnet_plan_build(P)
     F = tsnet_attr(P, Yd)
     torch.cuda.synchronize()
     pip, pix = P.indptr.cpu().numpy(), P.indices.cpu().numpy()

@@ -42,13 +42,13 @@ def dev(P):
                torch.from_numpy(P["values"].astype(np.float32)).cuda())
 
 
-def emulated_step(P, Y, vel, gains, gp, sp, world):
+def emulated_step(P, Y, vel, gains, gp, sp, world, plan=True):
     n = P.n
     bounds = T.tsnet_shard_rows(P.indptr.cpu().numpy(), world)
     shards = [T.Shard(r, world, bounds) for r in range(world)]
     Ps, wss, Ys = [], [], []
     for sh in shards:
-        Pr = T.tsnet_plan_build(P.without_plan(), sh)
+        Pr = T.tsnet_plan_build(P.without_plan(), sh) if plan else P.without_plan()
         ws = alloc_workspace(n, P.nnz, gp)
         Yr = Y.clone()
         T.tsnet_field_local(Pr, Yr, gp, ws, shard=sh)
@@ -67,9 +67,10 @@ def emulated_step(P, Y, vel, gains, gp, sp, world):
     return Yout, Vout, Gout, bounds
 
 
+@pytest.mark.parametrize("plan", [False, True], ids=["csr", "cb"])
 @pytest.mark.parametrize("cfg,world", [(1, 2), (2, 3), (2, 8), (3, 4)])
 @pytest.mark.parametrize("stage", [0, 1])
-def test_emulated_shards_equal_one_gpu_and_oracle(cfg, world, stage):
+def test_emulated_shards_equal_one_gpu_and_oracle(cfg, world, stage, plan):
     P = oracle_P(cfg)
     n = P["n"]
     Y = clustered_layout(n, 20.0, 5, 1.5, 7)
@@ -78,10 +79,10 @@ def test_emulated_shards_equal_one_gpu_and_oracle(cfg, world, stage):
     gp, sp = GradParams(*lam[0]), StepParams(eta=50.0, momentum=lam[1])
     Pd = dev(P)
     Yd, Vd, Gd = (torch.from_numpy(a.copy()).cuda() for a in (Y, vel, gains))
-    Ys, Vs, Gs, bounds = emulated_step(Pd, Yd, Vd, Gd, gp, sp, world)
+    Ys, Vs, Gs, bounds = emulated_step(Pd, Yd, Vd, Gd, gp, sp, world, plan)
     assert len(bounds) == world + 1 and bounds[0] == 0 and bounds[-1] == n
-    # unsharded, same plan kernel
-    P1 = T.tsnet_plan_build(Pd.without_plan())
+    # unsharded, same attractive kernel
+    P1 = T.tsnet_plan_build(Pd.without_plan()) if plan else Pd.without_plan()
     ws = alloc_workspace(n, Pd.nnz, gp)
     Y1, V1, G1 = Yd.clone(), Vd.clone(), Gd.clone()
     tsnet_step(P1, Y1, V1, G1, gp, sp, ws)
@@ -103,7 +104,7 @@ def test_nccl_one_rank_communicator_step():
     Y = clustered_layout(n, 20.0, 5, 1.5, 7)
     vel, gains = random_state(n, 3)
     gp, sp = GradParams(1.0, 0.01, 0.6), StepParams(eta=50.0, momentum=0.8)
-    Pd = T.tsnet_plan_build(dev(P))
+    Pd = dev(P)
     uid = T.tsnet_comm_unique_id()
     comm = T.tsnet_comm_init(uid, 1, 0)
     try:
@@ -134,12 +135,9 @@ def test_shard_argument_errors():
     P = oracle_P(1)
     n = P["n"]
     gp, sp = GradParams(), StepParams()
-    Pd = dev(P)
-    ws = alloc_workspace(n, Pd.nnz, gp)
+    ws = alloc_workspace(n, P["indptr"][-1], gp)
     Yd = torch.zeros((n, 2), device="cuda")
     V, G = torch.zeros_like(Yd), torch.ones_like(Yd)
-    with pytest.raises(T.TsnetError):      # shard without a plan
-        tsnet_step(Pd, Yd, V, G, gp, sp, ws, shard=T.Shard(0, 2, [0, n // 2, n]))
     Pp = T.tsnet_plan_build(dev(P), T.Shard(0, 2, [0, n // 2, n]))
     with pytest.raises(T.TsnetError):      # world > 1 without a communicator
         tsnet_step(Pp, Yd, V, G, gp, sp, ws, shard=T.Shard(0, 2, [0, n // 2, n]))

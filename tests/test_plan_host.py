@@ -30,9 +30,9 @@ def test_cut_covers_rows_balanced(T, base):
     n = len(ip) - 1
     r0, rr = T.tsnet_plan_partition(ip, 0, n, 11264, base)
     Tn = check_cut(ip, 0, n, 11264, base, r0, rr)
-    nnz = np.array([ip[a + b] - ip[a] for a, b in zip(r0, rr)])
-    # greedy cut at multiples of nnz/T: each task within one row of the target
-    assert nnz.max() <= ip[-1] / Tn + np.diff(ip).max()
+    wgt = np.array([ip[a + b] - ip[a] + b for a, b in zip(r0, rr)])
+    # greedy cut at multiples of (nnz + rows)/T: each task within one row of the target
+    assert wgt.max() <= (ip[-1] + n) / Tn + np.diff(ip).max() + 1
 
 
 def test_row_cap_forces_more_tasks(T):
@@ -63,3 +63,16 @@ def test_bad_arguments(T):
     ip = np.arange(11, dtype=np.int64)
     with pytest.raises(Exception):
         T.tsnet_plan_partition(ip, 5, 3, 10, 1)
+
+
+def test_trailing_and_leading_empty_rows(T):
+    """Rows with no entries at either end must still be covered (the cut used
+    to loop forever when the last rows were empty)."""
+    L = np.zeros(30011, np.int64)
+    L[100:20000] = 5
+    ip = np.zeros(len(L) + 1, np.int64)
+    np.cumsum(L, out=ip[1:])
+    r0, rr = T.tsnet_plan_partition(ip, 0, len(L), 11264, 148)
+    check_cut(ip, 0, len(L), 11264, 148, r0, rr)
+    r0, rr = T.tsnet_plan_partition(np.zeros(501, np.int64), 0, 500, 64, 4)   # no entries at all
+    check_cut(np.zeros(501, np.int64), 0, 500, 64, 4, r0, rr)
