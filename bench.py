@@ -289,12 +289,14 @@ def run_ours(args, rank, world, local_rank):
     # SURVEY §8(d) B_g: CSR + state of the own rows + the all-gather payload landing in HBM
     step_bytes = 8 * nnz_l + 8 * (nl + 1) + 48 * nl + 8 * (n - nl)
     traffic = None
+    limiter = None
     kname = "k_attr_cb" if args.plan else "k_spmv2"
     tp = os.path.join(ROOT, "profiles", f"{kname}_dram_bytes_cfg{args.config}.json")
     if os.path.exists(tp) and world == 1:
         with open(tp) as f:
             rec = json.load(f)
         traffic = float(rec["dram_bytes_per_launch"]) * (nnz / rec["nnz"])
+        limiter = rec.get("limiter")
 
     # end to end through the host-buffer API (H2D + step + D2H every step)
     e2e = None
@@ -339,7 +341,7 @@ def run_ours(args, rank, world, local_rank):
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic, "kernel": f"{kname} (tsnet_attr)",
                              "kernel_ms": spmv_ms, "algorithmic_bytes": spmv_bytes, "peak_source": peak_src,
-                             "share_of_step": spmv_ms / step_ms, "rank": 0},
+                             "share_of_step": spmv_ms / step_ms, "rank": 0, "limiter": limiter},
                 "step_roofline": {"achieved": step_bytes / (step_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                                   "frac": step_bytes / (step_ms * 1e-3) / 1e9 / peak, "algorithmic_bytes": step_bytes},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": KERNELS_PER_STEP * args.steps,

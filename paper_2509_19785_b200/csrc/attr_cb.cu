@@ -370,6 +370,8 @@ __global__ void __launch_bounds__((kCbWarps + 1) * 32, 1) k_attr_cb(const uint8_
         const int l2 = 2 * lane;
         // this warp's share of block J's segment, in pairs of entries (16 B), and the
         // keys of its first and last entries (rows possibly shared with neighbours)
+        // kf / kl come back as the raw words; the >> 16 happens after the Ys wait so
+        // the loads' latency hides behind the barrier instead of stalling here
         auto share = [&](int J, const uint4*& sp, int& npw, uint32_t& kf, uint32_t& kl) {
             const int64_t s0 = sg[J], s1 = sg[J + 1];
             const int np = (int)((s1 - s0) >> 1);
@@ -377,10 +379,10 @@ __global__ void __launch_bounds__((kCbWarps + 1) * 32, 1) k_attr_cb(const uint8_
             const int q0 = min(np, per * warp);
             npw = min(np, per * (warp + 1)) - q0;
             sp = ent + (s0 >> 1) + q0;
-            kf = kl = kCbSentinel;
+            kf = kl = kCbSentinel << 16;
             if (npw > 0) {
-                kf = __ldg(reinterpret_cast<const uint32_t*>(sp)) >> 16;
-                kl = __ldg(reinterpret_cast<const uint32_t*>(sp + npw - 1) + 2) >> 16;
+                kf = __ldg(reinterpret_cast<const uint32_t*>(sp));
+                kl = __ldg(reinterpret_cast<const uint32_t*>(sp + npw - 1) + 2);
             }
         };
         auto next_block = [&](int J) {
@@ -391,10 +393,10 @@ __global__ void __launch_bounds__((kCbWarps + 1) * 32, 1) k_attr_cb(const uint8_
         int J = next_block(0);
         const uint4* sp = ent;
         int npw = 0;
-        uint32_t kf = kCbSentinel, kl = kCbSentinel;
+        uint32_t kfw = kCbSentinel << 16, klw = kCbSentinel << 16;   // raw first / last words of the share
         uint4 a0 = pad, c0 = pad, a1 = pad, c1 = pad;
         if (J < NB) {
-            share(J, sp, npw, kf, kl);
+            share(J, sp, npw, kfw, klw);
             if (l2 < npw) a0 = ld_stream_v4(sp + l2, pol);
             if (l2 + 1 < npw) c0 = ld_stream_v4(sp + l2 + 1, pol);
             if (l2 + 64 < npw) a1 = ld_stream_v4(sp + l2 + 64, pol);
@@ -403,8 +405,9 @@ __global__ void __launch_bounds__((kCbWarps + 1) * 32, 1) k_attr_cb(const uint8_
         while (J < NB) {
             const int b = k & 1;
             const float2* Ys = b ? Ys1 : Ys0;
-            CbYi y0 = cb_yi(a0, c0, Yrow);
             mbar_wait(&bars[b], (k >> 1) & 1);
+            const uint32_t kf = kfw >> 16, kl = klw >> 16;
+            CbYi y0 = cb_yi(a0, c0, Yrow);
             const int nsw = (npw + 63) >> 6;
 #pragma unroll 1
             for (int sw = 0; sw < nsw; ++sw) {
@@ -434,7 +437,7 @@ __global__ void __launch_bounds__((kCbWarps + 1) * 32, 1) k_attr_cb(const uint8_
             J = next_block(J + 1);
             a0 = c0 = a1 = c1 = pad;
             if (J < NB) {
-                share(J, sp, npw, kf, kl);
+                share(J, sp, npw, kfw, klw);
                 if (l2 < npw) a0 = ld_stream_v4(sp + l2, pol);
                 if (l2 + 1 < npw) c0 = ld_stream_v4(sp + l2 + 1, pol);
                 if (l2 + 64 < npw) a1 = ld_stream_v4(sp + l2 + 64, pol);

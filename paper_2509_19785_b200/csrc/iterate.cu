@@ -140,12 +140,16 @@ __device__ __forceinline__ void spmv2_acc(const float2* __restrict__ Y, float2 y
 
 // Rows [rb, re): the stored entries indptr[rb] .. indptr[re] are cut into
 // chunks; F holds rows rb.. (F[r - rb]).
-template <int U, int CHUNK>
+template <int U>
 __global__ void __launch_bounds__(256) k_spmv2(int64_t rb, int64_t re_rows, const int64_t* __restrict__ indptr,
                                                const int32_t* __restrict__ indices, const float* __restrict__ values,
-                                               const float2* __restrict__ Y, float2* __restrict__ F) {
+                                               const float2* __restrict__ Y, float2* __restrict__ F, int cpw) {
     const int lane = threadIdx.x & 31;
     const int64_t e_begin = __ldg(indptr + rb), e_end = __ldg(indptr + re_rows);
+    const int64_t nwarps_total = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // every warp gets exactly cpw chunks (no tail wave): chunk length from the range
+    const int64_t CHUNK = std::max<int64_t>(
+        1024, (((e_end - e_begin + nwarps_total * cpw - 1) / (nwarps_total * cpw)) + 255) & ~int64_t(255));
     const int64_t nchunks = (e_end - e_begin + CHUNK - 1) / CHUNK;
     const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -202,15 +206,51 @@ __global__ void __launch_bounds__(256) k_spmv2(int64_t rb, int64_t re_rows, cons
     }
 }
 
-static int attr_kernel_choice() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TSNET_ATTR_KERNEL");   // probe hook: v1 | v2u8 (default: v2, 4 per lane)
-        v = 2;
-        if (e && !strcmp(e, "v1")) v = 1;
-        if (e && !strcmp(e, "v2u8")) v = 8;
+// Launch configuration of the row-wise kernel.  Defaults are the measured best
+// on B200 (profiles/); TSNET_SPMV_{U,CHUNK,CTAS,L1} override them for probing.
+// Launch configuration of the row-wise kernel.  Defaults are the measured best
+// on B200 (profiles/, scripts/gpu_spmv_sweep.sh); TSNET_SPMV_{U,CPW,CTAS,L1}
+// override them for probing.
+struct SpmvCfg {
+    int kernel = 2;      // 1: legacy k_spmv, 2: k_spmv2
+    int U = 4;           // entries per lane per batch
+    int cpw = 4;         // chunks per warp
+    int ctas_per_sm = 5; // 256-thread CTAs per SM
+    int l1 = 1;          // prefer L1 over shared memory (carveout 0)
+};
+
+static int env_int(const char* name, int def) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : def;
+}
+
+static const SpmvCfg& spmv_cfg() {
+    static SpmvCfg c;
+    static bool init = false;
+    if (!init) {
+        const char* k = getenv("TSNET_ATTR_KERNEL");
+        if (k && !strcmp(k, "v1")) c.kernel = 1;
+        c.U = env_int("TSNET_SPMV_U", c.U);
+        c.cpw = std::max(1, env_int("TSNET_SPMV_CPW", c.cpw));
+        c.ctas_per_sm = std::max(1, env_int("TSNET_SPMV_CTAS", c.ctas_per_sm));
+        c.l1 = env_int("TSNET_SPMV_L1", c.l1);
+        init = true;
     }
-    return v;
+    return c;
+}
+
+template <int U>
+static cudaError_t launch_spmv2_t(const GradArgs& a, float2* F, const SpmvCfg& c, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr && c.l1) {
+        cudaFuncSetAttribute(k_spmv2<U>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+        attr = true;
+    }
+    // small problems: fewer CTAs so that chunks stay >= 1024 entries
+    const int64_t want = std::max<int64_t>(1, a.nnz / (1024 * 8 * c.cpw));
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)kNumSMs * c.ctas_per_sm));
+    k_spmv2<U><<<blocks, 256, 0, s>>>(a.rb, a.re, a.indptr, a.indices, a.values, a.Y, F, c.cpw);
+    return cudaGetLastError();
 }
 
 // a6 for the rows [rb, re) of the call into w.f_attr (local rows): the
@@ -220,20 +260,18 @@ cudaError_t launch_spmv(const Ws& w, const GradArgs& a, cudaStream_t s) {
     const int64_t nl = a.re - a.rb;
     cudaError_t e = cudaMemsetAsync(w.f_attr, 0, sizeof(float2) * (size_t)nl, s);
     if (e != cudaSuccess || a.nnz == 0 || nl == 0) return e;
-    const int kc = attr_kernel_choice();
-    if (kc == 1 && a.rb == 0 && a.re == a.n) {
+    const SpmvCfg& c = spmv_cfg();
+    if (c.kernel == 1 && a.rb == 0 && a.re == a.n) {
         const int64_t nchunks = (a.nnz + kSpmvChunk - 1) / kSpmvChunk;
         const int blocks = (int)std::min<int64_t>((nchunks + 7) / 8, (int64_t)kNumSMs * 8);
         k_spmv<<<blocks, 256, 0, s>>>(a.n, a.nnz, a.indptr, a.indices, a.values, a.Y, w.f_attr);
         return cudaGetLastError();
     }
-    constexpr int kChunk = 8192;
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((a.nnz / kChunk + 8) / 8, (int64_t)kNumSMs * 8));
-    if (kc == 8)
-        k_spmv2<8, kChunk><<<blocks, 256, 0, s>>>(a.rb, a.re, a.indptr, a.indices, a.values, a.Y, w.f_attr);
-    else
-        k_spmv2<4, kChunk><<<blocks, 256, 0, s>>>(a.rb, a.re, a.indptr, a.indices, a.values, a.Y, w.f_attr);
-    return cudaGetLastError();
+    switch (c.U) {
+        case 2: return launch_spmv2_t<2>(a, w.f_attr, c, s);
+        case 8: return launch_spmv2_t<8>(a, w.f_attr, c, s);
+        default: return launch_spmv2_t<4>(a, w.f_attr, c, s);
+    }
 }
 
 // ------------------------------------------------------------- gather (a7)
