@@ -250,32 +250,36 @@ TSNET_API int tsnet_cost(const tsnet_csr* P, const float* Y, const tsnet_grad_pa
 /*
  * The attractive SpMV (Eq. 6 first term) gathers Y_j for every
  * stored entry of P.  On graphs without locality (config 4) those gathers, not
- * HBM, bound a CSR kernel.  A plan is P re-laid out for a shared-memory-staged
- * kernel: rows [row_begin, row_end) of `shard` (all rows if NULL)
- * are cut into nnz-balanced tasks of <= 11264 rows, columns into blocks of 8192
- * points; each task's entries are stored block by block as 8-byte words
- * ((row - task row0) << 16 | col - block col0, p_ij fp32), rows ascending.
+ * HBM, bound a CSR kernel (L2 request rate).  A plan is P re-laid out for a
+ * kernel that reads Y_j from shared-memory tiles: columns in
+ * blocks of 8192 points; rows of `shard` (all rows if NULL) in mini-tasks
+ * (runs of <= 704 consecutive rows with balanced nnz + rows, or one equal
+ * piece of a long row inside every block), 16 mini-tasks per CTA group; per
+ * (group, block, warp) a contiguous segment of 8-byte words
+ * ((row - mini-task row0) << 16 | col - block col0, p_ij fp32).
  * The plan holds the values: the kernel that uses it reads no CSR array.
  *
  * tsnet_plan_query : bytes of the plan and of the build workspace for this P
- *                    and shard.  BLOCKING (reads P->indptr to cut the tasks).
+ *                    and shard.  BLOCKING (reads P->indptr to cut the rows).
  * tsnet_plan_build : writes the plan into `plan` (device, 256-byte aligned,
  *                    >= plan_bytes) using `ws` as scratch.  BLOCKING.  Set
  *                    P->plan = plan afterwards to use it.  Needs nnz of the
  *                    shard < 2^31 and n < 2^31 (TSNET_E_ARG otherwise).
- * tsnet_plan_partition : the host task cut alone (for tests): rows
- *                    [row_begin, row_end) of the HOST indptr into T = base_tasks * w
- *                    tasks (smallest w >= 1 that respects rows_max), written to
- *                    task_row0 / task_rows (capacity max_tasks).  Returns T, or
- *                    -1 on bad arguments / overflow.  [host, pure]
+ * tsnet_plan_partition : the host cut alone (for tests): rows
+ *                    [row_begin, row_end) of the HOST indptr into warps * G
+ *                    mini-tasks (G = base_groups * k, smallest k that fits;
+ *                    capacity max_minitasks).  Per row q: row_mt[q] = its first
+ *                    mini-task, row_K[q] = pieces (1 = not split); per mini-task
+ *                    t: mt_r0[t] = first row, mt_info[t] = rows (>= 0) or -1 for
+ *                    a piece.  Returns G, or -1.  [host, pure]
  */
 TSNET_API int tsnet_plan_query(const tsnet_csr* P, const tsnet_shard* shard, size_t* plan_bytes, size_t* ws_bytes,
                                tsnet_stream_t stream);
 TSNET_API int tsnet_plan_build(const tsnet_csr* P, const tsnet_shard* shard, void* plan, size_t plan_bytes, void* ws,
                                size_t ws_bytes, tsnet_stream_t stream);
 TSNET_API int32_t tsnet_plan_partition(const int64_t* indptr_host, int64_t row_begin, int64_t row_end,
-                                       int32_t rows_max, int32_t base_tasks, int32_t max_tasks, int64_t* task_row0,
-                                       int32_t* task_rows);
+                                       int32_t warps, int32_t rows_max, int32_t base_groups, int64_t max_minitasks,
+                                       int32_t* row_mt, int32_t* row_K, int32_t* mt_r0, int32_t* mt_info);
 
 /* ------------------------------------------------------------- multi-GPU (§8(e)) */
 

@@ -2,28 +2,33 @@
 // PAPER.md:162): F_attr,i = sum_{j in row i} p_ij w_ij (X_i - X_j).
 //
 // Why a second layout of P: on the power-law graph of config 4
-// the CSR kernel (iterate.cu k_spmv) is bound by the L1TEX->L2 request path,
-// not by HBM -- every Y[j] gather is its own 32-B sector request (ncu r1a:
-// 2.75e8 L2 read sectors per launch against 5.2e7 for the CSR stream, 23% of
-// DRAM peak).  Here Y is read from shared memory instead:
+// every CSR kernel is bound by the L2 request rate of the random Y[j] gathers
+// (one 32-B sector request per stored entry; ncu: l1tex2xbar request cycles
+// ~80%, DRAM ~25%).  Here Y is read from shared memory instead:
 //
-//   * rows are cut into T tasks (contiguous row ranges, nnz-balanced, at most
-//     kCbRowsMax rows), one persistent CTA per SM walks its tasks;
-//   * columns are cut into blocks of kCbCols points; a task's entries are
-//     stored block by block ("segments"), each entry 8 bytes:
-//       word0 = (row - task_row0) << 16 | (col - block_col0),  word1 = p_ij (fp32 bits),
-//     rows ascending inside a segment, segments padded to an even length;
-//   * a producer warp streams the Y slice of each non-empty block into a
-//     double-buffered shared-memory tile with cp.async.bulk (TMA bulk copy,
-//     mbarrier completion) while the consumer warps stream the segment's
-//     entries from HBM (coalesced 16-B loads, L2 evict-first), gather Y_j from
-//     shared memory, and reduce runs of equal rows with a warp segmented scan
-//     into a per-task shared-memory accumulator F_s (fp32 shared atomics at run
-//     ends only);
-//   * at the end of a task F_s is written to F with plain stores (no global
-//     atomics, no memset of F).
-// HBM bytes per launch: 8 per stored entry (+ padding) + 8 per (task, block)
-// segment offset + 8 per row written; Y slices come from L2.
+//   * columns are cut into blocks of kCbCols points; a producer warp streams
+//     the Y slice of each block into a double-buffered shared tile with
+//     cp.async.bulk (TMA bulk copy, mbarrier completion);
+//   * rows are cut into mini-tasks: runs of consecutive rows (at most kCbRows
+//     rows, balanced nnz + rows), except that a long row (> cap entries) is
+//     split into K mini-tasks of one "piece" each -- piece k takes the k-th
+//     K-th of the row's entries inside EVERY block, so hub rows spread evenly
+//     over warps and blocks; kCbW mini-tasks form a group, processed by one
+//     CTA, one mini-task per consumer warp;
+//   * a warp accumulates its mini-task's rows in its own slice of shared
+//     memory (F_s), so nothing is shared between warps: no atomics and no
+//     barriers in the hot loop -- warps only meet at the Y-tile pipeline;
+//   * per (group, block, warp) the entries are a contiguous segment of 8-byte
+//     words ((row - mini-task row0) << 16 | col - block_col0, p_ij fp32 bits),
+//     rows ascending, padded to an even length; a warp streams its segment in
+//     sweeps of 128 entries (16-byte loads, two sweeps ahead, L2 evict-first),
+//     gathers Y_j from the tile and Y_i (one sweep ahead) from L2, reduces runs
+//     of equal rows in registers (hand-down between lanes, segmented scan when
+//     a run covers whole lanes) and adds run sums into F_s;
+//   * at the end of a group each warp writes its rows of F (plain stores; the
+//     pieces of split rows add with vector atomics into F, zeroed before).
+// HBM bytes per launch: 8 per stored entry (+ padding) + 8 per (group, block,
+// warp) segment offset + 8 per row of F; Y tiles come from L2.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -36,78 +41,114 @@
 namespace tsnet {
 
 constexpr int kCbCols = 8192;       // points per column block (2 x 64 KB shared tiles)
-constexpr int kCbRowsMax = 11264;   // rows per task (88 KB shared accumulator)
-constexpr int kCbWarpsDefault = 24;   // consumer warps per CTA (+1 producer warp); env TSNET_CB_WARPS
+constexpr int kCbW = 16;            // consumer warps per CTA = mini-tasks per group (+1 producer warp)
+constexpr int kCbRows = 704;        // rows per mini-task (16 x 704 x 8 B = 88 KB of F_s)
 constexpr uint32_t kCbSentinel = 0xFFFFu;
-constexpr uint64_t kCbMagic = 0x4243544e53545354ull;  // "TSTSNTCB"
+constexpr uint64_t kCbMagic = 0x3456434e53545354ull;  // "TSTSNCV4"
 
 struct CbHeader {
     uint64_t magic;
     int64_t n, row_begin, row_end, nnz, entries;
-    int32_t T, NB, C, rows_max;
-    int64_t off_row0, off_rows, off_seg, off_entries, bytes;
+    int32_t G, NB, C, W, rows_max, pad;
+    int64_t off_seg, off_mt, off_entries, bytes;
 };
 
 static size_t cb_align(size_t x) { return (x + 255) / 256 * 256; }
 
-static CbHeader cb_layout(int64_t n, int64_t rb, int64_t re, int64_t nnz, int32_t T) {
+static CbHeader cb_layout(int64_t n, int64_t rb, int64_t re, int64_t nnz, int32_t G) {
     CbHeader h{};
     h.magic = kCbMagic;
     h.n = n;
     h.row_begin = rb;
     h.row_end = re;
     h.nnz = nnz;
-    h.T = T;
+    h.G = G;
     h.C = kCbCols;
+    h.W = kCbW;
+    h.rows_max = kCbRows;
     h.NB = (int32_t)((n + kCbCols - 1) / kCbCols);
-    h.rows_max = kCbRowsMax;
-    const int64_t nseg = (int64_t)T * h.NB;
+    const int64_t nseg = (int64_t)G * h.NB * kCbW;
     h.entries = nnz + nseg;   // upper bound with padding
     size_t off = cb_align(sizeof(CbHeader));
-    h.off_row0 = (int64_t)off;
-    off = cb_align(off + sizeof(int64_t) * (size_t)T);
-    h.off_rows = (int64_t)off;
-    off = cb_align(off + sizeof(int32_t) * (size_t)T);
     h.off_seg = (int64_t)off;
     off = cb_align(off + sizeof(int64_t) * (size_t)(nseg + 1));
+    h.off_mt = (int64_t)off;
+    off = cb_align(off + sizeof(int2) * (size_t)((int64_t)G * kCbW));
     h.off_entries = (int64_t)off;
     off = cb_align(off + sizeof(uint2) * (size_t)h.entries);
     h.bytes = (int64_t)off;
     return h;
 }
 
-// Host partition of rows [rb, re) into tasks: T = 148 w (w = 1, 2, ...) tasks,
-// balanced on nnz + rows (greedy cut at multiples of (nnz + rows)/T) with at
-// most rows_max rows each.
-// ipr[q] = indptr[rb + q], q = 0 .. re - rb.
-static int32_t cb_partition(const int64_t* ipr, int64_t rb, int64_t re, int32_t rows_max, int32_t base,
-                            std::vector<int64_t>& row0, std::vector<int32_t>& rows) {
-    const int64_t nr = re - rb;
+// Host cut (pure).  ipr[q] = indptr[rb + q], q = 0 .. nr.  A row of L > cap
+// entries (cap = max(256, nnz / (base W) / 2)) is split into K = ceil(L / cap)
+// one-piece mini-tasks; the other rows form runs of consecutive rows (<=
+// rows_max each) with boundaries at multiples of their mean weight (entries +
+// rows); T = W G mini-tasks in row order, G = base k for the smallest k that
+// fits, padded with empty mini-tasks.  Output:
+//   row_mt[q]: first mini-task of row q; row_K[q]: its pieces (1 = not split);
+//   mt_r0[t]: first row of mini-task t; mt_info[t]: its rows (>= 0), or -1 for
+//   a piece.  Returns G, or -1.
+static int32_t cb_partition(const int64_t* ipr, int64_t nr, int32_t W, int32_t rows_max, int32_t base,
+                            std::vector<int32_t>& row_mt, std::vector<int32_t>& row_K, std::vector<int32_t>& mt_r0,
+                            std::vector<int32_t>& mt_info) {
     const int64_t nnz = ipr[nr] - ipr[0];
-    if (nr <= 0) {
-        row0.assign(1, rb);
-        rows.assign(1, 0);
-        return 1;
-    }
-    // enough tasks for the row cap, whatever the nnz balance asks
-    const int64_t wmax = 2 + (nr + (int64_t)rows_max * base - 1) / ((int64_t)rows_max * base);
-    for (int64_t w = 1; w <= wmax; ++w) {
-        const int64_t T = (int64_t)base * w;
-        row0.clear();
-        rows.clear();
-        int64_t r = rb;
-        for (int64_t t = 0; t < T; ++t) {
-            // balance nnz + rows (empty rows weigh 1); the last task takes every
-            // remaining row (trailing empty rows included)
-            const int64_t target = (t == T - 1) ? INT64_MAX : ((nnz + nr) * (t + 1) + T - 1) / T;
-            int64_t r1 = r;
-            // extend while the weight before the next row is below the target and the cap allows
-            while (r1 < re && (ipr[r1 - rb] - ipr[0]) + (r1 - rb) < target && r1 - r < rows_max) ++r1;
-            row0.push_back(r);
-            rows.push_back((int32_t)(r1 - r));
-            r = r1;
+    const int64_t cap = std::max<int64_t>(256, nnz / ((int64_t)base * W) / 2);
+    row_mt.assign(nr, 0);
+    row_K.assign(nr, 1);
+    int64_t pieces = 0, nsplit = 0;
+    double wrows = 0.0;
+    for (int64_t q = 0; q < nr; ++q) {
+        const int64_t L = ipr[q + 1] - ipr[q];
+        if (L > cap) {
+            row_K[q] = (int32_t)((L + cap - 1) / cap);
+            pieces += row_K[q];
+            ++nsplit;
+        } else {
+            wrows += (double)L + 1.0;
         }
-        if (r == re && T <= INT32_MAX) return (int32_t)T;
+    }
+    const int64_t kmax = 2 + (nr + (int64_t)rows_max * W * base - 1) / ((int64_t)rows_max * W * base) +
+                         (pieces + nsplit + (int64_t)W * base - 1) / ((int64_t)W * base);
+    for (int64_t k = 1; k <= kmax; ++k) {
+        const int64_t G = (int64_t)base * k, T = G * W;
+        if (G > INT32_MAX / W) break;
+        const int64_t T_rows = T - pieces - nsplit;   // a split may close a run early: reserve one each
+        if (T_rows < 1) continue;
+        const double target = wrows / (double)T_rows;
+        mt_r0.clear();
+        mt_info.clear();
+        double acc = 0.0;
+        int64_t open = -1, runs = 0;   // index of the open run in mt_*
+        for (int64_t q = 0; q < nr; ++q) {
+            const int64_t L = ipr[q + 1] - ipr[q];
+            if (row_K[q] > 1) {
+                open = -1;
+                row_mt[q] = (int32_t)mt_r0.size();
+                for (int32_t p = 0; p < row_K[q]; ++p) {
+                    mt_r0.push_back((int32_t)q);
+                    mt_info.push_back(-1);
+                }
+                continue;
+            }
+            // close the open run at multiples of the target, or when full
+            if (open >= 0 && (mt_info[open] >= rows_max || acc >= target * (double)runs)) open = -1;
+            if (open < 0) {
+                open = (int64_t)mt_r0.size();
+                mt_r0.push_back((int32_t)q);
+                mt_info.push_back(0);
+                ++runs;
+            }
+            mt_info[open] += 1;
+            row_mt[q] = (int32_t)open;
+            acc += (double)L + 1.0;
+        }
+        if ((int64_t)mt_r0.size() > T) continue;
+        while ((int64_t)mt_r0.size() < T) {   // empty mini-tasks
+            mt_r0.push_back(0);
+            mt_info.push_back(0);
+        }
+        return (int32_t)G;
     }
     return -1;
 }
@@ -156,9 +197,6 @@ __device__ __forceinline__ uint4 ld_stream_v4(const uint4* a, uint64_t pol) {
                  : "l"(a), "l"(pol));
     return v;
 }
-__device__ __forceinline__ void named_bar(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
 
 // ------------------------------------------------------------------ kernel
 // One entry: contribution p w (X_i - X_j) with w = 1 / (1 + r^2).  Padding
@@ -172,6 +210,22 @@ __device__ __forceinline__ float2 cb_term(float2 yi, float2 yj, float p) {
     return make_float2(pw * dx, pw * dy);
 }
 
+// Y_i of the lane's four entries (issued one sweep ahead): row = row0 + key
+// (a piece mini-task has the single row row0: key 0);
+// sentinel keys read row0 and are multiplied by p = 0.
+struct CbYi {
+    float2 y[4];
+};
+__device__ __forceinline__ CbYi cb_yi(uint4 a, uint4 b, const float2* __restrict__ Yr0) {
+    // four independent loads (repeated rows hit L1): selecting between a loaded
+    // value and another load would make the issue wait for the first one
+    const uint32_t k[4] = {a.x >> 16, a.z >> 16, b.x >> 16, b.z >> 16};
+    CbYi r;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) r.y[q] = __ldg(Yr0 + (k[q] == kCbSentinel ? 0u : k[q]));
+    return r;
+}
+
 __device__ __forceinline__ void fs_add(float2* Fs, uint32_t k, float x, float y) {
     float2 v = Fs[k];
     v.x += x;
@@ -179,43 +233,13 @@ __device__ __forceinline__ void fs_add(float2* Fs, uint32_t k, float x, float y)
     Fs[k] = v;
 }
 
-// Run-end update of F_s.  Inside one block segment a row is shared between
-// warps only at the two ends of a warp's share (keys kf, kl): those runs go to
-// the warp's private slots edge[0..1] and are folded into F_s with shared
-// atomics once per share; every other row of the share is owned by this warp
-// for the block -> plain read-modify-write (one emit per key per sweep; sweeps
-// of a warp are ordered by __syncwarp; blocks are separated by a barrier).
-__device__ __forceinline__ void cb_emit(bool on, uint32_t k, float x, float y, float2* Fs, float2* edge, uint32_t kf,
-                                        uint32_t kl) {
-    float2* dst = (k == kf) ? edge : ((k == kl) ? edge + 1 : Fs + k);
-    if (on) {
-        float2 v = *dst;
-        v.x += x;
-        v.y += y;
-        *dst = v;
-    }
-}
-
 // One sweep: lane holds entries 4 lane .. 4 lane + 3 of 128 consecutive entries
-// of the segment (keys = local rows, non-decreasing; masked entries carry the
-// sentinel key and p = 0 and sit at the end).
-// Y_i of the lane's four entries (issued one sweep ahead; one load per
-// distinct row of the lane, sentinel keys read row 0 and are multiplied by p = 0)
-struct CbYi {
-    float2 y[4];
-};
-__device__ __forceinline__ CbYi cb_yi(uint4 a, uint4 b, const float2* __restrict__ Yrow) {
-    const uint32_t k0 = a.x >> 16, k1 = a.z >> 16, k2 = b.x >> 16, k3 = b.z >> 16;
-    CbYi r;
-    r.y[0] = __ldg(Yrow + (k0 == kCbSentinel ? 0u : k0));
-    r.y[1] = (k1 == k0) ? r.y[0] : __ldg(Yrow + (k1 == kCbSentinel ? 0u : k1));
-    r.y[2] = (k2 == k1) ? r.y[1] : __ldg(Yrow + (k2 == kCbSentinel ? 0u : k2));
-    r.y[3] = (k3 == k2) ? r.y[2] : __ldg(Yrow + (k3 == kCbSentinel ? 0u : k3));
-    return r;
-}
-
+// of the warp's segment (keys = local rows, non-decreasing; masked entries
+// carry the sentinel key and p = 0 and sit at the end).  Run sums are added to
+// the warp's own F_s slice (one add per key per sweep; sweeps of a warp are
+// ordered by __syncwarp).
 __device__ __forceinline__ void cb_sweep(uint4 a, uint4 b, const CbYi& yi, const float2* __restrict__ Ys,
-                                         float2* Fs, int lane, float2* edge, uint32_t kf, uint32_t kl) {
+                                         float2* Fs, int lane) {
     const uint32_t wd[4] = {a.x, a.z, b.x, b.z};
     const float pv[4] = {__uint_as_float(a.y), __uint_as_float(a.w), __uint_as_float(b.y), __uint_as_float(b.w)};
     uint32_t k[4];
@@ -225,11 +249,10 @@ __device__ __forceinline__ void cb_sweep(uint4 a, uint4 b, const CbYi& yi, const
         k[q] = wd[q] >> 16;
         yj[q] = Ys[wd[q] & 0xFFFFu];
     }
-    const bool mid1 = k[1] != k[0] && k[1] != k[3], mid2 = k[2] != k[0] && k[2] != k[3];
     float2 f[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) f[q] = cb_term(yi.y[q], yj[q], pv[q]);
-    // lane runs: tail (key k3), head (key k0 if != k3), middles (rare)
+    // lane runs: head (key k0, if != k3), middles (keys strictly between), tail (key k3)
     const uint32_t tk = k[3];
     float tx = f[3].x, ty = f[3].y;
     float hx = 0.f, hy = 0.f;
@@ -242,34 +265,16 @@ __device__ __forceinline__ void cb_sweep(uint4 a, uint4 b, const CbYi& yi, const
         hy += (h && !t) ? f[q].y : 0.f;
     }
     const bool has_head = k[0] != tk;
-    // middle runs: keys k1 / k2 different from both ends (a row with <= 2 entries
-    // inside this lane); they are complete here
-    if (__any_sync(0xffffffffu, mid1 || mid2)) {
-        float m1x = 0.f, m1y = 0.f, m2x = 0.f, m2y = 0.f;
-        if (mid1) {
-            m1x = f[1].x;
-            m1y = f[1].y;
-            if (k[2] == k[1]) {
-                m1x += f[2].x;
-                m1y += f[2].y;
-            }
-        }
-        const bool m2 = mid2 && k[2] != k[1];
-        if (m2) {
-            m2x = f[2].x;
-            m2y = f[2].y;
-        }
-        cb_emit(mid1, k[1], m1x, m1y, Fs, edge, kf, kl);
-        cb_emit(m2, k[2], m2x, m2y, Fs, edge, kf, kl);
-    }
-    // join the lane runs across lanes.  Usually a run spans at most two lanes
-    // (the tail of lane l continues as the head of lane l+1): one hand-down.  When
-    // some run covers a whole lane (rows with many entries in this block), a
-    // segmented inclusive scan of the tails does the general case.
+    const bool mid1 = k[1] != k[0] && k[1] != tk;
+    const bool mid2 = k[2] != k[0] && k[2] != tk && k[2] != k[1];
+    if (mid1) fs_add(Fs, k[1], f[1].x + (k[2] == k[1] ? f[2].x : 0.f), f[1].y + (k[2] == k[1] ? f[2].y : 0.f));
+    if (mid2) fs_add(Fs, k[2], f[2].x, f[2].y);
+    // join runs across lanes: a tail continuing as the next lane's head is handed
+    // down; a run covering whole lanes needs the segmented scan
     const uint32_t pk = __shfl_up_sync(0xffffffffu, tk, 1);
     const uint32_t nk = __shfl_down_sync(0xffffffffu, tk, 1);
     float sx = tx, sy = ty;
-    const bool through = lane > 0 && !has_head && tk == pk;   // whole lane continues the previous run
+    const bool through = lane > 0 && !has_head && tk == pk;
     if (__any_sync(0xffffffffu, through)) {
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -282,50 +287,47 @@ __device__ __forceinline__ void cb_sweep(uint4 a, uint4 b, const CbYi& yi, const
         }
     }
     const bool last = (lane == 31) || (nk != tk);
-    // a head run continues the previous lane's tail run (hand it down), or stands alone
     const bool give = has_head && lane > 0 && k[0] == pk;
     const float gx = __shfl_down_sync(0xffffffffu, give ? hx : 0.f, 1);
     const float gy = __shfl_down_sync(0xffffffffu, give ? hy : 0.f, 1);
-    const bool gv = lane < 31;
-    cb_emit(has_head && !give && k[0] != kCbSentinel, k[0], hx, hy, Fs, edge, kf, kl);
-    // without the scan, a tail that continues into the next lane is not "last"
-    // there, so only run ends emit: sum = own tail (+ scanned prefix) + next head
-    cb_emit(last && tk != kCbSentinel, tk, sx + (gv ? gx : 0.f), sy + (gv ? gy : 0.f), Fs, edge, kf, kl);
+    if (has_head && !give) fs_add(Fs, k[0], hx, hy);
+    if (last && tk != kCbSentinel) fs_add(Fs, tk, sx + (lane < 31 ? gx : 0.f), sy + (lane < 31 ? gy : 0.f));
 }
 
-template <int kCbWarps>
-__global__ void __launch_bounds__((kCbWarps + 1) * 32, 1) k_attr_cb(const uint8_t* __restrict__ plan, const float2* __restrict__ Y,
-                                                           float2* __restrict__ F, int y_aligned) {
+__global__ void __launch_bounds__((kCbW + 1) * 32, 1) k_attr_cb(const uint8_t* __restrict__ plan,
+                                                                const float2* __restrict__ Y,
+                                                                float2* __restrict__ F, int y_aligned) {
     extern __shared__ __align__(128) uint8_t cb_smem[];
     float2* Ys0 = reinterpret_cast<float2*>(cb_smem);
     float2* Ys1 = Ys0 + kCbCols;
-    float* Fs = reinterpret_cast<float*>(Ys1 + kCbCols);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(Fs + 2 * kCbRowsMax);   // full[2], empty[2]
+    float2* Fs_all = Ys1 + kCbCols;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Fs_all + kCbW * kCbRows);   // full[2], empty[2]
     const CbHeader* h = reinterpret_cast<const CbHeader*>(plan);
-    const int T = h->T, NB = h->NB;
+    const int G = h->G, NB = h->NB;
     const int64_t n = h->n, rb = h->row_begin;
-    const int64_t* row0s = reinterpret_cast<const int64_t*>(plan + h->off_row0);
-    const int32_t* rowss = reinterpret_cast<const int32_t*>(plan + h->off_rows);
     const int64_t* seg = reinterpret_cast<const int64_t*>(plan + h->off_seg);
+    const int2* mt_desc = reinterpret_cast<const int2*>(plan + h->off_mt);   // (row0 - rb, rows | -1 piece)
     const uint4* ent = reinterpret_cast<const uint4*>(plan + h->off_entries);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
-        mbar_init(&bars[2], kCbWarps);
-        mbar_init(&bars[3], kCbWarps);
+        mbar_init(&bars[2], kCbW);
+        mbar_init(&bars[3], kCbW);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    // blocks any mini-task of group g needs: the group's block-J segments are contiguous
+    auto group_block_used = [&](const int64_t* og, int J) { return og[(int64_t)J * kCbW] < og[(int64_t)(J + 1) * kCbW]; };
 
-    if (warp == kCbWarps) {
-        // ---------------- producer: Y slices of the non-empty blocks, in order
+    if (warp == kCbW) {
+        // ---------------- producer: Y slices of the blocks the group uses, in order
         uint32_t k = 0;
-        for (int t = blockIdx.x; t < T; t += gridDim.x) {
-            const int64_t* sg = seg + (int64_t)t * NB;
+        for (int g = blockIdx.x; g < G; g += gridDim.x) {
+            const int64_t* og = seg + (int64_t)g * NB * kCbW;
             for (int J = 0; J < NB; ++J) {
-                if (sg[J] == sg[J + 1]) continue;
+                if (!group_block_used(og, J)) continue;
                 const int b = k & 1;
                 float2* dst = b ? Ys1 : Ys0;
                 if (k >= 2) mbar_wait(&bars[2 + b], ((k >> 1) - 1) & 1);
@@ -351,112 +353,106 @@ __global__ void __launch_bounds__((kCbWarps + 1) * 32, 1) k_attr_cb(const uint8_
         return;
     }
 
-    // ---------------- consumers
+    // ---------------- consumer warp: mini-task g * W + warp of every group g
     const uint64_t pol = cb_policy_evict_first();
-    const int nthr = kCbWarps * 32;
-    float2* F2s = reinterpret_cast<float2*>(Fs);
-    float2* edge = reinterpret_cast<float2*>(bars + 4) + 2 * warp;   // this warp's two boundary slots
-    if (lane < 2) edge[lane] = make_float2(0.f, 0.f);
-    __syncwarp();
+    float2* Fs = Fs_all + warp * kCbRows;
+    const uint4 pad = make_uint4(kCbSentinel << 16, 0u, kCbSentinel << 16, 0u);
+    const int l2 = 2 * lane;
     uint32_t k = 0;
-    for (int t = blockIdx.x; t < T; t += gridDim.x) {
-        const int64_t row0 = row0s[t];
-        const int rows = rowss[t];
-        const float2* Yrow = Y + row0;
-        for (int q = threadIdx.x; q < 2 * rows; q += nthr) Fs[q] = 0.f;
-        named_bar(1, nthr);
-        const int64_t* sg = seg + (int64_t)t * NB;
-        const uint4 pad = make_uint4(kCbSentinel << 16, 0u, kCbSentinel << 16, 0u);
-        const int l2 = 2 * lane;
-        // this warp's share of block J's segment, in pairs of entries (16 B), and the
-        // keys of its first and last entries (rows possibly shared with neighbours)
-        // kf / kl come back as the raw words; the >> 16 happens after the Ys wait so
-        // the loads' latency hides behind the barrier instead of stalling here
-        auto share = [&](int J, const uint4*& sp, int& npw, uint32_t& kf, uint32_t& kl) {
-            const int64_t s0 = sg[J], s1 = sg[J + 1];
-            const int np = (int)((s1 - s0) >> 1);
-            const int per = (np + kCbWarps - 1) / kCbWarps;
-            const int q0 = min(np, per * warp);
-            npw = min(np, per * (warp + 1)) - q0;
-            sp = ent + (s0 >> 1) + q0;
-            kf = kl = kCbSentinel << 16;
-            if (npw > 0) {
-                kf = __ldg(reinterpret_cast<const uint32_t*>(sp));
-                kl = __ldg(reinterpret_cast<const uint32_t*>(sp + npw - 1) + 2);
-            }
-        };
+    for (int g = blockIdx.x; g < G; g += gridDim.x) {
+        const int2 md = mt_desc[(int64_t)g * kCbW + warp];
+        const bool piece = md.y < 0;
+        const int nu = piece ? 1 : md.y;
+        const float2* Yr0 = Y + rb + md.x;
+        for (int q = lane; q < nu; q += 32) Fs[q] = make_float2(0.f, 0.f);
+        __syncwarp();
+        const int64_t* og = seg + (int64_t)g * NB * kCbW;
         auto next_block = [&](int J) {
-            while (J < NB && sg[J] == sg[J + 1]) ++J;
+            while (J < NB && !group_block_used(og, J)) ++J;
             return J;
         };
-        // prologue of the first block; later blocks are prefetched during the previous one
-        int J = next_block(0);
+        auto my_seg = [&](int J, const uint4*& sp, int& np) {
+            const int64_t s0 = og[(int64_t)J * kCbW + warp], s1 = og[(int64_t)J * kCbW + warp + 1];
+            sp = ent + (s0 >> 1);
+            np = (int)((s1 - s0) >> 1);
+        };
+        // Software pipeline over sweeps with four register sets rotated by
+        // unrolling (no register moves: a move of a value still in flight would
+        // wait for it): entries are loaded three sweeps ahead, Y_i one sweep
+        // ahead (two sweeps after its entries were issued).
+        struct Set {
+            uint4 a, c;
+            CbYi y;
+        };
+        Set S0, S1, S2, S3;
         const uint4* sp = ent;
-        int npw = 0;
-        uint32_t kfw = kCbSentinel << 16, klw = kCbSentinel << 16;   // raw first / last words of the share
-        uint4 a0 = pad, c0 = pad, a1 = pad, c1 = pad;
+        int np = 0;
+        auto load_e = [&](int sw, Set& S) {
+            const int o = sw * 64 + l2;
+            S.a = o < np ? ld_stream_v4(sp + o, pol) : pad;
+            S.c = o + 1 < np ? ld_stream_v4(sp + o + 1, pol) : pad;
+        };
+        auto load_y = [&](Set& S) { S.y = cb_yi(S.a, S.c, Yr0); };
+        int J = next_block(0);
         if (J < NB) {
-            share(J, sp, npw, kfw, klw);
-            if (l2 < npw) a0 = ld_stream_v4(sp + l2, pol);
-            if (l2 + 1 < npw) c0 = ld_stream_v4(sp + l2 + 1, pol);
-            if (l2 + 64 < npw) a1 = ld_stream_v4(sp + l2 + 64, pol);
-            if (l2 + 65 < npw) c1 = ld_stream_v4(sp + l2 + 65, pol);
+            my_seg(J, sp, np);
+            load_e(0, S0);
+            load_e(1, S1);
+            load_e(2, S2);
         }
         while (J < NB) {
             const int b = k & 1;
             const float2* Ys = b ? Ys1 : Ys0;
+            const int nsw = (np + 63) >> 6;
+            if (nsw > 0) load_y(S0);
             mbar_wait(&bars[b], (k >> 1) & 1);
-            const uint32_t kf = kfw >> 16, kl = klw >> 16;
-            CbYi y0 = cb_yi(a0, c0, Yrow);
-            const int nsw = (npw + 63) >> 6;
 #pragma unroll 1
-            for (int sw = 0; sw < nsw; ++sw) {
-                const int o = (sw + 2) * 64 + l2;
-                const uint4 a2 = o < npw ? ld_stream_v4(sp + o, pol) : pad;
-                const uint4 c2 = o + 1 < npw ? ld_stream_v4(sp + o + 1, pol) : pad;
-                const CbYi y1 = cb_yi(a1, c1, Yrow);   // rows of the next sweep, one sweep ahead
-                cb_sweep(a0, c0, y0, Ys, F2s, lane, edge, kf, kl);
+            for (int sw = 0; sw < nsw; sw += 4) {
+                load_e(sw + 3, S3);
+                if (sw + 1 < nsw) load_y(S1);
+                cb_sweep(S0.a, S0.c, S0.y, Ys, Fs, lane);
                 __syncwarp();
-                a0 = a1;
-                c0 = c1;
-                a1 = a2;
-                c1 = c2;
-                y0 = y1;
-            }
-            if (lane == 0) mbar_arrive(&bars[2 + b]);
-            if (lane < 4) {   // fold the two boundary rows: one shared atomic per lane
-                const uint32_t ke = (lane < 2) ? kf : kl;
-                const bool ok = ke != kCbSentinel && (lane < 2 || kl != kf);
-                float* e = reinterpret_cast<float*>(edge) + lane;
-                if (ok) atomicAdd(Fs + 2 * ke + (lane & 1), *e);
-                *e = 0.f;
+                if (sw + 1 >= nsw) break;
+                load_e(sw + 4, S0);
+                if (sw + 2 < nsw) load_y(S2);
+                cb_sweep(S1.a, S1.c, S1.y, Ys, Fs, lane);
+                __syncwarp();
+                if (sw + 2 >= nsw) break;
+                load_e(sw + 5, S1);
+                if (sw + 3 < nsw) load_y(S3);
+                cb_sweep(S2.a, S2.c, S2.y, Ys, Fs, lane);
+                __syncwarp();
+                if (sw + 3 >= nsw) break;
+                load_e(sw + 6, S2);
+                if (sw + 4 < nsw) load_y(S0);
+                cb_sweep(S3.a, S3.c, S3.y, Ys, Fs, lane);
+                __syncwarp();
             }
             __syncwarp();
+            if (lane == 0) mbar_arrive(&bars[2 + b]);
             ++k;
-            // prefetch the next block's first two sweeps before the barrier
+            // prefetch this warp's segment of the next block the group uses
             J = next_block(J + 1);
-            a0 = c0 = a1 = c1 = pad;
             if (J < NB) {
-                share(J, sp, npw, kfw, klw);
-                if (l2 < npw) a0 = ld_stream_v4(sp + l2, pol);
-                if (l2 + 1 < npw) c0 = ld_stream_v4(sp + l2 + 1, pol);
-                if (l2 + 64 < npw) a1 = ld_stream_v4(sp + l2 + 64, pol);
-                if (l2 + 65 < npw) c1 = ld_stream_v4(sp + l2 + 65, pol);
+                my_seg(J, sp, np);
+                load_e(0, S0);
+                load_e(1, S1);
+                load_e(2, S2);
             }
-            named_bar(1, nthr);   // rows owned by one warp in this block may be shared in the next
         }
-        named_bar(1, nthr);
-        float2* Fo = F + (row0 - rb);
-        const float2* Fs2 = reinterpret_cast<const float2*>(Fs);
-        for (int q = threadIdx.x; q < rows; q += nthr) Fo[q] = Fs2[q];
-        named_bar(1, nthr);
+        __syncwarp();
+        // rows of F: whole rows stored, pieces of split rows added (F zeroed before)
+        if (piece) {
+            if (lane == 0) atomicAdd(F + md.x, Fs[0]);
+        } else {
+            for (int q = lane; q < nu; q += 32) F[md.x + q] = Fs[q];
+        }
+        __syncwarp();
     }
 }
 
-constexpr int kCbWarpsMax = 31;
 size_t cb_smem_bytes() {
-    return sizeof(float2) * 2 * kCbCols + sizeof(float) * 2 * kCbRowsMax + 4 * sizeof(uint64_t) +
-           sizeof(float2) * 2 * kCbWarpsMax;
+    return sizeof(float2) * (2 * kCbCols + kCbW * kCbRows) + 4 * sizeof(uint64_t);
 }
 
 static int num_sms() {
@@ -469,63 +465,54 @@ static int num_sms() {
     return sms;
 }
 
-template <int W>
-static cudaError_t launch_cb_w(const void* plan, const float2* Y, float2* F, cudaStream_t s) {
+// F: rows [row_begin, row_end) of the plan's shard (nl = row_end - row_begin)
+cudaError_t launch_attr_cb(const void* plan, const float2* Y, float2* F, int64_t nl, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_attr_cb<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k_attr_cb, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)cb_smem_bytes());
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
+    cudaError_t e = cudaMemsetAsync(F, 0, sizeof(float2) * (size_t)nl, s);   // split rows accumulate
+    if (e != cudaSuccess) return e;
     const int aligned = ((uintptr_t)Y % 16) == 0;
-    k_attr_cb<W><<<num_sms(), (W + 1) * 32, cb_smem_bytes(), s>>>(reinterpret_cast<const uint8_t*>(plan), Y, F,
+    k_attr_cb<<<num_sms(), (kCbW + 1) * 32, cb_smem_bytes(), s>>>(reinterpret_cast<const uint8_t*>(plan), Y, F,
                                                                   aligned);
     return cudaGetLastError();
 }
 
-static int cb_warps() {
-    static int w = 0;
-    if (w == 0) {
-        const char* e = getenv("TSNET_CB_WARPS");
-        w = e ? atoi(e) : kCbWarpsDefault;
-        if (w != 8 && w != 12 && w != 16 && w != 24) w = kCbWarpsDefault;
-    }
-    return w;
-}
-
-cudaError_t launch_attr_cb(const void* plan, const float2* Y, float2* F, cudaStream_t s) {
-    switch (cb_warps()) {
-        case 8: return launch_cb_w<8>(plan, Y, F, s);
-        case 12: return launch_cb_w<12>(plan, Y, F, s);
-        case 16: return launch_cb_w<16>(plan, Y, F, s);
-        default: return launch_cb_w<24>(plan, Y, F, s);
-    }
-}
-
 // ------------------------------------------------------------------ plan build
-// Sort keys: (task, block) of every entry of the shard; payload: the packed
-// 8-byte entry.  A stable LSD radix sort keeps the CSR (row, col) order inside
-// each segment.
-__global__ void k_cb_row_task(const int64_t* row0, const int32_t* rows, int T, int64_t rb, int32_t* row_task) {
-    for (int t = blockIdx.x; t < T; t += gridDim.x)
-        for (int q = threadIdx.x; q < rows[t]; q += blockDim.x) row_task[row0[t] - rb + q] = t;
-}
-
+// Sort keys: (group, block, warp) of every entry of the shard; payload: the
+// packed 8-byte entry.  A stable LSD radix sort keeps the CSR (row, col)
+// order, i.e. rows ascending, inside each segment.
 __global__ void k_cb_keys(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                          const float* __restrict__ values, int64_t rb, int64_t re, const int64_t* __restrict__ row0,
-                          const int32_t* __restrict__ row_task, int NB, uint32_t* __restrict__ keys,
-                          unsigned long long* __restrict__ vals) {
+                          const float* __restrict__ values, int64_t rb, int64_t re, const int32_t* __restrict__ row_mt,
+                          const int32_t* __restrict__ row_K, const int2* __restrict__ mt_desc, int NB,
+                          uint32_t* __restrict__ keys, unsigned long long* __restrict__ vals) {
     const int lane = threadIdx.x & 31;
     const int64_t e0 = indptr[rb];
     for (int64_t r = rb + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); r < re;
          r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int t = row_task[r - rb];
-        const uint32_t lr = (uint32_t)(r - row0[t]);
-        for (int64_t e = indptr[r] + lane; e < indptr[r + 1]; e += 32) {
+        const int64_t a = indptr[r], z = indptr[r + 1];
+        const int32_t mt0 = row_mt[r - rb];
+        const int K = row_K[r - rb];
+        for (int64_t e = a + lane; e < z; e += 32) {
             const int32_t c = indices[e];
             const int J = c / kCbCols;
-            keys[e - e0] = (uint32_t)t * (uint32_t)NB + (uint32_t)J;
+            int32_t mt = mt0;
+            uint32_t lr = 0;
+            if (K > 1) {
+                // the row's entries inside block J: [lo, x) (columns ascending); piece by rank
+                int64_t lo = a, hi = z, x = a, y = z;
+                while (lo < hi) { const int64_t m = (lo + hi) >> 1; if (indices[m] < J * kCbCols) lo = m + 1; else hi = m; }
+                while (x < y) { const int64_t m = (x + y) >> 1; if (indices[m] < (J + 1) * kCbCols) x = m + 1; else y = m; }
+                mt += (int32_t)(((e - lo) * K) / (x - lo));
+            } else {
+                lr = (uint32_t)(r - rb - mt_desc[mt].x);
+            }
+            const uint32_t g = (uint32_t)(mt / kCbW), w = (uint32_t)(mt % kCbW);
+            keys[e - e0] = (g * (uint32_t)NB + (uint32_t)J) * (uint32_t)kCbW + w;
             const uint32_t word = (lr << 16) | (uint32_t)(c - J * kCbCols);
             vals[e - e0] = ((unsigned long long)__float_as_uint(values[e]) << 32) | word;
         }
@@ -564,7 +551,7 @@ __global__ void k_cb_fill(const uint32_t* __restrict__ keys, const unsigned long
 }
 
 struct CbWs {
-    int32_t* row_task;
+    int32_t *row_mt, *row_K;
     uint32_t *keys_a, *keys_b;
     unsigned long long *vals_a, *vals_b;
     int64_t *sstart, *slen;
@@ -586,7 +573,8 @@ static CbWs cb_ws_map(void* base, int64_t nr, int64_t m, int64_t nseg) {
         off = cb_align(off + b);
         return (char*)base + o;
     };
-    w.row_task = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(nr, 1));
+    w.row_mt = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(nr, 1));
+    w.row_K = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(nr, 1));
     w.keys_a = (uint32_t*)take(sizeof(uint32_t) * std::max<int64_t>(m, 1));
     w.keys_b = (uint32_t*)take(sizeof(uint32_t) * std::max<int64_t>(m, 1));
     w.vals_a = (unsigned long long*)take(sizeof(unsigned long long) * std::max<int64_t>(m, 1));
@@ -611,15 +599,22 @@ static int cb_rows(const tsnet_csr* P, const tsnet_shard* sh, int64_t& rb, int64
     return TSNET_OK;
 }
 
-static int cb_host_partition(const tsnet_csr* P, int64_t rb, int64_t re, cudaStream_t s, std::vector<int64_t>& row0,
-                             std::vector<int32_t>& rows, int64_t& nnz_s) {
-    std::vector<int64_t> ip(re - rb + 1);
-    TSNET_CUDA(cudaMemcpyAsync(ip.data(), P->indptr + rb, sizeof(int64_t) * ip.size(), cudaMemcpyDeviceToHost, s));
-    TSNET_CUDA(cudaStreamSynchronize(s));
-    nnz_s = ip.back() - ip.front();
-    TSNET_ARG(nnz_s < ((int64_t)1 << 31), "a plan holds < 2^31 entries per shard (got %lld)", (long long)nnz_s);
-    const int32_t T = cb_partition(ip.data(), rb, re, kCbRowsMax, num_sms(), row0, rows);
-    TSNET_ARG(T > 0, "row partition failed");
+struct CbCut {
+    std::vector<int32_t> row_mt, row_K, mt_r0, mt_info;
+    int32_t G = 0;
+    int64_t nnz_s = 0;
+};
+
+static int cb_host_cut(const tsnet_csr* P, int64_t rb, int64_t re, cudaStream_t s, CbCut& cut) {
+    std::vector<int64_t> ip(re - rb + 1, 0);
+    if (P->n > 0) {
+        TSNET_CUDA(cudaMemcpyAsync(ip.data(), P->indptr + rb, sizeof(int64_t) * ip.size(), cudaMemcpyDeviceToHost, s));
+        TSNET_CUDA(cudaStreamSynchronize(s));
+    }
+    cut.nnz_s = ip.back() - ip.front();
+    TSNET_ARG(cut.nnz_s < ((int64_t)1 << 31), "a plan holds < 2^31 entries per shard (got %lld)", (long long)cut.nnz_s);
+    cut.G = cb_partition(ip.data(), re - rb, kCbW, kCbRows, num_sms(), cut.row_mt, cut.row_K, cut.mt_r0, cut.mt_info);
+    TSNET_ARG(cut.G > 0, "row partition failed");
     return TSNET_OK;
 }
 
@@ -629,16 +624,20 @@ using namespace tsnet;
 
 extern "C" {
 
-int32_t tsnet_plan_partition(const int64_t* indptr_host, int64_t row_begin, int64_t row_end, int32_t rows_max,
-                             int32_t base_tasks, int32_t max_tasks, int64_t* task_row0, int32_t* task_rows) {
-    if (!indptr_host || row_begin < 0 || row_end < row_begin || rows_max < 1 || base_tasks < 1) return -1;
-    std::vector<int64_t> row0;
-    std::vector<int32_t> rows;
-    const int32_t T = cb_partition(indptr_host + row_begin, row_begin, row_end, rows_max, base_tasks, row0, rows);
-    if (T < 0 || T > max_tasks) return -1;
-    std::memcpy(task_row0, row0.data(), sizeof(int64_t) * T);
-    std::memcpy(task_rows, rows.data(), sizeof(int32_t) * T);
-    return T;
+int32_t tsnet_plan_partition(const int64_t* indptr_host, int64_t row_begin, int64_t row_end, int32_t warps,
+                             int32_t rows_max, int32_t base_groups, int64_t max_minitasks, int32_t* row_mt,
+                             int32_t* row_K, int32_t* mt_r0, int32_t* mt_info) {
+    if (!indptr_host || !row_mt || !row_K || !mt_r0 || !mt_info || row_begin < 0 || row_end < row_begin ||
+        warps < 1 || rows_max < 1 || base_groups < 1)
+        return -1;
+    std::vector<int32_t> a, b, c, d;
+    const int32_t G = cb_partition(indptr_host + row_begin, row_end - row_begin, warps, rows_max, base_groups, a, b, c, d);
+    if (G < 0 || (int64_t)G * warps > max_minitasks) return -1;
+    std::memcpy(row_mt, a.data(), sizeof(int32_t) * a.size());
+    std::memcpy(row_K, b.data(), sizeof(int32_t) * b.size());
+    std::memcpy(mt_r0, c.data(), sizeof(int32_t) * c.size());
+    std::memcpy(mt_info, d.data(), sizeof(int32_t) * d.size());
+    return G;
 }
 
 int tsnet_plan_query(const tsnet_csr* P, const tsnet_shard* shard, size_t* plan_bytes, size_t* ws_bytes,
@@ -648,18 +647,11 @@ int tsnet_plan_query(const tsnet_csr* P, const tsnet_shard* shard, size_t* plan_
     int64_t rb, re;
     int st = cb_rows(P, shard, rb, re);
     if (st != TSNET_OK) return st;
-    std::vector<int64_t> row0;
-    std::vector<int32_t> rows;
-    int64_t m = 0;
-    if (P->n == 0) {
-        row0.assign(1, 0);
-        rows.assign(1, 0);
-    } else if ((st = cb_host_partition(P, rb, re, (cudaStream_t)stream, row0, rows, m)) != TSNET_OK) {
-        return st;
-    }
-    const CbHeader h = cb_layout(P->n, rb, re, m, (int32_t)row0.size());
+    CbCut cut;
+    if ((st = cb_host_cut(P, rb, re, (cudaStream_t)stream, cut)) != TSNET_OK) return st;
+    const CbHeader h = cb_layout(P->n, rb, re, cut.nnz_s, cut.G);
     *plan_bytes = (size_t)h.bytes;
-    *ws_bytes = cb_ws_map(nullptr, re - rb, m, (int64_t)h.T * h.NB).bytes;
+    *ws_bytes = cb_ws_map(nullptr, re - rb, cut.nnz_s, (int64_t)h.G * h.NB * kCbW).bytes;
     return TSNET_OK;
 }
 
@@ -673,35 +665,32 @@ int tsnet_plan_build(const tsnet_csr* P, const tsnet_shard* shard, void* plan, s
     int64_t rb, re;
     int st = cb_rows(P, shard, rb, re);
     if (st != TSNET_OK) return st;
-    std::vector<int64_t> row0;
-    std::vector<int32_t> rows;
-    int64_t m = 0;
-    if (P->n == 0) {
-        row0.assign(1, 0);
-        rows.assign(1, 0);
-    } else if ((st = cb_host_partition(P, rb, re, s, row0, rows, m)) != TSNET_OK) {
-        return st;
-    }
-    CbHeader h = cb_layout(P->n, rb, re, m, (int32_t)row0.size());
+    CbCut cut;
+    if ((st = cb_host_cut(P, rb, re, s, cut)) != TSNET_OK) return st;
+    CbHeader h = cb_layout(P->n, rb, re, cut.nnz_s, cut.G);
     TSNET_ARG(plan_bytes >= (size_t)h.bytes, "plan buffer too small (%zu < %lld bytes)", plan_bytes, (long long)h.bytes);
-    const int64_t nseg = (int64_t)h.T * h.NB;
-    TSNET_ARG((uint64_t)nseg < ((uint64_t)1 << 32), "too many (task, block) segments");
-    CbWs w = cb_ws_map(ws, re - rb, m, nseg);
+    const int64_t nseg = (int64_t)h.G * h.NB * kCbW;
+    TSNET_ARG((uint64_t)nseg < ((uint64_t)1 << 32), "too many (group, block, warp) segments");
+    const int64_t nr = re - rb, T = (int64_t)h.G * kCbW;
+    CbWs w = cb_ws_map(ws, nr, cut.nnz_s, nseg);
     TSNET_ARG(ws != nullptr && ws_bytes >= w.bytes, "plan workspace too small (%zu < %zu bytes)", ws_bytes, w.bytes);
+    std::vector<int2> desc(T);
+    for (int64_t t = 0; t < T; ++t) desc[t] = make_int2(cut.mt_r0[t], cut.mt_info[t]);
     uint8_t* pb = reinterpret_cast<uint8_t*>(plan);
-    int64_t* d_row0 = reinterpret_cast<int64_t*>(pb + h.off_row0);
-    int32_t* d_rows = reinterpret_cast<int32_t*>(pb + h.off_rows);
     int64_t* d_seg = reinterpret_cast<int64_t*>(pb + h.off_seg);
+    int2* d_mt = reinterpret_cast<int2*>(pb + h.off_mt);
     uint2* d_ent = reinterpret_cast<uint2*>(pb + h.off_entries);
-    TSNET_CUDA(cudaMemcpyAsync(d_row0, row0.data(), sizeof(int64_t) * h.T, cudaMemcpyHostToDevice, s));
-    TSNET_CUDA(cudaMemcpyAsync(d_rows, rows.data(), sizeof(int32_t) * h.T, cudaMemcpyHostToDevice, s));
+    TSNET_CUDA(cudaMemcpyAsync(d_mt, desc.data(), sizeof(int2) * T, cudaMemcpyHostToDevice, s));
+    if (nr > 0) {
+        TSNET_CUDA(cudaMemcpyAsync(w.row_mt, cut.row_mt.data(), sizeof(int32_t) * nr, cudaMemcpyHostToDevice, s));
+        TSNET_CUDA(cudaMemcpyAsync(w.row_K, cut.row_K.data(), sizeof(int32_t) * nr, cudaMemcpyHostToDevice, s));
+    }
     TSNET_CUDA(cudaMemsetAsync(w.slen, 0, sizeof(int64_t) * (nseg + 1), s));
     TSNET_CUDA(cudaMemsetAsync(w.sstart, 0, sizeof(int64_t) * (nseg + 1), s));
+    const int64_t m = cut.nnz_s;
     if (m > 0) {
-        k_cb_row_task<<<std::min<int>(h.T, 4096), 256, 0, s>>>(d_row0, d_rows, h.T, rb, w.row_task);
-        TSNET_LAUNCH_CHECK();
-        k_cb_keys<<<num_sms() * 8, 256, 0, s>>>(P->indptr, P->indices, P->values, rb, re, d_row0, w.row_task, h.NB,
-                                                w.keys_a, w.vals_a);
+        k_cb_keys<<<num_sms() * 8, 256, 0, s>>>(P->indptr, P->indices, P->values, rb, re, w.row_mt, w.row_K, d_mt,
+                                                h.NB, w.keys_a, w.vals_a);
         TSNET_LAUNCH_CHECK();
         int end_bit = 1;
         while (end_bit < 32 && ((uint64_t)1 << end_bit) < (uint64_t)nseg) ++end_bit;

@@ -150,7 +150,7 @@ cudaError_t launch_field_phase(const Ws& w, const GradArgs& a, cudaStream_t s);
 cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, bool zero_all);
 cudaError_t launch_field_conv(const Ws& w, const GradArgs& a, cudaStream_t s);
 cudaError_t launch_spmv(const Ws& w, const GradArgs& a, cudaStream_t s);
-cudaError_t launch_attr_cb(const void* plan, const float2* Y, float2* F, cudaStream_t s);
+cudaError_t launch_attr_cb(const void* plan, const float2* Y, float2* F, int64_t nl, cudaStream_t s);
 cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2* f_field, double* Z,
                             cudaStream_t s);
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,

@@ -241,14 +241,17 @@ static const SpmvCfg& spmv_cfg() {
 
 template <int U>
 static cudaError_t launch_spmv2_t(const GradArgs& a, float2* F, const SpmvCfg& c, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr && c.l1) {
-        cudaFuncSetAttribute(k_spmv2<U>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-        attr = true;
+    static int resident = 0;
+    if (resident == 0) {
+        if (c.l1) cudaFuncSetAttribute(k_spmv2<U>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_spmv2<U>, 256, 0) != cudaSuccess || resident < 1)
+            resident = 1;
     }
+    // one wave: every warp runs concurrently (the chunk cut assumes it);
     // small problems: fewer CTAs so that chunks stay >= 1024 entries
     const int64_t want = std::max<int64_t>(1, a.nnz / (1024 * 8 * c.cpw));
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)kNumSMs * c.ctas_per_sm));
+    const int per_sm = std::min(c.ctas_per_sm, resident);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)kNumSMs * per_sm));
     k_spmv2<U><<<blocks, 256, 0, s>>>(a.rb, a.re, a.indptr, a.indices, a.values, a.Y, F, c.cpw);
     return cudaGetLastError();
 }

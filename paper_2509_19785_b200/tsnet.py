@@ -79,7 +79,7 @@ SIGNATURES = [
                                         ctypes.POINTER(c_sz), ctypes.POINTER(c_sz), c_vp]),
     ("tsnet_plan_build", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard), c_vp, c_sz, c_vp,
                                         c_sz, c_vp]),
-    ("tsnet_plan_partition", c_i32, [c_vp, c_i64, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp]),
+    ("tsnet_plan_partition", c_i32, [c_vp, c_i64, c_i64, c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp]),
     ("tsnet_comm_unique_id", ctypes.c_int, [c_vp]),
     ("tsnet_comm_init", ctypes.c_int, [c_vp, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     ("tsnet_comm_destroy", ctypes.c_int, [c_vp]),
@@ -261,18 +261,22 @@ def tsnet_plan_build(P: CSR, shard=None, stream=None) -> CSR:
     return P
 
 
-def tsnet_plan_partition(indptr_host, row_begin: int, row_end: int, rows_max: int, base_tasks: int,
-                         max_tasks: int = 1 << 16):
-    """Host task cut (pure): returns (task_row0, task_rows) numpy arrays."""
+def tsnet_plan_partition(indptr_host, row_begin: int, row_end: int, warps: int = 16, rows_max: int = 704,
+                         base_groups: int = 148, max_minitasks: int = 1 << 22):
+    """Host cut of the plan (pure): returns (G, row_mt, row_K, mt_r0, mt_info) numpy arrays."""
     import numpy as np
     ip = np.ascontiguousarray(indptr_host, dtype=np.int64)
-    r0 = np.zeros(max_tasks, np.int64)
-    rr = np.zeros(max_tasks, np.int32)
-    T = lib().tsnet_plan_partition(ip.ctypes.data, row_begin, row_end, rows_max, base_tasks, max_tasks,
-                                   r0.ctypes.data, rr.ctypes.data)
-    if T < 0:
-        raise TsnetError("tsnet_plan_partition", T)
-    return r0[:T], rr[:T]
+    nr = row_end - row_begin
+    row_mt = np.zeros(max(nr, 1), np.int32)
+    row_K = np.zeros(max(nr, 1), np.int32)
+    mt_r0 = np.zeros(max_minitasks, np.int32)
+    mt_info = np.zeros(max_minitasks, np.int32)
+    G = lib().tsnet_plan_partition(ip.ctypes.data, row_begin, row_end, warps, rows_max, base_groups, max_minitasks,
+                                   row_mt.ctypes.data, row_K.ctypes.data, mt_r0.ctypes.data, mt_info.ctypes.data)
+    if G < 0:
+        raise TsnetError("tsnet_plan_partition", G)
+    T = G * warps
+    return G, row_mt[:nr], row_K[:nr], mt_r0[:T], mt_info[:T]
 
 
 # ------------------------------------------------------ per-iteration path
