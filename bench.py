@@ -223,8 +223,8 @@ def run_ours(args, rank, world, local_rank):
     Y0 = torch.from_numpy(init_layout(n, 0)).to(dev)
     plan_s = None
     t0 = time.perf_counter()
-    if world > 1:
-        # row shards + NCCL communicator + the plan of the own rows (set-up, untimed)
+    if world > 1 or args.sharded:
+        # row shards + NCCL communicator (+ the plan of the own rows) (set-up, untimed)
         from paper_2509_19785_b200.distributed import ShardedLayout
         lay = ShardedLayout(P, Y0, rank, world, plan=args.plan)
         shard = lay.shard
@@ -235,7 +235,7 @@ def run_ours(args, rank, world, local_rank):
         lay = Layout(P, Y0, use_graphs=True)
         shard, rb, re = None, 0, n
     torch.cuda.synchronize()
-    if world > 1 or args.plan:
+    if world > 1 or args.plan or args.sharded:
         plan_s = time.perf_counter() - t0
     nnz_l = int(P.indptr[re].item() - P.indptr[rb].item())
     nl = re - rb
@@ -327,7 +327,7 @@ def run_ours(args, rank, world, local_rank):
 
     if rank == 0:
         value = args.steps / (ms * 1e-3)       # whole-job iterations/s: every rank takes part in each iteration
-        par = ("single GPU" if world == 1 else
+        par = ("single GPU" if (world == 1 and not args.sharded) else
                f"{world} row shards (nnz-balanced), NCCL all-reduce of the charge grid + all-gather of Y")
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
@@ -347,7 +347,7 @@ def run_ours(args, rank, world, local_rank):
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": KERNELS_PER_STEP * args.steps,
                 "clocks": clk, "nonfinite": stats["nonfinite"]}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or args.sharded:
         lay.close()
 
 
@@ -362,6 +362,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--plan", action="store_true", help="column-blocked plan kernel for the SpMV instead of CSR")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU (NCCL) path even on one rank (needs torchrun / a process group)")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     assert args.warmup >= 3, "at least 3 warm-up steps"
@@ -372,13 +374,13 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl")
     run_ours(args, rank, world, local_rank)
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch.distributed as dist
         dist.destroy_process_group()
 

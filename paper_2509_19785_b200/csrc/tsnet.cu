@@ -3,6 +3,7 @@
 // field.cu / iterate.cu / cost.cu / knn.cu on the caller's stream.
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -103,15 +104,62 @@ static int prepare(const tsnet_csr* P, const float* Y, const tsnet_grad_params* 
 static size_t grid_floats(const Ws& w) { return (size_t)4 * w.N_max * w.N_max; }
 
 // field (with the grid all-reduce when world > 1) + attractive SpMV of the own rows
+// A second stream per (host thread, device) for the field phase, which is
+// independent of the attractive SpMV until the gather/update: the two chains
+// run concurrently (fork/join by events, so the pattern is also captured into
+// a CUDA graph as two branches).  TSNET_FIELD_STREAM=0 keeps one stream.
+struct SideStream {
+    int dev = -1;
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+static bool side_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TSNET_FIELD_STREAM");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+static cudaError_t side_stream(SideStream*& out) {
+    static thread_local SideStream ss[16];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    SideStream& x = ss[dev & 15];
+    if (x.dev != dev) {
+        if ((e = cudaStreamCreateWithFlags(&x.side, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming)) != cudaSuccess) return e;
+        x.dev = dev;
+    }
+    out = &x;
+    return cudaSuccess;
+}
+
 static int eval_gradient_parts(const Ws& w, const GradArgs& a, const tsnet_shard* sh, cudaStream_t s) {
     int st;
     if ((st = check_comm(sh, a)) != TSNET_OK) return st;
     const bool multi = sh != nullptr && sh->comm != nullptr;   // collectives (also with a 1-rank comm)
-    TSNET_CUDA(launch_field_local(w, a, s, multi));
+    SideStream* ss = nullptr;
+    const bool fork = side_enabled() && !multi;   // NCCL calls stay on the caller's stream
+    if (fork) TSNET_CUDA(side_stream(ss));
+    cudaStream_t fs = fork ? ss->side : s;
+    if (fork) {
+        TSNET_CUDA(cudaEventRecord(ss->fork, s));
+        TSNET_CUDA(cudaStreamWaitEvent(fs, ss->fork, 0));
+    }
+    TSNET_CUDA(launch_field_local(w, a, fs, multi));
     if (multi && (st = comm_allreduce_grid(sh->comm, reinterpret_cast<float*>(w.wgrid), grid_floats(w), s)) != TSNET_OK)
         return st;
-    TSNET_CUDA(launch_field_conv(w, a, s));
+    TSNET_CUDA(launch_field_conv(w, a, fs));
     TSNET_CUDA(launch_spmv(w, a, s));
+    if (fork) {
+        TSNET_CUDA(cudaEventRecord(ss->join, fs));
+        TSNET_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
+    }
     return TSNET_OK;
 }
 
