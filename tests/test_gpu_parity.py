@@ -421,3 +421,41 @@ def test_ragged_sizes(n):
     else:
         # no pairs: only compression survives; the entropy self term cancels to fp32 round-off
         assert relL2(g, 0.01 * Y.astype(np.float64)) <= GRAD_TOL
+
+
+def _sub_csr(ip_full, ix_dev, pv_dev, r0, B):
+    """CSR view the oracle's row functions can read for rows [r0, r0 + B) only:
+    a full-length indptr that is meaningful on those rows, and their entries."""
+    a, z = int(ip_full[r0]), int(ip_full[r0 + B])
+    fake = np.zeros(len(ip_full), np.int64)
+    fake[r0:r0 + B + 1] = ip_full[r0:r0 + B + 1] - a
+    return fake, ix_dev[a:z].cpu().numpy(), pv_dev[a:z].cpu().numpy().astype(np.float64)
+
+
+def test_config5_full_size_sampled():
+    """3-D grid 160^3 (n = 4,096,000), the scaling workload: kNN rows of sampled
+    sources bit-exact vs the oracle; the interpolated gradient and the attractive
+    term of sampled row blocks vs the oracle (field from all 4.1M points)."""
+    ip, ix = config_graph(5)
+    n = len(ip) - 1
+    got = tsnet_build_P(*dev_graph(ip, ix), u=40.0, seed=0)
+    rng = np.random.default_rng(5)
+    src = np.unique(np.concatenate([rng.choice(n, 500, replace=False), [0, n - 1, n // 2]]))
+    oi, oh, ol = oracle.knn(ip, ix, 120, 0, src=src)
+    assert np.array_equal(got["knn_len"].cpu().numpy()[src], ol)
+    assert np.array_equal(got["knn_idx"].cpu().numpy()[src], oi)
+    assert np.array_equal(got["knn_hop"].cpu().numpy()[src], oh)
+    P = got["P"]
+    pip = P.indptr.cpu().numpy()
+    Y = clustered_layout(n, 30.0, 40, 2.0, 5)
+    g, Z, fa, ff, st = gpu_grad(P, Y, GradParams(*STAGE_B))
+    fs = oracle.interp.field_state(Y.astype(np.float64))
+    assert st["I"] == fs["geo"]["I"]
+    assert abs(Z - fs["Z"]) <= 1e-5 * fs["Z"]
+    for r0 in (0, n // 3, n - 3000):
+        B = 3000
+        fip, fix, fpv = _sub_csr(pip, P.indices, P.values, r0, B)
+        go = oracle.interp.gradient_rows(fs, Y.astype(np.float64), fip, fix, fpv, *STAGE_B, r0, B)
+        fo = oracle.attr_sparse_rows(Y.astype(np.float64), fip, fix, fpv, r0, B)
+        assert relL2(fa[r0:r0 + B], fo) <= 1e-5
+        assert relL2(g[r0:r0 + B], go) <= GRAD_TOL, (r0, relL2(g[r0:r0 + B], go))
