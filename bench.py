@@ -297,6 +297,9 @@ def run_ours(args, rank, world, local_rank):
             rec = json.load(f)
         traffic = float(rec["dram_bytes_per_launch"]) * (nnz / rec["nnz"])
         limiter = rec.get("limiter")
+        if "l2_request_path_utilization" in rec:
+            limiter = {"what": limiter, "l1tex_to_l2_request_path_util": rec["l2_request_path_utilization"],
+                       "lts_tag_request_util": rec["lts_tag_request_utilization"], "source": rec["source"]}
 
     # end to end through the host-buffer API (H2D + step + D2H every step)
     e2e = None

@@ -17,6 +17,7 @@ echo "smoke exit $?" >> gpurun_out/${TAG}_smoke.log
 timeout 900 python bench.py > gpurun_out/${TAG}_bench4.log 2>&1
 echo "bench exit $?" >> gpurun_out/${TAG}_bench4.log
 timeout 900 python bench.py --plan --no-cpu-baseline --no-e2e --steps 200 > gpurun_out/${TAG}_bench4_plan.log 2>&1
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29531 bench.py --sharded --no-cpu-baseline --steps 200 > gpurun_out/${TAG}_bench4_sharded1.log 2>&1
 timeout 1200 python bench.py --config 5 --no-cpu-baseline --no-e2e --steps 200 > gpurun_out/${TAG}_bench5.log 2>&1
 B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e"
 timeout 600 $B > gpurun_out/${TAG}_plain.log 2>&1 && \
