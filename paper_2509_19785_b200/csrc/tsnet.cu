@@ -144,7 +144,9 @@ static int eval_gradient_parts(const Ws& w, const GradArgs& a, const tsnet_shard
     if ((st = check_comm(sh, a)) != TSNET_OK) return st;
     const bool multi = sh != nullptr && sh->comm != nullptr;   // collectives (also with a 1-rank comm)
     SideStream* ss = nullptr;
-    const bool fork = side_enabled() && !multi;   // NCCL calls stay on the caller's stream
+    // the grid chain (field + its all-reduce) runs on the side stream, overlapped
+    // with the SpMV (SURVEY §8(e) "chain G"); the Y all-gather stays on `s`
+    const bool fork = side_enabled();
     if (fork) TSNET_CUDA(side_stream(ss));
     cudaStream_t fs = fork ? ss->side : s;
     if (fork) {
@@ -152,7 +154,7 @@ static int eval_gradient_parts(const Ws& w, const GradArgs& a, const tsnet_shard
         TSNET_CUDA(cudaStreamWaitEvent(fs, ss->fork, 0));
     }
     TSNET_CUDA(launch_field_local(w, a, fs, multi));
-    if (multi && (st = comm_allreduce_grid(sh->comm, reinterpret_cast<float*>(w.wgrid), grid_floats(w), s)) != TSNET_OK)
+    if (multi && (st = comm_allreduce_grid(sh->comm, reinterpret_cast<float*>(w.wgrid), grid_floats(w), fs)) != TSNET_OK)
         return st;
     TSNET_CUDA(launch_field_conv(w, a, fs));
     TSNET_CUDA(launch_spmv(w, a, s));
