@@ -217,6 +217,7 @@ struct SpmvCfg {
     int cpw = 4;         // chunks per warp
     int ctas_per_sm = 5; // 256-thread CTAs per SM
     int l1 = 1;          // prefer L1 over shared memory (carveout 0)
+    int reserve = 0;     // SMs left free for the concurrent field phase (side stream)
 };
 
 static int env_int(const char* name, int def) {
@@ -234,6 +235,7 @@ static const SpmvCfg& spmv_cfg() {
         c.cpw = std::max(1, env_int("TSNET_SPMV_CPW", c.cpw));
         c.ctas_per_sm = std::max(1, env_int("TSNET_SPMV_CTAS", c.ctas_per_sm));
         c.l1 = env_int("TSNET_SPMV_L1", c.l1);
+        c.reserve = std::max(0, std::min(64, env_int("TSNET_SPMV_RESERVE_SMS", c.reserve)));
         init = true;
     }
     return c;
@@ -251,7 +253,8 @@ static cudaError_t launch_spmv2_t(const GradArgs& a, float2* F, const SpmvCfg& c
     // small problems: fewer CTAs so that chunks stay >= 1024 entries
     const int64_t want = std::max<int64_t>(1, a.nnz / (1024 * 8 * c.cpw));
     const int per_sm = std::min(c.ctas_per_sm, resident);
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)kNumSMs * per_sm));
+    const int blocks =
+        (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)(kNumSMs - c.reserve) * per_sm));
     k_spmv2<U><<<blocks, 256, 0, s>>>(a.rb, a.re, a.indptr, a.indices, a.values, a.Y, F, c.cpw);
     return cudaGetLastError();
 }
