@@ -240,7 +240,8 @@ TSNET_API int tsnet_step_host(const tsnet_csr* P, float* Y_host, float* vel_host
  *   C_CMP = lambda_c / (2n) sum_i |X_i|^2                       (Eq. 1)
  *   C_ENT* = -lambda_r / (4 n^2) sum_{i != j} ln(eps + r2_ij)   (reading R1 of PAPER.md:90)
  * mode 0: exact (Z and C_ENT* by O(n^2) tiles, fp64 accumulation);
- * mode 1: Z from the interpolation grid, C_ENT* = NaN (not computed; NEXT).
+ * mode 1: O(n) -- Z and sum_{i != j} ln(eps + r2) from the interpolation grid
+ *         (Parseval sums of the spread W1 against K1 and ln(eps + d^2)).
  */
 TSNET_API int tsnet_cost(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, int32_t mode,
                const tsnet_shard* shard, double* out3, void* ws, size_t ws_bytes, tsnet_stream_t stream);

@@ -55,6 +55,7 @@ struct Geo {
     unsigned int ticket;               // last-block-done counter of the bbox kernel
     unsigned bbox[4];                  // ~u(min x), ~u(min y), u(max x), u(max y); 0 = empty (field.cu)
     double sum_x, sum_y;               // centroid accumulation (recenter)
+    double eacc;                       // cost mode 1: Parseval accumulator <W1, K_ln * W1> * M^2
     unsigned int pad2;
     int pad;
 };
@@ -156,5 +157,6 @@ cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,
                           const tsnet_step_params& sp, cudaStream_t s);
 cudaError_t launch_cost(const Ws& w, const GradArgs& a, int mode, double* out3, cudaStream_t s);
+cudaError_t launch_entropy_sum(const Ws& w, const GradArgs& a, cudaStream_t s);
 
 }  // namespace tsnet

@@ -3,7 +3,8 @@
 //         = lambda_kl [ sum p ln p + sum p ln(1 + r^2) + (sum p) ln Z ]
 //   C_CMP = lambda_c / (2n) sum |X_i|^2
 //   C_ENT* = -lambda_r / (4 n^2) sum_{i != j} ln(eps + r^2)      (reading R1)
-// mode 0: exact O(n^2) tiles for Z and C_ENT*; mode 1: Z from the grid.
+// mode 0: exact O(n^2) tiles for Z and C_ENT*; mode 1: Z and the entropy sum
+// from the interpolation grid (O(n): sparse pass + grid Parseval sums).
 #include <algorithm>
 
 #include "common.cuh"
@@ -74,12 +75,15 @@ __global__ void __launch_bounds__(kTile) k_cost_pairs(int64_t n, const float2* _
 }
 
 __global__ void k_cost_final(int64_t n, const double* acc, const Geo* g, int mode, float lambda_kl, float lambda_c,
-                             float lambda_r, double* out3) {
+                             float lambda_r, float eps, double* out3) {
     const double nn = (double)n;
     const double Z = (mode == 0) ? acc[2] : g->Z;
     out3[0] = (double)lambda_kl * (acc[0] + acc[1] * log(Z));
     out3[1] = (double)lambda_c / (2.0 * nn) * acc[4];
-    out3[2] = (mode == 0) ? -(double)lambda_r / (4.0 * nn * nn) * acc[3] : NAN;
+    // mode 1: interpolated sum_{i != j} ln(eps + r^2) = <W1, K_ln * W1> - n ln(eps) (field.cu)
+    const double M2 = (double)g->M * (double)g->M;
+    const double ent = (mode == 0) ? acc[3] : g->eacc / M2 - nn * log((double)eps);
+    out3[2] = -(double)lambda_r / (4.0 * nn * nn) * ent;
 }
 
 cudaError_t launch_cost(const Ws& w, const GradArgs& a, int mode, double* out3, cudaStream_t s) {
@@ -87,7 +91,7 @@ cudaError_t launch_cost(const Ws& w, const GradArgs& a, int mode, double* out3, 
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((a.n + 255) / 256, (int64_t)kNumSMs * 4));
     k_cost_sparse<<<blocks, 256, 0, s>>>(a.n, a.indptr, a.indices, a.values, a.Y, w.cost);
     if (mode == 0) k_cost_pairs<<<(int)((a.n + kTile - 1) / kTile), kTile, 0, s>>>(a.n, a.Y, a.eps, w.cost);
-    k_cost_final<<<1, 1, 0, s>>>(a.n, w.cost, w.geo, mode, a.lambda_kl, a.lambda_c, a.lambda_r, out3);
+    k_cost_final<<<1, 1, 0, s>>>(a.n, w.cost, w.geo, mode, a.lambda_kl, a.lambda_c, a.lambda_r, a.eps, out3);
     return cudaGetLastError();
 }
 

@@ -514,6 +514,88 @@ __global__ void __launch_bounds__(kInvThreads) k_row_inv(Geo* __restrict__ gp, c
     }
 }
 
+// ---------------------------------------------- interpolated entropy sum (cost)
+// sum_{i != j} ln(eps + r_ij^2) ~ <W1, K_ln * W1> - n ln(eps) with the same
+// spread W1 and the kernel table K_ln = ln(eps + d^2) on node offsets
+// (tsnet_cost mode 1; the smooth log kernel is interpolated like K1 for Z).
+// Row pass: per row y of the M x M circulant, FFT of (W1 + i K_ln) along x,
+// half spectra of both stored transposed; column pass: FFT along y and the
+// Parseval sum (K_ln is even, its spectrum real) into g->eacc (fp64).
+__global__ void __launch_bounds__(kInvThreads) k_ent_row(const Geo* __restrict__ gp, const float4* __restrict__ wgrid,
+                                                         const float2* __restrict__ twg, float2* __restrict__ spec,
+                                                         int M_max, float eps) {
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* buf = sm + M_max;
+    float2* scr = buf + M_max;
+    const int M = gp->M, N = gp->N, half = M / 2 + 1, nrad = gp->nrad;
+    const unsigned long long plan = gp->plan;
+    const int half_max = M_max / 2 + 1;
+    const double dlt = gp->delta;
+    for (int k = threadIdx.x; k < M; k += blockDim.x) tw[k] = twg[k];
+    for (int y = blockIdx.x; y < M; y += gridDim.x) {
+        const int dy = (y <= M / 2) ? y : y - M;
+        const bool ky = (dy < N) && (-dy < N);
+        for (int x = threadIdx.x; x < M; x += blockDim.x) {
+            const int dx = (x <= M / 2) ? x : x - M;
+            const float w1 = (y < N && x < N) ? wgrid[(int64_t)y * N + x].x : 0.f;
+            float kl = 0.f;
+            if (ky && dx < N && -dx < N) {
+                const double ox = dx * dlt, oy = dy * dlt;
+                kl = (float)log((double)eps + ox * ox + oy * oy);
+            }
+            buf[x] = make_float2(w1, kl);
+        }
+        __syncthreads();
+        fft_block(buf, scr, M, 1, M, plan, nrad, tw, false);
+        for (int k = threadIdx.x; k < half; k += blockDim.x) {
+            const float2 Zk = buf[k];
+            const float2 Zm = cconj(buf[k == 0 ? 0 : M - k]);
+            spec[((int64_t)0 * half_max + k) * M_max + y] = make_float2(0.5f * (Zk.x + Zm.x), 0.5f * (Zk.y + Zm.y));
+            spec[((int64_t)1 * half_max + k) * M_max + y] = mul_mi(make_float2(0.5f * (Zk.x - Zm.x), 0.5f * (Zk.y - Zm.y)));
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kInvThreads) k_ent_col(Geo* __restrict__ gp, const float2* __restrict__ spec,
+                                                         const float2* __restrict__ twg, int M_max) {
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* buf = sm + M_max;            // 2 * M
+    float2* scr = buf + 2 * M_max;       // 2 * M
+    __shared__ double red[kInvThreads / 32];
+    const int M = gp->M, half = M / 2 + 1, nrad = gp->nrad;
+    const unsigned long long plan = gp->plan;
+    const int half_max = M_max / 2 + 1;
+    for (int k = threadIdx.x; k < M; k += blockDim.x) tw[k] = twg[k];
+    double part = 0.0;
+    for (int kx = blockIdx.x; kx < half; kx += gridDim.x) {
+        for (int t = threadIdx.x; t < 2 * M; t += blockDim.x) {
+            const int a = t / M, y = t - a * M;
+            buf[t] = spec[((int64_t)a * half_max + kx) * M_max + y];
+        }
+        __syncthreads();
+        fft_block(buf, scr, M, 2, M, plan, nrad, tw, false);
+        const double wt = (kx == 0 || 2 * kx == M) ? 1.0 : 2.0;
+        for (int k = threadIdx.x; k < M; k += blockDim.x) {
+            const float2 W = buf[k], K = buf[M + k];
+            part += wt * (double)K.x * ((double)W.x * W.x + (double)W.y * W.y);
+        }
+        __syncthreads();
+    }
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double z = 0.0;
+        for (int k = 0; k < kInvThreads / 32; ++k) z += red[k];
+        atomicAdd(&gp->eacc, z);
+    }
+}
+
+__global__ void k_ent_zero(Geo* g) { g->eacc = 0.0; }
+
 size_t field_smem_row(int M_max) { return sizeof(float2) * (size_t)M_max * 11; }
 size_t field_smem_col(int M_max) { return sizeof(float2) * (size_t)M_max * 17; }
 size_t field_smem_inv(int M_max) { return sizeof(float2) * (size_t)M_max * 5; }
@@ -559,6 +641,20 @@ cudaError_t launch_field_conv(const Ws& w, const GradArgs& a, cudaStream_t s) {
     k_col<<<kNumSMs, kColThreads, field_smem_col(w.M_max), s>>>(w.geo, w.spec, w.tw, w.colout, w.M_max, w.N_max);
     k_row_inv<<<kNumSMs * 2, kInvThreads, field_smem_inv(w.M_max), s>>>(w.geo, w.colout, w.tw, w.fgrid, w.M_max,
                                                                         w.N_max, a.n, a.lambda_kl, a.lambda_r);
+    return cudaGetLastError();
+}
+
+// sum_{i != j} ln(eps + r^2) * M^2 + n ln(eps) M^2 into g->eacc, after launch_field_local
+cudaError_t launch_entropy_sum(const Ws& w, const GradArgs& a, cudaStream_t s) {
+    cudaError_t e;
+    const size_t smr = sizeof(float2) * (size_t)w.M_max * 3, smc = sizeof(float2) * (size_t)w.M_max * 5;
+    if ((e = cudaFuncSetAttribute(k_ent_row, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr)) != cudaSuccess)
+        return e;
+    if ((e = cudaFuncSetAttribute(k_ent_col, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc)) != cudaSuccess)
+        return e;
+    k_ent_zero<<<1, 1, 0, s>>>(w.geo);
+    k_ent_row<<<kNumSMs * 2, kInvThreads, smr, s>>>(w.geo, w.wgrid, w.tw, w.spec, w.M_max, a.eps);
+    k_ent_col<<<kNumSMs, kInvThreads, smc, s>>>(w.geo, w.spec, w.tw, w.M_max);
     return cudaGetLastError();
 }
 

@@ -344,7 +344,7 @@ int tsnet_cost(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, 
     GradArgs a;
     int st = prepare(P, Y, gp, shard, ws, ws_bytes, w, a);
     if (st != TSNET_OK) return st;
-    TSNET_ARG(mode == 0 || mode == 1, "cost mode must be 0 (exact) or 1 (interpolated Z)");
+    TSNET_ARG(mode == 0 || mode == 1, "cost mode must be 0 (exact) or 1 (interpolated)");
     TSNET_ARG(!sharded(shard, a.n), "tsnet_cost is single-GPU only");
     TSNET_ARG(out3 != nullptr, "out3 is NULL");
     cudaStream_t s = (cudaStream_t)stream;
@@ -352,7 +352,10 @@ int tsnet_cost(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, 
         TSNET_CUDA(cudaMemsetAsync(out3, 0, 3 * sizeof(double), s));
         return TSNET_OK;
     }
-    if (mode == 1) TSNET_CUDA(launch_field_phase(w, a, s));
+    if (mode == 1) {
+        TSNET_CUDA(launch_field_phase(w, a, s));
+        TSNET_CUDA(launch_entropy_sum(w, a, s));
+    }
     TSNET_CUDA(launch_cost(w, a, mode, out3, s));
     return TSNET_OK;
 }

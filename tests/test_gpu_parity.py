@@ -354,9 +354,16 @@ def test_runner_graphs_match_eager():
 
 
 # ----------------------------------------------------------------- cost
-def test_cost_exact_and_interpolated():
-    P = oracle_P(1)
-    Y = uniform_layout(P["n"], 20.0, 4)
+@pytest.mark.parametrize("cfg,lay", [(1, "uniform20"), (2, "clustered"), (1, "init")])
+def test_cost_exact_and_interpolated(cfg, lay):
+    """mode 0 = the exact cost O4b; mode 1 = sparse KL with the interpolated Z
+    and the interpolated entropy sum sum_{i!=j} ln(eps + r^2) (Parseval of the
+    spread W1 against the ln kernel): vs the oracle's interpolation of the same
+    sums (oracle.interp_fields, fp64) and vs the exact cost."""
+    P = oracle_P(cfg)
+    n = P["n"]
+    Y = {"uniform20": uniform_layout(n, 20.0, 4), "clustered": clustered_layout(n, 25.0, 7, 1.2, 2),
+         "init": init_layout(n, 0)}[lay]
     gp = GradParams(*STAGE_B)
     Pd = dev_P(P)
     ws = alloc_workspace(Pd.n, Pd.nnz, gp)
@@ -365,8 +372,20 @@ def test_cost_exact_and_interpolated():
     c1 = tsnet_cost(Pd, Yd, gp, ws, mode=1).cpu().numpy()
     want = oracle.exact_cost(Y.astype(np.float64), P["indptr"], P["indices"], p32(P), *STAGE_B)
     assert np.allclose(c0, want, rtol=2e-5)
-    assert abs(c1[0] - want[0]) <= 1e-3 * abs(want[0]) and abs(c1[1] - want[1]) <= 1e-6 * abs(want[1])
-    assert np.isnan(c1[2])
+    assert abs(c1[1] - want[1]) <= 1e-6 * abs(want[1])
+    # oracle interpolation of the two grid sums
+    Y64 = Y.astype(np.float64)
+    (phi1,), _ = oracle.interp_fields(Y64, [np.ones(n)], oracle.interp.k1)
+    (phil,), _ = oracle.interp_fields(Y64, [np.ones(n)], lambda r2: np.log(0.05 + r2))
+    Zi = phi1.sum() - n
+    Si = phil.sum() - n * np.log(0.05)
+    lkl, lc, lr = STAGE_B
+    kl_sparse = want[0] - lkl * np.log(oracle.exact_Z(Y64)) * p32(P).sum()   # sum p ln(p/w) part
+    assert abs(c1[0] - (kl_sparse + lkl * np.log(Zi) * p32(P).sum())) <= 1e-5 * abs(want[0]) + 1e-9
+    ent_i = -lr / (4.0 * n * n) * Si
+    assert abs(c1[2] - ent_i) <= 1e-4 * abs(ent_i) + 1e-7 * abs(want[2])
+    # and the interpolated entropy cost is close to the exact one
+    assert abs(c1[2] - want[2]) <= 2e-2 * abs(want[2]) + 1e-6
 
 
 # ----------------------------------------------------------------- edges
