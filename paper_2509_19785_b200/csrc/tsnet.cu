@@ -110,8 +110,8 @@ static size_t grid_floats(const Ws& w) { return (size_t)4 * w.N_max * w.N_max; }
 // a CUDA graph as two branches).  TSNET_FIELD_STREAM=0 keeps one stream.
 struct SideStream {
     int dev = -1;
-    cudaStream_t side = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaStream_t side = nullptr, copy = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr, copied = nullptr;
 };
 
 static bool side_enabled() {
@@ -131,8 +131,10 @@ static cudaError_t side_stream(SideStream*& out) {
     SideStream& x = ss[dev & 15];
     if (x.dev != dev) {
         if ((e = cudaStreamCreateWithFlags(&x.side, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithFlags(&x.copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
         if ((e = cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
         if ((e = cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&x.copied, cudaEventDisableTiming)) != cudaSuccess) return e;
         x.dev = dev;
     }
     out = &x;
@@ -250,9 +252,14 @@ int tsnet_grad(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, 
     return TSNET_OK;
 }
 
-int tsnet_step(const tsnet_csr* P, float* Y, float* vel, float* gains, const tsnet_grad_params* gp,
-               const tsnet_step_params* sp, const tsnet_shard* shard, void* ws, size_t ws_bytes,
-               tsnet_stream_t stream) {
+}  // extern "C"
+
+namespace tsnet {
+// One iteration; if `before_update` is given, the move waits for it (the host
+// path's velocity/gains upload runs concurrently with the field phase + SpMV).
+static int step_impl(const tsnet_csr* P, float* Y, float* vel, float* gains, const tsnet_grad_params* gp,
+                     const tsnet_step_params* sp, const tsnet_shard* shard, void* ws, size_t ws_bytes,
+                     cudaStream_t s, cudaEvent_t before_update) {
     Ws w;
     GradArgs a;
     int st = prepare(P, Y, gp, shard, ws, ws_bytes, w, a);
@@ -263,12 +270,21 @@ int tsnet_step(const tsnet_csr* P, float* Y, float* vel, float* gains, const tsn
     const bool multi = shard != nullptr && shard->comm != nullptr;
     TSNET_ARG(!multi || shard->bounds != nullptr, "a communicating shard needs shard->bounds to all-gather Y");
     if (a.n == 0) return TSNET_OK;
-    cudaStream_t s = (cudaStream_t)stream;
     if ((st = eval_gradient_parts(w, a, shard, s)) != TSNET_OK) return st;
+    if (before_update) TSNET_CUDA(cudaStreamWaitEvent(s, before_update, 0));
     TSNET_CUDA(launch_update(w, a, reinterpret_cast<float2*>(Y), reinterpret_cast<float2*>(vel),
                              reinterpret_cast<float2*>(gains), *sp, s));
     if (multi) return comm_allgather_rows(shard->comm, Y, shard->bounds, shard->world, s);
     return TSNET_OK;
+}
+}  // namespace tsnet
+
+extern "C" {
+
+int tsnet_step(const tsnet_csr* P, float* Y, float* vel, float* gains, const tsnet_grad_params* gp,
+               const tsnet_step_params* sp, const tsnet_shard* shard, void* ws, size_t ws_bytes,
+               tsnet_stream_t stream) {
+    return step_impl(P, Y, vel, gains, gp, sp, shard, ws, ws_bytes, (cudaStream_t)stream, nullptr);
 }
 
 int tsnet_field_local(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, const tsnet_shard* shard,
@@ -325,11 +341,18 @@ int tsnet_step_host(const tsnet_csr* P, float* Y_host, float* vel_host, float* g
     float2* dV = w0.state + n;
     float2* dG = w0.state + 2 * n;
     const size_t b = sizeof(float2) * (size_t)n;
+    // Y first (the field phase and the SpMV need it); velocity and gains are only
+    // read by the move, so they upload on a copy stream under the field + SpMV
+    SideStream* ss = nullptr;
+    TSNET_CUDA(side_stream(ss));
+    TSNET_CUDA(cudaEventRecord(ss->fork, s));                  // after the previous work on s
+    TSNET_CUDA(cudaStreamWaitEvent(ss->copy, ss->fork, 0));
     TSNET_CUDA(cudaMemcpyAsync(dY, Y_host, b, cudaMemcpyHostToDevice, s));
-    TSNET_CUDA(cudaMemcpyAsync(dV, vel_host, b, cudaMemcpyHostToDevice, s));
-    TSNET_CUDA(cudaMemcpyAsync(dG, gains_host, b, cudaMemcpyHostToDevice, s));
-    int st = tsnet_step(P, reinterpret_cast<float*>(dY), reinterpret_cast<float*>(dV), reinterpret_cast<float*>(dG),
-                        gp, sp, shard, ws, ws_bytes, stream);
+    TSNET_CUDA(cudaMemcpyAsync(dV, vel_host, b, cudaMemcpyHostToDevice, ss->copy));
+    TSNET_CUDA(cudaMemcpyAsync(dG, gains_host, b, cudaMemcpyHostToDevice, ss->copy));
+    TSNET_CUDA(cudaEventRecord(ss->copied, ss->copy));
+    int st = step_impl(P, reinterpret_cast<float*>(dY), reinterpret_cast<float*>(dV), reinterpret_cast<float*>(dG),
+                       gp, sp, shard, ws, ws_bytes, s, ss->copied);
     if (st != TSNET_OK) return st;
     TSNET_CUDA(cudaMemcpyAsync(Y_host, dY, b, cudaMemcpyDeviceToHost, s));
     TSNET_CUDA(cudaMemcpyAsync(vel_host, dV, b, cudaMemcpyDeviceToHost, s));
