@@ -304,7 +304,7 @@ __device__ __forceinline__ float2 gather_field(const Geo& g, const float4* __res
         const float ey = (u.y - s[bb]) * h_b;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            const float4 f = __ldg(row + a);
+            const float4 f = row[a];   // generic load: fgrid may be the shared-memory copy
             const float wgt = Lx[a] * Ly[bb];
             const float ex = (u.x - s[a]) * h_b;
             fx = fmaf(wgt, fmaf(ex, f.x, f.y), fx);
@@ -342,17 +342,32 @@ __device__ __forceinline__ void gains_move(float gr, float& v, float& gn, float&
     y = y + v;
 }
 
-// n = rows of this call (local; Y, vel, gains point at the first own row); cn = lambda_c / n_global
-__global__ void __launch_bounds__(256) k_update(int64_t n, Geo* __restrict__ gp, const float4* __restrict__ fgrid,
-                                                const int* __restrict__ box, const float2* __restrict__ uv,
-                                                float2* __restrict__ Y, const float2* __restrict__ Fa,
-                                                float2* __restrict__ vel, float2* __restrict__ gains, float lambda_kl,
-                                                float cn, tsnet_step_params sp) {
+// n = rows of this call (local; Y, vel, gains point at the first own row); cn = lambda_c / n_global.
+// When the field grid (N^2 float4) fits the dynamic shared memory of the launch
+// (grid_cap cells), each CTA stages it first: the 9 node gathers per point then
+// cost no L2 requests (they were ~9 sector requests per point).
+constexpr int kUpdateThreads = 1024;
+constexpr int kGridSmemCells = 12800;   // 200 KB of float4
+__global__ void __launch_bounds__(kUpdateThreads, 1) k_update(int64_t n, Geo* __restrict__ gp,
+                                                              const float4* __restrict__ fgrid,
+                                                              const int* __restrict__ box, const float2* __restrict__ uv,
+                                                              float2* __restrict__ Y, const float2* __restrict__ Fa,
+                                                              float2* __restrict__ vel, float2* __restrict__ gains,
+                                                              float lambda_kl, float cn, tsnet_step_params sp,
+                                                              int grid_cap) {
+    extern __shared__ float4 fsm[];
     const Geo g = *gp;
+    const int cells = g.N * g.N;
+    const float4* fg = fgrid;
+    if (cells <= grid_cap) {
+        for (int q = threadIdx.x; q < cells; q += blockDim.x) fsm[q] = __ldg(fgrid + q);
+        __syncthreads();
+        fg = fsm;
+    }
     double sx = 0.0, sy = 0.0;
     bool bad = false;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const float2 ff = gather_field(g, fgrid, box[i], uv[i]);
+        const float2 ff = gather_field(g, fg, box[i], uv[i]);
         float2 y = Y[i];
         const float2 fa = Fa[i];
         const float gx = fmaf(4.0f * lambda_kl, fa.x, ff.x) + cn * y.x;
@@ -410,8 +425,18 @@ cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,
                           const tsnet_step_params& sp, cudaStream_t s) {
     const int64_t nl = a.re - a.rb;
-    k_update<<<pts_blocks(nl), 256, 0, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, Y + a.rb, w.f_attr, vel + a.rb,
-                                            gains + a.rb, a.lambda_kl, cn_of(a), sp);
+    const int cap = (int)std::min<int64_t>((int64_t)w.N_max * w.N_max, kGridSmemCells);
+    const size_t smem = sizeof(float4) * (size_t)cap;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(sizeof(float4) * kGridSmemCells));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nl + kUpdateThreads - 1) / kUpdateThreads, kNumSMs));
+    k_update<<<blocks, kUpdateThreads, smem, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, Y + a.rb, w.f_attr, vel + a.rb,
+                                                  gains + a.rb, a.lambda_kl, cn_of(a), sp, cap);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !sp.recenter) return e;
     k_recenter<<<pts_blocks(a.n), 256, 0, s>>>(a.n, w.geo, Y);
