@@ -315,6 +315,16 @@ def run_ours(args, rank, world, local_rank):
         if "l2_request_path_utilization" in rec:
             limiter = {"what": limiter, "l1tex_to_l2_request_path_util": rec["l2_request_path_utilization"],
                        "lts_tag_request_util": rec["lts_tag_request_utilization"], "source": rec["source"]}
+    gc = os.path.join(ROOT, "profiles", "gather_ceiling_b200.json")
+    if os.path.exists(gc) and not args.plan:
+        with open(gc) as f:
+            ceil = float(json.load(f)["global_gathers_per_s"])
+        # one Y[j] gather per stored entry; the measured random-gather ceiling bounds the SpMV
+        # at nnz / ceiling whatever the HBM bandwidth
+        g = {"gathers_per_s": nnz_l / (spmv_ms * 1e-3), "ceiling_gathers_per_s": ceil,
+             "frac": nnz_l / (spmv_ms * 1e-3) / ceil, "hbm_frac_at_ceiling": spmv_bytes * ceil / nnz_l / 1e9 / peak,
+             "source": "profiles/gather_ceiling_b200.json"}
+        limiter = {"what": limiter, "gather_ceiling": g} if not isinstance(limiter, dict) else {**limiter, "gather_ceiling": g}
 
     # end to end through the host-buffer API (H2D + step + D2H every step)
     e2e = None

@@ -226,9 +226,16 @@ TSNET_API int tsnet_step(const tsnet_csr* P, float* Y, float* vel, float* gains,
 /*
  * Same as tsnet_step with HOST state buffers (pinned host memory recommended):
  * copies Y, vel, gains host -> device into the workspace, runs one iteration
- * and copies them back device -> host, all on `stream`.  P stays on the device.
- * BLOCKING (synchronises `stream` before returning).  Used for the end-to-end
- * measurement of the host-facing API.
+ * and copies them back device -> host.  P stays on the device.  BLOCKING
+ * (returns after the results are in the host buffers; work is ordered after
+ * earlier work on `stream`).  Used for the end-to-end measurement of the
+ * host-facing API.
+ * Without recentring, shards or a plan (and n >= 8 * 16384), the rows are
+ * processed in TSNET_HOST_CHUNKS (default 8) row chunks so that the download
+ * of a moved chunk overlaps the attractive SpMV of the next ones; the new
+ * positions go to a separate workspace buffer until every chunk's SpMV has
+ * read the old ones.  Results equal tsnet_step's up to fp32 summation order
+ * of rows split across warps.
  */
 TSNET_API int tsnet_step_host(const tsnet_csr* P, float* Y_host, float* vel_host, float* gains_host,
                     const tsnet_grad_params* gp, const tsnet_step_params* sp, const tsnet_shard* shard,

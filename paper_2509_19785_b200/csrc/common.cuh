@@ -84,7 +84,7 @@ struct Ws {
     float2* spec;        // 10 * (M_max/2+1) * M_max : forward row spectra, [a][kx][y]
     float2* colout;      // 6 * (M_max/2+1) * N_max  : after column pass, [b][kx][y]
     float4* fgrid;       // N_max^2 fields (P0, Qx, Qy, 0), row-major [gy][gx]
-    float2* state;       // 3 n : host-facing step staging (Y, vel, gains)
+    float2* state;       // 4 n : host-facing step staging (Y, vel, gains, next Y)
     double* cost;        // scratch for tsnet_cost (4 doubles)
     int64_t n, nnz;
     int I_max, N_max, M_max, max_items;
@@ -127,7 +127,7 @@ inline Ws ws_map(void* base, int64_t n, int64_t nnz, int I_max) {
     w.spec = (float2*)take(sizeof(float2) * 10 * half * (size_t)w.M_max);
     w.colout = (float2*)take(sizeof(float2) * 6 * half * (size_t)w.N_max);
     w.fgrid = (float4*)take(sizeof(float4) * (size_t)w.N_max * w.N_max);
-    w.state = (float2*)take(sizeof(float2) * 3 * n);
+    w.state = (float2*)take(sizeof(float2) * 4 * n);
     w.cost = (double*)take(sizeof(double) * 8);
     w.bytes = off;
     return w;
@@ -156,6 +156,16 @@ cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2
                             cudaStream_t s);
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,
                           const tsnet_step_params& sp, cudaStream_t s);
+// Row-chunk pieces of the same two steps (rows [r0, r1) inside the call's [rb, re)),
+// used by the pipelined host step: the SpMV of a chunk (its rows of w.f_attr
+// must be zero before the call; nnz_rows = its stored entries, which size the
+// grid), and the move of a chunk
+// reading a.Y and writing the new positions to Yout (never a.Y: the other chunks'
+// SpMV still gathers the old positions).  No recentring.
+cudaError_t launch_spmv_rows(const Ws& w, const GradArgs& a, int64_t r0, int64_t r1, int64_t nnz_rows,
+                             cudaStream_t s);
+cudaError_t launch_update_rows(const Ws& w, const GradArgs& a, int64_t r0, int64_t r1, float2* Yout, float2* vel,
+                               float2* gains, const tsnet_step_params& sp, cudaStream_t s);
 cudaError_t launch_cost(const Ws& w, const GradArgs& a, int mode, double* out3, cudaStream_t s);
 cudaError_t launch_entropy_sum(const Ws& w, const GradArgs& a, cudaStream_t s);
 

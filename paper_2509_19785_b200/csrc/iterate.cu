@@ -207,8 +207,6 @@ __global__ void __launch_bounds__(256) k_spmv2(int64_t rb, int64_t re_rows, cons
 }
 
 // Launch configuration of the row-wise kernel.  Defaults are the measured best
-// on B200 (profiles/); TSNET_SPMV_{U,CHUNK,CTAS,L1} override them for probing.
-// Launch configuration of the row-wise kernel.  Defaults are the measured best
 // on B200 (profiles/, scripts/gpu_spmv_sweep.sh); TSNET_SPMV_{U,CPW,CTAS,L1}
 // override them for probing.
 struct SpmvCfg {
@@ -218,6 +216,7 @@ struct SpmvCfg {
     int ctas_per_sm = 5; // 256-thread CTAs per SM
     int l1 = 1;          // prefer L1 over shared memory (carveout 0)
     int reserve = 0;     // SMs left free for the concurrent field phase (side stream)
+    int cpw_rows = 2;    // chunks per warp in the row-chunk launches of the pipelined host step
 };
 
 static int env_int(const char* name, int def) {
@@ -233,6 +232,7 @@ static const SpmvCfg& spmv_cfg() {
         if (k && !strcmp(k, "v1")) c.kernel = 1;
         c.U = env_int("TSNET_SPMV_U", c.U);
         c.cpw = std::max(1, env_int("TSNET_SPMV_CPW", c.cpw));
+        c.cpw_rows = std::max(1, env_int("TSNET_SPMV_CPW_ROWS", c.cpw_rows));
         c.ctas_per_sm = std::max(1, env_int("TSNET_SPMV_CTAS", c.ctas_per_sm));
         c.l1 = env_int("TSNET_SPMV_L1", c.l1);
         c.reserve = std::max(0, std::min(64, env_int("TSNET_SPMV_RESERVE_SMS", c.reserve)));
@@ -351,7 +351,8 @@ constexpr int kGridSmemCells = 12800;   // 200 KB of float4
 __global__ void __launch_bounds__(kUpdateThreads, 1) k_update(int64_t n, Geo* __restrict__ gp,
                                                               const float4* __restrict__ fgrid,
                                                               const int* __restrict__ box, const float2* __restrict__ uv,
-                                                              float2* __restrict__ Y, const float2* __restrict__ Fa,
+                                                              const float2* Yin, float2* Yout,
+                                                              const float2* __restrict__ Fa,
                                                               float2* __restrict__ vel, float2* __restrict__ gains,
                                                               float lambda_kl, float cn, tsnet_step_params sp,
                                                               int grid_cap) {
@@ -368,7 +369,7 @@ __global__ void __launch_bounds__(kUpdateThreads, 1) k_update(int64_t n, Geo* __
     bool bad = false;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float2 ff = gather_field(g, fg, box[i], uv[i]);
-        float2 y = Y[i];
+        float2 y = Yin[i];
         const float2 fa = Fa[i];
         const float gx = fmaf(4.0f * lambda_kl, fa.x, ff.x) + cn * y.x;
         const float gy = fmaf(4.0f * lambda_kl, fa.y, ff.y) + cn * y.y;
@@ -376,7 +377,7 @@ __global__ void __launch_bounds__(kUpdateThreads, 1) k_update(int64_t n, Geo* __
         gains_move(gx, v.x, gn.x, y.x, sp);
         gains_move(gy, v.y, gn.y, y.y, sp);
         bad |= !(isfinite(y.x) && isfinite(y.y));
-        Y[i] = y;
+        Yout[i] = y;
         vel[i] = v;
         gains[i] = gn;
         sx += y.x;
@@ -421,25 +422,64 @@ cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2
     return e;
 }
 
+static cudaError_t update_smem_attr() {
+    static bool done = false;
+    if (done) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(float4) * kGridSmemCells));
+    done = e == cudaSuccess;
+    return e;
+}
+
 // Y, vel, gains: full n x 2 arrays; rows [rb, re) are updated
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,
                           const tsnet_step_params& sp, cudaStream_t s) {
     const int64_t nl = a.re - a.rb;
     const int cap = (int)std::min<int64_t>((int64_t)w.N_max * w.N_max, kGridSmemCells);
     const size_t smem = sizeof(float4) * (size_t)cap;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(sizeof(float4) * kGridSmemCells));
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    cudaError_t ea = update_smem_attr();
+    if (ea != cudaSuccess) return ea;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nl + kUpdateThreads - 1) / kUpdateThreads, kNumSMs));
-    k_update<<<blocks, kUpdateThreads, smem, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, Y + a.rb, w.f_attr, vel + a.rb,
-                                                  gains + a.rb, a.lambda_kl, cn_of(a), sp, cap);
+    k_update<<<blocks, kUpdateThreads, smem, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, Y + a.rb, Y + a.rb, w.f_attr,
+                                                  vel + a.rb, gains + a.rb, a.lambda_kl, cn_of(a), sp, cap);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !sp.recenter) return e;
     k_recenter<<<pts_blocks(a.n), 256, 0, s>>>(a.n, w.geo, Y);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_spmv_rows(const Ws& w, const GradArgs& a, int64_t r0, int64_t r1, int64_t nnz_rows,
+                             cudaStream_t s) {
+    if (a.plan || r0 < a.rb || r1 > a.re || r0 > r1) return cudaErrorInvalidValue;
+    const int64_t nc = r1 - r0;
+    float2* F = w.f_attr + (r0 - a.rb);     // zeroed by the caller (rows split across warps add)
+    if (a.nnz == 0 || nc == 0) return cudaSuccess;
+    GradArgs b = a;
+    b.rb = r0;
+    b.re = r1;
+    b.nnz = std::max<int64_t>(1, nnz_rows);     // sizes the grid
+    // a chunk is ~1/8 of P: fewer, longer pieces per warp (each piece starts
+    // with a row search and a pipeline ramp)
+    SpmvCfg c = spmv_cfg();
+    c.cpw = c.cpw_rows;
+    switch (c.U) {
+        case 2: return launch_spmv2_t<2>(b, F, c, s);
+        case 8: return launch_spmv2_t<8>(b, F, c, s);
+        default: return launch_spmv2_t<4>(b, F, c, s);
+    }
+}
+
+cudaError_t launch_update_rows(const Ws& w, const GradArgs& a, int64_t r0, int64_t r1, float2* Yout, float2* vel,
+                               float2* gains, const tsnet_step_params& sp, cudaStream_t s) {
+    if (sp.recenter || r0 < a.rb || r1 > a.re || r0 > r1) return cudaErrorInvalidValue;
+    const int64_t nc = r1 - r0, q = r0 - a.rb;
+    if (nc == 0) return cudaSuccess;
+    // no shared-memory grid here: this move runs beside the SpMV of the next
+    // chunk, whose CTAs run with the whole L1 carveout (a 200 KB shared-memory
+    // CTA would wait for an idle SM); the field nodes are read through L1/L2
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nc + kUpdateThreads - 1) / kUpdateThreads, kNumSMs));
+    k_update<<<blocks, kUpdateThreads, 0, s>>>(nc, w.geo, w.fgrid, w.box + q, w.uv + q, a.Y + r0, Yout + r0,
+                                               w.f_attr + q, vel + r0, gains + r0, a.lambda_kl, cn_of(a), sp, 0);
     return cudaGetLastError();
 }
 

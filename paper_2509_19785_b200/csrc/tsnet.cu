@@ -108,10 +108,13 @@ static size_t grid_floats(const Ws& w) { return (size_t)4 * w.N_max * w.N_max; }
 // independent of the attractive SpMV until the gather/update: the two chains
 // run concurrently (fork/join by events, so the pattern is also captured into
 // a CUDA graph as two branches).  TSNET_FIELD_STREAM=0 keeps one stream.
+constexpr int kHostChunksMax = 16;
+
 struct SideStream {
     int dev = -1;
-    cudaStream_t side = nullptr, copy = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr, copied = nullptr;
+    cudaStream_t side = nullptr, copy = nullptr, d2h = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr, copied = nullptr, y_in = nullptr, drained = nullptr;
+    cudaEvent_t attr_done[kHostChunksMax] = {}, moved[kHostChunksMax] = {}, state_in[kHostChunksMax] = {};
 };
 
 static bool side_enabled() {
@@ -130,11 +133,24 @@ static cudaError_t side_stream(SideStream*& out) {
     if (e != cudaSuccess) return e;
     SideStream& x = ss[dev & 15];
     if (x.dev != dev) {
-        if ((e = cudaStreamCreateWithFlags(&x.side, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        // the field chain is a row of short dependent kernels: at the highest
+        // priority its CTAs go ahead of queued SpMV CTAs instead of waiting
+        // for the SpMV's waves to drain
+        int lo = 0, hi = 0;
+        if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithPriority(&x.side, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
         if ((e = cudaStreamCreateWithFlags(&x.copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithFlags(&x.d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
         if ((e = cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
         if ((e = cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming)) != cudaSuccess) return e;
         if ((e = cudaEventCreateWithFlags(&x.copied, cudaEventDisableTiming)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&x.y_in, cudaEventDisableTiming)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&x.drained, cudaEventDisableTiming)) != cudaSuccess) return e;
+        for (int c = 0; c < kHostChunksMax; ++c) {
+            if ((e = cudaEventCreateWithFlags(&x.attr_done[c], cudaEventDisableTiming)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&x.moved[c], cudaEventDisableTiming)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&x.state_in[c], cudaEventDisableTiming)) != cudaSuccess) return e;
+        }
         x.dev = dev;
     }
     out = &x;
@@ -327,6 +343,175 @@ int tsnet_step_finish(const tsnet_csr* P, float* Y, float* vel, float* gains, co
     return TSNET_OK;
 }
 
+}  // extern "C"
+
+namespace tsnet {
+
+// Row chunks of the pipelined host step (TSNET_HOST_CHUNKS, default 8; 1 = no pipeline).
+static int host_chunks(int64_t n) {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TSNET_HOST_CHUNKS");
+        v = e ? std::max(1, std::min(kHostChunksMax, atoi(e))) : 8;
+    }
+    return n >= (int64_t)v * 16384 ? v : 1;
+}
+
+// Row cut of the pipelined host step: chunk c ends at the first row whose
+// indptr reaches nnz * (c + 1) / chunks (equal SpMV work per chunk).  Found by
+// binary search over the device indptr with single-entry reads, once per
+// (indptr, n, nnz, chunks) and cached; any cut is correct, the cut only
+// balances the pipeline.
+static int chunk_rows(const tsnet_csr* P, int chunks, int64_t* cut, int64_t* cut_nnz) {
+    struct Entry {
+        const void* indptr = nullptr;
+        int64_t n = -1, nnz = -1;
+        int chunks = 0;
+        int64_t cut[kHostChunksMax + 1], cut_nnz[kHostChunksMax + 1];
+    };
+    static thread_local Entry cache[4];
+    static thread_local int next = 0;
+    for (auto& e : cache)
+        if (e.indptr == P->indptr && e.n == P->n && e.nnz == P->nnz && e.chunks == chunks) {
+            std::memcpy(cut, e.cut, sizeof(int64_t) * (chunks + 1));
+            std::memcpy(cut_nnz, e.cut_nnz, sizeof(int64_t) * (chunks + 1));
+            return TSNET_OK;
+        }
+    const int64_t n = P->n;
+    cut[0] = 0;
+    cut[chunks] = n;
+    cut_nnz[0] = 0;
+    cut_nnz[chunks] = P->nnz;
+    for (int c = 1; c < chunks; ++c) {
+        const int64_t target = (int64_t)((double)P->nnz * c / chunks);
+        int64_t lo = cut[c - 1], hi = n;          // first row r with indptr[r] >= target
+        while (lo < hi) {
+            const int64_t mid = lo + (hi - lo) / 2;
+            int64_t v = 0;
+            TSNET_CUDA(cudaMemcpy(&v, P->indptr + mid, sizeof(int64_t), cudaMemcpyDeviceToHost));
+            if (v >= target) hi = mid; else lo = mid + 1;
+        }
+        cut[c] = std::max(lo, cut[c - 1]);
+        TSNET_CUDA(cudaMemcpy(&cut_nnz[c], P->indptr + cut[c], sizeof(int64_t), cudaMemcpyDeviceToHost));
+    }
+    Entry& e = cache[next++ & 3];
+    e.indptr = P->indptr;
+    e.n = P->n;
+    e.nnz = P->nnz;
+    e.chunks = chunks;
+    std::memcpy(e.cut, cut, sizeof(int64_t) * (chunks + 1));
+    std::memcpy(e.cut_nnz, cut_nnz, sizeof(int64_t) * (chunks + 1));
+    return TSNET_OK;
+}
+
+// TSNET_HOST_TRACE=1: the pipelined host step records timing events at its
+// stage boundaries and prints them (ms after the call's first copy) to stderr.
+struct HostTrace {
+    bool on = false;
+    int k = 0;
+    cudaEvent_t ev[64] = {};
+    const char* name[64] = {};
+    int idx[64] = {};
+    void init() {
+        static int v = -1;
+        if (v < 0) v = getenv("TSNET_HOST_TRACE") ? 1 : 0;
+        on = v == 1;
+    }
+    void mark(const char* what, int i, cudaStream_t st) {
+        if (!on || k >= 64) return;
+        if (!ev[k]) cudaEventCreate(&ev[k]);
+        cudaEventRecord(ev[k], st);
+        name[k] = what;
+        idx[k++] = i;
+    }
+    void print() {
+        if (!on || k == 0) return;
+        cudaEventSynchronize(ev[k - 1]);
+        for (int q = 0; q < k; ++q) {
+            cudaEventSynchronize(ev[q]);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[0], ev[q]);
+            fprintf(stderr, "%s%s[%d] %.3f", q ? "  " : "trace ", name[q], idx[q], ms);
+        }
+        fprintf(stderr, "\n");
+        for (int q = 0; q < k; ++q) cudaEventDestroy(ev[q]);
+        k = 0;
+    }
+};
+
+// tsnet_step_host without recentring, shards or a plan: the host transfers of
+// the state overlap the attractive SpMV.  Rows are cut into `chunks` chunks.
+// Streams: `s` uploads Y, then runs the SpMV of chunk after chunk; `copy`
+// uploads vel/gains chunk by chunk after Y; the side stream runs the field chain,
+// then the move of each chunk once its SpMV and its vel/gains are in (new
+// positions into a second buffer: later chunks' SpMV still gathers the old Y);
+// `d2h` downloads each moved chunk.  Same arithmetic as step_impl.
+static int step_host_pipelined(const tsnet_csr* P, float* Y_host, float* vel_host, float* gains_host,
+                               const tsnet_grad_params* gp, const tsnet_step_params* sp, void* ws, size_t ws_bytes,
+                               cudaStream_t s, SideStream* ss, int chunks, float2* state) {
+    const int64_t n = P->n;
+    float2* dY = state;
+    float2* dV = state + n;
+    float2* dG = state + 2 * n;
+    float2* dYn = state + 3 * n;
+    const size_t b = sizeof(float2) * (size_t)n;
+    int64_t cut[kHostChunksMax + 1], cut_nnz[kHostChunksMax + 1];
+    int st0 = chunk_rows(P, chunks, cut, cut_nnz);
+    if (st0 != TSNET_OK) return st0;
+    auto rows = [&](int c) { return cut[c]; };
+    HostTrace tr;
+    tr.init();
+    tr.mark("start", 0, s);
+    TSNET_CUDA(cudaMemcpyAsync(dY, Y_host, b, cudaMemcpyHostToDevice, s));
+    TSNET_CUDA(cudaEventRecord(ss->y_in, s));
+    tr.mark("y_in", 0, s);
+    // vel/gains after Y (they share the host link; Y gates everything)
+    TSNET_CUDA(cudaStreamWaitEvent(ss->copy, ss->y_in, 0));
+    for (int c = 0; c < chunks; ++c) {
+        const size_t o = 2 * (size_t)rows(c), cb = sizeof(float2) * (size_t)(rows(c + 1) - rows(c));
+        TSNET_CUDA(cudaMemcpyAsync(dV + rows(c), vel_host + o, cb, cudaMemcpyHostToDevice, ss->copy));
+        TSNET_CUDA(cudaMemcpyAsync(dG + rows(c), gains_host + o, cb, cudaMemcpyHostToDevice, ss->copy));
+        TSNET_CUDA(cudaEventRecord(ss->state_in[c], ss->copy));
+        tr.mark("vg_in", c, ss->copy);
+    }
+    Ws w;
+    GradArgs a;
+    int st = prepare(P, reinterpret_cast<float*>(dY), gp, nullptr, ws, ws_bytes, w, a);
+    if (st != TSNET_OK) return st;
+    cudaStream_t fs = ss->side;
+    TSNET_CUDA(cudaStreamWaitEvent(fs, ss->y_in, 0));
+    TSNET_CUDA(launch_field_local(w, a, fs, false));
+    TSNET_CUDA(launch_field_conv(w, a, fs));
+    tr.mark("field", 0, fs);
+    TSNET_CUDA(cudaMemsetAsync(w.f_attr, 0, b, s));
+    for (int c = 0; c < chunks; ++c) {
+        const int64_t r0 = rows(c), r1 = rows(c + 1);
+        TSNET_CUDA(launch_spmv_rows(w, a, r0, r1, cut_nnz[c + 1] - cut_nnz[c], s));
+        TSNET_CUDA(cudaEventRecord(ss->attr_done[c], s));
+        tr.mark("spmv", c, s);
+        TSNET_CUDA(cudaStreamWaitEvent(fs, ss->attr_done[c], 0));
+        TSNET_CUDA(cudaStreamWaitEvent(fs, ss->state_in[c], 0));
+        TSNET_CUDA(launch_update_rows(w, a, r0, r1, dYn, dV, dG, *sp, fs));
+        TSNET_CUDA(cudaEventRecord(ss->moved[c], fs));
+        tr.mark("move", c, fs);
+        TSNET_CUDA(cudaStreamWaitEvent(ss->d2h, ss->moved[c], 0));
+        const size_t o = 2 * (size_t)r0, cb = sizeof(float2) * (size_t)(r1 - r0);
+        TSNET_CUDA(cudaMemcpyAsync(Y_host + o, dYn + r0, cb, cudaMemcpyDeviceToHost, ss->d2h));
+        TSNET_CUDA(cudaMemcpyAsync(vel_host + o, dV + r0, cb, cudaMemcpyDeviceToHost, ss->d2h));
+        TSNET_CUDA(cudaMemcpyAsync(gains_host + o, dG + r0, cb, cudaMemcpyDeviceToHost, ss->d2h));
+        tr.mark("d2h", c, ss->d2h);
+    }
+    TSNET_CUDA(cudaEventRecord(ss->drained, ss->d2h));
+    TSNET_CUDA(cudaStreamWaitEvent(s, ss->drained, 0));
+    TSNET_CUDA(cudaStreamSynchronize(s));
+    tr.print();
+    return TSNET_OK;
+}
+
+}  // namespace tsnet
+
+extern "C" {
+
 int tsnet_step_host(const tsnet_csr* P, float* Y_host, float* vel_host, float* gains_host,
                     const tsnet_grad_params* gp, const tsnet_step_params* sp, const tsnet_shard* shard, void* ws,
                     size_t ws_bytes, tsnet_stream_t stream) {
@@ -346,6 +531,13 @@ int tsnet_step_host(const tsnet_csr* P, float* Y_host, float* vel_host, float* g
     SideStream* ss = nullptr;
     TSNET_CUDA(side_stream(ss));
     TSNET_CUDA(cudaEventRecord(ss->fork, s));                  // after the previous work on s
+    const int chunks = host_chunks(n);
+    if (chunks > 1 && sp != nullptr && !sp->recenter && P->plan == nullptr && !sharded(shard, n) &&
+        (shard == nullptr || shard->comm == nullptr) && side_enabled()) {
+        TSNET_CUDA(cudaStreamWaitEvent(ss->side, ss->fork, 0));
+        TSNET_CUDA(cudaStreamWaitEvent(ss->copy, ss->fork, 0));
+        return step_host_pipelined(P, Y_host, vel_host, gains_host, gp, sp, ws, ws_bytes, s, ss, chunks, w0.state);
+    }
     TSNET_CUDA(cudaStreamWaitEvent(ss->copy, ss->fork, 0));
     TSNET_CUDA(cudaMemcpyAsync(dY, Y_host, b, cudaMemcpyHostToDevice, s));
     TSNET_CUDA(cudaMemcpyAsync(dV, vel_host, b, cudaMemcpyHostToDevice, ss->copy));

@@ -15,7 +15,8 @@ import torch
 
 import oracle
 from paper_2509_19785_b200 import (CSR, GradParams, StepParams, TsnetError, alloc_workspace, tsnet_build_P,
-                                   tsnet_cost, tsnet_grad, tsnet_grad_parts, tsnet_read_stats, tsnet_step)
+                                   tsnet_cost, tsnet_grad, tsnet_grad_parts, tsnet_read_stats, tsnet_step,
+                                   tsnet_step_host)
 from paper_2509_19785_b200 import tsnet as T
 from workloads import (clustered_layout, config_graph, erdos_renyi, grid2d, init_layout, path_graph, random_state,
                        star_graph, uniform_layout)
@@ -316,6 +317,35 @@ def test_step_parity_common_state(stage):
     assert relL2(Yd.cpu().numpy(), Yo) <= 1e-6
     small = np.abs(r["g"]) < 1e-6 * np.abs(r["g"]).max()
     assert np.array_equal(np.isclose(Gd.cpu().numpy(), Go, rtol=1e-5)[~small], np.ones((~small).sum(), bool))
+
+
+@pytest.mark.parametrize("cfg,recenter", [(3, 0), (3, 1), (2, 0)])
+def test_step_host_equals_device_step(cfg, recenter):
+    """tsnet_step_host (host buffers; cfg 3 takes the pipelined row-chunk path,
+    cfg 2 and recentring the plain one) gives tsnet_step's iteration, and the
+    oracle's."""
+    P = oracle_P(cfg)
+    n = P["n"]
+    Y = clustered_layout(n, 20.0, 5, 1.5, 7)
+    vel, gains = random_state(n, 3)
+    gp, sp = GradParams(*STAGE_B), StepParams(eta=50.0, momentum=0.8, recenter=recenter)
+    Pd = dev_P(P)
+    ws = alloc_workspace(n, Pd.nnz, gp)
+    Yh, Vh, Gh = (torch.from_numpy(a.copy()).pin_memory() for a in (Y, vel, gains))
+    tsnet_step_host(Pd, Yh, Vh, Gh, gp, sp, ws)
+    Yd, Vd, Gd = (torch.from_numpy(a.copy()).cuda() for a in (Y, vel, gains))
+    tsnet_step(Pd, Yd, Vd, Gd, gp, sp, alloc_workspace(n, Pd.nnz, gp))
+    torch.cuda.synchronize()
+    assert relL2(Vh.numpy(), Vd.cpu().numpy()) <= 1e-5
+    assert relL2(Yh.numpy(), Yd.cpu().numpy()) <= 1e-6
+    assert relL2(Gh.numpy(), Gd.cpu().numpy()) <= 1e-6
+    r = oracle_grad(P, Y, STAGE_B)
+    Yo, Vo, _ = oracle.update_step(Y, vel, gains, r["g"], eta=50.0, mu=0.8)
+    assert relL2(Vh.numpy(), Vo) <= GRAD_TOL
+    if recenter:
+        assert np.abs(Yh.numpy().astype(np.float64).mean(0)).max() <= 1e-4 * np.abs(Yo).max()
+    else:
+        assert relL2(Yh.numpy(), Yo) <= 1e-6
 
 
 def test_ten_iterations_config1():
