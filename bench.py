@@ -208,7 +208,7 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_2509_19785_b200 import (Layout, tsnet_attr, tsnet_build_P, tsnet_plan_build, tsnet_read_stats,
-                                       tsnet_step_host)
+                                       tsnet_sell_build, tsnet_step_host)
     from workloads import config_graph, init_layout
 
     dev = torch.device("cuda", local_rank)
@@ -226,12 +226,14 @@ def run_ours(args, rank, world, local_rank):
     if world > 1 or args.sharded:
         # row shards + NCCL communicator (+ the plan of the own rows) (set-up, untimed)
         from paper_2509_19785_b200.distributed import ShardedLayout
-        lay = ShardedLayout(P, Y0, rank, world, plan=args.plan)
+        lay = ShardedLayout(P, Y0, rank, world, plan=args.plan or False)
         shard = lay.shard
         rb, re = lay.rows
     else:
-        if args.plan:
+        if args.plan == "cb":
             tsnet_plan_build(P)               # column-blocked layout of P (set-up, untimed)
+        elif args.plan == "sell":
+            tsnet_sell_build(P)               # sliced-ELL layout of P (set-up, untimed)
         lay = Layout(P, Y0, use_graphs=True)
         shard, rb, re = None, 0, n
     torch.cuda.synchronize()
@@ -305,7 +307,7 @@ def run_ours(args, rank, world, local_rank):
     step_bytes = 8 * nnz_l + 8 * (nl + 1) + 48 * nl + 8 * (n - nl)
     traffic = None
     limiter = None
-    kname = "k_attr_cb" if args.plan else "k_spmv2"
+    kname = {"cb": "k_attr_cb", "sell": "k_attr_sell"}.get(args.plan, "k_spmv2")
     tp = os.path.join(ROOT, "profiles", f"{kname}_dram_bytes_cfg{args.config}.json")
     if os.path.exists(tp) and world == 1:
         with open(tp) as f:
@@ -366,7 +368,8 @@ def run_ours(args, rank, world, local_rank):
                                        "grid_N_window_start": grid_start["N"], "span_window_start":
                                        round(grid_start["S"], 3), "stage_a_iters_per_s": None if stage_a_ms is None else round(1e3 / stage_a_ms, 1),
                                        "c0_gpu_s": round(c0_s, 3), "parallelism": par,
-                                       "attr_layout": "column-blocked plan" if args.plan else "CSR",
+                                       "attr_layout": {"cb": "column-blocked plan", "sell": "sliced-ELL plan"}.get(
+                                           args.plan, "CSR"),
                                        "plan_build_s": None if plan_s is None else round(plan_s, 3)}),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic, "kernel": f"{kname} (tsnet_attr)",
@@ -391,7 +394,9 @@ def main():
     ap.add_argument("--pre-iters", type=int, default=250)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--plan", action="store_true", help="column-blocked plan kernel for the SpMV instead of CSR")
+    ap.add_argument("--plan", nargs="?", const="cb", default=None, choices=["cb", "sell"],
+                    help="plan kernel for the SpMV instead of CSR: cb = column-blocked (default of a bare --plan), "
+                         "sell = sliced ELL")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU (NCCL) path even on one rank (needs torchrun / a process group)")
     ap.add_argument("--cpu-budget", type=float, default=12.0)

@@ -64,11 +64,14 @@ typedef struct {
 /* Sparse symmetric affinity matrix P (Eq. 2) in CSR.
  * `capacity` = allocated length of indices/values (input to tsnet_build_P),
  * `nnz` = stored entries (output of tsnet_build_P, input elsewhere).
- * `plan` = optional column-blocked copy of the same P built by
- * tsnet_plan_build (device, caller-owned; NULL = none).  When set, the
- * attractive SpMV (step a6) reads the plan instead of indices/values; the
- * caller must rebuild it whenever P's pattern or values change (the library
- * cannot detect a stale plan). */
+ * `plan` = optional re-laid-out copy of the same P (device, caller-owned;
+ * NULL = none) of kind `plan_kind`: TSNET_PLAN_CB (column-blocked,
+ * tsnet_plan_build; 0 also means this kind) or TSNET_PLAN_SELL (sliced ELL,
+ * tsnet_sell_build).  When set, the attractive SpMV (step a6) reads the plan
+ * instead of indices/values; the caller must rebuild it whenever P's pattern
+ * or values change (the library cannot detect a stale plan). */
+#define TSNET_PLAN_CB 1
+#define TSNET_PLAN_SELL 2
 typedef struct {
     int64_t n;
     int64_t nnz;
@@ -76,7 +79,8 @@ typedef struct {
     int64_t* indptr;         /* device, n+1 */
     int32_t* indices;        /* device, capacity */
     float* values;           /* device, capacity */
-    const void* plan;        /* device, tsnet_plan_build output, or NULL */
+    const void* plan;        /* device, tsnet_plan_build / tsnet_sell_build output, or NULL */
+    int32_t plan_kind;       /* TSNET_PLAN_CB (or 0) / TSNET_PLAN_SELL; ignored without a plan */
 } tsnet_csr;
 
 /* Cost multipliers and interpolation grid policy.
@@ -285,6 +289,30 @@ TSNET_API int tsnet_plan_query(const tsnet_csr* P, const tsnet_shard* shard, siz
                                tsnet_stream_t stream);
 TSNET_API int tsnet_plan_build(const tsnet_csr* P, const tsnet_shard* shard, void* plan, size_t plan_bytes, void* ws,
                                size_t ws_bytes, tsnet_stream_t stream);
+/* ------------------------------------------------- sliced-ELL layout of P (a6) */
+
+/*
+ * Same product as the CSR SpMV (Eq. 6 first term), P re-laid
+ * out for graphs whose consecutive vertices have similar neighbourhoods
+ * (meshes, config 5): rows of `shard` (all rows if NULL) in slices of 32
+ * consecutive rows; a lane owns a row, a warp a slice; slot (slice s, step k,
+ * lane) = (column, p_ij) of the k-th stored entry of row 32 s + lane (CSR
+ * order), at base[s] + 32 k + lane, base = exclusive scan of 32 * (longest row
+ * of the slice); missing entries = (own row, 0.0), which add exactly 0.
+ * Result identical to the CSR kernel's up to fp32 summation order.
+ *
+ * tsnet_sell_query : bytes of the plan, and slots per stored entry (>= 1; the
+ *                    padding; large on power-law graphs, where the CSR kernel
+ *                    is the better choice).  BLOCKING (reads P->indptr).
+ * tsnet_sell_build : writes the plan into `plan` (device, 256-byte aligned,
+ *                    >= plan_bytes).  BLOCKING.  Then set P->plan = plan and
+ *                    P->plan_kind = TSNET_PLAN_SELL.  Needs n < 2^31.
+ */
+TSNET_API int tsnet_sell_query(const tsnet_csr* P, const tsnet_shard* shard, size_t* plan_bytes,
+                               double* slots_per_nnz, tsnet_stream_t stream);
+TSNET_API int tsnet_sell_build(const tsnet_csr* P, const tsnet_shard* shard, void* plan, size_t plan_bytes,
+                               tsnet_stream_t stream);
+
 TSNET_API int32_t tsnet_plan_partition(const int64_t* indptr_host, int64_t row_begin, int64_t row_end,
                                        int32_t warps, int32_t rows_max, int32_t base_groups, int64_t max_minitasks,
                                        int32_t* row_mt, int32_t* row_K, int32_t* mt_r0, int32_t* mt_info);

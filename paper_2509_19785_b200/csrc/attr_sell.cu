@@ -1,0 +1,263 @@
+// attr_sell.cu -- sliced-ELL attractive SpMV (step a6, Eq. 6 first term,
+// PAPER.md:162): F_attr,i = sum_{j in row i} p_ij w_ij (X_i - X_j),
+// w_ij = 1 / (1 + |X_i - X_j|^2).
+//
+// Why a third layout of P: on a mesh (config 5) the CSR
+// kernel, one warp per row, gathers Y_j for 32 consecutive entries of ONE row;
+// those columns lie on ~11 different 128-byte lines (the row's ball spans
+// x-, y- and z-neighbours), so the kernel is bound by L1 wavefronts (ncu:
+// l1tex 84%) at ~52% of HBM.  Here a lane owns a row and a warp a slice of 32
+// consecutive rows; at step k every lane reads the k-th entry of its row.  On
+// a mesh the k-th neighbours of consecutive vertices are themselves mostly
+// consecutive, so the 32 gathers of a step touch ~5 lines, and the entry loads
+// are fully coalesced (32 x 8 bytes).  No warp reduction, no atomics: each
+// lane writes its own F_i.
+//
+// Layout (one plan = rows [row_begin, row_end) of P):
+//   slice s = rows row_begin + 32 s .. + 31; K_s = its longest row;
+//   slot (s, k, lane) at base[s] + 32 k + lane, base = exclusive scan of 32 K_s;
+//   slot = (col, p_ij fp32 bits) as a uint2; slots past a row's end hold
+//   (its own row, +0.0f) and add exactly 0 (X_i - X_i = 0, p = 0).
+// On a power-law graph (config 4) slices pad heavily (a hub in a slice) and
+// the gathers stay random: tsnet_sell_query reports the slots per entry so a
+// caller can keep the CSR kernel there.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "common.cuh"
+#include "tsnet.h"
+
+namespace tsnet {
+
+constexpr uint64_t kSellMagic = 0x4c4c455354534e54ull;   // "TNSTSELL"
+
+struct SellHeader {
+    uint64_t magic;
+    int64_t n, row_begin, row_end, nnz, slices, slots;
+    int64_t off_base, off_slots, bytes;
+};
+
+static size_t sell_align(size_t x) { return (x + 255) / 256 * 256; }
+
+__device__ __forceinline__ uint64_t sell_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint2 sell_ld_stream(const uint2* a, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y)
+                 : "l"(a), "l"(pol));
+    return v;
+}
+
+static SellHeader sell_layout(int64_t n, int64_t rb, int64_t re, int64_t nnz, int64_t slots) {
+    SellHeader h{};
+    h.magic = kSellMagic;
+    h.n = n;
+    h.row_begin = rb;
+    h.row_end = re;
+    h.nnz = nnz;
+    h.slices = (re - rb + 31) / 32;
+    h.slots = slots;
+    size_t off = sell_align(sizeof(SellHeader));
+    h.off_base = (int64_t)off;
+    off = sell_align(off + sizeof(int64_t) * (size_t)(h.slices + 1));
+    h.off_slots = (int64_t)off;
+    off = sell_align(off + sizeof(uint2) * (size_t)slots);
+    h.bytes = (int64_t)off;
+    return h;
+}
+
+__device__ __forceinline__ void sell_acc(const float2* __restrict__ Y, float2 yi, uint2 e, float& fx, float& fy) {
+    const float2 yj = __ldg(Y + (int)e.x);
+    const float dx = yi.x - yj.x, dy = yi.y - yj.y;
+    const float w = __frcp_rn(fmaf(dx, dx, fmaf(dy, dy, 1.0f)));
+    const float pw = __uint_as_float(e.y) * w;
+    fx = fmaf(pw, dx, fx);
+    fy = fmaf(pw, dy, fy);
+}
+
+// One warp per slice (grid-stride).  The entry stream is prefetched NS - 1
+// register sets of U steps ahead (HBM latency), the sets rotate by unrolling
+// (no copies of in-flight loads); each set's U gathers of Y_j are in flight
+// together.
+template <int U, int NS>
+__global__ void __launch_bounds__(256) k_attr_sell(const uint8_t* __restrict__ plan, const float2* __restrict__ Y,
+                                                   float2* __restrict__ F) {
+    const SellHeader* h = reinterpret_cast<const SellHeader*>(plan);
+    const int64_t rb = h->row_begin, re = h->row_end, S = h->slices;
+    const int64_t* __restrict__ base = reinterpret_cast<const int64_t*>(plan + h->off_base);
+    const uint2* __restrict__ slots = reinterpret_cast<const uint2*>(plan + h->off_slots);
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t pol = sell_policy_evict_first();
+    for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < S; s += nw) {
+        const int64_t b0 = __ldg(base + s), K = (__ldg(base + s + 1) - b0) >> 5;
+        const int64_t r = rb + s * 32 + lane;
+        const bool live = r < re;
+        const float2 yi = live ? __ldg(Y + r) : make_float2(0.f, 0.f);
+        const uint2* p = slots + b0 + lane;
+        float fx = 0.f, fy = 0.f;
+        uint2 E[NS][U];
+#pragma unroll
+        for (int j = 0; j < NS - 1; ++j)
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                E[j][q] = j * U + q < K ? sell_ld_stream(p + 32 * (j * U + q), pol) : make_uint2(0u, 0u);
+        for (int64_t k = 0; k < K; k += NS * U) {
+#pragma unroll
+            for (int j = 0; j < NS; ++j) {
+                const int jl = (j + NS - 1) % NS;            // the set consumed one set ago
+                const int64_t kl = k + (int64_t)(j + NS - 1) * U;
+#pragma unroll
+                for (int q = 0; q < U; ++q)
+                    E[jl][q] = kl + q < K ? sell_ld_stream(p + 32 * (kl + q), pol) : make_uint2(0u, 0u);
+                // steps past K hold (0, +0.0f): they add p w d = 0 exactly, and
+                // computing them unconditionally lets the U gathers issue together
+#pragma unroll
+                for (int q = 0; q < U; ++q) sell_acc(Y, yi, E[j][q], fx, fy);
+            }
+        }
+        if (live) F[r - rb] = make_float2(fx, fy);
+    }
+}
+
+using SellKernel = void (*)(const uint8_t*, const float2*, float2*);
+
+// TSNET_SELL=U,NS selects the pipeline shape (probing); default 2,4 (measured
+// best on config 5: 0.921 ms; 4,2 0.937; 4,3 0.943; 2,6 1.011; 8,2 1.185)
+static SellKernel sell_kernel() {
+    static SellKernel k = nullptr;
+    if (!k) {
+        const char* e = getenv("TSNET_SELL");
+        int u = 2, ns = 4;
+        if (e) sscanf(e, "%d,%d", &u, &ns);
+        if (u == 4 && ns == 2) k = k_attr_sell<4, 2>;
+        else if (u == 4 && ns == 4) k = k_attr_sell<4, 4>;
+        else if (u == 8 && ns == 2) k = k_attr_sell<8, 2>;
+        else if (u == 8 && ns == 3) k = k_attr_sell<8, 3>;
+        else if (u == 4 && ns == 3) k = k_attr_sell<4, 3>;
+        else if (u == 2 && ns == 6) k = k_attr_sell<2, 6>;
+        else k = k_attr_sell<2, 4>;
+    }
+    return k;
+}
+
+static int sell_resident() {
+    static int v = 0;
+    if (v == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, sell_kernel(), 256, 0) != cudaSuccess || v < 1))
+        v = 1;
+    return v;
+}
+
+// F: rows [row_begin, row_end) of the plan's shard (nl = row_end - row_begin)
+cudaError_t launch_attr_sell(const void* plan, const float2* Y, float2* F, int64_t nl, cudaStream_t s) {
+    if (nl == 0) return cudaSuccess;
+    const int64_t slices = (nl + 31) / 32;
+    const int64_t blocks = std::min<int64_t>((slices + 7) / 8, (int64_t)kNumSMs * sell_resident());
+    sell_kernel()<<<(int)std::max<int64_t>(1, blocks), 256, 0, s>>>(reinterpret_cast<const uint8_t*>(plan), Y, F);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ plan build
+// one warp per slice: lane = row; every slot of the slice written once
+__global__ void k_sell_fill(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                            const float* __restrict__ values, int64_t rb, int64_t re, int64_t S,
+                            const int64_t* __restrict__ base, uint2* __restrict__ slots) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < S;
+         s += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t r = rb + s * 32 + lane;
+        const int64_t b0 = base[s], K = (base[s + 1] - b0) >> 5;
+        const int64_t a = r < re ? indptr[r] : 0, L = r < re ? indptr[r + 1] - a : 0;
+        const uint32_t self = (uint32_t)(r < re ? r : rb);
+        for (int64_t k = 0; k < K; ++k)
+            slots[b0 + 32 * k + lane] = k < L ? make_uint2((uint32_t)indices[a + k], __float_as_uint(values[a + k]))
+                                              : make_uint2(self, 0u);
+    }
+}
+
+static int sell_rows(const tsnet_csr* P, const tsnet_shard* sh, int64_t& rb, int64_t& re) {
+    rb = 0;
+    re = P->n;
+    if (sh) {
+        TSNET_ARG(sh->row_begin >= 0 && sh->row_begin <= sh->row_end && sh->row_end <= P->n, "bad shard rows");
+        rb = sh->row_begin;
+        re = sh->row_end;
+    }
+    TSNET_ARG(P->n < ((int64_t)1 << 31), "a sliced-ELL plan needs n < 2^31");
+    return TSNET_OK;
+}
+
+// Slot offsets base[0..S] of the slices (host; reads indptr[rb..re], blocking).
+static int sell_base(const tsnet_csr* P, int64_t rb, int64_t re, cudaStream_t s, std::vector<int64_t>& base,
+                     int64_t& nnz_s) {
+    const int64_t nr = re - rb, S = (nr + 31) / 32;
+    std::vector<int64_t> ip((size_t)nr + 1, 0);
+    if (nr > 0) {
+        TSNET_CUDA(cudaMemcpyAsync(ip.data(), P->indptr + rb, sizeof(int64_t) * (size_t)(nr + 1),
+                                   cudaMemcpyDeviceToHost, s));
+        TSNET_CUDA(cudaStreamSynchronize(s));
+    }
+    base.assign((size_t)S + 1, 0);
+    for (int64_t q = 0; q < S; ++q) {
+        int64_t K = 0;
+        for (int64_t r = 32 * q; r < std::min(nr, 32 * q + 32); ++r) K = std::max(K, ip[r + 1] - ip[r]);
+        base[q + 1] = base[q] + 32 * K;
+    }
+    nnz_s = ip[nr] - ip[0];
+    return TSNET_OK;
+}
+
+}  // namespace tsnet
+
+using namespace tsnet;
+
+extern "C" {
+
+int tsnet_sell_query(const tsnet_csr* P, const tsnet_shard* shard, size_t* plan_bytes, double* slots_per_nnz,
+                     tsnet_stream_t stream) {
+    TSNET_ARG(P != nullptr && plan_bytes != nullptr, "NULL argument");
+    TSNET_ARG(P->n >= 0 && P->nnz >= 0 && (P->n == 0 || P->indptr), "invalid P");
+    int64_t rb, re, nnz_s = 0;
+    int st = sell_rows(P, shard, rb, re);
+    if (st != TSNET_OK) return st;
+    std::vector<int64_t> base;
+    if ((st = sell_base(P, rb, re, (cudaStream_t)stream, base, nnz_s)) != TSNET_OK) return st;
+    *plan_bytes = (size_t)sell_layout(P->n, rb, re, nnz_s, base.back()).bytes;
+    if (slots_per_nnz) *slots_per_nnz = nnz_s > 0 ? (double)base.back() / (double)nnz_s : 1.0;
+    return TSNET_OK;
+}
+
+int tsnet_sell_build(const tsnet_csr* P, const tsnet_shard* shard, void* plan, size_t plan_bytes,
+                     tsnet_stream_t stream) {
+    TSNET_ARG(P != nullptr && plan != nullptr, "NULL argument");
+    TSNET_ARG(((uintptr_t)plan % 256) == 0, "plan buffer must be 256-byte aligned");
+    TSNET_ARG(P->n >= 0 && P->nnz >= 0 && (P->n == 0 || P->indptr), "invalid P");
+    TSNET_ARG(P->nnz == 0 || (P->indices && P->values), "P arrays are NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t rb, re, nnz_s = 0;
+    int st = sell_rows(P, shard, rb, re);
+    if (st != TSNET_OK) return st;
+    std::vector<int64_t> base;
+    if ((st = sell_base(P, rb, re, s, base, nnz_s)) != TSNET_OK) return st;
+    const SellHeader h = sell_layout(P->n, rb, re, nnz_s, base.back());
+    TSNET_ARG(plan_bytes >= (size_t)h.bytes, "plan buffer too small (%zu < %lld bytes)", plan_bytes,
+              (long long)h.bytes);
+    uint8_t* pb = reinterpret_cast<uint8_t*>(plan);
+    int64_t* d_base = reinterpret_cast<int64_t*>(pb + h.off_base);
+    TSNET_CUDA(cudaMemcpyAsync(pb, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+    TSNET_CUDA(cudaMemcpyAsync(d_base, base.data(), sizeof(int64_t) * base.size(), cudaMemcpyHostToDevice, s));
+    if (h.slices > 0 && h.slots > 0) {
+        k_sell_fill<<<kNumSMs * 8, 256, 0, s>>>(P->indptr, P->indices, P->values, rb, re, h.slices, d_base,
+                                                reinterpret_cast<uint2*>(pb + h.off_slots));
+        TSNET_LAUNCH_CHECK();
+    }
+    TSNET_CUDA(cudaStreamSynchronize(s));   // the host copies of h and base are stack/heap memory
+    return TSNET_OK;
+}
+
+}  // extern "C"

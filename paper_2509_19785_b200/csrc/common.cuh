@@ -141,7 +141,8 @@ struct GradArgs {
     const int64_t* indptr;
     const int32_t* indices;
     const float* values;
-    const void* plan;     // column-blocked P (attr_cb.cu) or nullptr
+    const void* plan;     // re-laid-out P (attr_cb.cu / attr_sell.cu) or nullptr
+    int plan_kind;        // TSNET_PLAN_CB / TSNET_PLAN_SELL (with a plan)
     const float2* Y;
     float lambda_kl, lambda_c, lambda_r, eps, h_max;
     int I_min, I_max;
@@ -152,6 +153,7 @@ cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, b
 cudaError_t launch_field_conv(const Ws& w, const GradArgs& a, cudaStream_t s);
 cudaError_t launch_spmv(const Ws& w, const GradArgs& a, cudaStream_t s);
 cudaError_t launch_attr_cb(const void* plan, const float2* Y, float2* F, int64_t nl, cudaStream_t s);
+cudaError_t launch_attr_sell(const void* plan, const float2* Y, float2* F, int64_t nl, cudaStream_t s);
 cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2* f_field, double* Z,
                             cudaStream_t s);
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,

@@ -260,8 +260,10 @@ static cudaError_t launch_spmv2_t(const GradArgs& a, float2* F, const SpmvCfg& c
 }
 
 // a6 for the rows [rb, re) of the call into w.f_attr (local rows): the
-// column-blocked plan kernel when P has a plan, else the row-wise CSR kernel.
+// plan kernel when P has a plan (column-blocked or sliced ELL), else the
+// row-wise CSR kernel.
 cudaError_t launch_spmv(const Ws& w, const GradArgs& a, cudaStream_t s) {
+    if (a.plan && a.plan_kind == TSNET_PLAN_SELL) return launch_attr_sell(a.plan, a.Y, w.f_attr, a.re - a.rb, s);
     if (a.plan) return launch_attr_cb(a.plan, a.Y, w.f_attr, a.re - a.rb, s);   // rows of the plan's shard
     const int64_t nl = a.re - a.rb;
     cudaError_t e = cudaMemsetAsync(w.f_attr, 0, sizeof(float2) * (size_t)nl, s);

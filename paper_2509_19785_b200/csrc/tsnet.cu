@@ -90,6 +90,7 @@ static int prepare(const tsnet_csr* P, const float* Y, const tsnet_grad_params* 
     a.indices = P->indices;
     a.values = P->values;
     a.plan = P->plan;
+    a.plan_kind = P->plan ? (P->plan_kind == TSNET_PLAN_SELL ? TSNET_PLAN_SELL : TSNET_PLAN_CB) : 0;
     a.Y = reinterpret_cast<const float2*>(Y);
     a.lambda_kl = gp->lambda_kl;
     a.lambda_c = gp->lambda_c;
@@ -234,6 +235,7 @@ int tsnet_attr(const tsnet_csr* P, const float* Y, float* f_attr, tsnet_stream_t
     a.indices = P->indices;
     a.values = P->values;
     a.plan = P->plan;
+    a.plan_kind = P->plan ? (P->plan_kind == TSNET_PLAN_SELL ? TSNET_PLAN_SELL : TSNET_PLAN_CB) : 0;
     a.Y = reinterpret_cast<const float2*>(Y);
     TSNET_CUDA(launch_spmv(w, a, (cudaStream_t)stream));
     return TSNET_OK;

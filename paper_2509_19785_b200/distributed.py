@@ -14,7 +14,8 @@ import torch
 
 from .runner import STAGE_SWITCH, stage_of, stage_params
 from .tsnet import (CSR, GradParams, Shard, alloc_workspace, tsnet_comm_destroy, tsnet_comm_init,
-                    tsnet_comm_unique_id, tsnet_plan_build, tsnet_read_stats, tsnet_shard_rows, tsnet_step)
+                    tsnet_comm_unique_id, tsnet_plan_build, tsnet_read_stats, tsnet_sell_build, tsnet_shard_rows,
+                    tsnet_step)
 
 
 def shard_bounds(indptr_host, world: int):
@@ -37,7 +38,7 @@ class ShardedLayout:
 
     def __init__(self, P: CSR, Y0: torch.Tensor, rank: int, world: int, base: GradParams | None = None,
                  use_graphs: bool = True, eta: float = 50.0, stage_switch: int = STAGE_SWITCH, group=None,
-                 plan: bool = False):
+                 plan: bool | str = False):
         assert Y0.is_cuda and Y0.shape == (P.n, 2)
         self.rank, self.world = rank, world
         bounds = shard_bounds(P.indptr.cpu().numpy(), world)
@@ -45,7 +46,11 @@ class ShardedLayout:
         self.comm = tsnet_comm_init(uid, world, rank)
         self.shard = Shard(rank, world, bounds, self.comm)
         # the attractive SpMV reads the own rows of P (CSR), or a plan of them
-        self.P = tsnet_plan_build(P, self.shard) if plan else P
+        # (plan True / "cb": column-blocked, "sell": sliced ELL)
+        if plan == "sell":
+            self.P = tsnet_sell_build(P, self.shard)
+        else:
+            self.P = tsnet_plan_build(P, self.shard) if plan else P
         self.Y = Y0.clone()
         self.vel = torch.zeros_like(self.Y)
         self.gains = torch.ones_like(self.Y)

@@ -23,6 +23,7 @@ c_i32, c_i64, c_f32, c_f64, c_sz, c_vp, c_u64 = (ctypes.c_int32, ctypes.c_int64,
 
 TSNET_OK, TSNET_E_ARG, TSNET_E_CAPACITY, TSNET_E_CUDA, TSNET_E_NCCL, TSNET_E_NONFINITE, TSNET_W_PERPLEXITY = range(7)
 TSNET_I_MAX_LIMIT = 256
+PLAN_CB, PLAN_SELL = 1, 2     # tsnet_csr.plan_kind (include/tsnet.h)
 
 
 class tsnet_graph(ctypes.Structure):
@@ -31,7 +32,7 @@ class tsnet_graph(ctypes.Structure):
 
 class tsnet_csr(ctypes.Structure):
     _fields_ = [("n", c_i64), ("nnz", c_i64), ("capacity", c_i64), ("indptr", c_vp), ("indices", c_vp),
-                ("values", c_vp), ("plan", c_vp)]
+                ("values", c_vp), ("plan", c_vp), ("plan_kind", c_i32)]
 
 
 class tsnet_grad_params(ctypes.Structure):
@@ -79,6 +80,9 @@ SIGNATURES = [
                                         ctypes.POINTER(c_sz), ctypes.POINTER(c_sz), c_vp]),
     ("tsnet_plan_build", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard), c_vp, c_sz, c_vp,
                                         c_sz, c_vp]),
+    ("tsnet_sell_query", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard), ctypes.POINTER(c_sz),
+                                        ctypes.POINTER(ctypes.c_double), c_vp]),
+    ("tsnet_sell_build", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard), c_vp, c_sz, c_vp]),
     ("tsnet_plan_partition", c_i32, [c_vp, c_i64, c_i64, c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp]),
     ("tsnet_comm_unique_id", ctypes.c_int, [c_vp]),
     ("tsnet_comm_init", ctypes.c_int, [c_vp, c_i32, c_i32, ctypes.POINTER(c_vp)]),
@@ -174,9 +178,10 @@ class StepParams:
 
 
 class CSR:
-    """Device CSR matrix P (int64 indptr, int32 indices, fp32 values), plus the
-    optional column-blocked plan of the same P (tsnet_plan_build; `plan` is a
-    uint8 device tensor, None = CSR kernel)."""
+    """Device CSR matrix P (int64 indptr, int32 indices, fp32 values), plus an
+    optional plan of the same P: column-blocked (tsnet_plan_build) or sliced ELL
+    (tsnet_sell_build); `plan` is a uint8 device tensor (None = CSR kernel),
+    `plan_kind` PLAN_CB / PLAN_SELL."""
 
     def __init__(self, indptr: torch.Tensor, indices: torch.Tensor, values: torch.Tensor, nnz: int | None = None):
         _require_cuda(indptr, indices, values)
@@ -185,12 +190,14 @@ class CSR:
         self.n = indptr.numel() - 1
         self.nnz = int(indices.numel()) if nnz is None else int(nnz)
         self.plan = None
+        self.plan_kind = 0
 
     def c(self):
         return tsnet_csr(self.n, self.nnz, int(self.indices.numel()), self.indptr.data_ptr(),
                          self.indices.data_ptr() if self.indices.numel() else None,
                          self.values.data_ptr() if self.values.numel() else None,
-                         self.plan.data_ptr() if self.plan is not None else None)
+                         self.plan.data_ptr() if self.plan is not None else None,
+                         self.plan_kind if self.plan is not None else 0)
 
     def without_plan(self) -> "CSR":
         """Same P, CSR kernel (shares the tensors)."""
@@ -258,6 +265,30 @@ def tsnet_plan_build(P: CSR, shard=None, stream=None) -> CSR:
                                                       wbytes, _stream(stream)))
     del ws
     P.plan = plan
+    P.plan_kind = PLAN_CB
+    return P
+
+
+# ------------------------------------------------------ sliced-ELL plan of P
+def tsnet_sell_query(P: CSR, shard=None, stream=None):
+    """(plan bytes, slots per stored entry) of the sliced-ELL plan."""
+    pb, ratio = c_sz(0), ctypes.c_double(0.0)
+    Pc = P.c()
+    _check("tsnet_sell_query", lib().tsnet_sell_query(ctypes.byref(Pc), _shard(shard), ctypes.byref(pb),
+                                                      ctypes.byref(ratio), _stream(stream)))
+    return int(pb.value), float(ratio.value)
+
+
+def tsnet_sell_build(P: CSR, shard=None, stream=None) -> CSR:
+    """Build the sliced-ELL plan of P (set-up, blocking) and attach it: P.plan."""
+    pbytes, _ = tsnet_sell_query(P, shard, stream)
+    plan = torch.empty(max(pbytes, 1), dtype=torch.uint8, device=P.indptr.device)
+    P.plan = None
+    Pc = P.c()
+    _check("tsnet_sell_build", lib().tsnet_sell_build(ctypes.byref(Pc), _shard(shard), _ptr(plan), pbytes,
+                                                      _stream(stream)))
+    P.plan = plan
+    P.plan_kind = PLAN_SELL
     return P
 
 

@@ -1,6 +1,7 @@
 """Attractive SpMV kernels vs the oracle: the column-blocked plan kernel
-(attr_cb.cu, tsnet_plan_build) and the streamed CSR kernel (attr_csr.cu, used
-when P has no plan).
+(attr_cb.cu, tsnet_plan_build), the sliced-ELL plan kernel (attr_sell.cu,
+tsnet_sell_build) and the row-wise CSR kernel (iterate.cu, used when P has no
+plan).
 
 F_attr,i = sum_j p_ij w_ij (X_i - X_j) (Eq. 6 first term) is
 computed by oracle.attr_sparse in fp64 from the same fp32 P and fp32 Y.
@@ -44,13 +45,19 @@ def dev_csr(ip, ix, pv):
                torch.from_numpy(np.asarray(pv, np.float32)).cuda())
 
 
-def check(ip, ix, pv, Y, shard=None, y_offset_rows=0, plan=True):
-    """Plan + CB kernel (or the CSR kernel) vs oracle on rows [rb, re)."""
+def attach(P, plan, shard=None):
+    if plan in (True, "cb"):
+        T.tsnet_plan_build(P, shard=shard)
+    elif plan == "sell":
+        T.tsnet_sell_build(P, shard=shard)
+    return P
+
+
+def check(ip, ix, pv, Y, shard=None, y_offset_rows=0, plan="cb"):
+    """Plan kernel ("cb", "sell") or the CSR kernel ("csr") vs oracle on rows [rb, re)."""
     n = len(ip) - 1
     pv32 = np.asarray(pv, np.float32).astype(np.float64)
-    P = dev_csr(ip, ix, pv32)
-    if plan:
-        T.tsnet_plan_build(P, shard=shard)
+    P = attach(dev_csr(ip, ix, pv32), plan, shard)
     rb, re = (0, n) if shard is None else (shard.row_begin, shard.row_end)
     # optionally place Y at an 8-byte (not 16-byte) aligned address -> non-TMA copy path
     base = torch.zeros((n + y_offset_rows, 2), dtype=torch.float32, device="cuda")
@@ -73,7 +80,7 @@ def check(ip, ix, pv, Y, shard=None, y_offset_rows=0, plan=True):
     return P
 
 
-@pytest.mark.parametrize("plan", [True, False], ids=["cb", "csr"])
+@pytest.mark.parametrize("plan", ["cb", "sell", "csr"])
 @pytest.mark.parametrize("cfg", [1, 2, 3])
 def test_configs(cfg, plan):
     ip, ix = config_graph(cfg)
@@ -83,7 +90,7 @@ def test_configs(cfg, plan):
         check(P["indptr"], P["indices"], P["values"], Y, plan=plan)
 
 
-@pytest.mark.parametrize("plan", [True, False], ids=["cb", "csr"])
+@pytest.mark.parametrize("plan", ["cb", "sell", "csr"])
 @pytest.mark.parametrize("n,kind", [(1, "single"), (7, "tiny"), (8191, "one_block_minus"), (8192, "one_block"),
                                     (8193, "block_plus_one"), (24577, "odd_tail"), (20011, "hub_and_empty"),
                                     (50000, "short_rows"), (30011, "many_empty")])
@@ -111,7 +118,7 @@ def test_unaligned_Y_uses_copy_path():
     check(ip, ix, pv, uniform_layout(n, 5.0, 1), y_offset_rows=1)
 
 
-@pytest.mark.parametrize("plan", [True, False], ids=["cb", "csr"])
+@pytest.mark.parametrize("plan", ["cb", "sell", "csr"])
 def test_long_rows_many_tasks(plan):
     """Rows longer than a sweep and more than one wave of tasks (rows > 148 * 11264)."""
     n = 148 * 11264 + 5000
@@ -121,16 +128,17 @@ def test_long_rows_many_tasks(plan):
     check(ip, ix, pv, uniform_layout(n, 20.0, 2), plan=plan)
 
 
-def test_shards_partition_the_rows():
+@pytest.mark.parametrize("plan", ["cb", "sell"])
+def test_shards_partition_the_rows(plan):
     ip, ix = config_graph(2)
     P = oracle.build_P(ip, ix, 40.0, seed=0)
     n = P["n"]
     Y = clustered_layout(n, 25.0, 7, 1.2, 2)
-    for rb, re in ((0, n // 3), (n // 3, n // 3 + 1), (n // 3 + 1, n), (n, n)):
-        check(P["indptr"], P["indices"], P["values"], Y, shard=T.tsnet_shard(0, 1, rb, re))
+    for rb, re in ((0, n // 3), (n // 3, n // 3 + 1), (n // 3 + 1, n), (n, n), (33, 97)):
+        check(P["indptr"], P["indices"], P["values"], Y, shard=T.tsnet_shard(0, 1, rb, re), plan=plan)
 
 
-@pytest.mark.parametrize("plan", [True, False], ids=["cb", "csr"])
+@pytest.mark.parametrize("plan", ["cb", "csr"])
 def test_config4_full_size_sampled_rows(plan):
     """The bench workload (n ~ 0.95M, nnz ~ 2.06e8), GPU C0 output."""
     from paper_2509_19785_b200 import tsnet_build_P
@@ -140,8 +148,7 @@ def test_config4_full_size_sampled_rows(plan):
     n = P.n
     Y = clustered_layout(n, 30.0, 40, 2.0, 5)
     Yd = torch.from_numpy(Y).cuda()
-    if plan:
-        T.tsnet_plan_build(P)
+    attach(P, plan)
     F = tsnet_attr(P, Yd)
     torch.cuda.synchronize()
     pip, pix = P.indptr.cpu().numpy(), P.indices.cpu().numpy()
@@ -154,3 +161,29 @@ def test_config4_full_size_sampled_rows(plan):
     sc = row_scale(Y.astype(np.float64), pip, pix, pv, rows)
     err = np.abs(got - want).sum(1)
     assert np.all(err <= TOL * sc), float((err / sc).max())
+
+
+def test_sell_config5_full_size():
+    """Sliced ELL on the 3-D mesh at full size (n = 4.1M, nnz ~ 5.3e8, GPU C0):
+    padding is small (slots per entry), sampled rows match the oracle, and all
+    rows match the CSR kernel."""
+    from paper_2509_19785_b200 import tsnet_build_P
+    ip, ix = config_graph(5)
+    P = tsnet_build_P(torch.from_numpy(ip).cuda(), torch.from_numpy(ix).cuda(), u=40.0, seed=0)["P"]
+    n = P.n
+    Y = clustered_layout(n, 30.0, 40, 2.0, 5)
+    Yd = torch.from_numpy(Y).cuda()
+    F_csr = tsnet_attr(P, Yd)
+    _, ratio = T.tsnet_sell_query(P)
+    assert 1.0 <= ratio <= 1.3
+    T.tsnet_sell_build(P)
+    F = tsnet_attr(P, Yd)
+    torch.cuda.synchronize()
+    assert relL2(F.cpu().numpy(), F_csr.cpu().numpy()) <= 1e-6
+    pip, pix = P.indptr.cpu().numpy(), P.indices.cpu().numpy()
+    pv = P.values.cpu().numpy().astype(np.float64)
+    rows = np.unique(np.concatenate([np.random.default_rng(0).choice(n, 2000, replace=False), [0, 31, 32, n - 1]]))
+    want = np.stack([oracle.attr_sparse_rows(Y.astype(np.float64), pip, pix, pv, int(i), 1)[0] for i in rows])
+    got = F.cpu().numpy()[rows].astype(np.float64)
+    sc = row_scale(Y.astype(np.float64), pip, pix, pv, rows)
+    assert np.all(np.abs(got - want).sum(1) <= TOL * sc), "sampled rows"

@@ -42,13 +42,23 @@ def dev(P):
                torch.from_numpy(P["values"].astype(np.float32)).cuda())
 
 
-def emulated_step(P, Y, vel, gains, gp, sp, world, plan=True):
+def with_plan(P, plan, shard=None):
+    """P without a plan ("csr"), or with its column-blocked ("cb") / sliced-ELL ("sell") plan."""
+    Q = P.without_plan()
+    if plan == "cb":
+        return T.tsnet_plan_build(Q, shard)
+    if plan == "sell":
+        return T.tsnet_sell_build(Q, shard)
+    return Q
+
+
+def emulated_step(P, Y, vel, gains, gp, sp, world, plan="cb"):
     n = P.n
     bounds = T.tsnet_shard_rows(P.indptr.cpu().numpy(), world)
     shards = [T.Shard(r, world, bounds) for r in range(world)]
     Ps, wss, Ys = [], [], []
     for sh in shards:
-        Pr = T.tsnet_plan_build(P.without_plan(), sh) if plan else P.without_plan()
+        Pr = with_plan(P, plan, sh)
         ws = alloc_workspace(n, P.nnz, gp)
         Yr = Y.clone()
         T.tsnet_field_local(Pr, Yr, gp, ws, shard=sh)
@@ -67,7 +77,7 @@ def emulated_step(P, Y, vel, gains, gp, sp, world, plan=True):
     return Yout, Vout, Gout, bounds
 
 
-@pytest.mark.parametrize("plan", [False, True], ids=["csr", "cb"])
+@pytest.mark.parametrize("plan", ["csr", "cb", "sell"])
 @pytest.mark.parametrize("cfg,world", [(1, 2), (2, 3), (2, 8), (3, 4)])
 @pytest.mark.parametrize("stage", [0, 1])
 def test_emulated_shards_equal_one_gpu_and_oracle(cfg, world, stage, plan):
@@ -82,7 +92,7 @@ def test_emulated_shards_equal_one_gpu_and_oracle(cfg, world, stage, plan):
     Ys, Vs, Gs, bounds = emulated_step(Pd, Yd, Vd, Gd, gp, sp, world, plan)
     assert len(bounds) == world + 1 and bounds[0] == 0 and bounds[-1] == n
     # unsharded, same attractive kernel
-    P1 = T.tsnet_plan_build(Pd.without_plan()) if plan else Pd.without_plan()
+    P1 = with_plan(Pd, plan)
     ws = alloc_workspace(n, Pd.nnz, gp)
     Y1, V1, G1 = Yd.clone(), Vd.clone(), Gd.clone()
     tsnet_step(P1, Y1, V1, G1, gp, sp, ws)
