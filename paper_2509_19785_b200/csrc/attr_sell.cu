@@ -23,9 +23,11 @@
 // caller can keep the CSR kernel there.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
+#include "ptx.cuh"
 #include "tsnet.h"
 
 namespace tsnet {
@@ -125,40 +127,249 @@ __global__ void __launch_bounds__(256) k_attr_sell(const uint8_t* __restrict__ p
     }
 }
 
-using SellKernel = void (*)(const uint8_t*, const float2*, float2*);
-
-// TSNET_SELL=U,NS selects the pipeline shape (probing); default 2,4 (measured
-// best on config 5: 0.921 ms; 4,2 0.937; 4,3 0.943; 2,6 1.011; 8,2 1.185)
-static SellKernel sell_kernel() {
-    static SellKernel k = nullptr;
-    if (!k) {
-        const char* e = getenv("TSNET_SELL");
-        int u = 2, ns = 4;
-        if (e) sscanf(e, "%d,%d", &u, &ns);
-        if (u == 4 && ns == 2) k = k_attr_sell<4, 2>;
-        else if (u == 4 && ns == 4) k = k_attr_sell<4, 4>;
-        else if (u == 8 && ns == 2) k = k_attr_sell<8, 2>;
-        else if (u == 8 && ns == 3) k = k_attr_sell<8, 3>;
-        else if (u == 4 && ns == 3) k = k_attr_sell<4, 3>;
-        else if (u == 2 && ns == 6) k = k_attr_sell<2, 6>;
-        else k = k_attr_sell<2, 4>;
+// Same, with the Y_j gathers pipelined too: the gathers of set j + 1 are
+// issued before set j is computed (two gather sets in flight per warp).
+// NS even (the unrolled body covers NS sets; gather sets alternate).
+template <int U, int NS>
+__global__ void __launch_bounds__(256) k_attr_sell_g(const uint8_t* __restrict__ plan, const float2* __restrict__ Y,
+                                                     float2* __restrict__ F) {
+    static_assert(NS % 2 == 0, "NS must be even");
+    const SellHeader* h = reinterpret_cast<const SellHeader*>(plan);
+    const int64_t rb = h->row_begin, re = h->row_end, S = h->slices;
+    const int64_t* __restrict__ base = reinterpret_cast<const int64_t*>(plan + h->off_base);
+    const uint2* __restrict__ slots = reinterpret_cast<const uint2*>(plan + h->off_slots);
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t pol = sell_policy_evict_first();
+    for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < S; s += nw) {
+        const int64_t b0 = __ldg(base + s), K = (__ldg(base + s + 1) - b0) >> 5;
+        const int64_t r = rb + s * 32 + lane;
+        const bool live = r < re;
+        const float2 yi = live ? __ldg(Y + r) : make_float2(0.f, 0.f);
+        const uint2* p = slots + b0 + lane;
+        float fx = 0.f, fy = 0.f;
+        uint2 E[NS][U];
+        float2 G[2][U];
+#pragma unroll
+        for (int j = 0; j < NS - 1; ++j)
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                E[j][q] = j * U + q < K ? sell_ld_stream(p + 32 * (j * U + q), pol) : make_uint2(0u, 0u);
+#pragma unroll
+        for (int q = 0; q < U; ++q) G[0][q] = __ldg(Y + (int)E[0][q].x);
+        for (int64_t k = 0; k < K; k += NS * U) {
+#pragma unroll
+            for (int j = 0; j < NS; ++j) {
+                const int jl = (j + NS - 1) % NS;
+                const int64_t kl = k + (int64_t)(j + NS - 1) * U;
+#pragma unroll
+                for (int q = 0; q < U; ++q)
+                    E[jl][q] = kl + q < K ? sell_ld_stream(p + 32 * (kl + q), pol) : make_uint2(0u, 0u);
+                const int jn = (j + 1) % NS;
+#pragma unroll
+                for (int q = 0; q < U; ++q) G[(j + 1) & 1][q] = __ldg(Y + (int)E[jn][q].x);
+#pragma unroll
+                for (int q = 0; q < U; ++q) {
+                    const float dx = yi.x - G[j & 1][q].x, dy = yi.y - G[j & 1][q].y;
+                    const float w = __frcp_rn(fmaf(dx, dx, fmaf(dy, dy, 1.0f)));
+                    const float pw = __uint_as_float(E[j][q].y) * w;
+                    fx = fmaf(pw, dx, fx);
+                    fy = fmaf(pw, dy, fy);
+                }
+            }
+        }
+        if (live) F[r - rb] = make_float2(fx, fy);
     }
-    return k;
 }
 
-static int sell_resident() {
-    static int v = 0;
-    if (v == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, sell_kernel(), 256, 0) != cudaSuccess || v < 1))
-        v = 1;
-    return v;
+// TMA-staged variant.  A warp owns a contiguous run of slices [s0, s1)
+// (balanced on slots), so its entries are ONE contiguous byte range; lane 0
+// streams it into a per-warp ring of R stages of CS steps (CS x 256 bytes)
+// with cp.async.bulk (mbarrier completion), R - 1 stages ahead.  The ring
+// holds the bytes in flight, not registers, so the warp count per SM is not
+// cut by the prefetch depth.  Per U steps: U entries from shared memory, U
+// gathers of Y_j in flight together, then the U updates in order, closing a
+// slice (writing its 32 F_i) whenever its last step is done.
+template <int U, int CS, int R>
+__global__ void __launch_bounds__(256) k_attr_sell_tma(const uint8_t* __restrict__ plan,
+                                                       const float2* __restrict__ Y, float2* __restrict__ F) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    const SellHeader* h = reinterpret_cast<const SellHeader*>(plan);
+    const int64_t rb = h->row_begin, re = h->row_end, S = h->slices;
+    const int64_t* __restrict__ base = reinterpret_cast<const int64_t*>(plan + h->off_base);
+    const uint2* __restrict__ slots = reinterpret_cast<const uint2*>(plan + h->off_slots);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint2* ring = reinterpret_cast<uint2*>(sm) + (size_t)warp * R * CS * 32;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + (size_t)8 * R * CS * 32 * sizeof(uint2)) + warp * R;
+    if (lane == 0) {
+        for (int q = 0; q < R; ++q) mbar_init(&bars[q], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    // slices of this warp: lower bounds of its share of the slots in base[0..S]
+    const int64_t NW = (int64_t)gridDim.x * 8, wg = (int64_t)blockIdx.x * 8 + warp;
+    const int64_t total = __ldg(base + S);
+    auto lower_bound = [&](int64_t target) {   // first i in [0, S] with base[i] >= target (warp-uniform)
+        int64_t lo = 0, hi = S;
+        while (hi - lo > 0) {
+            const int64_t step = (hi - lo + 31) / 32;
+            const int64_t q = lo + lane * step;
+            const bool below = q < hi && __ldg(base + q) < target;
+            const unsigned m = __ballot_sync(0xffffffffu, below);
+            const int c = __popc(m);                  // probes lo, lo+step, ... below target
+            if (c == 0) {
+                hi = lo;
+            } else {
+                lo = lo + (int64_t)(c - 1) * step + 1;
+                hi = std::min(hi, lo - 1 + step);
+            }
+        }
+        return lo;
+    };
+    const int64_t s0 = lower_bound((int64_t)((double)total * wg / NW));
+    const int64_t s1 = wg == NW - 1 ? S : lower_bound((int64_t)((double)total * (wg + 1) / NW));
+    if (s0 >= s1) return;
+    const int64_t e0 = __ldg(base + s0), T = (__ldg(base + s1) - e0) >> 5;   // steps of the run
+    const uint64_t pol = sell_policy_evict_first();
+    auto issue = [&](int64_t t) {                     // lane 0: stage t into buffer t % R
+        const int64_t k0 = t * CS, nst = std::min<int64_t>(CS, T - k0);
+        const uint32_t bytes = (uint32_t)(nst * 32 * sizeof(uint2));
+        mbar_arrive_tx(&bars[t % R], bytes);
+        bulk_g2s_hint(ring + (size_t)(t % R) * CS * 32, slots + e0 + k0 * 32, bytes, &bars[t % R], pol);
+    };
+    if (lane == 0)
+        for (int64_t t = 0; t < R && t * CS < T; ++t) issue(t);
+    // consume cursor
+    int64_t s = s0, rem = 0;
+    float2 yi = make_float2(0.f, 0.f);
+    float fx = 0.f, fy = 0.f;
+    auto enter = [&](int64_t q) {                    // start slice q (< s1)
+        const int64_t r = rb + q * 32 + lane;
+        yi = r < re ? __ldg(Y + r) : make_float2(0.f, 0.f);
+        rem = (__ldg(base + q + 1) - __ldg(base + q)) >> 5;
+        fx = fy = 0.f;
+    };
+    auto close_empty = [&]() {                        // write finished slices, enter the next with steps
+        while (rem == 0 && s < s1) {
+            const int64_t r = rb + s * 32 + lane;
+            if (r < re) F[r - rb] = make_float2(fx, fy);
+            ++s;
+            if (s < s1) enter(s);
+        }
+    };
+    enter(s);
+    close_empty();
+    for (int64_t t = 0; t * CS < T; ++t) {
+        const int b = (int)(t % R);
+        mbar_wait(&bars[b], (uint32_t)((t / R) & 1));
+        const int64_t nst = std::min<int64_t>(CS, T - t * CS);
+        const uint2* st = ring + (size_t)b * CS * 32 + lane;
+#pragma unroll
+        for (int q0 = 0; q0 < CS; q0 += U) {
+            if (q0 >= nst) break;
+            uint2 e[U];
+            float2 yj[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) e[q] = q0 + q < nst ? st[(q0 + q) * 32] : make_uint2(0u, 0u);
+#pragma unroll
+            for (int q = 0; q < U; ++q) yj[q] = __ldg(Y + (int)e[q].x);
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                if (q0 + q < nst) {
+                    const float dx = yi.x - yj[q].x, dy = yi.y - yj[q].y;
+                    const float w = __frcp_rn(fmaf(dx, dx, fmaf(dy, dy, 1.0f)));
+                    const float pw = __uint_as_float(e[q].y) * w;
+                    fx = fmaf(pw, dx, fx);
+                    fy = fmaf(pw, dy, fy);
+                    --rem;
+                    close_empty();
+                }
+            }
+        }
+        __syncwarp();                                 // every lane is done with buffer b
+        if (lane == 0 && (t + R) * CS < T) {
+            fence_proxy_async_smem();
+            issue(t + R);
+        }
+    }
+}
+
+template <int U, int CS, int R>
+static constexpr size_t sell_tma_smem() {
+    return (size_t)8 * R * CS * 32 * sizeof(uint2) + (size_t)8 * R * sizeof(uint64_t);
+}
+
+using SellKernel = void (*)(const uint8_t*, const float2*, float2*);
+
+struct SellLaunch {
+    SellKernel k = nullptr;
+    size_t smem = 0;
+    int resident = 1;
+};
+
+// Kernel choice (measured on config 5, kernel alone, B200; CSR kernel 1.22 ms):
+//   gU,NS  entries and gathers pipelined (k_attr_sell_g): g4,4 0.801 ms (default),
+//          g4,2 0.820, g2,4 0.879, g2,6 1.137, g1,8 1.537;
+//   U,NS   entries pipelined only (k_attr_sell): 2,4 0.921, 4,2 0.937, 4,3 0.943;
+//   tma:U,CS,R  TMA-staged entries (k_attr_sell_tma): 8,8,4 1.012, 4,8,3 1.052,
+//          4,8,4 1.138, 8,4,4 1.143 -- the ring's shared memory takes L1
+//          capacity from the Y_j gathers, which hit L1 on a mesh.
+// TSNET_SELL selects one for probing.
+template <int U, int CS, int R>
+static void pick_tma(SellLaunch& L) {
+    L.k = k_attr_sell_tma<U, CS, R>;
+    L.smem = sell_tma_smem<U, CS, R>();
+}
+
+static const SellLaunch& sell_launch() {
+    static SellLaunch L;
+    if (!L.k) {
+        const char* e = getenv("TSNET_SELL");
+        if (!e) e = "g4,4";
+        int u = 4, cs = 8, r = 4;
+        if (strncmp(e, "tma:", 4) != 0) {
+            int ns = 4;
+            u = 2;
+            const bool g = strchr(e, 'g') != nullptr;    // "g2,4": gathers pipelined too
+            sscanf(g ? e + 1 : e, "%d,%d", &u, &ns);
+            if (g && u == 2 && ns == 4) L.k = k_attr_sell_g<2, 4>;
+            else if (g && u == 4 && ns == 4) L.k = k_attr_sell_g<4, 4>;
+            else if (g && u == 2 && ns == 6) L.k = k_attr_sell_g<2, 6>;
+            else if (g && u == 4 && ns == 2) L.k = k_attr_sell_g<4, 2>;
+            else if (g && u == 1 && ns == 8) L.k = k_attr_sell_g<1, 8>;
+            else if (g && u == 8 && ns == 2) L.k = k_attr_sell_g<8, 2>;
+            else if (g && u == 4 && ns == 6) L.k = k_attr_sell_g<4, 6>;
+            else if (g && u == 3 && ns == 4) L.k = k_attr_sell_g<3, 4>;
+            else if (g && u == 6 && ns == 2) L.k = k_attr_sell_g<6, 2>;
+            else if (u == 4 && ns == 2) L.k = k_attr_sell<4, 2>;
+            else if (u == 4 && ns == 3) L.k = k_attr_sell<4, 3>;
+            else L.k = k_attr_sell<2, 4>;
+        } else {
+            sscanf(e + 4, "%d,%d,%d", &u, &cs, &r);
+            if (u == 4 && cs == 4 && r == 6) pick_tma<4, 4, 6>(L);
+            else if (u == 4 && cs == 16 && r == 3) pick_tma<4, 16, 3>(L);
+            else if (u == 8 && cs == 8 && r == 4) pick_tma<8, 8, 4>(L);
+            else if (u == 2 && cs == 8 && r == 4) pick_tma<2, 8, 4>(L);
+            else if (u == 4 && cs == 8 && r == 3) pick_tma<4, 8, 3>(L);
+            else if (u == 8 && cs == 4 && r == 4) pick_tma<8, 4, 4>(L);
+            else if (u == 8 && cs == 4 && r == 3) pick_tma<8, 4, 3>(L);
+            else pick_tma<4, 8, 4>(L);
+        }
+        if (L.smem > 0) cudaFuncSetAttribute(L.k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&L.resident, L.k, 256, L.smem) != cudaSuccess ||
+            L.resident < 1)
+            L.resident = 1;
+    }
+    return L;
 }
 
 // F: rows [row_begin, row_end) of the plan's shard (nl = row_end - row_begin)
 cudaError_t launch_attr_sell(const void* plan, const float2* Y, float2* F, int64_t nl, cudaStream_t s) {
     if (nl == 0) return cudaSuccess;
+    const SellLaunch& L = sell_launch();
     const int64_t slices = (nl + 31) / 32;
-    const int64_t blocks = std::min<int64_t>((slices + 7) / 8, (int64_t)kNumSMs * sell_resident());
-    sell_kernel()<<<(int)std::max<int64_t>(1, blocks), 256, 0, s>>>(reinterpret_cast<const uint8_t*>(plan), Y, F);
+    const int64_t blocks = std::min<int64_t>((slices + 7) / 8, (int64_t)kNumSMs * L.resident);
+    L.k<<<(int)std::max<int64_t>(1, blocks), 256, L.smem, s>>>(reinterpret_cast<const uint8_t*>(plan), Y, F);
     return cudaGetLastError();
 }
 
