@@ -207,8 +207,8 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
-    from paper_2509_19785_b200 import (Layout, tsnet_attr, tsnet_build_P, tsnet_plan_build, tsnet_read_stats,
-                                       tsnet_sell_build, tsnet_step_host)
+    from paper_2509_19785_b200 import Layout, attach_plan, tsnet_attr, tsnet_build_P, tsnet_read_stats, tsnet_step_host
+    from paper_2509_19785_b200.tsnet import PLAN_CB, PLAN_SELL
     from workloads import config_graph, init_layout
 
     dev = torch.device("cuda", local_rank)
@@ -226,18 +226,15 @@ def run_ours(args, rank, world, local_rank):
     if world > 1 or args.sharded:
         # row shards + NCCL communicator (+ the plan of the own rows) (set-up, untimed)
         from paper_2509_19785_b200.distributed import ShardedLayout
-        lay = ShardedLayout(P, Y0, rank, world, plan=args.plan or False)
+        lay = ShardedLayout(P, Y0, rank, world, plan=args.plan)
         shard = lay.shard
         rb, re = lay.rows
     else:
-        if args.plan == "cb":
-            tsnet_plan_build(P)               # column-blocked layout of P (set-up, untimed)
-        elif args.plan == "sell":
-            tsnet_sell_build(P)               # sliced-ELL layout of P (set-up, untimed)
+        attach_plan(P, args.plan)             # SpMV layout of P (set-up, untimed)
         lay = Layout(P, Y0, use_graphs=True)
         shard, rb, re = None, 0, n
     torch.cuda.synchronize()
-    if world > 1 or args.plan or args.sharded:
+    if world > 1 or P.plan is not None or args.sharded:
         plan_s = time.perf_counter() - t0
     nnz_l = int(P.indptr[re].item() - P.indptr[rb].item())
     nl = re - rb
@@ -307,7 +304,8 @@ def run_ours(args, rank, world, local_rank):
     step_bytes = 8 * nnz_l + 8 * (nl + 1) + 48 * nl + 8 * (n - nl)
     traffic = None
     limiter = None
-    kname = {"cb": "k_attr_cb", "sell": "k_attr_sell"}.get(args.plan, "k_spmv2")
+    layout = {PLAN_CB: "cb", PLAN_SELL: "sell"}.get(lay.P.plan_kind, "csr") if lay.P.plan is not None else "csr"
+    kname = {"cb": "k_attr_cb", "sell": "k_attr_sell_g"}.get(layout, "k_spmv2")
     tp = os.path.join(ROOT, "profiles", f"{kname}_dram_bytes_cfg{args.config}.json")
     if os.path.exists(tp) and world == 1:
         with open(tp) as f:
@@ -318,7 +316,7 @@ def run_ours(args, rank, world, local_rank):
             limiter = {"what": limiter, "l1tex_to_l2_request_path_util": rec["l2_request_path_utilization"],
                        "lts_tag_request_util": rec["lts_tag_request_utilization"], "source": rec["source"]}
     gc = os.path.join(ROOT, "profiles", "gather_ceiling_b200.json")
-    if os.path.exists(gc) and not args.plan:
+    if os.path.exists(gc) and layout == "csr":
         with open(gc) as f:
             ceil = float(json.load(f)["global_gathers_per_s"])
         # one Y[j] gather per stored entry; the measured random-gather ceiling bounds the SpMV
@@ -369,7 +367,7 @@ def run_ours(args, rank, world, local_rank):
                                        round(grid_start["S"], 3), "stage_a_iters_per_s": None if stage_a_ms is None else round(1e3 / stage_a_ms, 1),
                                        "c0_gpu_s": round(c0_s, 3), "parallelism": par,
                                        "attr_layout": {"cb": "column-blocked plan", "sell": "sliced-ELL plan"}.get(
-                                           args.plan, "CSR"),
+                                           layout, "CSR"),
                                        "plan_build_s": None if plan_s is None else round(plan_s, 3)}),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic, "kernel": f"{kname} (tsnet_attr)",
@@ -394,9 +392,9 @@ def main():
     ap.add_argument("--pre-iters", type=int, default=250)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--plan", nargs="?", const="cb", default=None, choices=["cb", "sell"],
-                    help="plan kernel for the SpMV instead of CSR: cb = column-blocked (default of a bare --plan), "
-                         "sell = sliced ELL")
+    ap.add_argument("--plan", nargs="?", const="cb", default="auto", choices=["auto", "csr", "cb", "sell"],
+                    help="SpMV layout of P: auto (default: sliced ELL when it pads <= 1.6 slots per entry, else "
+                         "CSR), csr, cb (column-blocked; a bare --plan), sell (sliced ELL)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU (NCCL) path even on one rank (needs torchrun / a process group)")
     ap.add_argument("--cpu-budget", type=float, default=12.0)

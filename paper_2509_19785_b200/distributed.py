@@ -13,9 +13,8 @@ from __future__ import annotations
 import torch
 
 from .runner import STAGE_SWITCH, stage_of, stage_params
-from .tsnet import (CSR, GradParams, Shard, alloc_workspace, tsnet_comm_destroy, tsnet_comm_init,
-                    tsnet_comm_unique_id, tsnet_plan_build, tsnet_read_stats, tsnet_sell_build, tsnet_shard_rows,
-                    tsnet_step)
+from .tsnet import (CSR, GradParams, Shard, attach_plan, alloc_workspace, tsnet_comm_destroy, tsnet_comm_init,
+                    tsnet_comm_unique_id, tsnet_read_stats, tsnet_shard_rows, tsnet_step)
 
 
 def shard_bounds(indptr_host, world: int):
@@ -46,11 +45,8 @@ class ShardedLayout:
         self.comm = tsnet_comm_init(uid, world, rank)
         self.shard = Shard(rank, world, bounds, self.comm)
         # the attractive SpMV reads the own rows of P (CSR), or a plan of them
-        # (plan True / "cb": column-blocked, "sell": sliced ELL)
-        if plan == "sell":
-            self.P = tsnet_sell_build(P, self.shard)
-        else:
-            self.P = tsnet_plan_build(P, self.shard) if plan else P
+        # (attach_plan: "csr", "cb", "sell", "auto")
+        self.P = attach_plan(P, plan, self.shard)
         self.Y = Y0.clone()
         self.vel = torch.zeros_like(self.Y)
         self.gains = torch.ones_like(self.Y)

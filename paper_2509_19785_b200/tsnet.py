@@ -279,6 +279,27 @@ def tsnet_sell_query(P: CSR, shard=None, stream=None):
     return int(pb.value), float(ratio.value)
 
 
+SELL_AUTO_MAX_SLOTS_PER_NNZ = 1.6
+
+
+def attach_plan(P: CSR, plan="auto", shard=None, stream=None) -> CSR:
+    """Attach the SpMV layout `plan` to P: "csr" (none), "cb" (column-blocked),
+    "sell" (sliced ELL), or "auto": sliced ELL when its padding is at most
+    SELL_AUTO_MAX_SLOTS_PER_NNZ slots per stored entry (meshes, block models:
+    measured faster than CSR there), else CSR (power-law graphs, where hub rows
+    pad the slices and the gathers are random anyway)."""
+    if plan in (None, False, "csr"):
+        return P
+    if plan in (True, "cb"):
+        return tsnet_plan_build(P, shard, stream)
+    if plan == "sell":
+        return tsnet_sell_build(P, shard, stream)
+    if plan == "auto":
+        _, ratio = tsnet_sell_query(P, shard, stream)
+        return tsnet_sell_build(P, shard, stream) if ratio <= SELL_AUTO_MAX_SLOTS_PER_NNZ else P
+    raise ValueError(f"unknown plan {plan!r}")
+
+
 def tsnet_sell_build(P: CSR, shard=None, stream=None) -> CSR:
     """Build the sliced-ELL plan of P (set-up, blocking) and attach it: P.plan."""
     pbytes, _ = tsnet_sell_query(P, shard, stream)

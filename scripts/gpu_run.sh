@@ -24,3 +24,7 @@ timeout 600 $B > gpurun_out/${TAG}_plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 3000 -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv $B > gpurun_out/${TAG}_ncu_launch.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX} -s 5 -c 1 -o gpurun_out/${TAG}_top $B > gpurun_out/${TAG}_ncu.log 2>&1
 echo done
+B5="python bench.py --config 5 --steps 20 --warmup 3 --no-cpu-baseline --no-e2e"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_attr_sell_g -s 5 -c 1 -o gpurun_out/${TAG}_sell5 $B5 > gpurun_out/${TAG}_ncu_sell5.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 3000 -c 400 --csv --log-file gpurun_out/${TAG}_launches5.csv $B5 > gpurun_out/${TAG}_ncu_launch5.log 2>&1
+echo done5
