@@ -163,13 +163,19 @@ __global__ void k_prep(Geo* g, int* box_cnt, float4* wgrid, float2* tw) {
 }
 
 // a1: box of every point (fp64 arithmetic, R16) and its rank inside the box.
-// Each CTA takes a contiguous chunk of points.  When the I^2 box counters fit
-// in shared memory (kBoxSmem), the CTA counts its chunk there (warp-aggregated
-// shared atomics), reserves one range per non-empty box with a single global
-// atomicAdd, and offsets the local ranks -- so a layout packed into a few boxes
-// (stage A: 1e6 points in <= 400 boxes) does not serialise on global atomics.
-// Otherwise (many boxes, little contention) warp-aggregated global atomics.
-constexpr int kBoxSmem = 12288;   // counters (48 KB)
+// Each CTA takes kBoxChunk consecutive points (kBoxPts per thread, loads of
+// all of them in flight together).  When the I^2 box counters fit in shared
+// memory (kBoxSmem), the CTA counts its chunk there (shared atomics, native
+// on sm_100), reserves one range per non-empty box with a single global
+// atomicAdd, and adds that offset to the local ranks it kept in registers --
+// so a layout packed into a few boxes (stage A: 1e6 points in <= 400 boxes)
+// does not serialise on global atomics, and box/rank are written once.
+// Otherwise (many boxes, little contention) global atomics per point.  The
+// order of points inside a box is not deterministic (neither is the fp32
+// spread that follows).
+constexpr int kBoxSmem = 4096;     // counters (16 KB): I <= 64
+constexpr int kBoxPts = 8;         // points per thread
+constexpr int kBoxChunk = 256 * kBoxPts;
 
 __device__ __forceinline__ void box_of(float2 y, double lo_x, double lo_y, double h_b, int I, int& b, float& ux,
                                        float& uy) {
@@ -183,53 +189,55 @@ __device__ __forceinline__ void box_of(float2 y, double lo_x, double lo_y, doubl
     b = by * I + bx;
 }
 
-__global__ void __launch_bounds__(256) k_box_count(const float2* __restrict__ Y, int64_t n, const Geo* __restrict__ g,
+__global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__ Y, int64_t n, const Geo* __restrict__ g,
                                                    int* __restrict__ box_cnt, int* __restrict__ box,
                                                    int* __restrict__ rank, float2* __restrict__ uv) {
-    extern __shared__ int hist[];
+    __shared__ int hist[kBoxSmem];
     const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b;
     const int I = g->I;
     const int nb = I * I;
     const bool local = nb <= kBoxSmem;
-    const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
-    const int64_t c0 = blockIdx.x * chunk, c1 = std::min<int64_t>(n, c0 + chunk);
-    const int lane = threadIdx.x & 31;
+    const int64_t c0 = (int64_t)blockIdx.x * kBoxChunk + threadIdx.x;
     if (local) {
         for (int q = threadIdx.x; q < nb; q += blockDim.x) hist[q] = 0;
         __syncthreads();
     }
     int* cnt = local ? hist : box_cnt;
-    for (int64_t i0 = c0; i0 < c1; i0 += blockDim.x) {
-        const int64_t i = i0 + threadIdx.x;
-        const bool act = i < c1;
-        int b = -1;
-        float ux = 0.f, uy = 0.f;
-        if (act) box_of(Y[i], lo_x, lo_y, h_b, I, b, ux, uy);
-        // warp-aggregated atomic: one atomicAdd per distinct box in the warp
-        const unsigned act_mask = __ballot_sync(0xffffffffu, act);
-        if (act) {
-            const unsigned peers = __match_any_sync(act_mask, b);
-            const int leader = __ffs(peers) - 1;
-            int base = 0;
-            if (lane == leader) base = atomicAdd(&cnt[b], __popc(peers));
-            base = __shfl_sync(peers, base, leader);
-            box[i] = b;
-            rank[i] = base + __popc(peers & ((1u << lane) - 1u));
+    float2 y[kBoxPts];
+#pragma unroll
+    for (int j = 0; j < kBoxPts; ++j) {
+        const int64_t i = c0 + (int64_t)j * 256;
+        y[j] = i < n ? Y[i] : make_float2(0.f, 0.f);
+    }
+    int bj[kBoxPts], rj[kBoxPts];
+#pragma unroll
+    for (int j = 0; j < kBoxPts; ++j) {
+        const int64_t i = c0 + (int64_t)j * 256;
+        bj[j] = -1;
+        rj[j] = 0;
+        if (i < n) {
+            float ux, uy;
+            box_of(y[j], lo_x, lo_y, h_b, I, bj[j], ux, uy);
             uv[i] = make_float2(ux, uy);
+            rj[j] = atomicAdd(&cnt[bj[j]], 1);
         }
     }
-    if (!local) return;
-    __syncthreads();
-    for (int q = threadIdx.x; q < nb; q += blockDim.x) {
-        const int c = hist[q];
-        if (c) hist[q] = atomicAdd(&box_cnt[q], c);   // this CTA's range inside box q
+    if (local) {
+        __syncthreads();
+        for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+            const int c = hist[q];
+            if (c) hist[q] = atomicAdd(&box_cnt[q], c);   // this CTA's range inside box q
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) rank[i] += hist[box[i]];
-}
-
-static size_t box_smem_bytes(int I_max) {
-    return sizeof(int) * (size_t)std::min<int64_t>((int64_t)I_max * I_max, kBoxSmem);
+#pragma unroll
+    for (int j = 0; j < kBoxPts; ++j) {
+        const int64_t i = c0 + (int64_t)j * 256;
+        if (i < n) {
+            box[i] = bj[j];
+            rank[i] = rj[j] + (local ? hist[bj[j]] : 0);
+        }
+    }
 }
 
 // a1: exclusive scan of box counts -> box_start, and the spread work list
@@ -274,11 +282,29 @@ __global__ void __launch_bounds__(1024) k_box_scan(Geo* g, const int* __restrict
     }
 }
 
+// 4 points per thread and iteration: their loads, then the box_start
+// gathers, then the stores, each in flight together
 __global__ void __launch_bounds__(256) k_box_scatter(int64_t n, const int* __restrict__ box, const int* __restrict__ rank,
                                                      const int* __restrict__ box_start, const float2* __restrict__ uv,
                                                      float2* __restrict__ sorted_uv) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        sorted_uv[box_start[box[i]] + rank[i]] = uv[i];
+    constexpr int V = 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += V * stride) {
+        int b[V], r[V], st[V];
+        float2 u[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const int64_t i = i0 + v * stride;
+            b[v] = i < n ? box[i] : 0;
+            r[v] = i < n ? rank[i] : 0;
+            u[v] = i < n ? uv[i] : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) st[v] = __ldg(box_start + b[v]);
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            if (i0 + v * stride < n) sorted_uv[st[v] + r[v]] = u[v];
+    }
 }
 
 __device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float c) {
@@ -617,15 +643,15 @@ cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, b
     cudaError_t e;
     if ((e = field_set_attrs(w.M_max)) != cudaSuccess) return e;
     const int64_t n = a.n, nl = a.re - a.rb;
-    const int pb = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)kNumSMs * 2));
+    const int pb = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)kNumSMs * 8));
     const int pbl = (int)std::max<int64_t>(1, std::min<int64_t>((nl + 255) / 256, (int64_t)kNumSMs * 8));
     k_bbox<<<pb, 256, 0, s>>>(a.Y, n, w.geo, a.h_max, a.I_min, a.I_max);
     if (zero_all && (e = cudaMemsetAsync(w.wgrid, 0, sizeof(float4) * (size_t)w.N_max * w.N_max, s)) != cudaSuccess)
         return e;
     k_prep<<<kNumSMs * 4, 256, 0, s>>>(w.geo, w.box_cnt, w.wgrid, w.tw);
     const float2* Yl = a.Y + a.rb;
-    const int cb = (int)std::max<int64_t>(1, std::min<int64_t>((nl + 2047) / 2048, (int64_t)kNumSMs * 8));
-    k_box_count<<<cb, 256, box_smem_bytes(a.I_max), s>>>(Yl, nl, w.geo, w.box_cnt, w.box, w.rank, w.uv);
+    const int cb = (int)std::max<int64_t>(1, (nl + kBoxChunk - 1) / kBoxChunk);
+    k_box_count<<<cb, 256, 0, s>>>(Yl, nl, w.geo, w.box_cnt, w.box, w.rank, w.uv);
     k_box_scan<<<1, 1024, 0, s>>>(w.geo, w.box_cnt, w.box_start, w.items, nl);
     k_box_scatter<<<pbl, 256, 0, s>>>(nl, w.box, w.rank, w.box_start, w.uv, w.sorted_uv);
     k_spread<<<kNumSMs * 8, 256, 0, s>>>(w.geo, w.items, w.box_start, w.sorted_uv, w.wgrid);

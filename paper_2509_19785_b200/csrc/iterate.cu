@@ -294,7 +294,9 @@ __device__ __forceinline__ void lagrange3u(float u, float (&L)[3]) {
 __device__ __forceinline__ float2 gather_field(const Geo& g, const float4* __restrict__ fgrid, int b, float2 u) {
     const int I = g.I, N = g.N;
     const float h_b = (float)g.h_b;
-    const int bx = b % I, by = b / I;
+    // b / I by a float reciprocal: (b + 1/2) / I is >= 1/(2I) away from an
+    // integer, far more than the fp32 error for b < I^2 <= 768^2
+    const int by = __float2int_rz(((float)b + 0.5f) * __frcp_rn((float)I)), bx = b - by * I;
     float Lx[3], Ly[3];
     lagrange3u(u.x, Lx);
     lagrange3u(u.y, Ly);
@@ -369,21 +371,41 @@ __global__ void __launch_bounds__(kUpdateThreads, 1) k_update(int64_t n, Geo* __
     }
     double sx = 0.0, sy = 0.0;
     bool bad = false;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const float2 ff = gather_field(g, fg, box[i], uv[i]);
-        float2 y = Yin[i];
-        const float2 fa = Fa[i];
-        const float gx = fmaf(4.0f * lambda_kl, fa.x, ff.x) + cn * y.x;
-        const float gy = fmaf(4.0f * lambda_kl, fa.y, ff.y) + cn * y.y;
-        float2 v = vel[i], gn = gains[i];
-        gains_move(gx, v.x, gn.x, y.x, sp);
-        gains_move(gy, v.y, gn.y, y.y, sp);
-        bad |= !(isfinite(y.x) && isfinite(y.y));
-        Yout[i] = y;
-        vel[i] = v;
-        gains[i] = gn;
-        sx += y.x;
-        sy += y.y;
+    // two points per thread and iteration: all their loads in flight together
+    constexpr int V = 2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += V * stride) {
+        int b[V];
+        float2 u[V], y[V], fa[V], v[V], gn[V];
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+            const int64_t i = i0 + q * stride;
+            const bool h = i < n;
+            b[q] = h ? box[i] : 0;
+            u[q] = h ? uv[i] : make_float2(0.5f, 0.5f);
+            y[q] = h ? Yin[i] : make_float2(0.f, 0.f);
+            fa[q] = h ? Fa[i] : make_float2(0.f, 0.f);
+            v[q] = h ? vel[i] : make_float2(0.f, 0.f);
+            gn[q] = h ? gains[i] : make_float2(1.f, 1.f);
+        }
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+            const int64_t i = i0 + q * stride;
+            if (i >= n) break;
+            const float2 ff = gather_field(g, fg, b[q], u[q]);
+            const float gx = fmaf(4.0f * lambda_kl, fa[q].x, ff.x) + cn * y[q].x;
+            const float gy = fmaf(4.0f * lambda_kl, fa[q].y, ff.y) + cn * y[q].y;
+            gains_move(gx, v[q].x, gn[q].x, y[q].x, sp);
+            gains_move(gy, v[q].y, gn[q].y, y[q].y, sp);
+            bad |= !(isfinite(y[q].x) && isfinite(y[q].y));
+            Yout[i] = y[q];
+            vel[i] = v[q];
+            gains[i] = gn[q];
+            if (sp.recenter) {
+                sx += y[q].x;
+                sy += y[q].y;
+            }
+        }
     }
     if (sp.recenter) {
         for (int o = 16; o > 0; o >>= 1) {

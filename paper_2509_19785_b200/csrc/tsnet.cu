@@ -137,9 +137,12 @@ static cudaError_t side_stream(SideStream*& out) {
         // the field chain is a row of short dependent kernels: at the highest
         // priority its CTAs go ahead of queued SpMV CTAs instead of waiting
         // for the SpMV's waves to drain
+        // (TSNET_FIELD_PRIORITY=0: default priority, for probing)
         int lo = 0, hi = 0;
         if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return e;
-        if ((e = cudaStreamCreateWithPriority(&x.side, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
+        const char* pe = getenv("TSNET_FIELD_PRIORITY");
+        const int prio = (pe && pe[0] == '0') ? lo : hi;
+        if ((e = cudaStreamCreateWithPriority(&x.side, cudaStreamNonBlocking, prio)) != cudaSuccess) return e;
         if ((e = cudaStreamCreateWithFlags(&x.copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
         if ((e = cudaStreamCreateWithFlags(&x.d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
         if ((e = cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
