@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "move.cuh"
 #include "ptx.cuh"
 #include "tsnet.h"
 
@@ -130,9 +131,15 @@ __global__ void __launch_bounds__(256) k_attr_sell(const uint8_t* __restrict__ p
 // Same, with the Y_j gathers pipelined too: the gathers of set j + 1 are
 // issued before set j is computed (two gather sets in flight per warp).
 // NS even (the unrolled body covers NS sets; gather sets alternate).
-template <int U, int NS>
+//
+// MOVE: step a7 fused into the epilogue -- each lane, holding its row's
+// F_attr,i in registers, gathers the field at its point, forms the gradient
+// and moves the point (gains/momentum), writing the new position to m.Ynew
+// (never Y: other warps still gather the old positions) and vel/gains in
+// place.  Same arithmetic as k_update.
+template <int U, int NS, bool MOVE>
 __global__ void __launch_bounds__(256) k_attr_sell_g(const uint8_t* __restrict__ plan, const float2* __restrict__ Y,
-                                                     float2* __restrict__ F) {
+                                                     float2* __restrict__ F, SellMoveArgs m) {
     static_assert(NS % 2 == 0, "NS must be even");
     const SellHeader* h = reinterpret_cast<const SellHeader*>(plan);
     const int64_t rb = h->row_begin, re = h->row_end, S = h->slices;
@@ -178,7 +185,26 @@ __global__ void __launch_bounds__(256) k_attr_sell_g(const uint8_t* __restrict__
                 }
             }
         }
-        if (live) F[r - rb] = make_float2(fx, fy);
+        if constexpr (MOVE) {
+            bool bad = false;
+            if (live) {
+                const int64_t q = r - rb;
+                const Geo g = *m.geo;
+                const float2 ff = gather_field(g, m.fgrid, m.box[q], m.uv[q]);
+                float2 y = yi, v = m.vel[q], gn = m.gains[q];
+                const float gx = fmaf(4.0f * m.lambda_kl, fx, ff.x) + m.cn * y.x;
+                const float gy = fmaf(4.0f * m.lambda_kl, fy, ff.y) + m.cn * y.y;
+                gains_move(gx, v.x, gn.x, y.x, m.sp);
+                gains_move(gy, v.y, gn.y, y.y, m.sp);
+                bad = !(isfinite(y.x) && isfinite(y.y));
+                m.Ynew[q] = y;
+                m.vel[q] = v;
+                m.gains[q] = gn;
+            }
+            if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&m.geo->nonfinite, 1);
+        } else {
+            if (live) F[r - rb] = make_float2(fx, fy);
+        }
     }
 }
 
@@ -300,9 +326,11 @@ static constexpr size_t sell_tma_smem() {
 }
 
 using SellKernel = void (*)(const uint8_t*, const float2*, float2*);
+using SellGKernel = void (*)(const uint8_t*, const float2*, float2*, SellMoveArgs);
 
 struct SellLaunch {
-    SellKernel k = nullptr;
+    SellKernel k = nullptr;        // register / TMA variants (probing)
+    SellGKernel kg = nullptr;      // gather-pipelined variant (default)
     size_t smem = 0;
     int resident = 1;
 };
@@ -325,22 +353,17 @@ static const SellLaunch& sell_launch() {
     static SellLaunch L;
     if (!L.k) {
         const char* e = getenv("TSNET_SELL");
-        if (!e) e = "g4,4";
+        if (!e) e = "g4,4";   // the fused move (launch_attr_sell_move) uses this shape too
         int u = 4, cs = 8, r = 4;
         if (strncmp(e, "tma:", 4) != 0) {
             int ns = 4;
             u = 2;
             const bool g = strchr(e, 'g') != nullptr;    // "g2,4": gathers pipelined too
             sscanf(g ? e + 1 : e, "%d,%d", &u, &ns);
-            if (g && u == 2 && ns == 4) L.k = k_attr_sell_g<2, 4>;
-            else if (g && u == 4 && ns == 4) L.k = k_attr_sell_g<4, 4>;
-            else if (g && u == 2 && ns == 6) L.k = k_attr_sell_g<2, 6>;
-            else if (g && u == 4 && ns == 2) L.k = k_attr_sell_g<4, 2>;
-            else if (g && u == 1 && ns == 8) L.k = k_attr_sell_g<1, 8>;
-            else if (g && u == 8 && ns == 2) L.k = k_attr_sell_g<8, 2>;
-            else if (g && u == 4 && ns == 6) L.k = k_attr_sell_g<4, 6>;
-            else if (g && u == 3 && ns == 4) L.k = k_attr_sell_g<3, 4>;
-            else if (g && u == 6 && ns == 2) L.k = k_attr_sell_g<6, 2>;
+            if (g && u == 2 && ns == 4) L.kg = k_attr_sell_g<2, 4, false>;
+            else if (g && u == 4 && ns == 4) L.kg = k_attr_sell_g<4, 4, false>;
+            else if (g && u == 4 && ns == 2) L.kg = k_attr_sell_g<4, 2, false>;
+            else if (g && u == 6 && ns == 2) L.kg = k_attr_sell_g<6, 2, false>;
             else if (u == 4 && ns == 2) L.k = k_attr_sell<4, 2>;
             else if (u == 4 && ns == 3) L.k = k_attr_sell<4, 3>;
             else L.k = k_attr_sell<2, 4>;
@@ -356,9 +379,9 @@ static const SellLaunch& sell_launch() {
             else pick_tma<4, 8, 4>(L);
         }
         if (L.smem > 0) cudaFuncSetAttribute(L.k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&L.resident, L.k, 256, L.smem) != cudaSuccess ||
-            L.resident < 1)
-            L.resident = 1;
+        const cudaError_t oe = L.kg ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&L.resident, L.kg, 256, 0)
+                                    : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&L.resident, L.k, 256, L.smem);
+        if (oe != cudaSuccess || L.resident < 1) L.resident = 1;
     }
     return L;
 }
@@ -368,8 +391,26 @@ cudaError_t launch_attr_sell(const void* plan, const float2* Y, float2* F, int64
     if (nl == 0) return cudaSuccess;
     const SellLaunch& L = sell_launch();
     const int64_t slices = (nl + 31) / 32;
-    const int64_t blocks = std::min<int64_t>((slices + 7) / 8, (int64_t)kNumSMs * L.resident);
-    L.k<<<(int)std::max<int64_t>(1, blocks), 256, L.smem, s>>>(reinterpret_cast<const uint8_t*>(plan), Y, F);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((slices + 7) / 8, (int64_t)kNumSMs * L.resident));
+    const uint8_t* pl = reinterpret_cast<const uint8_t*>(plan);
+    if (L.kg) L.kg<<<blocks, 256, 0, s>>>(pl, Y, F, SellMoveArgs{});
+    else L.k<<<blocks, 256, L.smem, s>>>(pl, Y, F);
+    return cudaGetLastError();
+}
+
+// SpMV + move of the plan's rows (the default gather-pipelined kernel with
+// the a7 epilogue); F_attr is not stored.
+cudaError_t launch_attr_sell_move(const void* plan, const float2* Y, int64_t nl, const SellMoveArgs& m,
+                                  cudaStream_t s) {
+    if (nl == 0) return cudaSuccess;
+    static int resident = 0;
+    if (resident == 0 &&
+        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_attr_sell_g<4, 4, true>, 256, 0) != cudaSuccess ||
+         resident < 1))
+        resident = 1;
+    const int64_t slices = (nl + 31) / 32;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((slices + 7) / 8, (int64_t)kNumSMs * resident));
+    k_attr_sell_g<4, 4, true><<<blocks, 256, 0, s>>>(reinterpret_cast<const uint8_t*>(plan), Y, nullptr, m);
     return cudaGetLastError();
 }
 

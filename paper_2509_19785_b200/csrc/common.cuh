@@ -85,6 +85,7 @@ struct Ws {
     float2* colout;      // 6 * (M_max/2+1) * N_max  : after column pass, [b][kx][y]
     float4* fgrid;       // N_max^2 fields (P0, Qx, Qy, 0), row-major [gy][gx]
     float2* state;       // 4 n : host-facing step staging (Y, vel, gains, next Y)
+    float2* ynext;       // n   : new positions of the fused SpMV + move (sliced-ELL plan)
     double* cost;        // scratch for tsnet_cost (4 doubles)
     int64_t n, nnz;
     int I_max, N_max, M_max, max_items;
@@ -128,6 +129,7 @@ inline Ws ws_map(void* base, int64_t n, int64_t nnz, int I_max) {
     w.colout = (float2*)take(sizeof(float2) * 6 * half * (size_t)w.N_max);
     w.fgrid = (float4*)take(sizeof(float4) * (size_t)w.N_max * w.N_max);
     w.state = (float2*)take(sizeof(float2) * 4 * n);
+    w.ynext = (float2*)take(sizeof(float2) * n);
     w.cost = (double*)take(sizeof(double) * 8);
     w.bytes = off;
     return w;
@@ -154,6 +156,21 @@ cudaError_t launch_field_conv(const Ws& w, const GradArgs& a, cudaStream_t s);
 cudaError_t launch_spmv(const Ws& w, const GradArgs& a, cudaStream_t s);
 cudaError_t launch_attr_cb(const void* plan, const float2* Y, float2* F, int64_t nl, cudaStream_t s);
 cudaError_t launch_attr_sell(const void* plan, const float2* Y, float2* F, int64_t nl, cudaStream_t s);
+// step a7 fused into the sliced-ELL SpMV (attr_sell.cu); pointers index the
+// plan's rows (row r at r - row_begin)
+struct SellMoveArgs {
+    Geo* geo;
+    const float4* fgrid;
+    const int* box;
+    const float2* uv;
+    float2* Ynew;
+    float2* vel;
+    float2* gains;
+    float lambda_kl, cn;
+    tsnet_step_params sp;
+};
+cudaError_t launch_attr_sell_move(const void* plan, const float2* Y, int64_t nl, const SellMoveArgs& m,
+                                  cudaStream_t s);
 cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2* f_field, double* Z,
                             cudaStream_t s);
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,

@@ -1,0 +1,54 @@
+// move.cuh -- step a7 pieces shared by the stand-alone move (k_update,
+// iterate.cu) and the move fused into the sliced-ELL SpMV (attr_sell.cu):
+// the field gather at a point and the gains/momentum update (reading R12).
+#pragma once
+
+#include "common.cuh"
+
+namespace tsnet {
+
+__device__ __forceinline__ void lagrange3u(float u, float (&L)[3]) {
+    const float s0 = 1.0f / 6.0f, s1 = 0.5f, s2 = 5.0f / 6.0f;
+    L[0] = 4.5f * (u - s1) * (u - s2);
+    L[1] = -9.0f * (u - s0) * (u - s2);
+    L[2] = 4.5f * (u - s0) * (u - s1);
+}
+
+// f_field_i = sum_{a,b} L_a(u_x) L_b(u_y) [ (X_i - t_ab) P0 + Q ],  X_i - t_ab = (u - s) h_b
+__device__ __forceinline__ float2 gather_field(const Geo& g, const float4* __restrict__ fgrid, int b, float2 u) {
+    const int I = g.I, N = g.N;
+    const float h_b = (float)g.h_b;
+    // b / I by a float reciprocal: (b + 1/2) / I is >= 1/(2I) away from an
+    // integer, far more than the fp32 error for b < I^2 <= 768^2
+    const int by = __float2int_rz(((float)b + 0.5f) * __frcp_rn((float)I)), bx = b - by * I;
+    float Lx[3], Ly[3];
+    lagrange3u(u.x, Lx);
+    lagrange3u(u.y, Ly);
+    const float s[3] = {1.0f / 6.0f, 0.5f, 5.0f / 6.0f};
+    float fx = 0.f, fy = 0.f;
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb) {
+        const float4* row = fgrid + (int64_t)(3 * by + bb) * N + 3 * bx;
+        const float ey = (u.y - s[bb]) * h_b;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float4 f = row[a];   // generic load: fgrid may be the shared-memory copy
+            const float wgt = Lx[a] * Ly[bb];
+            const float ex = (u.x - s[a]) * h_b;
+            fx = fmaf(wgt, fmaf(ex, f.x, f.y), fx);
+            fy = fmaf(wgt, fmaf(ey, f.x, f.z), fy);
+        }
+    }
+    return make_float2(fx, fy);
+}
+
+__device__ __forceinline__ float sgnf(float x) { return (float)((x > 0.f) - (x < 0.f)); }
+
+__device__ __forceinline__ void gains_move(float gr, float& v, float& gn, float& y, const tsnet_step_params& sp) {
+    gn = (sgnf(gr) != sgnf(v)) ? gn + sp.gain_inc : gn * sp.gain_dec;
+    gn = fmaxf(gn, sp.gain_min);
+    v = sp.momentum * v - sp.eta * gn * gr;
+    y = y + v;
+}
+
+}  // namespace tsnet

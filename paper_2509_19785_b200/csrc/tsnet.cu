@@ -161,6 +161,19 @@ static cudaError_t side_stream(SideStream*& out) {
     return cudaSuccess;
 }
 
+// TSNET_FUSED_MOVE=1: with a sliced-ELL plan, run the field phase first and
+// fuse the move into the SpMV epilogue.  Off by default: measured 1015 vs
+// 1007 it/s on cfg 5 and 5577 vs 5965 it/s on cfg 3 -- the field phase then
+// no longer overlaps the SpMV, which costs about what k_update did.
+static bool fused_move_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TSNET_FUSED_MOVE");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 static int eval_gradient_parts(const Ws& w, const GradArgs& a, const tsnet_shard* sh, cudaStream_t s) {
     int st;
     if ((st = check_comm(sh, a)) != TSNET_OK) return st;
@@ -291,6 +304,26 @@ static int step_impl(const tsnet_csr* P, float* Y, float* vel, float* gains, con
     const bool multi = shard != nullptr && shard->comm != nullptr;
     TSNET_ARG(!multi || shard->bounds != nullptr, "a communicating shard needs shard->bounds to all-gather Y");
     if (a.n == 0) return TSNET_OK;
+    if (a.plan && a.plan_kind == TSNET_PLAN_SELL && !sp->recenter && fused_move_enabled()) {
+        // sliced-ELL plan: field phase first, then the SpMV with the move fused
+        // into its epilogue (no F_attr round trip, no k_update), new positions
+        // via w.ynext (the SpMV still gathers the old ones) copied back
+        if ((st = check_comm(shard, a)) != TSNET_OK) return st;
+        TSNET_CUDA(launch_field_local(w, a, s, multi));
+        if (multi && (st = comm_allreduce_grid(shard->comm, reinterpret_cast<float*>(w.wgrid), grid_floats(w), s)) !=
+                         TSNET_OK)
+            return st;
+        TSNET_CUDA(launch_field_conv(w, a, s));
+        if (before_update) TSNET_CUDA(cudaStreamWaitEvent(s, before_update, 0));
+        const int64_t nl = a.re - a.rb;
+        SellMoveArgs m{w.geo, w.fgrid, w.box, w.uv, w.ynext,
+                       reinterpret_cast<float2*>(vel) + a.rb, reinterpret_cast<float2*>(gains) + a.rb,
+                       a.lambda_kl, (float)((double)a.lambda_c / (double)a.n), *sp};
+        TSNET_CUDA(launch_attr_sell_move(a.plan, a.Y, nl, m, s));
+        TSNET_CUDA(cudaMemcpyAsync(Y + 2 * a.rb, w.ynext, sizeof(float2) * (size_t)nl, cudaMemcpyDeviceToDevice, s));
+        if (multi) return comm_allgather_rows(shard->comm, Y, shard->bounds, shard->world, s);
+        return TSNET_OK;
+    }
     if ((st = eval_gradient_parts(w, a, shard, s)) != TSNET_OK) return st;
     if (before_update) TSNET_CUDA(cudaStreamWaitEvent(s, before_update, 0));
     TSNET_CUDA(launch_update(w, a, reinterpret_cast<float2*>(Y), reinterpret_cast<float2*>(vel),

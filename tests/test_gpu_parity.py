@@ -348,6 +348,55 @@ def test_step_host_equals_device_step(cfg, recenter):
         assert relL2(Yh.numpy(), Yo) <= 1e-6
 
 
+@pytest.mark.parametrize("cfg,stage,recenter", [(2, 0, 0), (2, 1, 0), (3, 1, 0), (2, 1, 1)])
+def test_step_sell_plan_equals_csr_step(cfg, stage, recenter):
+    """tsnet_step with a sliced-ELL plan equals the CSR step and the oracle's.
+    Run in a subprocess with TSNET_FUSED_MOVE=1 too (the move fused into the
+    SpMV epilogue; with recentring the separate move): see the next test."""
+    P = oracle_P(cfg)
+    n = P["n"]
+    Y = clustered_layout(n, 20.0, 5, 1.5, 7)
+    vel, gains = random_state(n, 3)
+    lam = STAGE_A if stage == 0 else STAGE_B
+    mu = 0.5 if stage == 0 else 0.8
+    gp, sp = GradParams(*lam), StepParams(eta=50.0, momentum=mu, recenter=recenter)
+    out = {}
+    for plan in ("csr", "sell"):
+        Pd = dev_P(P)
+        if plan == "sell":
+            T.tsnet_sell_build(Pd)
+        Yd, Vd, Gd = (torch.from_numpy(a.copy()).cuda() for a in (Y, vel, gains))
+        ws = alloc_workspace(n, Pd.nnz, gp)
+        for _ in range(3):                       # three steps: the fused path reads its own output
+            tsnet_step(Pd, Yd, Vd, Gd, gp, sp, ws)
+        torch.cuda.synchronize()
+        out[plan] = (Yd.cpu().numpy(), Vd.cpu().numpy(), Gd.cpu().numpy())
+    assert relL2(out["sell"][0], out["csr"][0]) <= 1e-6
+    assert relL2(out["sell"][1], out["csr"][1]) <= 1e-5
+    assert relL2(out["sell"][2], out["csr"][2]) <= 1e-5
+    # one step against the oracle
+    Pd = T.tsnet_sell_build(dev_P(P))
+    Yd, Vd, Gd = (torch.from_numpy(a.copy()).cuda() for a in (Y, vel, gains))
+    tsnet_step(Pd, Yd, Vd, Gd, gp, StepParams(eta=50.0, momentum=mu), alloc_workspace(n, Pd.nnz, gp))
+    torch.cuda.synchronize()
+    r = oracle_grad(P, Y, lam)
+    _, Vo, _ = oracle.update_step(Y, vel, gains, r["g"], eta=50.0, mu=mu)
+    assert relL2(Vd.cpu().numpy(), Vo) <= GRAD_TOL
+
+
+def test_step_sell_fused_move_subprocess():
+    """The fused SpMV + move (TSNET_FUSED_MOVE=1, read once per process) passes
+    the sliced-ELL step tests."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, TSNET_FUSED_MOVE="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
+                        __file__ + "::test_step_sell_plan_equals_csr_step"], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
 def test_ten_iterations_config1():
     """Free-running 10 iterations (config 1: stage-B multipliers, momentum 0.5)."""
     P = oracle_P(1)
