@@ -505,7 +505,8 @@ static int step_host_pipelined(const tsnet_csr* P, float* Y_host, float* vel_hos
     tr.mark("y_in", 0, s);
     // vel/gains after Y (they share the host link; Y gates everything)
     TSNET_CUDA(cudaStreamWaitEvent(ss->copy, ss->y_in, 0));
-    for (int c = 0; c < chunks; ++c) {
+    for (int k = 0; k < chunks; ++k) {   // in processing order (last chunk first, below)
+        const int c = chunks - 1 - k;
         const size_t o = 2 * (size_t)rows(c), cb = sizeof(float2) * (size_t)(rows(c + 1) - rows(c));
         TSNET_CUDA(cudaMemcpyAsync(dV + rows(c), vel_host + o, cb, cudaMemcpyHostToDevice, ss->copy));
         TSNET_CUDA(cudaMemcpyAsync(dG + rows(c), gains_host + o, cb, cudaMemcpyHostToDevice, ss->copy));
@@ -522,7 +523,11 @@ static int step_host_pipelined(const tsnet_csr* P, float* Y_host, float* vel_hos
     TSNET_CUDA(launch_field_conv(w, a, fs));
     tr.mark("field", 0, fs);
     TSNET_CUDA(cudaMemsetAsync(w.f_attr, 0, b, s));
-    for (int c = 0; c < chunks; ++c) {
+    // last chunk first: chunks have equal nnz, so the first rows (hubs of a
+    // power-law graph) form the chunk with the fewest rows -- processed last,
+    // its download is the short tail that nothing overlaps
+    for (int k = 0; k < chunks; ++k) {
+        const int c = chunks - 1 - k;
         const int64_t r0 = rows(c), r1 = rows(c + 1);
         TSNET_CUDA(launch_spmv_rows(w, a, r0, r1, cut_nnz[c + 1] - cut_nnz[c], s));
         TSNET_CUDA(cudaEventRecord(ss->attr_done[c], s));
