@@ -153,6 +153,35 @@ typedef struct {
  * k_req; capped at n-1 (reading R5).  [host, pure] */
 TSNET_API int32_t tsnet_resolve_k(int64_t n, double perplexity_u, int32_t k_req);
 
+/* ------------------------------------------------ Pivot MDS initial layout */
+
+/*
+ * Alg. 3 line 2, "Compute initial layout D of G using Pivot MDS" (
+ * tsNET* = tsNET with a PMDS initialisation).  Set-up,
+ * outside the iteration loop.  Readings (R20-R22; the paper gives no
+ * parameters):
+ *   pivots: farthest-first -- the first is splitmix64(seed) mod n, each next
+ *           maximises the hop distance to the chosen set (ties: smallest id);
+ *           unreachable vertices count as distance n;
+ *   layout: D2 = hop^2 (n x p), C = -1/2 (D2 - row means - column means +
+ *           grand mean), v1, v2 = top-2 eigenvectors of C^T C (power
+ *           iteration from splitmix64 start vectors, <= 1000 iterations,
+ *           stop at |v' - v| < 1e-10; each flipped so its largest-magnitude
+ *           entry is positive), Y = C [v1 v2] (zero mean by construction);
+ *           a second eigenvalue <= 1e-12 of the first gives Y[:, 1] = 0.
+ * g       : graph (device CSR), 1 <= n < 2^31 - 1.
+ * pivots  : p, 1 <= p <= min(n, 1024) (SPEC default min(n, 250)).
+ * Y       : out, device, n x 2 fp32 interleaved.
+ * pivots_out (device int32[p]), hops_out (device int32[p][n], pivot-major),
+ * eig_out (device fp64[2]: the two eigenvalues): optional outputs, NULL = skip.
+ * ws      : device scratch of tsnet_pmds_workspace_bytes(n, p) bytes
+ *           (~4 n p bytes for the hop matrix).
+ * BLOCKING (one host round trip per BFS level).  TSNET_E_ARG on bad sizes.
+ */
+TSNET_API size_t tsnet_pmds_workspace_bytes(int64_t n, int32_t pivots);
+TSNET_API int tsnet_pmds(const tsnet_graph* g, int32_t pivots, uint64_t seed, float* Y, int32_t* pivots_out,
+                         int32_t* hops_out, double* eig_out, void* ws, size_t ws_bytes, tsnet_stream_t stream);
+
 /* Device scratch bytes tsnet_build_P needs for n vertices and k neighbours. [host] */
 TSNET_API size_t tsnet_build_P_workspace_bytes(int64_t n, int32_t k);
 

@@ -122,8 +122,11 @@ def embed(hops: np.ndarray, seed: int = 0):
     p = G.shape[0]
     l1, v1 = power_top(G, start_vector(p, seed, 1))
     v1 = orient(v1)
-    G2 = G - l1 * np.outer(v1, v1)
-    l2, v2 = power_top(G2, start_vector(p, seed, 2), ortho=v1)
+    if p < 2:                                         # one pivot: rank 1 (R22)
+        l2, v2 = 0.0, np.zeros(p)
+    else:
+        G2 = G - l1 * np.outer(v1, v1)
+        l2, v2 = power_top(G2, start_vector(p, seed, 2), ortho=v1)
     if l2 <= RANK_TOL * l1:
         v2 = np.zeros(p)
     else:

@@ -80,6 +80,9 @@ SIGNATURES = [
                                         ctypes.POINTER(c_sz), ctypes.POINTER(c_sz), c_vp]),
     ("tsnet_plan_build", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard), c_vp, c_sz, c_vp,
                                         c_sz, c_vp]),
+    ("tsnet_pmds_workspace_bytes", c_sz, [c_i64, c_i32]),
+    ("tsnet_pmds", ctypes.c_int, [ctypes.POINTER(tsnet_graph), c_i32, ctypes.c_uint64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                  c_sz, c_vp]),
     ("tsnet_sell_query", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard), ctypes.POINTER(c_sz),
                                         ctypes.POINTER(ctypes.c_double), c_vp]),
     ("tsnet_sell_build", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard), c_vp, c_sz, c_vp]),
@@ -243,6 +246,32 @@ def tsnet_build_P(indptr: torch.Tensor, indices: torch.Tensor, u: float = 40.0, 
     del ws
     return dict(P=CSR(P_ip, P_ix[:nnz].clone(), P_v[:nnz].clone()), knn_idx=knn_idx[:, :k], knn_hop=knn_hop[:, :k],
                 knn_len=knn_len[:n], beta=beta[:n], k=k, status=st)
+
+
+# ------------------------------------------------------ Pivot MDS layout
+def tsnet_pmds(indptr: torch.Tensor, indices: torch.Tensor, pivots: int = 250, seed: int = 0, hops: bool = False,
+               stream=None):
+    """Pivot MDS initial layout of the graph (set-up, blocking).  Returns a dict:
+    Y (n x 2 fp32, device), pivots (int32[p]), eig (fp64[2]) and, with
+    hops=True, the hop matrix (int32 p x n, pivot-major)."""
+    _require_cuda(indptr, indices)
+    n = indptr.numel() - 1
+    p = min(int(pivots), n)
+    dev = indptr.device
+    g = tsnet_graph(n, indptr.data_ptr(), indices.data_ptr() if indices.numel() else None)
+    Y = torch.empty((n, 2), dtype=torch.float32, device=dev)
+    piv = torch.empty(p, dtype=torch.int32, device=dev)
+    eig = torch.empty(2, dtype=torch.float64, device=dev)
+    H = torch.empty((p, n), dtype=torch.int32, device=dev) if hops else None
+    wb = int(lib().tsnet_pmds_workspace_bytes(n, p))
+    ws = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
+    _check("tsnet_pmds", lib().tsnet_pmds(ctypes.byref(g), p, ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), _ptr(Y),
+                                          _ptr(piv), _ptr(H) if H is not None else None, _ptr(eig), _ptr(ws), wb,
+                                          _stream(stream)))
+    out = {"Y": Y, "pivots": piv, "eig": eig}
+    if H is not None:
+        out["hops"] = H
+    return out
 
 
 # ------------------------------------------------ column-blocked plan of P
