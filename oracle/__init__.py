@@ -15,6 +15,7 @@ Layout of the oracle:
   interp.py O5    FFT-accelerated Lagrange-interpolation gradient (numpy, fp64)
   update.py O6/O7 momentum/gains update and stage schedule (numpy, fp64)
   pmds.py  O8    Pivot MDS initial layout (numpy, fp64; NEXT-2)
+  bh.py    O9    quadtree (Barnes-Hut) repulsion/entropy of BH-/FIt-tsNET (fp64; NEXT-3)
 
 Parity status of each function is listed in DESIGN.md §"Oracle pins"; every
 function here is pinned by a `-m "not gpu"` test in tests/test_oracle_*.py.
@@ -211,3 +212,4 @@ def exact_cost(X, indptr, indices, pval, lkl, lc, lr, eps=0.05):
 from .interp import geometry, lagrange_weights, interp_gradient, interp_fields  # noqa: E402
 from .update import update_step, stage_params, run_layout  # noqa: E402
 from . import pmds  # noqa: E402,F401
+from . import bh  # noqa: E402,F401
