@@ -286,6 +286,30 @@ TSNET_API int tsnet_step_host(const tsnet_csr* P, float* Y_host, float* vel_host
 TSNET_API int tsnet_cost(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, int32_t mode,
                const tsnet_shard* shard, double* out3, void* ws, size_t ws_bytes, tsnet_stream_t stream);
 
+/* ------------------------------------- quadtree variants (BH-/FIt-tsNET) */
+
+/*
+ * The gradient of the paper's other two algorithms (NEXT-3), on one GPU:
+ * BH-tsNET (variant 0, Alg. 2): KL repulsion
+ * (Eq. 6 second term, Z summed the same way) and the entropy gradient of Eq. 7
+ * (read with R2/R3) by a Barnes-Hut walk of a quadtree of Y
+ * (PAPER.md:172-173); FIt-tsNET (variant 1): the repulsion
+ * from the interpolation grid (as tsnet_grad with lambda_r = 0) and only the
+ * entropy from the quadtree.  Attraction: the same SpMV as tsnet_grad.
+ * Tree (R23): root = square of the bounding box, depth 16, nodes = runs of
+ * the Morton-sorted points; a node of > 1 point summarises for X_i when
+ * side^2 < theta^2 |X_i - com|^2 (fp64).  theta in [0, 0.7); theta = 0 gives
+ * the exact O(n^2) gradient.
+ * grad  : out, device n x 2 fp32 (the full gradient, as tsnet_grad).
+ * Z_out : optional device fp64: Z of the tree (variant 0) or of the grid (1).
+ * ws    : the tsnet_workspace_bytes workspace; tree_ws: device scratch of
+ *         tsnet_tree_workspace_bytes(n) bytes.  Single GPU, n < 2^26.
+ */
+TSNET_API size_t tsnet_tree_workspace_bytes(int64_t n);
+TSNET_API int tsnet_grad_tree(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, double theta,
+                              int32_t variant, float* grad, double* Z_out, void* ws, size_t ws_bytes, void* tree_ws,
+                              size_t tree_ws_bytes, tsnet_stream_t stream);
+
 /* ------------------------------------------- column-blocked layout of P (a6) */
 
 /*

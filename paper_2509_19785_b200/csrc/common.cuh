@@ -186,6 +186,9 @@ cudaError_t launch_spmv_rows(const Ws& w, const GradArgs& a, int64_t r0, int64_t
 cudaError_t launch_update_rows(const Ws& w, const GradArgs& a, int64_t r0, int64_t r1, float2* Yout, float2* vel,
                                float2* gains, const tsnet_step_params& sp, cudaStream_t s);
 cudaError_t launch_cost(const Ws& w, const GradArgs& a, int mode, double* out3, cudaStream_t s);
+// quadtree gradient of BH-tsNET (variant 0) / FIt-tsNET (variant 1), tree.cu
+int tree_gradient(const Ws& w, const GradArgs& a, double theta, int variant, float2* grad, double* Z_out,
+                  void* tws, size_t tws_bytes, cudaStream_t s);
 cudaError_t launch_entropy_sum(const Ws& w, const GradArgs& a, cudaStream_t s);
 
 }  // namespace tsnet

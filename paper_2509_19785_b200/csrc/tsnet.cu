@@ -596,6 +596,19 @@ int tsnet_step_host(const tsnet_csr* P, float* Y_host, float* vel_host, float* g
     return TSNET_OK;
 }
 
+int tsnet_grad_tree(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, double theta, int32_t variant,
+                    float* grad, double* Z_out, void* ws, size_t ws_bytes, void* tree_ws, size_t tree_ws_bytes,
+                    tsnet_stream_t stream) {
+    Ws w;
+    GradArgs a;
+    int st = prepare(P, Y, gp, nullptr, ws, ws_bytes, w, a);
+    if (st != TSNET_OK) return st;
+    TSNET_ARG(grad != nullptr, "grad is NULL");
+    if (a.n == 0) return TSNET_OK;
+    return tree_gradient(w, a, theta, variant, reinterpret_cast<float2*>(grad), Z_out, tree_ws, tree_ws_bytes,
+                         (cudaStream_t)stream);
+}
+
 int tsnet_cost(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, int32_t mode, const tsnet_shard* shard,
                double* out3, void* ws, size_t ws_bytes, tsnet_stream_t stream) {
     Ws w;

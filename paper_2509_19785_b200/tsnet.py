@@ -83,6 +83,9 @@ SIGNATURES = [
     ("tsnet_pmds_workspace_bytes", c_sz, [c_i64, c_i32]),
     ("tsnet_pmds", ctypes.c_int, [ctypes.POINTER(tsnet_graph), c_i32, ctypes.c_uint64, c_vp, c_vp, c_vp, c_vp, c_vp,
                                   c_sz, c_vp]),
+    ("tsnet_tree_workspace_bytes", c_sz, [c_i64]),
+    ("tsnet_grad_tree", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, ctypes.POINTER(tsnet_grad_params),
+                                       ctypes.c_double, c_i32, c_vp, c_vp, c_vp, c_sz, c_vp, c_sz, c_vp]),
     ("tsnet_sell_query", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard), ctypes.POINTER(c_sz),
                                         ctypes.POINTER(ctypes.c_double), c_vp]),
     ("tsnet_sell_build", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard), c_vp, c_sz, c_vp]),
@@ -379,6 +382,22 @@ def tsnet_grad(P: CSR, Y: torch.Tensor, gp: GradParams, ws: torch.Tensor, grad=N
     Pc, g = P.c(), gp.c()
     _check("tsnet_grad", lib().tsnet_grad(ctypes.byref(Pc), _ptr(Y), ctypes.byref(g), _shard(shard), _ptr(grad),
                                           _ptr(Z), _ptr(ws), ws.numel(), _stream(stream)))
+    return grad, Z
+
+
+def tsnet_grad_tree(P: CSR, Y: torch.Tensor, gp: GradParams, ws: torch.Tensor, theta: float = 0.5, variant: int = 0,
+                    tree_ws=None, grad=None, Z=None, stream=None):
+    """Quadtree gradient: variant 0 = BH-tsNET, 1 = FIt-tsNET (tsnet_grad_tree)."""
+    _require_cuda(Y, ws)
+    grad = torch.empty_like(Y) if grad is None else grad
+    Z = torch.empty(1, dtype=torch.float64, device=Y.device) if Z is None else Z
+    if tree_ws is None:
+        tree_ws = torch.empty(max(int(lib().tsnet_tree_workspace_bytes(Y.shape[0])), 1), dtype=torch.uint8,
+                              device=Y.device)
+    Pc, g = P.c(), gp.c()
+    _check("tsnet_grad_tree", lib().tsnet_grad_tree(ctypes.byref(Pc), _ptr(Y), ctypes.byref(g), float(theta),
+                                                    int(variant), _ptr(grad), _ptr(Z), _ptr(ws), ws.numel(),
+                                                    _ptr(tree_ws), tree_ws.numel(), _stream(stream)))
     return grad, Z
 
 
