@@ -16,6 +16,7 @@ Layout of the oracle:
   update.py O6/O7 momentum/gains update and stage schedule (numpy, fp64)
   pmds.py  O8    Pivot MDS initial layout (numpy, fp64; NEXT-2)
   bh.py    O9    quadtree (Barnes-Hut) repulsion/entropy of BH-/FIt-tsNET (fp64; NEXT-3)
+  quality.py O10  neighbourhood preservation and stress of a drawing (fp64; NEXT-4)
 
 Parity status of each function is listed in DESIGN.md §"Oracle pins"; every
 function here is pinned by a `-m "not gpu"` test in tests/test_oracle_*.py.
@@ -213,3 +214,4 @@ from .interp import geometry, lagrange_weights, interp_gradient, interp_fields  
 from .update import update_step, stage_params, run_layout  # noqa: E402
 from . import pmds  # noqa: E402,F401
 from . import bh  # noqa: E402,F401
+from . import quality  # noqa: E402,F401
