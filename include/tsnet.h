@@ -310,6 +310,30 @@ TSNET_API int tsnet_grad_tree(const tsnet_csr* P, const float* Y, const tsnet_gr
                               int32_t variant, float* grad, double* Z_out, void* ws, size_t ws_bytes, void* tree_ws,
                               size_t tree_ws_bytes, tsnet_stream_t stream);
 
+/* ----------------------------------------- drawing quality; stand-alone move */
+
+/*
+ * Quality metrics of §4.3 (NEXT-4) of a drawing Y (device n x 2 fp32) of g:
+ * out2[0] = neighbourhood preservation NP (mean over v of the
+ * Jaccard index of the r-hop neighbourhood and the same number of nearest
+ * drawn vertices, fp64 squared distances, ties by smaller id; r = 2 in the
+ * paper), out2[1] = aggregated stress with the optimal scale (PAPER.md:607-611,
+ * SPEC stress; NaN on a disconnected graph).  Readings R25-R26.  out2: device
+ * fp64[2].  2 <= n <= 24576 (an evaluation of small drawings: a CTA per vertex,
+ * O(n (n + m)) work).  ws: device scratch of tsnet_quality_workspace_bytes(n).
+ */
+TSNET_API size_t tsnet_quality_workspace_bytes(int64_t n);
+TSNET_API int tsnet_quality(const tsnet_graph* g, const float* Y, int32_t r, double* out2, void* ws, size_t ws_bytes,
+                            tsnet_stream_t stream);
+
+/*
+ * The gains/momentum move of step a7 (reading R12) for a
+ * gradient computed elsewhere (e.g. tsnet_grad_tree): in place on Y, vel,
+ * gains (device n x 2 fp32 each); grad device n x 2 fp32.  No recentring.
+ */
+TSNET_API int tsnet_move(float* Y, float* vel, float* gains, const float* grad, int64_t n,
+                         const tsnet_step_params* sp, tsnet_stream_t stream);
+
 /* ------------------------------------------- column-blocked layout of P (a6) */
 
 /*

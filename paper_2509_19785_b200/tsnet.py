@@ -86,6 +86,9 @@ SIGNATURES = [
     ("tsnet_tree_workspace_bytes", c_sz, [c_i64]),
     ("tsnet_grad_tree", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, ctypes.POINTER(tsnet_grad_params),
                                        ctypes.c_double, c_i32, c_vp, c_vp, c_vp, c_sz, c_vp, c_sz, c_vp]),
+    ("tsnet_quality_workspace_bytes", c_sz, [c_i64]),
+    ("tsnet_quality", ctypes.c_int, [ctypes.POINTER(tsnet_graph), c_vp, c_i32, c_vp, c_vp, c_sz, c_vp]),
+    ("tsnet_move", ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, ctypes.POINTER(tsnet_step_params), c_vp]),
     ("tsnet_sell_query", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard), ctypes.POINTER(c_sz),
                                         ctypes.POINTER(ctypes.c_double), c_vp]),
     ("tsnet_sell_build", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard), c_vp, c_sz, c_vp]),
@@ -275,6 +278,29 @@ def tsnet_pmds(indptr: torch.Tensor, indices: torch.Tensor, pivots: int = 250, s
     if H is not None:
         out["hops"] = H
     return out
+
+
+# ---------------------------------------------- quality metrics, stand-alone move
+def tsnet_quality(indptr: torch.Tensor, indices: torch.Tensor, Y: torch.Tensor, r: int = 2, stream=None):
+    """(NP, stress) of the drawing Y of the graph (device tensors)."""
+    _require_cuda(indptr, indices, Y)
+    n = indptr.numel() - 1
+    g = tsnet_graph(n, indptr.data_ptr(), indices.data_ptr() if indices.numel() else None)
+    out = torch.empty(2, dtype=torch.float64, device=Y.device)
+    wb = int(lib().tsnet_quality_workspace_bytes(n))
+    ws = torch.empty(max(wb, 1), dtype=torch.uint8, device=Y.device)
+    _check("tsnet_quality", lib().tsnet_quality(ctypes.byref(g), _ptr(Y), int(r), _ptr(out), _ptr(ws), wb,
+                                                _stream(stream)))
+    o = out.cpu().tolist()
+    return o[0], o[1]
+
+
+def tsnet_move(Y, vel, gains, grad, sp: StepParams, stream=None):
+    """Gains/momentum move of step a7 with a given gradient (in place)."""
+    _require_cuda(Y, vel, gains, grad)
+    s = sp.c()
+    _check("tsnet_move", lib().tsnet_move(_ptr(Y), _ptr(vel), _ptr(gains), _ptr(grad), Y.shape[0], ctypes.byref(s),
+                                          _stream(stream)))
 
 
 # ------------------------------------------------ column-blocked plan of P
