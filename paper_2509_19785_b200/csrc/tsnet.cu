@@ -113,8 +113,8 @@ constexpr int kHostChunksMax = 16;
 
 struct SideStream {
     int dev = -1;
-    cudaStream_t side = nullptr, copy = nullptr, d2h = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr, copied = nullptr, y_in = nullptr, drained = nullptr;
+    cudaStream_t side = nullptr, copy = nullptr, d2h = nullptr, spmv2 = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr, copied = nullptr, y_in = nullptr, drained = nullptr, zeroed = nullptr;
     cudaEvent_t attr_done[kHostChunksMax] = {}, moved[kHostChunksMax] = {}, state_in[kHostChunksMax] = {};
 };
 
@@ -145,6 +145,8 @@ static cudaError_t side_stream(SideStream*& out) {
         if ((e = cudaStreamCreateWithPriority(&x.side, cudaStreamNonBlocking, prio)) != cudaSuccess) return e;
         if ((e = cudaStreamCreateWithFlags(&x.copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
         if ((e = cudaStreamCreateWithFlags(&x.d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithFlags(&x.spmv2, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&x.zeroed, cudaEventDisableTiming)) != cudaSuccess) return e;
         if ((e = cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
         if ((e = cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming)) != cudaSuccess) return e;
         if ((e = cudaEventCreateWithFlags(&x.copied, cudaEventDisableTiming)) != cudaSuccess) return e;
@@ -385,6 +387,15 @@ int tsnet_step_finish(const tsnet_csr* P, float* Y, float* vel, float* gains, co
 
 namespace tsnet {
 
+static int host_spmv_streams() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TSNET_HOST_SPMV_STREAMS");
+        v = (e && e[0] == '1') ? 1 : 2;
+    }
+    return v;
+}
+
 // Row chunks of the pipelined host step (TSNET_HOST_CHUNKS, default 8; 1 = no pipeline).
 static int host_chunks(int64_t n) {
     static int v = -1;
@@ -523,15 +534,23 @@ static int step_host_pipelined(const tsnet_csr* P, float* Y_host, float* vel_hos
     TSNET_CUDA(launch_field_conv(w, a, fs));
     tr.mark("field", 0, fs);
     TSNET_CUDA(cudaMemsetAsync(w.f_attr, 0, b, s));
+    // the chunks' SpMV alternate between two streams, so that one chunk's
+    // last wave overlaps the next chunk's first (TSNET_HOST_SPMV_STREAMS=1: one)
+    const bool two = host_spmv_streams() == 2;
+    if (two) {
+        TSNET_CUDA(cudaEventRecord(ss->zeroed, s));
+        TSNET_CUDA(cudaStreamWaitEvent(ss->spmv2, ss->zeroed, 0));
+    }
     // last chunk first: chunks have equal nnz, so the first rows (hubs of a
     // power-law graph) form the chunk with the fewest rows -- processed last,
     // its download is the short tail that nothing overlaps
     for (int k = 0; k < chunks; ++k) {
         const int c = chunks - 1 - k;
         const int64_t r0 = rows(c), r1 = rows(c + 1);
-        TSNET_CUDA(launch_spmv_rows(w, a, r0, r1, cut_nnz[c + 1] - cut_nnz[c], s));
-        TSNET_CUDA(cudaEventRecord(ss->attr_done[c], s));
-        tr.mark("spmv", c, s);
+        cudaStream_t sa = (two && (k & 1)) ? ss->spmv2 : s;
+        TSNET_CUDA(launch_spmv_rows(w, a, r0, r1, cut_nnz[c + 1] - cut_nnz[c], sa));
+        TSNET_CUDA(cudaEventRecord(ss->attr_done[c], sa));
+        tr.mark("spmv", c, sa);
         TSNET_CUDA(cudaStreamWaitEvent(fs, ss->attr_done[c], 0));
         TSNET_CUDA(cudaStreamWaitEvent(fs, ss->state_in[c], 0));
         TSNET_CUDA(launch_update_rows(w, a, r0, r1, dYn, dV, dG, *sp, fs));

@@ -15,19 +15,21 @@ from .tsnet import CSR, alloc_workspace, lib, tsnet_grad_tree, tsnet_move, tsnet
 METHODS = ("tsnet", "bh", "fit", "linear")
 
 
-def run_method(P: CSR, Y0: torch.Tensor, method: str, iters: int = 500, theta: float = 0.5, stream=None):
-    """Layout after `iters` iterations of `method` from Y0 (device n x 2 fp32)."""
+def run_method(P: CSR, Y0: torch.Tensor, method: str, iters: int = 500, theta: float = 0.5, stream=None,
+               start: int = 0, state=None):
+    """Layout after iterations start .. start + iters of `method` from Y0
+    (device n x 2 fp32); `state` = (vel, gains) to continue a run (updated in
+    place), else zero velocity and unit gains."""
     assert method in METHODS
     Y = Y0.clone()
-    vel = torch.zeros_like(Y)
-    gains = torch.ones_like(Y)
+    vel, gains = state if state is not None else (torch.zeros_like(Y), torch.ones_like(Y))
     params = [stage_params(0), stage_params(1)]
     ws = alloc_workspace(P.n, P.nnz, params[0][0], device=Y.device)
     tws = None
     if method != "linear":
         tws = torch.empty(max(int(lib().tsnet_tree_workspace_bytes(P.n)), 1), dtype=torch.uint8, device=Y.device)
     grad = torch.empty_like(Y)
-    for it in range(iters):
+    for it in range(start, start + iters):
         gp, sp = params[stage_of(it)]
         if method == "linear":
             tsnet_step(P, Y, vel, gains, gp, sp, ws, stream=stream)
