@@ -387,11 +387,14 @@ int tsnet_step_finish(const tsnet_csr* P, float* Y, float* vel, float* gains, co
 
 namespace tsnet {
 
+// TSNET_HOST_SPMV_STREAMS=2 alternates the chunks' SpMV over two streams
+// (probing; measured 821 vs 835 it/s e2e on cfg 4 for one stream: the
+// overlapping chunks delay the first moves more than the tails cost)
 static int host_spmv_streams() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("TSNET_HOST_SPMV_STREAMS");
-        v = (e && e[0] == '1') ? 1 : 2;
+        v = (e && e[0] == '2') ? 2 : 1;
     }
     return v;
 }
@@ -534,8 +537,8 @@ static int step_host_pipelined(const tsnet_csr* P, float* Y_host, float* vel_hos
     TSNET_CUDA(launch_field_conv(w, a, fs));
     tr.mark("field", 0, fs);
     TSNET_CUDA(cudaMemsetAsync(w.f_attr, 0, b, s));
-    // the chunks' SpMV alternate between two streams, so that one chunk's
-    // last wave overlaps the next chunk's first (TSNET_HOST_SPMV_STREAMS=1: one)
+    // optionally the chunks' SpMV alternate between two streams, so that one
+    // chunk's last wave overlaps the next chunk's first
     const bool two = host_spmv_streams() == 2;
     if (two) {
         TSNET_CUDA(cudaEventRecord(ss->zeroed, s));
