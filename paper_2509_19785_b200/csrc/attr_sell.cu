@@ -386,12 +386,23 @@ static const SellLaunch& sell_launch() {
     return L;
 }
 
+// CTAs = TSNET_SELL_WAVES (default 1) x the resident CTAs (grid-stride over slices)
+static int sell_waves() {
+    static int v = 0;
+    if (v == 0) {
+        const char* e = getenv("TSNET_SELL_WAVES");
+        v = e ? std::max(1, std::min(64, atoi(e))) : 1;
+    }
+    return v;
+}
+
 // F: rows [row_begin, row_end) of the plan's shard (nl = row_end - row_begin)
 cudaError_t launch_attr_sell(const void* plan, const float2* Y, float2* F, int64_t nl, cudaStream_t s) {
     if (nl == 0) return cudaSuccess;
     const SellLaunch& L = sell_launch();
     const int64_t slices = (nl + 31) / 32;
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((slices + 7) / 8, (int64_t)kNumSMs * L.resident));
+    const int blocks = (int)std::max<int64_t>(
+        1, std::min<int64_t>((slices + 7) / 8, (int64_t)kNumSMs * L.resident * sell_waves()));
     const uint8_t* pl = reinterpret_cast<const uint8_t*>(plan);
     if (L.kg) L.kg<<<blocks, 256, 0, s>>>(pl, Y, F, SellMoveArgs{});
     else L.k<<<blocks, 256, L.smem, s>>>(pl, Y, F);

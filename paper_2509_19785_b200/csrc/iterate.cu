@@ -213,11 +213,13 @@ __global__ void __launch_bounds__(256) k_spmv2(int64_t rb, int64_t re_rows, cons
 struct SpmvCfg {
     int kernel = 2;      // 1: legacy k_spmv, 2: k_spmv2
     int U = 4;           // entries per lane per batch
-    int cpw = 4;         // chunks per warp
+    int cpw = 1;         // chunks per warp
     int ctas_per_sm = 5; // 256-thread CTAs per SM
     int l1 = 1;          // prefer L1 over shared memory (carveout 0)
     int reserve = 0;     // SMs left free for the concurrent field phase (side stream)
-    int cpw_rows = 2;    // chunks per warp in the row-chunk launches of the pipelined host step
+    int waves = 16;      // CTAs = waves x resident: short CTAs balance the power-law rows dynamically
+                         // (cfg 4 kernel 0.83 -> 0.80 ms, step 0.889 -> 0.865 ms vs one wave with cpw 4)
+    int cpw_rows = 1;    // chunks per warp in the row-chunk launches of the pipelined host step
 };
 
 static int env_int(const char* name, int def) {
@@ -237,6 +239,7 @@ static const SpmvCfg& spmv_cfg() {
         c.ctas_per_sm = std::max(1, env_int("TSNET_SPMV_CTAS", c.ctas_per_sm));
         c.l1 = env_int("TSNET_SPMV_L1", c.l1);
         c.reserve = std::max(0, std::min(64, env_int("TSNET_SPMV_RESERVE_SMS", c.reserve)));
+        c.waves = std::max(1, std::min(64, env_int("TSNET_SPMV_WAVES", c.waves)));
         init = true;
     }
     return c;
@@ -250,12 +253,13 @@ static cudaError_t launch_spmv2_t(const GradArgs& a, float2* F, const SpmvCfg& c
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_spmv2<U>, 256, 0) != cudaSuccess || resident < 1)
             resident = 1;
     }
-    // one wave: every warp runs concurrently (the chunk cut assumes it);
-    // small problems: fewer CTAs so that chunks stay >= 1024 entries
+    // `waves` x the resident CTAs, each warp `cpw` equal chunks (the hardware
+    // scheduler balances the CTAs); small problems: fewer CTAs so that chunks
+    // stay >= 1024 entries
     const int64_t want = std::max<int64_t>(1, a.nnz / (1024 * 8 * c.cpw));
     const int per_sm = std::min(c.ctas_per_sm, resident);
     const int blocks =
-        (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)(kNumSMs - c.reserve) * per_sm));
+        (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)(kNumSMs - c.reserve) * per_sm * c.waves));
     k_spmv2<U><<<blocks, 256, 0, s>>>(a.rb, a.re, a.indptr, a.indices, a.values, a.Y, F, c.cpw);
     return cudaGetLastError();
 }

@@ -399,12 +399,13 @@ static int host_spmv_streams() {
     return v;
 }
 
-// Row chunks of the pipelined host step (TSNET_HOST_CHUNKS, default 8; 1 = no pipeline).
+// Row chunks of the pipelined host step (TSNET_HOST_CHUNKS, default 4; 1 = no pipeline):
+// measured on cfg 4 with the multi-wave SpMV, e2e 815 / 850 / 851 / 827 / 823 / 770 it/s for 2 / 3 / 4 / 5 / 6 / 8.
 static int host_chunks(int64_t n) {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("TSNET_HOST_CHUNKS");
-        v = e ? std::max(1, std::min(kHostChunksMax, atoi(e))) : 8;
+        v = e ? std::max(1, std::min(kHostChunksMax, atoi(e))) : 4;
     }
     return n >= (int64_t)v * 16384 ? v : 1;
 }
