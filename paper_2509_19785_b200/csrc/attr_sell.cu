@@ -137,9 +137,10 @@ __global__ void __launch_bounds__(256) k_attr_sell(const uint8_t* __restrict__ p
 // and moves the point (gains/momentum), writing the new position to m.Ynew
 // (never Y: other warps still gather the old positions) and vel/gains in
 // place.  Same arithmetic as k_update.
-template <int U, int NS, bool MOVE>
-__global__ void __launch_bounds__(256) k_attr_sell_g(const uint8_t* __restrict__ plan, const float2* __restrict__ Y,
-                                                     float2* __restrict__ F, SellMoveArgs m) {
+template <int U, int NS, bool MOVE, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_attr_sell_g(const uint8_t* __restrict__ plan,
+                                                           const float2* __restrict__ Y, float2* __restrict__ F,
+                                                           SellMoveArgs m) {
     static_assert(NS % 2 == 0, "NS must be even");
     const SellHeader* h = reinterpret_cast<const SellHeader*>(plan);
     const int64_t rb = h->row_begin, re = h->row_end, S = h->slices;
@@ -336,8 +337,10 @@ struct SellLaunch {
 };
 
 // Kernel choice (measured on config 5, kernel alone, B200; CSR kernel 1.22 ms):
-//   gU,NS  entries and gathers pipelined (k_attr_sell_g): g4,4 0.801 ms (default),
-//          g4,2 0.820, g2,4 0.879, g2,6 1.137, g1,8 1.537;
+//   gU,NS[,MINB]  entries and gathers pipelined (k_attr_sell_g), MINB = CTAs per
+//          SM promised to ptxas: g4,4,4 0.751 ms (default; 64 registers, 87% of
+//          the measured HBM peak), g4,4,3 0.771, g4,4,1 0.996 (94 registers, 2
+//          CTAs/SM), g4,2 0.816, g2,4 0.879, g2,6 1.137, g1,8 1.537;
 //   U,NS   entries pipelined only (k_attr_sell): 2,4 0.921, 4,2 0.937, 4,3 0.943;
 //   tma:U,CS,R  TMA-staged entries (k_attr_sell_tma): 8,8,4 1.012, 4,8,3 1.052,
 //          4,8,4 1.138, 8,4,4 1.143 -- the ring's shared memory takes L1
@@ -357,12 +360,16 @@ static const SellLaunch& sell_launch() {
         int u = 4, cs = 8, r = 4;
         if (strncmp(e, "tma:", 4) != 0) {
             int ns = 4;
-            u = 2;
-            const bool g = strchr(e, 'g') != nullptr;    // "g2,4": gathers pipelined too
-            sscanf(g ? e + 1 : e, "%d,%d", &u, &ns);
+            u = 4;
+            const bool g = strchr(e, 'g') != nullptr;    // "gU,NS[,MINB]": gathers pipelined too
+            int mb = 4;
+            sscanf(g ? e + 1 : e, "%d,%d,%d", &u, &ns, &mb);
             if (g && u == 2 && ns == 4) L.kg = k_attr_sell_g<2, 4, false>;
-            else if (g && u == 4 && ns == 4) L.kg = k_attr_sell_g<4, 4, false>;
-            else if (g && u == 4 && ns == 2) L.kg = k_attr_sell_g<4, 2, false>;
+            else if (g && u == 4 && ns == 4 && mb == 1) L.kg = k_attr_sell_g<4, 4, false, 1>;
+            else if (g && u == 4 && ns == 4 && mb == 3) L.kg = k_attr_sell_g<4, 4, false, 3>;
+            else if (g && u == 4 && ns == 4) L.kg = k_attr_sell_g<4, 4, false, 4>;
+            else if (g && u == 4 && ns == 2 && mb == 1) L.kg = k_attr_sell_g<4, 2, false, 1>;
+            else if (g && u == 4 && ns == 2) L.kg = k_attr_sell_g<4, 2, false, 4>;
             else if (g && u == 6 && ns == 2) L.kg = k_attr_sell_g<6, 2, false>;
             else if (u == 4 && ns == 2) L.k = k_attr_sell<4, 2>;
             else if (u == 4 && ns == 3) L.k = k_attr_sell<4, 3>;
@@ -416,12 +423,12 @@ cudaError_t launch_attr_sell_move(const void* plan, const float2* Y, int64_t nl,
     if (nl == 0) return cudaSuccess;
     static int resident = 0;
     if (resident == 0 &&
-        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_attr_sell_g<4, 4, true>, 256, 0) != cudaSuccess ||
+        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_attr_sell_g<4, 4, true, 3>, 256, 0) != cudaSuccess ||
          resident < 1))
         resident = 1;
     const int64_t slices = (nl + 31) / 32;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((slices + 7) / 8, (int64_t)kNumSMs * resident));
-    k_attr_sell_g<4, 4, true><<<blocks, 256, 0, s>>>(reinterpret_cast<const uint8_t*>(plan), Y, nullptr, m);
+    k_attr_sell_g<4, 4, true, 3><<<blocks, 256, 0, s>>>(reinterpret_cast<const uint8_t*>(plan), Y, nullptr, m);
     return cudaGetLastError();
 }
 

@@ -337,15 +337,16 @@ def tsnet_sell_query(P: CSR, shard=None, stream=None):
     return int(pb.value), float(ratio.value)
 
 
-SELL_AUTO_MAX_SLOTS_PER_NNZ = 1.6
+SELL_AUTO_MAX_SLOTS_PER_NNZ = 1.3
 
 
 def attach_plan(P: CSR, plan="auto", shard=None, stream=None) -> CSR:
     """Attach the SpMV layout `plan` to P: "csr" (none), "cb" (column-blocked),
     "sell" (sliced ELL), or "auto": sliced ELL when its padding is at most
-    SELL_AUTO_MAX_SLOTS_PER_NNZ slots per stored entry (meshes, block models:
-    measured faster than CSR there), else CSR (power-law graphs, where hub rows
-    pad the slices and the gathers are random anyway)."""
+    SELL_AUTO_MAX_SLOTS_PER_NNZ slots per stored entry (meshes: cfg 5 pads
+    1.027, 1028 vs 710 it/s), else CSR (power-law graphs, where hub rows pad
+    the slices and the gathers are random anyway, and block models: cfg 3 pads
+    1.49, CSR 6188 vs 5337 it/s)."""
     if plan in (None, False, "csr"):
         return P
     if plan in (True, "cb"):
