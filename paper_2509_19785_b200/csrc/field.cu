@@ -19,6 +19,7 @@
 //           = -4 lambda_kl F_rep + lambda_r g_ent   (local-moment form).
 #include "common.cuh"
 #include "fft.cuh"
+#include "move.cuh"
 
 namespace tsnet {
 
@@ -177,17 +178,7 @@ constexpr int kBoxSmem = 4096;     // counters (16 KB): I <= 64
 constexpr int kBoxPts = 8;         // points per thread
 constexpr int kBoxChunk = 256 * kBoxPts;
 
-__device__ __forceinline__ void box_of(float2 y, double lo_x, double lo_y, double h_b, int I, int& b, float& ux,
-                                       float& uy) {
-    double rx = ((double)y.x - lo_x) / h_b;
-    double ry = ((double)y.y - lo_y) / h_b;
-    double fx = floor(rx), fy = floor(ry);
-    int bx = (int)fmin(fmax(fx, 0.0), (double)(I - 1));
-    int by = (int)fmin(fmax(fy, 0.0), (double)(I - 1));
-    ux = (float)(rx - (double)bx);
-    uy = (float)(ry - (double)by);
-    b = by * I + bx;
-}
+// box_of (the box of a point and its in-box coordinates): move.cuh
 
 __global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__ Y, int64_t n, const Geo* __restrict__ g,
                                                    int* __restrict__ box_cnt, int* __restrict__ box,

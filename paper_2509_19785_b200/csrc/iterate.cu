@@ -314,6 +314,10 @@ __global__ void __launch_bounds__(256) k_grad_out(int64_t n, const Geo* __restri
 // cost no L2 requests (they were ~9 sector requests per point).
 constexpr int kUpdateThreads = 1024;
 constexpr int kGridSmemCells = 12800;   // 200 KB of float4
+// V points per thread and iteration (their loads in flight together); RECOMPUTE:
+// the box and in-box coordinates from the position (as k_box_count) instead of
+// reading them back (12 B/point less traffic, some fp64 arithmetic more)
+template <int V, bool RECOMPUTE>
 __global__ void __launch_bounds__(kUpdateThreads, 1) k_update(int64_t n, Geo* __restrict__ gp,
                                                               const float4* __restrict__ fgrid,
                                                               const int* __restrict__ box, const float2* __restrict__ uv,
@@ -333,8 +337,6 @@ __global__ void __launch_bounds__(kUpdateThreads, 1) k_update(int64_t n, Geo* __
     }
     double sx = 0.0, sy = 0.0;
     bool bad = false;
-    // two points per thread and iteration: all their loads in flight together
-    constexpr int V = 2;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += V * stride) {
         int b[V];
@@ -343,12 +345,18 @@ __global__ void __launch_bounds__(kUpdateThreads, 1) k_update(int64_t n, Geo* __
         for (int q = 0; q < V; ++q) {
             const int64_t i = i0 + q * stride;
             const bool h = i < n;
-            b[q] = h ? box[i] : 0;
-            u[q] = h ? uv[i] : make_float2(0.5f, 0.5f);
+            if (!RECOMPUTE) {
+                b[q] = h ? box[i] : 0;
+                u[q] = h ? uv[i] : make_float2(0.5f, 0.5f);
+            }
             y[q] = h ? Yin[i] : make_float2(0.f, 0.f);
             fa[q] = h ? Fa[i] : make_float2(0.f, 0.f);
             v[q] = h ? vel[i] : make_float2(0.f, 0.f);
             gn[q] = h ? gains[i] : make_float2(1.f, 1.f);
+        }
+        if (RECOMPUTE) {
+#pragma unroll
+            for (int q = 0; q < V; ++q) box_of(y[q], g.lo_x, g.lo_y, g.h_b, g.I, b[q], u[q].x, u[q].y);
         }
 #pragma unroll
         for (int q = 0; q < V; ++q) {
@@ -408,10 +416,29 @@ cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2
     return e;
 }
 
+using UpdateKernel = void (*)(int64_t, Geo*, const float4*, const int*, const float2*, const float2*, float2*,
+                              const float2*, float2*, float2*, float, float, tsnet_step_params, int);
+
+// TSNET_UPDATE=V,R (probing): V points per thread, R = 1 recompute the box.
+// All four within noise on the step (r1cd: cfg 5 1027-1039 it/s, cfg 4
+// 1150-1156): the move is ~2% of the step; default 2 points, read the box.
+static UpdateKernel update_kernel() {
+    static UpdateKernel k = nullptr;
+    if (!k) {
+        int v = 2, r = 0;
+        if (const char* e = getenv("TSNET_UPDATE")) sscanf(e, "%d,%d", &v, &r);
+        if (v == 1 && r) k = k_update<1, true>;
+        else if (v == 1) k = k_update<1, false>;
+        else if (r) k = k_update<2, true>;
+        else k = k_update<2, false>;
+    }
+    return k;
+}
+
 static cudaError_t update_smem_attr() {
     static bool done = false;
     if (done) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(update_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(sizeof(float4) * kGridSmemCells));
     done = e == cudaSuccess;
     return e;
@@ -426,7 +453,7 @@ cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel
     cudaError_t ea = update_smem_attr();
     if (ea != cudaSuccess) return ea;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nl + kUpdateThreads - 1) / kUpdateThreads, kNumSMs));
-    k_update<<<blocks, kUpdateThreads, smem, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, Y + a.rb, Y + a.rb, w.f_attr,
+    update_kernel()<<<blocks, kUpdateThreads, smem, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, Y + a.rb, Y + a.rb, w.f_attr,
                                                   vel + a.rb, gains + a.rb, a.lambda_kl, cn_of(a), sp, cap);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !sp.recenter) return e;
@@ -464,7 +491,7 @@ cudaError_t launch_update_rows(const Ws& w, const GradArgs& a, int64_t r0, int64
     // chunk, whose CTAs run with the whole L1 carveout (a 200 KB shared-memory
     // CTA would wait for an idle SM); the field nodes are read through L1/L2
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nc + kUpdateThreads - 1) / kUpdateThreads, kNumSMs));
-    k_update<<<blocks, kUpdateThreads, 0, s>>>(nc, w.geo, w.fgrid, w.box + q, w.uv + q, a.Y + r0, Yout + r0,
+    update_kernel()<<<blocks, kUpdateThreads, 0, s>>>(nc, w.geo, w.fgrid, w.box + q, w.uv + q, a.Y + r0, Yout + r0,
                                                w.f_attr + q, vel + r0, gains + r0, a.lambda_kl, cn_of(a), sp, 0);
     return cudaGetLastError();
 }

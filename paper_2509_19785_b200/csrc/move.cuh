@@ -7,6 +7,21 @@
 
 namespace tsnet {
 
+// a1: box of a point and its in-box coordinates (fp64 arithmetic, reading
+// R16); shared by the box sort (field.cu) and the move, which recomputes it
+// from the position it reads anyway instead of reading it back (12 B/point)
+__device__ __forceinline__ void box_of(float2 y, double lo_x, double lo_y, double h_b, int I, int& b, float& ux,
+                                       float& uy) {
+    double rx = ((double)y.x - lo_x) / h_b;
+    double ry = ((double)y.y - lo_y) / h_b;
+    double fx = floor(rx), fy = floor(ry);
+    int bx = (int)fmin(fmax(fx, 0.0), (double)(I - 1));
+    int by = (int)fmin(fmax(fy, 0.0), (double)(I - 1));
+    ux = (float)(rx - (double)bx);
+    uy = (float)(ry - (double)by);
+    b = by * I + bx;
+}
+
 __device__ __forceinline__ void lagrange3u(float u, float (&L)[3]) {
     const float s0 = 1.0f / 6.0f, s1 = 0.5f, s2 = 5.0f / 6.0f;
     L[0] = 4.5f * (u - s1) * (u - s2);
