@@ -17,6 +17,7 @@
 namespace tsnet {
 
 constexpr int kSpmvChunk = 2048;   // stored entries of P per warp work item
+constexpr double kHubFactor = 4.0; // hot-column L1 policy threshold (k_spmv2)
 constexpr int kSpmvUnroll = 4;
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -122,12 +123,31 @@ __device__ __forceinline__ void spmv2_load(const int32_t* __restrict__ indices, 
     }
 }
 
-template <int U>
+__device__ __forceinline__ float2 ld_y_keep(const float2* a) {
+    float2 v;
+    asm volatile("ld.global.nc.L1::evict_last.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
+    return v;
+}
+__device__ __forceinline__ float2 ld_y_pass(const float2* a) {
+    float2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(a));
+    return v;
+}
+
+// HUB: columns below `hub` are kept in L1 (evict_last) and the others bypass
+// it, so the hot lines are not flushed by the stream of one-off gathers
+// (hub_columns() decides when)
+template <int U, bool HUB>
 __device__ __forceinline__ void spmv2_acc(const float2* __restrict__ Y, float2 yi, const int (&col)[U],
-                                          const float (&val)[U], float& fx, float& fy) {
+                                          const float (&val)[U], float& fx, float& fy, int hub) {
     float2 yj[U];
+    if (HUB) {
 #pragma unroll
-    for (int q = 0; q < U; ++q) yj[q] = __ldg(Y + col[q]);
+        for (int q = 0; q < U; ++q) yj[q] = col[q] < hub ? ld_y_keep(Y + col[q]) : ld_y_pass(Y + col[q]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < U; ++q) yj[q] = __ldg(Y + col[q]);
+    }
 #pragma unroll
     for (int q = 0; q < U; ++q) {
         const float dx = yi.x - yj[q].x, dy = yi.y - yj[q].y;
@@ -141,10 +161,11 @@ __device__ __forceinline__ void spmv2_acc(const float2* __restrict__ Y, float2 y
 
 // Rows [rb, re): the stored entries indptr[rb] .. indptr[re] are cut into
 // chunks; F holds rows rb.. (F[r - rb]).
-template <int U>
+template <int U, bool HUB>
 __global__ void __launch_bounds__(256) k_spmv2(int64_t rb, int64_t re_rows, const int64_t* __restrict__ indptr,
                                                const int32_t* __restrict__ indices, const float* __restrict__ values,
-                                               const float2* __restrict__ Y, float2* __restrict__ F, int cpw) {
+                                               const float2* __restrict__ Y, float2* __restrict__ F, int cpw,
+                                               int hub) {
     const int lane = threadIdx.x & 31;
     const int64_t e_begin = __ldg(indptr + rb), e_end = __ldg(indptr + re_rows);
     const int64_t nwarps_total = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -176,12 +197,12 @@ __global__ void __launch_bounds__(256) k_spmv2(int64_t rb, int64_t re_rows, cons
             }
             const float2 yi = __ldg(Y + r);
             float fx = 0.f, fy = 0.f;
-            spmv2_acc<U>(Y, yi, col, val, fx, fy);
+            spmv2_acc<U, HUB>(Y, yi, col, val, fx, fy, hub);
             for (int64_t b = rs + 32 * U; b < re; b += 32 * U) {   // long rows: further batches
                 int cb[U];
                 float vb[U];
                 spmv2_load<U>(indices, values, b, re, lane, cb, vb, (int)r, pol);
-                spmv2_acc<U>(Y, yi, cb, vb, fx, fy);
+                spmv2_acc<U, HUB>(Y, yi, cb, vb, fx, fy, hub);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
@@ -220,6 +241,8 @@ struct SpmvCfg {
     int waves = 16;      // CTAs = waves x resident: short CTAs balance the power-law rows dynamically
                          // (cfg 4 kernel 0.83 -> 0.80 ms, step 0.889 -> 0.865 ms vs one wave with cpw 4)
     int cpw_rows = 1;    // chunks per warp in the row-chunk launches of the pipelined host step
+    int hub = 8192;      // hot-column L1 policy candidate (hub_columns() decides per P; 0 = off):
+                         // cfg 4 kernel 0.792 -> 0.769 ms (r1cg; 4096: 0.778, 12288: 0.767, 16384: 0.771)
 };
 
 static int env_int(const char* name, int def) {
@@ -236,6 +259,7 @@ static const SpmvCfg& spmv_cfg() {
         c.U = env_int("TSNET_SPMV_U", c.U);
         c.cpw = std::max(1, env_int("TSNET_SPMV_CPW", c.cpw));
         c.cpw_rows = std::max(1, env_int("TSNET_SPMV_CPW_ROWS", c.cpw_rows));
+        c.hub = std::max(0, env_int("TSNET_SPMV_HUB_COLS", c.hub));
         c.ctas_per_sm = std::max(1, env_int("TSNET_SPMV_CTAS", c.ctas_per_sm));
         c.l1 = env_int("TSNET_SPMV_L1", c.l1);
         c.reserve = std::max(0, std::min(64, env_int("TSNET_SPMV_RESERVE_SMS", c.reserve)));
@@ -245,12 +269,46 @@ static const SpmvCfg& spmv_cfg() {
     return c;
 }
 
-template <int U>
-static cudaError_t launch_spmv2_t(const GradArgs& a, float2* F, const SpmvCfg& c, cudaStream_t s) {
+// Hot-column L1 policy for this P: on when its first `cand` columns (P is
+// symmetric: column count = row length) hold >= kHubFactor x their share of
+// the stored entries -- a power-law graph numbered by weight (cfg 4: 10% of
+// the entries in the first 8192 columns, 12x their share; meshes, block
+// models and random numberings stay off).  Decided once per P (three indptr
+// reads, cached); never inside a stream capture (then off until an eager call).
+static int hub_columns(const GradArgs& a, int cand, cudaStream_t s) {
+    if (cand <= 0 || cand >= a.n) return 0;
+    struct Entry {
+        const void* indptr = nullptr;
+        int64_t n = -1;
+        int cand = 0, hub = 0;
+    };
+    static thread_local Entry cache[4];
+    static thread_local int next = 0;
+    for (const auto& e : cache)
+        if (e.indptr == a.indptr && e.n == a.n && e.cand == cand) return e.hub;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return 0;
+    int64_t v[3] = {0, 0, 0};
+    if (cudaMemcpy(&v[0], a.indptr, sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(&v[1], a.indptr + cand, sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(&v[2], a.indptr + a.n, sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return 0;
+    const double share = (double)(v[1] - v[0]) / (double)std::max<int64_t>(1, v[2] - v[0]);
+    Entry& e = cache[next++ & 3];
+    e.indptr = a.indptr;
+    e.n = a.n;
+    e.cand = cand;
+    e.hub = share >= kHubFactor * (double)cand / (double)a.n ? cand : 0;
+    return e.hub;
+}
+
+template <int U, bool HUB>
+static cudaError_t launch_spmv2_h(const GradArgs& a, float2* F, const SpmvCfg& c, int hub, cudaStream_t s) {
     static int resident = 0;
     if (resident == 0) {
-        if (c.l1) cudaFuncSetAttribute(k_spmv2<U>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_spmv2<U>, 256, 0) != cudaSuccess || resident < 1)
+        if (c.l1) cudaFuncSetAttribute(k_spmv2<U, HUB>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_spmv2<U, HUB>, 256, 0) != cudaSuccess ||
+            resident < 1)
             resident = 1;
     }
     // `waves` x the resident CTAs, each warp `cpw` equal chunks (the hardware
@@ -260,8 +318,14 @@ static cudaError_t launch_spmv2_t(const GradArgs& a, float2* F, const SpmvCfg& c
     const int per_sm = std::min(c.ctas_per_sm, resident);
     const int blocks =
         (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)(kNumSMs - c.reserve) * per_sm * c.waves));
-    k_spmv2<U><<<blocks, 256, 0, s>>>(a.rb, a.re, a.indptr, a.indices, a.values, a.Y, F, c.cpw);
+    k_spmv2<U, HUB><<<blocks, 256, 0, s>>>(a.rb, a.re, a.indptr, a.indices, a.values, a.Y, F, c.cpw, hub);
     return cudaGetLastError();
+}
+
+template <int U>
+static cudaError_t launch_spmv2_t(const GradArgs& a, float2* F, const SpmvCfg& c, cudaStream_t s) {
+    const int hub = hub_columns(a, c.hub, s);
+    return hub > 0 ? launch_spmv2_h<U, true>(a, F, c, hub, s) : launch_spmv2_h<U, false>(a, F, c, 0, s);
 }
 
 // a6 for the rows [rb, re) of the call into w.f_attr (local rows): the
