@@ -55,7 +55,12 @@ def measured_peak():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi clocks/throttle reasons every 100 ms with a timestamp per
+    sample; start() well before the timed region (nvidia-smi needs ~1 s to
+    produce its first line), stop(t0, t1) keeps the samples taken inside the
+    timed wall-clock window [t0, t1] (widened to the nearest samples when the
+    window is shorter than the sampling period)."""
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -73,8 +78,15 @@ class ClockSampler:
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+        if self.proc is not None:
+            import atexit
+            atexit.register(self._kill)      # never leave the sampler running (error paths)
 
-    def stop(self):
+    def _kill(self):
+        if self.proc is not None and self.proc.poll() is None:
+            self.proc.kill()
+
+    def stop(self, t0: float | None = None, t1: float | None = None):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         self.proc.terminate()
@@ -82,23 +94,29 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-        sm, smax, reasons = [], [], set()
+        import datetime
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         with open(self.path) as f:
             for ln in f:
                 parts = [p.strip() for p in ln.split(",")]
                 if len(parts) < 9:
                     continue
                 try:
-                    sm.append(float(parts[1]))
-                    smax.append(float(parts[2]))
+                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                    rows.append((ts, float(parts[1]), float(parts[2]),
+                                 {nm for nm, v in zip(names, parts[5:9]) if v.lower().startswith("active")}))
                 except ValueError:
                     continue
-                for nm, v in zip(names, parts[5:9]):
-                    if v.lower().startswith("active"):
-                        reasons.add(nm)
         os.unlink(self.path)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+        if t0 is not None and t1 is not None and rows:
+            inside = [r for r in rows if t0 <= r[0] <= t1]
+            if not inside:                      # window shorter than the period: the nearest samples
+                inside = sorted(rows, key=lambda r: min(abs(r[0] - t0), abs(r[0] - t1)))[:2]
+            rows = inside
+        sm = [r[1] for r in rows]
+        reasons = set().union(*[r[3] for r in rows]) if rows else set()
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(r[2] for r in rows) if rows else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
@@ -213,6 +231,8 @@ def run_ours(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    clocks = ClockSampler(local_rank)          # started early: nvidia-smi's first sample takes ~1 s
+    clocks.start()
     ip, ix = config_graph(args.config)
     t0 = time.perf_counter()
     built = tsnet_build_P(torch.from_numpy(ip).to(dev), torch.from_numpy(ix).to(dev), u=40.0, seed=0)
@@ -256,8 +276,6 @@ def run_ours(args, rank, world, local_rank):
     it += args.pre_iters
     lay.sync()
     grid_start = tsnet_read_stats(lay.ws, stream=lay.stream)
-    clocks = ClockSampler(local_rank)
-    clocks.start()
     lay.run(args.warmup, start=it)
     it += args.warmup
     lay.sync()
@@ -266,13 +284,14 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.time()
     e0.record(lay.stream)
     lay.run(args.steps, start=it)
     e1.record(lay.stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clk = clocks.stop()
+    clk = clocks.stop(w0, time.time())
     ms = e0.elapsed_time(e1)
     it += args.steps
     if world > 1:
