@@ -352,9 +352,10 @@ static void pick_tma(SellLaunch& L) {
     L.smem = sell_tma_smem<U, CS, R>();
 }
 
+// chosen once (function-local static: thread-safe initialisation)
 static const SellLaunch& sell_launch() {
-    static SellLaunch L;
-    if (!L.k) {
+    static const SellLaunch launch = [] {
+        SellLaunch L;
         const char* e = getenv("TSNET_SELL");
         if (!e) e = "g4,4";   // the fused move (launch_attr_sell_move) uses this shape too
         int u = 4, cs = 8, r = 4;
@@ -389,8 +390,9 @@ static const SellLaunch& sell_launch() {
         const cudaError_t oe = L.kg ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&L.resident, L.kg, 256, 0)
                                     : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&L.resident, L.k, 256, L.smem);
         if (oe != cudaSuccess || L.resident < 1) L.resident = 1;
-    }
-    return L;
+        return L;
+    }();
+    return launch;
 }
 
 // CTAs = TSNET_SELL_WAVES (default 1) x the resident CTAs (grid-stride over slices)

@@ -250,10 +250,10 @@ static int env_int(const char* name, int def) {
     return e ? atoi(e) : def;
 }
 
+// read once (function-local static: thread-safe initialisation)
 static const SpmvCfg& spmv_cfg() {
-    static SpmvCfg c;
-    static bool init = false;
-    if (!init) {
+    static const SpmvCfg cfg = [] {
+        SpmvCfg c;
         const char* k = getenv("TSNET_ATTR_KERNEL");
         if (k && !strcmp(k, "v1")) c.kernel = 1;
         c.U = env_int("TSNET_SPMV_U", c.U);
@@ -264,9 +264,9 @@ static const SpmvCfg& spmv_cfg() {
         c.l1 = env_int("TSNET_SPMV_L1", c.l1);
         c.reserve = std::max(0, std::min(64, env_int("TSNET_SPMV_RESERVE_SMS", c.reserve)));
         c.waves = std::max(1, std::min(64, env_int("TSNET_SPMV_WAVES", c.waves)));
-        init = true;
-    }
-    return c;
+        return c;
+    }();
+    return cfg;
 }
 
 // Hot-column L1 policy for this P: on when its first `cand` columns (P is
