@@ -113,7 +113,11 @@ constexpr int kHostChunksMax = 16;
 
 struct SideStream {
     int dev = -1;
-    cudaStream_t side = nullptr, copy = nullptr, d2h = nullptr, spmv2 = nullptr;
+    // side: the field chain + moves of the pipelined host step (highest
+    // priority: its moves gate the downloads); field: the field chain forked
+    // beside the SpMV in a device step (normal priority: preempting the SpMV's
+    // CTAs cost 1% there, r1cn)
+    cudaStream_t side = nullptr, field = nullptr, copy = nullptr, d2h = nullptr, spmv2 = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr, copied = nullptr, y_in = nullptr, drained = nullptr, zeroed = nullptr;
     cudaEvent_t attr_done[kHostChunksMax] = {}, moved[kHostChunksMax] = {}, state_in[kHostChunksMax] = {};
 };
@@ -134,15 +138,19 @@ static cudaError_t side_stream(SideStream*& out) {
     if (e != cudaSuccess) return e;
     SideStream& x = ss[dev & 15];
     if (x.dev != dev) {
-        // the field chain is a row of short dependent kernels: at the highest
-        // priority its CTAs go ahead of queued SpMV CTAs instead of waiting
-        // for the SpMV's waves to drain
-        // (TSNET_FIELD_PRIORITY=0: default priority, for probing)
+        // side (pipelined host step): the field chain is a row of short
+        // dependent kernels; at the highest priority its CTAs go ahead of
+        // queued SpMV CTAs, so the first moves start early (TSNET_FIELD_PRIORITY=0:
+        // default priority); field (device step): default priority
+        // (TSNET_FIELD_PRIORITY=1: highest), both probing knobs
         int lo = 0, hi = 0;
         if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return e;
         const char* pe = getenv("TSNET_FIELD_PRIORITY");
         const int prio = (pe && pe[0] == '0') ? lo : hi;
         if ((e = cudaStreamCreateWithPriority(&x.side, cudaStreamNonBlocking, prio)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithPriority(&x.field, cudaStreamNonBlocking, pe && pe[0] == '1' ? hi : lo)) !=
+            cudaSuccess)
+            return e;
         if ((e = cudaStreamCreateWithFlags(&x.copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
         if ((e = cudaStreamCreateWithFlags(&x.d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
         if ((e = cudaStreamCreateWithFlags(&x.spmv2, cudaStreamNonBlocking)) != cudaSuccess) return e;
@@ -185,7 +193,7 @@ static int eval_gradient_parts(const Ws& w, const GradArgs& a, const tsnet_shard
     // with the SpMV (SURVEY §8(e) "chain G"); the Y all-gather stays on `s`
     const bool fork = side_enabled();
     if (fork) TSNET_CUDA(side_stream(ss));
-    cudaStream_t fs = fork ? ss->side : s;
+    cudaStream_t fs = fork ? ss->field : s;
     if (fork) {
         TSNET_CUDA(cudaEventRecord(ss->fork, s));
         TSNET_CUDA(cudaStreamWaitEvent(fs, ss->fork, 0));
