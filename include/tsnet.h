@@ -16,6 +16,14 @@
  * Delta_ij = X_i - X_j, r2 = |Delta_ij|^2, w_ij = 1/(1 + r2),
  * Z = sum_{k != l} w_kl, K_e = 1/(eps + r2).
  *
+ * Entry points: the iteration (tsnet_grad, tsnet_grad_parts, tsnet_attr,
+ * tsnet_step, tsnet_step_host, tsnet_cost; the phases tsnet_field_local /
+ * tsnet_step_finish and the NCCL communicator for row shards); its set-up
+ * (tsnet_build_P = C0, tsnet_pmds = the Pivot MDS initial layout; the
+ * column-blocked and sliced-ELL re-layouts of P); the paper's other two
+ * algorithms (tsnet_grad_tree: BH-tsNET, FIt-tsNET; tsnet_move); the quality
+ * metrics of its evaluation (tsnet_quality).
+ *
  * Data layout:
  *   layout Y / velocity / gains / gradient : n x 2 fp32, interleaved (x, y)
  *   graph and P                            : CSR, int64 indptr[n+1],
