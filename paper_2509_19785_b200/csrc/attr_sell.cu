@@ -340,7 +340,9 @@ struct SellLaunch {
 //   gU,NS[,MINB]  entries and gathers pipelined (k_attr_sell_g), MINB = CTAs per
 //          SM promised to ptxas: g4,4,4 0.751 ms (default; 64 registers, 87% of
 //          the measured HBM peak), g4,4,3 0.771, g4,4,1 0.996 (94 registers, 2
-//          CTAs/SM), g4,2 0.816, g2,4 0.879, g2,6 1.137, g1,8 1.537;
+//          CTAs/SM), g4,2 0.816, g2,4 0.879, g2,6 1.137, g1,8 1.537; with the
+//          4-CTA bound (r1cq): g3,4 0.762, g2,4 0.872, g2,6 0.899, g4,6 1.030
+//          (spills), g4,4 at 5 CTAs/SM 1.327 (spills);
 //   U,NS   entries pipelined only (k_attr_sell): 2,4 0.921, 4,2 0.937, 4,3 0.943;
 //   tma:U,CS,R  TMA-staged entries (k_attr_sell_tma): 8,8,4 1.012, 4,8,3 1.052,
 //          4,8,4 1.138, 8,4,4 1.143 -- the ring's shared memory takes L1
