@@ -108,7 +108,10 @@ typedef struct {
     int32_t I_min, I_max;
 } tsnet_grad_params;
 
-#define TSNET_I_MAX_LIMIT 256
+/* I <= 1024 (reading R9; N = 3 I <= 3072 nodes, FFT size M = 6 I <= 6144).
+ * Workspace grid buffers are sized by the call's I_max (tsnet_workspace_bytes):
+ * ~2.3 GB at I_max = 1024, ~150 MB at 256. */
+#define TSNET_I_MAX_LIMIT 1024
 
 /* Momentum/gains update (reading R12; the paper only says "Move each vertex v
  * in the direction of dC/dv"):
@@ -347,33 +350,48 @@ TSNET_API int tsnet_move(float* Y, float* vel, float* gains, const float* grad, 
 /*
  * The attractive SpMV (Eq. 6 first term) gathers Y_j for every
  * stored entry of P.  On graphs without locality (config 4) those gathers, not
- * HBM, bound a CSR kernel (L2 request rate).  A plan is P re-laid out for a
- * kernel that reads Y_j from shared-memory tiles: columns in
- * blocks of 8192 points; rows of `shard` (all rows if NULL) in mini-tasks
- * (runs of <= 704 consecutive rows with balanced nnz + rows, or one equal
- * piece of a long row inside every block), 16 mini-tasks per CTA group; per
- * (group, block, warp) a contiguous segment of 8-byte words
- * ((row - mini-task row0) << 16 | col - block col0, p_ij fp32).
+ * HBM, bound a row-wise CSR kernel (the L1->L2 request path: about one random
+ * gather per SM-cycle).  A plan is P re-laid out for a kernel that reads Y_j
+ * from shared memory instead:
+ *   panels  : the rows of `shard` (all rows if NULL) dealt to P = 148 k panels
+ *             (k = ceil(rows / (148 * 8192))) by longest-processing-time on
+ *             (entries + 8), at most 8192 rows each; one CTA per panel keeps
+ *             Y_i and the partial F_i of its rows in shared memory;
+ *   blocks  : columns in blocks of 4096 points, streamed through a shared
+ *             ring by TMA bulk copies;
+ *   tiles   : per (panel, block) the entries sorted by (row, column) and cut
+ *             into 512 equal contiguous chunks, one per lane; slot (step k,
+ *             lane L) = k-th entry of chunk L as (column in block | local row
+ *             << 12 | run flags, p_ij fp32), tiles padded to whole steps with
+ *             (0, +0.0) slots.
  * The plan holds the values: the kernel that uses it reads no CSR array.
+ * Results equal the CSR kernel's up to fp32 summation order.
  *
- * tsnet_plan_query : bytes of the plan and of the build workspace for this P
- *                    and shard.  BLOCKING (reads P->indptr to cut the rows).
+ * tsnet_plan_query : bytes of the plan (an upper bound) and of the build
+ *                    workspace for this P and shard.  BLOCKING (reads
+ *                    P->indptr to cut the rows).
  * tsnet_plan_build : writes the plan into `plan` (device, 256-byte aligned,
- *                    >= plan_bytes) using `ws` as scratch.  BLOCKING.  Set
- *                    P->plan = plan afterwards to use it.  Needs nnz of the
- *                    shard < 2^31 and n < 2^31 (TSNET_E_ARG otherwise).
- * tsnet_plan_partition : the host cut alone (for tests): rows
- *                    [row_begin, row_end) of the HOST indptr into warps * G
- *                    mini-tasks (G = base_groups * k, smallest k that fits;
- *                    capacity max_minitasks).  Per row q: row_mt[q] = its first
- *                    mini-task, row_K[q] = pieces (1 = not split); per mini-task
- *                    t: mt_r0[t] = first row, mt_info[t] = rows (>= 0) or -1 for
- *                    a piece.  Returns G, or -1.  [host, pure]
+ *                    >= plan_bytes) using `ws` as scratch (~24 bytes per
+ *                    stored entry; CUB radix sort).  BLOCKING.  Set P->plan =
+ *                    plan and P->plan_kind = TSNET_PLAN_CB afterwards.  Needs
+ *                    fewer than 2^32 entries in the shard and n < 2^31
+ *                    (TSNET_E_ARG otherwise).
+ * tsnet_plan_partition : the host cut alone (for tests): rows [row_begin,
+ *                    row_end) of the HOST indptr into P = groups * k panels of
+ *                    at most rows_cap rows.  Per row q (shard-local):
+ *                    row_panel[q], row_local[q] (its index inside the panel,
+ *                    rows ascending); panel_off[P + 1] = exclusive scan of
+ *                    the panel sizes; panel_rows[panel_off[p] + l] = the row
+ *                    of panel p with local index l.  Returns P (<= max_panels),
+ *                    or -1.  [host, pure]
  */
 TSNET_API int tsnet_plan_query(const tsnet_csr* P, const tsnet_shard* shard, size_t* plan_bytes, size_t* ws_bytes,
                                tsnet_stream_t stream);
 TSNET_API int tsnet_plan_build(const tsnet_csr* P, const tsnet_shard* shard, void* plan, size_t plan_bytes, void* ws,
                                size_t ws_bytes, tsnet_stream_t stream);
+TSNET_API int32_t tsnet_plan_partition(const int64_t* indptr_host, int64_t row_begin, int64_t row_end,
+                                       int32_t groups, int32_t rows_cap, int32_t* row_panel, int32_t* row_local,
+                                       int32_t* panel_off, int32_t* panel_rows, int64_t max_panels);
 /* ------------------------------------------------- sliced-ELL layout of P (a6) */
 
 /*
@@ -398,9 +416,6 @@ TSNET_API int tsnet_sell_query(const tsnet_csr* P, const tsnet_shard* shard, siz
 TSNET_API int tsnet_sell_build(const tsnet_csr* P, const tsnet_shard* shard, void* plan, size_t plan_bytes,
                                tsnet_stream_t stream);
 
-TSNET_API int32_t tsnet_plan_partition(const int64_t* indptr_host, int64_t row_begin, int64_t row_end,
-                                       int32_t warps, int32_t rows_max, int32_t base_groups, int64_t max_minitasks,
-                                       int32_t* row_mt, int32_t* row_K, int32_t* mt_r0, int32_t* mt_info);
 
 /* ------------------------------------------------------------- multi-GPU (§8(e)) */
 

@@ -51,9 +51,10 @@ def five_smooth_at_most(m: int) -> int:
     return m
 
 
-def geometry(Y, h_max: float = 0.25, I_min: int = 20, I_max: int = 256, p: int = 3):
+def geometry(Y, h_max: float = 0.25, I_min: int = 20, I_max: int = 1024, p: int = 3):
     """O5.1 grid geometry (R9): square cells of width h_b = S/I over the
-    bounding box, S = max(span_x, span_y) floored at 1e-12,
+    bounding box, S = max(span_x, span_y) floored at 1e-12, I_max = 1024 by
+    default (the paper fixes I as a constant),
     I = clamp(ceil(S/h_max), I_min, I_max) rounded up to 5-smooth (down to the
     largest 5-smooth <= I_max if that exceeds I_max); p nodes per interval at
     in-box positions (t+1/2)/p ("P interpolation points for interval i",
@@ -184,7 +185,7 @@ def ke_factory(eps):
     return lambda r2: 1.0 / (eps + r2)
 
 
-def interp_fields(Y, charges, kernel, geo=None, method="auto", h_max=0.25, I_min=20, I_max=256, p=3):
+def interp_fields(Y, charges, kernel, geo=None, method="auto", h_max=0.25, I_min=20, I_max=1024, p=3):
     """Generic FFT-interpolated field phi_c(i) ~= sum_j K(|X_i - X_j|^2) c_j,
     INCLUDING j = i (SPEC.md:276 evaluate_field), one array per charge."""
     if geo is None:
@@ -197,7 +198,7 @@ def interp_fields(Y, charges, kernel, geo=None, method="auto", h_max=0.25, I_min
 
 # -------------------------------------------------------------- the gradient
 def interp_gradient(Y, indptr, indices, pval, lkl, lc, lr, eps=0.05, h_max=0.25, I_min=20,
-                    I_max=256, p=3, form="plain", method="auto", kernels=None):
+                    I_max=1024, p=3, form="plain", method="auto", kernels=None):
     """O5: the L-tsNET gradient at layout Y (Alg. 3 l.396-404).
 
       Z      = sum_i phi^{K1}_1(i) - n                                 (R10, R11)
@@ -276,7 +277,7 @@ def interp_gradient(Y, indptr, indices, pval, lkl, lc, lr, eps=0.05, h_max=0.25,
 # and per-row-block parts (gather, sparse attraction, assembly).  Same
 # arithmetic as interp_gradient(form="plain"); pinned equal to it by
 # tests/test_oracle_interp.py::test_row_blocks_equal_full_gradient.
-def field_state(Y, eps=0.05, h_max=0.25, I_min=20, I_max=256, p=3, method="auto"):
+def field_state(Y, eps=0.05, h_max=0.25, I_min=20, I_max=1024, p=3, method="auto"):
     Y = np.asarray(Y, dtype=np.float64)
     n = Y.shape[0]
     geo = geometry(Y, h_max, I_min, I_max, p)

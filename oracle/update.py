@@ -45,7 +45,7 @@ def stage_params(it: int, stage_switch: int = 250):
 
 
 def run_layout(Y0, indptr, indices, pval, iters, start_iter=0, vel=None, gains=None, eta=50.0,
-               eps=0.05, h_max=0.25, I_min=20, I_max=256, exact=False, fp32_state=True,
+               eps=0.05, h_max=0.25, I_min=20, I_max=1024, exact=False, fp32_state=True,
                recenter=False, callback=None):
     """Alg. 3 main loop with the O6/O7 update.
 

@@ -2,36 +2,47 @@
 // PAPER.md:162): F_attr,i = sum_{j in row i} p_ij w_ij (X_i - X_j).
 //
 // Why a second layout of P: on the power-law graph of config 4
-// every CSR kernel is bound by the L2 request rate of the random Y[j] gathers
-// (one 32-B sector request per stored entry; ncu: l1tex2xbar request cycles
-// ~80%, DRAM ~25%).  Here Y is read from shared memory instead:
+// every row-wise CSR kernel is bound by the L1->L2 request path of the random
+// Y[j] gathers (one 32-B sector request per stored entry; ncu: l1tex2xbar
+// request cycles 88 %, DRAM 33 %; a measured ceiling of ~1 gather per
+// SM-cycle).  Here every Y[j] comes from shared memory (~4 gathers per
+// SM-cycle) and nothing per entry leaves the SM except the 8-byte entry
+// stream itself:
 //
-//   * columns are cut into blocks of kCbCols points; a producer warp streams
-//     the Y slice of each block into a double-buffered shared tile with
-//     cp.async.bulk (TMA bulk copy, mbarrier completion);
-//   * rows are cut into mini-tasks: runs of consecutive rows (at most kCbRows
-//     rows, balanced nnz + rows), except that a long row (> cap entries) is
-//     split into K mini-tasks of one "piece" each -- piece k takes the k-th
-//     K-th of the row's entries inside EVERY block, so hub rows spread evenly
-//     over warps and blocks; kCbW mini-tasks form a group, processed by one
-//     CTA, one mini-task per consumer warp;
-//   * a warp accumulates its mini-task's rows in its own slice of shared
-//     memory (F_s), so nothing is shared between warps: no atomics and no
-//     barriers in the hot loop -- warps only meet at the Y-tile pipeline;
-//   * per (group, block, warp) the entries are a contiguous segment of 8-byte
-//     words ((row - mini-task row0) << 16 | col - block_col0, p_ij fp32 bits),
-//     rows ascending, padded to an even length; a warp streams its segment in
-//     sweeps of 128 entries (16-byte loads, two sweeps ahead, L2 evict-first),
-//     gathers Y_j from the tile and Y_i (one sweep ahead) from L2, reduces runs
-//     of equal rows in registers (hand-down between lanes, segmented scan when
-//     a run covers whole lanes) and adds run sums into F_s;
-//   * at the end of a group each warp writes its rows of F (plain stores; the
-//     pieces of split rows add with vector atomics into F, zeroed before).
-// HBM bytes per launch: 8 per stored entry (+ padding) + 8 per (group, block,
-// warp) segment offset + 8 per row of F; Y tiles come from L2.
+//   * panels: the rows of P (or of a shard) are dealt to P panels, 148 k of
+//     them, by longest-processing-time on (entries + 8) with at most kTR rows
+//     each, so every CTA gets the same work whatever the degree distribution
+//     (hub rows go first, short rows fill the gaps); inside a panel the rows
+//     keep ascending order and get a local index < kTR;
+//   * column blocks of kTB points: one CTA per panel sweeps all blocks; a
+//     producer warp streams Y[block] into a kTS-stage shared ring with
+//     cp.async.bulk (TMA bulk copy, mbarrier completion) and prefetches the
+//     tile's entries into L2 (cp.async.bulk.prefetch.L2), kTS - 1 blocks
+//     ahead of the consumers;
+//   * warps: the rows of a panel are cut into kTW contiguous ranges of
+//     balanced entries, one per consumer warp, for the whole sweep -- a row is
+//     only ever touched by its warp, so warps need no barrier between blocks
+//     (each releases a ring stage on its own; the ring absorbs the drift);
+//   * per (panel, block, warp) tile the entries are sorted by (local row,
+//     column) and cut into 32 equal contiguous chunks, one per lane; slot
+//     (step k, lane l) = k-th entry of chunk l, so a warp's step is one
+//     coalesced 256-B load, and the tile is padded to whole steps (< 32
+//     slots) with (0, p = 0) slots that add exactly 0;
+//   * a lane accumulates its run of equal rows in registers and adds it to
+//     the row's accumulator in shared memory when the run ends inside its
+//     chunk (FLUSH bit; the lane that sees a run end is unique).  A run that
+//     continues past the chunk's end is carried out: after the tile the
+//     carries are summed per row across lanes (segmented warp scan, merge-path
+//     style) and added by one lane, after the row's own flush in program
+//     order -- no atomics anywhere (shared-memory float atomics are CAS loops
+//     on sm_100, and hub rows would serialise them);
+// HBM bytes per launch: 8 per slot (stored entries + < 512 pads per tile) +
+// 4 per tile + 12 per row (row list, Y_i, F_i); Y blocks come from L2
+// (P x 8 n bytes of L2 reads).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <queue>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -41,269 +52,314 @@
 
 namespace tsnet {
 
-constexpr int kCbCols = 8192;       // points per column block (2 x 64 KB shared tiles)
-constexpr int kCbW = 16;            // consumer warps per CTA = mini-tasks per group (+1 producer warp)
-constexpr int kCbRows = 704;        // rows per mini-task (16 x 704 x 8 B = 88 KB of F_s)
-constexpr uint32_t kCbSentinel = 0xFFFFu;
-constexpr uint64_t kCbMagic = 0x3456434e53545354ull;  // "TSTSNCV4"
+constexpr int kTB = 4096;            // points per column block (12-bit column in block)
+constexpr int kTS = 3;               // Y ring stages (3 x 32 KB)
+constexpr int kTPre = 4;             // blocks of entries prefetched into L2 ahead of the Y ring
+constexpr int kTW = 16;              // consumer warps per CTA (+1 producer warp)
+constexpr int kTL = kTW * 32;        // consumer threads
+constexpr int kTR = 8192;            // max rows per panel (13-bit local row; 16 B of shared memory each)
+constexpr int kTRbits = 13;
+// slot word: column in block * 8 (bits 0-14, the byte offset of Y_j in the
+// ring stage) | local row (bits 15-27; * 8 = byte offset of Y_i and F_i) |
+// NEWROW (bit 30: a run starts here) | FLUSH (bit 31: a run ends here).  Real
+// entries have p > 0 (C0 drops exact zeros); pads are (0, p = 0).
+constexpr uint32_t kColMask = 0x7FF8u, kRowMask = 0xFFF8u, kNewRow = 1u << 30, kFlush = 1u << 31;
+// byte offset of a dummy float2 from the Y_i array (Y_i[kTR], F_i[kTR], dummy):
+// lanes with nothing to read there all read it (one broadcast address)
+constexpr uint32_t kDummyFromYi = 2u * kTR * 8u, kDummyFromFs = kTR * 8u;
+constexpr uint64_t kTileMagic = 0x3654534e53545354ull;   // "TSTSNST6"
 
-struct CbHeader {
+struct TileHeader {
     uint64_t magic;
-    int64_t n, row_begin, row_end, nnz, entries;
-    int32_t G, NB, C, W, rows_max, pad;
-    int64_t off_seg, off_mt, off_entries, bytes;
+    int64_t n, row_begin, row_end, nnz;
+    int32_t P, NB, R_max, pad;
+    int64_t steps;                      // total warp steps (slots / 32)
+    int64_t off_wtab, off_rowoff, off_rows, off_slots, bytes;
 };
 
-static size_t cb_align(size_t x) { return (x + 255) / 256 * 256; }
+static size_t t_align(size_t x) { return (x + 255) / 256 * 256; }
 
-static CbHeader cb_layout(int64_t n, int64_t rb, int64_t re, int64_t nnz, int32_t G) {
-    CbHeader h{};
-    h.magic = kCbMagic;
+static TileHeader tile_layout(int64_t n, int64_t rb, int64_t re, int64_t nnz, int32_t P, int32_t R_max,
+                              int64_t steps) {
+    TileHeader h{};
+    h.magic = kTileMagic;
     h.n = n;
     h.row_begin = rb;
     h.row_end = re;
     h.nnz = nnz;
-    h.G = G;
-    h.C = kCbCols;
-    h.W = kCbW;
-    h.rows_max = kCbRows;
-    h.NB = (int32_t)((n + kCbCols - 1) / kCbCols);
-    const int64_t nseg = (int64_t)G * h.NB * kCbW;
-    h.entries = nnz + nseg;   // upper bound with padding
-    size_t off = cb_align(sizeof(CbHeader));
-    h.off_seg = (int64_t)off;
-    off = cb_align(off + sizeof(int64_t) * (size_t)(nseg + 1));
-    h.off_mt = (int64_t)off;
-    off = cb_align(off + sizeof(int2) * (size_t)((int64_t)G * kCbW));
-    h.off_entries = (int64_t)off;
-    off = cb_align(off + sizeof(uint2) * (size_t)h.entries);
+    h.P = P;
+    h.NB = (int32_t)std::max<int64_t>(1, (n + kTB - 1) / kTB);
+    h.R_max = R_max;
+    h.steps = steps;
+    size_t off = t_align(sizeof(TileHeader));
+    h.off_wtab = (int64_t)off;
+    off = t_align(off + sizeof(int2) * ((size_t)P * kTW * h.NB));
+    h.off_rowoff = (int64_t)off;
+    off = t_align(off + sizeof(int32_t) * ((size_t)P + 1));
+    h.off_rows = (int64_t)off;
+    off = t_align(off + sizeof(int32_t) * (size_t)std::max<int64_t>(re - rb, 1));
+    h.off_slots = (int64_t)off;
+    off = t_align(off + sizeof(uint2) * 32 * (size_t)steps);
     h.bytes = (int64_t)off;
     return h;
 }
 
-// Host cut (pure).  ipr[q] = indptr[rb + q], q = 0 .. nr.  A row of L > cap
-// entries (cap = max(256, nnz / (base W) / 2)) is split into K = ceil(L / cap)
-// one-piece mini-tasks; the other rows form runs of consecutive rows (<=
-// rows_max each) with boundaries at multiples of their mean weight (entries +
-// rows); T = W G mini-tasks in row order, G = base k for the smallest k that
-// fits, padded with empty mini-tasks.  Output:
-//   row_mt[q]: first mini-task of row q; row_K[q]: its pieces (1 = not split);
-//   mt_r0[t]: first row of mini-task t; mt_info[t]: its rows (>= 0), or -1 for
-//   a piece.  Returns G, or -1.
-static int32_t cb_partition(const int64_t* ipr, int64_t nr, int32_t W, int32_t rows_max, int32_t base,
-                            std::vector<int32_t>& row_mt, std::vector<int32_t>& row_K, std::vector<int32_t>& mt_r0,
-                            std::vector<int32_t>& mt_info) {
-    const int64_t nnz = ipr[nr] - ipr[0];
-    const int64_t cap = std::max<int64_t>(256, nnz / ((int64_t)base * W) / 2);
-    row_mt.assign(nr, 0);
-    row_K.assign(nr, 1);
-    int64_t pieces = 0, nsplit = 0;
-    double wrows = 0.0;
+static int num_sms() {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = kNumSMs;
+    return sms;
+}
+
+// Host cut (pure).  ipr[q] = indptr[rb + q], q = 0 .. nr.  Panels:
+// P = G ceil(nr / (G R_cap)) (at most nr, at least 1), rows dealt by LPT on
+// weight (entries + 8): rows in decreasing weight (ties: smaller row), each to
+// the panel with the least weight so far (ties: smaller panel) among those
+// with < R_cap rows.  Inside a panel rows are in ascending order.  Outputs:
+// row_panel[q], row_local[q], panel_off[P + 1] (exclusive scan of the panel
+// sizes), panel_rows[panel_off[p] + l] = the row q with local index l.
+// Returns P, or -1.
+static int32_t tile_partition(const int64_t* ipr, int64_t nr, int32_t G, int32_t R_cap, std::vector<int32_t>& row_panel,
+                              std::vector<int32_t>& row_local, std::vector<int32_t>& panel_off,
+                              std::vector<int32_t>& panel_rows) {
+    if (nr < 0 || G < 1 || R_cap < 1 || nr >= ((int64_t)1 << 31)) return -1;
+    int64_t P64 = (int64_t)G * ((nr + (int64_t)G * R_cap - 1) / ((int64_t)G * R_cap));
+    P64 = std::max<int64_t>(1, std::min<int64_t>(P64, std::max<int64_t>(nr, 1)));
+    if (P64 >= ((int64_t)1 << 31)) return -1;
+    const int32_t P = (int32_t)P64;
+    row_panel.assign(nr, 0);
+    row_local.assign(nr, 0);
+    panel_off.assign(P + 1, 0);
+    panel_rows.assign(nr, 0);
+    std::vector<int64_t> order(nr);
+    for (int64_t q = 0; q < nr; ++q) order[q] = q;
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+        return (ipr[a + 1] - ipr[a]) > (ipr[b + 1] - ipr[b]);
+    });
+    using Item = std::pair<int64_t, int32_t>;   // (weight, panel): min-heap
+    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
+    for (int32_t p = 0; p < P; ++p) heap.push({0, p});
+    std::vector<int32_t> cnt(P, 0);
+    for (int64_t t = 0; t < nr; ++t) {
+        if (heap.empty()) return -1;
+        const int64_t q = order[t];
+        Item it = heap.top();
+        heap.pop();
+        row_panel[q] = it.second;
+        ++cnt[it.second];
+        if (cnt[it.second] < R_cap) heap.push({it.first + (ipr[q + 1] - ipr[q]) + 8, it.second});
+    }
+    for (int32_t p = 0; p < P; ++p) panel_off[p + 1] = panel_off[p] + cnt[p];
+    std::vector<int32_t> fill(panel_off.begin(), panel_off.end() - 1);
     for (int64_t q = 0; q < nr; ++q) {
-        const int64_t L = ipr[q + 1] - ipr[q];
-        if (L > cap) {
-            row_K[q] = (int32_t)((L + cap - 1) / cap);
-            pieces += row_K[q];
-            ++nsplit;
-        } else {
-            wrows += (double)L + 1.0;
-        }
+        const int32_t p = row_panel[q];
+        row_local[q] = fill[p] - panel_off[p];
+        panel_rows[fill[p]++] = (int32_t)q;
     }
-    const int64_t kmax = 2 + (nr + (int64_t)rows_max * W * base - 1) / ((int64_t)rows_max * W * base) +
-                         (pieces + nsplit + (int64_t)W * base - 1) / ((int64_t)W * base);
-    for (int64_t k = 1; k <= kmax; ++k) {
-        const int64_t G = (int64_t)base * k, T = G * W;
-        if (G > INT32_MAX / W) break;
-        const int64_t T_rows = T - pieces - nsplit;   // a split may close a run early: reserve one each
-        if (T_rows < 1) continue;
-        const double target = wrows / (double)T_rows;
-        mt_r0.clear();
-        mt_info.clear();
-        double acc = 0.0;
-        int64_t open = -1, runs = 0;   // index of the open run in mt_*
-        for (int64_t q = 0; q < nr; ++q) {
-            const int64_t L = ipr[q + 1] - ipr[q];
-            if (row_K[q] > 1) {
-                open = -1;
-                row_mt[q] = (int32_t)mt_r0.size();
-                for (int32_t p = 0; p < row_K[q]; ++p) {
-                    mt_r0.push_back((int32_t)q);
-                    mt_info.push_back(-1);
-                }
-                continue;
-            }
-            // close the open run at multiples of the target, or when full
-            if (open >= 0 && (mt_info[open] >= rows_max || acc >= target * (double)runs)) open = -1;
-            if (open < 0) {
-                open = (int64_t)mt_r0.size();
-                mt_r0.push_back((int32_t)q);
-                mt_info.push_back(0);
-                ++runs;
-            }
-            mt_info[open] += 1;
-            row_mt[q] = (int32_t)open;
-            acc += (double)L + 1.0;
-        }
-        if ((int64_t)mt_r0.size() > T) continue;
-        while ((int64_t)mt_r0.size() < T) {   // empty mini-tasks
-            mt_r0.push_back(0);
-            mt_info.push_back(0);
-        }
-        return (int32_t)G;
-    }
-    return -1;
+    return P;
 }
 
-// PTX helpers (mbarrier, bulk copy): ptx.cuh
-
-__device__ __forceinline__ uint64_t cb_policy_evict_first() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ uint4 ld_stream_v4(const uint4* a, uint64_t pol) {
-    uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(a), "l"(pol));
-    return v;
+// The rows of each panel (in local order) cut into W contiguous ranges of
+// balanced entries: the row with local index l and e entries before it in the
+// panel (of E) goes to warp min(W - 1, floor(W (e + L_l / 2) / E)) -- its
+// midpoint decides, so ranges stay contiguous.  Pure host code.
+static void tile_warps(const int64_t* ipr, int32_t P, int32_t W, const std::vector<int32_t>& panel_off,
+                       const std::vector<int32_t>& panel_rows, std::vector<int32_t>& row_warp) {
+    row_warp.assign(panel_rows.size(), 0);
+    for (int32_t p = 0; p < P; ++p) {
+        int64_t E = 0;
+        for (int32_t l = panel_off[p]; l < panel_off[p + 1]; ++l) E += ipr[panel_rows[l] + 1] - ipr[panel_rows[l]];
+        int64_t e = 0;
+        for (int32_t l = panel_off[p]; l < panel_off[p + 1]; ++l) {
+            const int64_t q = panel_rows[l], L = ipr[q + 1] - ipr[q];
+            const double mid = (double)e + 0.5 * (double)L;
+            row_warp[q] = E > 0 ? (int32_t)std::min<double>(W - 1, std::floor((double)W * mid / (double)E)) : 0;
+            e += L;
+        }
+    }
 }
 
 // ------------------------------------------------------------------ kernel
-// One entry: contribution p w (X_i - X_j) with w = 1 / (1 + r^2).  Padding
-// entries (p = 0) contribute exactly 0.  rcp.approx: 1 + r^2 >= 1, relative
-// error <= 2^-22, far below the fp32 summation error of a row.
-__device__ __forceinline__ float2 cb_term(float2 yi, float2 yj, float p) {
-    const float dx = yi.x - yj.x, dy = yi.y - yj.y;
-    float w;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(w) : "f"(fmaf(dx, dx, fmaf(dy, dy, 1.0f))));
-    const float pw = p * w;
-    return make_float2(pw * dx, pw * dy);
+__device__ __forceinline__ uint2 ld_slot(const uint2* a) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(a));
+    return v;
 }
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(kTL) : "memory"); }
 
-// Y_i of the lane's four entries (issued one sweep ahead): row = row0 + key
-// (a piece mini-task has the single row row0: key 0);
-// sentinel keys read row0 and are multiplied by p = 0.
-struct CbYi {
-    float2 y[4];
+struct TileSet {
+    uint2 s[4];
 };
-__device__ __forceinline__ CbYi cb_yi(uint4 a, uint4 b, const float2* __restrict__ Yr0) {
-    // four independent loads (repeated rows hit L1): selecting between a loaded
-    // value and another load would make the issue wait for the first one
-    const uint32_t k[4] = {a.x >> 16, a.z >> 16, b.x >> 16, b.z >> 16};
-    CbYi r;
+
+// Four consecutive steps of this lane (steps >= K are pad slots: no load).
+__device__ __forceinline__ void load4(TileSet& S, const uint2* __restrict__ base, int k0, int K) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) r.y[q] = __ldg(Yr0 + (k[q] == kCbSentinel ? 0u : k[q]));
-    return r;
+    for (int q = 0; q < 4; ++q) S.s[q] = (k0 + q < K) ? ld_slot(base + (size_t)(k0 + q) * 32) : make_uint2(0u, 0u);
 }
 
-__device__ __forceinline__ void fs_add(float2* Fs, uint32_t k, float x, float y) {
-    float2 v = Fs[k];
-    v.x += x;
-    v.y += y;
-    Fs[k] = v;
+__device__ __forceinline__ float2 lds2(const char* base, uint32_t off) {
+    return *reinterpret_cast<const float2*>(base + off);
 }
 
-// One sweep: lane holds entries 4 lane .. 4 lane + 3 of 128 consecutive entries
-// of the warp's segment (keys = local rows, non-decreasing; masked entries
-// carry the sentinel key and p = 0 and sit at the end).  Run sums are added to
-// the warp's own F_s slice (one add per key per sweep; sweeps of a warp are
-// ordered by __syncwarp).
-__device__ __forceinline__ void cb_sweep(uint4 a, uint4 b, const CbYi& yi, const float2* __restrict__ Ys,
-                                         float2* Fs, int lane) {
-    const uint32_t wd[4] = {a.x, a.z, b.x, b.z};
-    const float pv[4] = {__uint_as_float(a.y), __uint_as_float(a.w), __uint_as_float(b.y), __uint_as_float(b.w)};
-    uint32_t k[4];
-    float2 yj[4];
+// NQ consecutive entries of this lane: contribution p w (X_i - X_j), w = 1 /
+// (1 + r^2) (rcp.approx: 1 + r^2 >= 1, relative error <= 2^-22); pad slots
+// (p = 0) add exactly 0.  Y_i is read when a run starts (NEWROW) and kept in
+// registers; a run's sum goes to its row when it ends here (FLUSH).  All loads
+// of the NQ entries are issued first; lanes with nothing to read address one
+// dummy float2 (a broadcast), so bank conflicts come only from real reads.  The
+// flush values are formed in registers and the (distinct: a row is one run of
+// a lane) rows read-modified-written together.  kc = byte offset of the row of
+// the last real entry, cv = its run continues past the chunk (the carry-out
+// (ax, ay), possibly exactly 0, belongs to kc).
+template <int NQ>
+__device__ __forceinline__ void tileq(const TileSet& S, const char* Ys, const char* Yi, char* Fs, float2& yi,
+                                      float& ax, float& ay, int& kc, bool& cv) {
+    float2 yj[NQ], yl[NQ];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        k[q] = wd[q] >> 16;
-        yj[q] = Ys[wd[q] & 0xFFFFu];
+    for (int q = 0; q < NQ; ++q) {
+        const uint32_t w = S.s[q].x;
+        yj[q] = lds2(Ys, w & kColMask);
+        yl[q] = lds2(Yi, (w & kNewRow) ? ((w >> 12) & kRowMask) : kDummyFromYi);
     }
-    float2 f[4];
+    float fx[NQ], fy[NQ];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) f[q] = cb_term(yi.y[q], yj[q], pv[q]);
-    // lane runs: head (key k0, if != k3), middles (keys strictly between), tail (key k3)
-    const uint32_t tk = k[3];
-    float tx = f[3].x, ty = f[3].y;
-    float hx = 0.f, hy = 0.f;
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        const bool t = k[q] == tk, h = k[q] == k[0];
-        tx += t ? f[q].x : 0.f;
-        ty += t ? f[q].y : 0.f;
-        hx += (h && !t) ? f[q].x : 0.f;
-        hy += (h && !t) ? f[q].y : 0.f;
-    }
-    const bool has_head = k[0] != tk;
-    const bool mid1 = k[1] != k[0] && k[1] != tk;
-    const bool mid2 = k[2] != k[0] && k[2] != tk && k[2] != k[1];
-    if (mid1) fs_add(Fs, k[1], f[1].x + (k[2] == k[1] ? f[2].x : 0.f), f[1].y + (k[2] == k[1] ? f[2].y : 0.f));
-    if (mid2) fs_add(Fs, k[2], f[2].x, f[2].y);
-    // join runs across lanes: a tail continuing as the next lane's head is handed
-    // down; a run covering whole lanes needs the segmented scan
-    const uint32_t pk = __shfl_up_sync(0xffffffffu, tk, 1);
-    const uint32_t nk = __shfl_down_sync(0xffffffffu, tk, 1);
-    float sx = tx, sy = ty;
-    const bool through = lane > 0 && !has_head && tk == pk;
-    if (__any_sync(0xffffffffu, through)) {
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t uk = __shfl_up_sync(0xffffffffu, tk, o);
-            const float ux = __shfl_up_sync(0xffffffffu, sx, o);
-            const float uy = __shfl_up_sync(0xffffffffu, sy, o);
-            const bool add = lane >= o && uk == tk;
-            sx += add ? ux : 0.f;
-            sy += add ? uy : 0.f;
+    for (int q = 0; q < NQ; ++q) {
+        const uint32_t w = S.s[q].x;
+        const float p = __uint_as_float(S.s[q].y);
+        if (w & kNewRow) yi = yl[q];
+        const float dx = yi.x - yj[q].x, dy = yi.y - yj[q].y;
+        float rw;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rw) : "f"(fmaf(dx, dx, fmaf(dy, dy, 1.0f))));
+        const float pw = p * rw;
+        ax = fmaf(pw, dx, ax);
+        ay = fmaf(pw, dy, ay);
+        const bool fl = (int)w < 0;
+        fx[q] = ax;
+        fy[q] = ay;
+        ax = fl ? 0.f : ax;
+        ay = fl ? 0.f : ay;
+        if (p != 0.f) {
+            kc = (int)((w >> 12) & kRowMask);
+            cv = !fl;
         }
     }
-    const bool last = (lane == 31) || (nk != tk);
-    const bool give = has_head && lane > 0 && k[0] == pk;
-    const float gx = __shfl_down_sync(0xffffffffu, give ? hx : 0.f, 1);
-    const float gy = __shfl_down_sync(0xffffffffu, give ? hy : 0.f, 1);
-    if (has_head && !give) fs_add(Fs, k[0], hx, hy);
-    if (last && tk != kCbSentinel) fs_add(Fs, tk, sx + (lane < 31 ? gx : 0.f), sy + (lane < 31 ? gy : 0.f));
+    float2 v[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const uint32_t w = S.s[q].x;
+        v[q] = lds2(Fs, ((int)w < 0) ? ((w >> 12) & kRowMask) : kDummyFromFs);
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+        if ((int)S.s[q].x < 0)
+            *reinterpret_cast<float2*>(Fs + ((S.s[q].x >> 12) & kRowMask)) = make_float2(v[q].x + fx[q], v[q].y + fy[q]);
 }
 
-__global__ void __launch_bounds__((kCbW + 1) * 32, 1) k_attr_cb(const uint8_t* __restrict__ plan,
-                                                                const float2* __restrict__ Y,
-                                                                float2* __restrict__ F, int y_aligned) {
-    extern __shared__ __align__(128) uint8_t cb_smem[];
-    float2* Ys0 = reinterpret_cast<float2*>(cb_smem);
-    float2* Ys1 = Ys0 + kCbCols;
-    float2* Fs_all = Ys1 + kCbCols;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(Fs_all + kCbW * kCbRows);   // full[2], empty[2]
-    const CbHeader* h = reinterpret_cast<const CbHeader*>(plan);
-    const int G = h->G, NB = h->NB;
+// the last r = 1..3 steps of a tile (set S, statically indexed)
+__device__ __forceinline__ void tile_tail(const TileSet& S, int r, const char* Ys, const char* Yi, char* Fs, float2& yi,
+                                          float& ax, float& ay, int& kc, bool& cv) {
+    if (r == 3) tileq<3>(S, Ys, Yi, Fs, yi, ax, ay, kc, cv);
+    else if (r == 2) tileq<2>(S, Ys, Yi, Fs, yi, ax, ay, kc, cv);
+    else tileq<1>(S, Ys, Yi, Fs, yi, ax, ay, kc, cv);
+}
+
+// After a tile: carry-outs (ax, ay) of runs that continue into the next lane's
+// chunk (cv), keyed by row kc.  Sum them per row over consecutive lanes (a
+// run's lanes are consecutive: rows are sorted; every lane a run passes through
+// carries, so a row forms exactly one group) and add each sum once, by the last
+// lane of its group.  The row's own flush (by the lane where the run ends, in
+// this warp) happened earlier in program order.
+__device__ __forceinline__ void tile_carry(float ax, float ay, int kc, bool cv, char* Fs, int lane) {
+    const unsigned full = 0xffffffffu;
+    const bool nz = kc >= 0 && cv;
+    const int kp = __shfl_up_sync(full, nz ? kc : -1, 1);
+    if (__any_sync(full, nz && lane > 0 && kp == kc)) {
+        // runs carried over more than one lane boundary: segmented inclusive
+        // scan with head flags (a lane without a carry is its own segment)
+        const int key = nz ? kc : -1 - lane;
+        bool head = lane == 0 || kp != key;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float ux = __shfl_up_sync(full, ax, o), uy = __shfl_up_sync(full, ay, o);
+            const bool uh = __shfl_up_sync(full, head, o);
+            if (lane >= o) {
+                if (!head) {
+                    ax += ux;
+                    ay += uy;
+                }
+                head = head || uh;
+            }
+        }
+        const int kn = __shfl_down_sync(full, key, 1);
+        if (nz && (lane == 31 || kn != key)) {
+            float2* f = reinterpret_cast<float2*>(Fs + kc);
+            const float2 v = *f;
+            *f = make_float2(v.x + ax, v.y + ay);
+        }
+    } else if (nz) {
+        float2* f = reinterpret_cast<float2*>(Fs + kc);
+        const float2 v = *f;
+        *f = make_float2(v.x + ax, v.y + ay);
+    }
+}
+
+__device__ __forceinline__ int2 ld_tab(const int2* __restrict__ t, int J, int NB) {
+    return J < NB ? __ldg(t + J) : make_int2(0, 0);
+}
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(20000u)
+        : "memory");
+    return ok != 0;
+}
+
+__global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* __restrict__ plan,
+                                                                 const float2* __restrict__ Y, float2* __restrict__ F,
+                                                                 int y_aligned) {
+    extern __shared__ __align__(128) uint8_t t_smem[];
+    float2* ring = reinterpret_cast<float2*>(t_smem);                 // kTS x kTB
+    const TileHeader* h = reinterpret_cast<const TileHeader*>(plan);
+    const int P = h->P, NB = h->NB;
+    float2* Yi = ring + kTS * kTB;                                    // kTR
+    float2* Fs = Yi + kTR;                                            // kTR, then the dummy float2 (+ pad)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Fs + kTR + 2);       // full[kTS], empty[kTS]
     const int64_t n = h->n, rb = h->row_begin;
-    const int64_t* seg = reinterpret_cast<const int64_t*>(plan + h->off_seg);
-    const int2* mt_desc = reinterpret_cast<const int2*>(plan + h->off_mt);   // (row0 - rb, rows | -1 piece)
-    const uint4* ent = reinterpret_cast<const uint4*>(plan + h->off_entries);
+    const int2* wtab = reinterpret_cast<const int2*>(plan + h->off_wtab);   // [(p kTW + w) NB + J] = (step, K)
+    const int32_t* roff = reinterpret_cast<const int32_t*>(plan + h->off_rowoff);
+    const int32_t* rows = reinterpret_cast<const int32_t*>(plan + h->off_rows);
+    const uint2* slots = reinterpret_cast<const uint2*>(plan + h->off_slots);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        mbar_init(&bars[2], kCbW);
-        mbar_init(&bars[3], kCbW);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int s = 0; s < kTS; ++s) {
+            mbar_init(&bars[s], 1);
+            mbar_init(&bars[kTS + s], kTW);
+        }
+        Fs[kTR] = make_float2(0.f, 0.f);
+        fence_mbar_init();
     }
     __syncthreads();
-    // blocks any mini-task of group g needs: the group's block-J segments are contiguous
-    auto group_block_used = [&](const int64_t* og, int J) { return og[(int64_t)J * kCbW] < og[(int64_t)(J + 1) * kCbW]; };
 
-    if (warp == kCbW) {
-        // ---------------- producer: Y slices of the blocks the group uses, in order
+    if (warp == kTW) {
+        // ---------------- producer: Y of every block, in order, for each panel
         uint32_t k = 0;
-        for (int g = blockIdx.x; g < G; g += gridDim.x) {
-            const int64_t* og = seg + (int64_t)g * NB * kCbW;
+        for (int p = blockIdx.x; p < P; p += gridDim.x) {
             for (int J = 0; J < NB; ++J) {
-                if (!group_block_used(og, J)) continue;
-                const int b = k & 1;
-                float2* dst = b ? Ys1 : Ys0;
-                if (k >= 2) mbar_wait(&bars[2 + b], ((k >> 1) - 1) & 1);
-                const int64_t lo = (int64_t)J * kCbCols;
-                const int cnt = (int)std::min<int64_t>(kCbCols, n - lo);
+                const int b = (int)(k % kTS);
+                float2* dst = ring + b * kTB;
+                if (k >= (uint32_t)kTS) mbar_wait(&bars[kTS + b], ((k / kTS) - 1) & 1);
+                const int64_t lo = (int64_t)J * kTB;
+                const int cnt = (int)std::min<int64_t>(kTB, n - lo);
                 if (y_aligned) {
                     const int even = cnt & ~1;
                     if (lane == 0) {
@@ -324,240 +380,232 @@ __global__ void __launch_bounds__((kCbW + 1) * 32, 1) k_attr_cb(const uint8_t* _
         return;
     }
 
-    // ---------------- consumer warp: mini-task g * W + warp of every group g
-    const uint64_t pol = cb_policy_evict_first();
-    float2* Fs = Fs_all + warp * kCbRows;
-    const uint4 pad = make_uint4(kCbSentinel << 16, 0u, kCbSentinel << 16, 0u);
-    const int l2 = 2 * lane;
+    // ---------------- consumer warp `warp`: its tile of every block, lane = chunk
+    const char* Yib = reinterpret_cast<const char*>(Yi);
+    char* Fsb = reinterpret_cast<char*>(Fs);
+    const unsigned full = 0xffffffffu;
     uint32_t k = 0;
-    for (int g = blockIdx.x; g < G; g += gridDim.x) {
-        const int2 md = mt_desc[(int64_t)g * kCbW + warp];
-        const bool piece = md.y < 0;
-        const int nu = piece ? 1 : md.y;
-        const float2* Yr0 = Y + rb + md.x;
-        for (int q = lane; q < nu; q += 32) Fs[q] = make_float2(0.f, 0.f);
-        __syncwarp();
-        const int64_t* og = seg + (int64_t)g * NB * kCbW;
-        auto next_block = [&](int J) {
-            while (J < NB && !group_block_used(og, J)) ++J;
-            return J;
-        };
-        auto my_seg = [&](int J, const uint4*& sp, int& np) {
-            const int64_t s0 = og[(int64_t)J * kCbW + warp], s1 = og[(int64_t)J * kCbW + warp + 1];
-            sp = ent + (s0 >> 1);
-            np = (int)((s1 - s0) >> 1);
-        };
-        // Software pipeline over sweeps with four register sets rotated by
-        // unrolling (no register moves: a move of a value still in flight would
-        // wait for it): entries are loaded three sweeps ahead, Y_i one sweep
-        // ahead (two sweeps after its entries were issued).
-        struct Set {
-            uint4 a, c;
-            CbYi y;
-        };
-        Set S0, S1, S2, S3;
-        const uint4* sp = ent;
-        int np = 0;
-        auto load_e = [&](int sw, Set& S) {
-            const int o = sw * 64 + l2;
-            S.a = o < np ? ld_stream_v4(sp + o, pol) : pad;
-            S.c = o + 1 < np ? ld_stream_v4(sp + o + 1, pol) : pad;
-        };
-        auto load_y = [&](Set& S) { S.y = cb_yi(S.a, S.c, Yr0); };
-        int J = next_block(0);
-        if (J < NB) {
-            my_seg(J, sp, np);
-            load_e(0, S0);
-            load_e(1, S1);
-            load_e(2, S2);
+    for (int p = blockIdx.x; p < P; p += gridDim.x) {
+        const int r0 = roff[p], R = roff[p + 1] - r0;
+        for (int r = threadIdx.x; r < R; r += kTL) {
+            Yi[r] = Y[rb + (rows[r0 + r] & 0x7FFFFFFF)];
+            Fs[r] = make_float2(0.f, 0.f);
         }
-        while (J < NB) {
-            const int b = k & 1;
-            const float2* Ys = b ? Ys1 : Ys0;
-            const int nsw = (np + 63) >> 6;
-            if (nsw > 0) load_y(S0);
-            mbar_wait(&bars[b], (k >> 1) & 1);
+        bar_consumers();
+        // this warp's (first step, steps) of blocks J0 .. J0 + 31 in tv (lane J - J0),
+        // of the next 32 blocks in tn
+        const int2* wt = wtab + ((int64_t)p * kTW + warp) * NB;
+        int2 tv = ld_tab(wt, lane, NB), tn = ld_tab(wt, 32 + lane, NB);
+        auto tile_of = [&](int J, int J0) {   // (first step, K) of block J >= J0 (warp-uniform)
+            const int2 src = (J - J0 < 32) ? tv : tn;
+            return make_int2(__shfl_sync(full, src.x, (J - J0) & 31), __shfl_sync(full, src.y, (J - J0) & 31));
+        };
+        auto prefetch_tile = [&](int2 t) {     // the warp's entries of a later block into L2
+            if (lane == 0 && t.y > 0) prefetch_l2(slots + (size_t)t.x * 32, (uint32_t)t.y * 32u * (uint32_t)sizeof(uint2));
+        };
+        int2 cur = tile_of(0, 0);
+        prefetch_tile(cur);
+        if (NB > 1) prefetch_tile(tile_of(1, 0));
+        TileSet A, B, C;
+        load4(A, slots + (size_t)cur.x * 32 + lane, 0, cur.y);
+        load4(B, slots + (size_t)cur.x * 32 + lane, 4, cur.y);
+        int J0 = 0;
+        for (int J = 0; J < NB; ++J) {
+            if (J - J0 == 32) {              // next 32 blocks
+                J0 += 32;
+                tv = tn;
+                tn = ld_tab(wt, J0 + 32 + lane, NB);
+            }
+            const int K = cur.y;
+            const uint2* base = slots + (size_t)cur.x * 32 + lane;
+            const int2 nxt = (J + 1 < NB) ? tile_of(J + 1, J0) : make_int2(0, 0);
+            if (J + 2 < NB) prefetch_tile(tile_of(J + 2, J0));
+            const int b = (int)(k % kTS);
+            const char* Ys = reinterpret_cast<const char*>(ring + b * kTB);
+            while (!mbar_try_wait_hint(&bars[b], (k / kTS) & 1)) {
+            }
+            if (K > 0) {
+                float ax = 0.f, ay = 0.f;
+                float2 yi = make_float2(0.f, 0.f);
+                int kc = -1;
+                bool cv = false;
+                // three register sets rotated by unrolling, loads two groups ahead;
+                // the last 1-3 steps of the tile run exactly (no pad steps computed)
 #pragma unroll 1
-            for (int sw = 0; sw < nsw; sw += 4) {
-                load_e(sw + 3, S3);
-                if (sw + 1 < nsw) load_y(S1);
-                cb_sweep(S0.a, S0.c, S0.y, Ys, Fs, lane);
-                __syncwarp();
-                if (sw + 1 >= nsw) break;
-                load_e(sw + 4, S0);
-                if (sw + 2 < nsw) load_y(S2);
-                cb_sweep(S1.a, S1.c, S1.y, Ys, Fs, lane);
-                __syncwarp();
-                if (sw + 2 >= nsw) break;
-                load_e(sw + 5, S1);
-                if (sw + 3 < nsw) load_y(S3);
-                cb_sweep(S2.a, S2.c, S2.y, Ys, Fs, lane);
-                __syncwarp();
-                if (sw + 3 >= nsw) break;
-                load_e(sw + 6, S2);
-                if (sw + 4 < nsw) load_y(S0);
-                cb_sweep(S3.a, S3.c, S3.y, Ys, Fs, lane);
-                __syncwarp();
+                for (int k0 = 0;;) {
+                    load4(C, base, k0 + 8, K);
+                    if (K - k0 < 4) { tile_tail(A, K - k0, Ys, Yib, Fsb, yi, ax, ay, kc, cv); break; }
+                    tileq<4>(A, Ys, Yib, Fsb, yi, ax, ay, kc, cv);
+                    k0 += 4;
+                    if (k0 >= K) break;
+                    load4(A, base, k0 + 8, K);
+                    if (K - k0 < 4) { tile_tail(B, K - k0, Ys, Yib, Fsb, yi, ax, ay, kc, cv); break; }
+                    tileq<4>(B, Ys, Yib, Fsb, yi, ax, ay, kc, cv);
+                    k0 += 4;
+                    if (k0 >= K) break;
+                    load4(B, base, k0 + 8, K);
+                    if (K - k0 < 4) { tile_tail(C, K - k0, Ys, Yib, Fsb, yi, ax, ay, kc, cv); break; }
+                    tileq<4>(C, Ys, Yib, Fsb, yi, ax, ay, kc, cv);
+                    k0 += 4;
+                    if (k0 >= K) break;
+                }
+                tile_carry(ax, ay, kc, cv, Fsb, lane);
             }
+            // every set is free here (loads past K are pads): the next tile's first groups
+            cur = nxt;
+            load4(A, slots + (size_t)cur.x * 32 + lane, 0, cur.y);
+            load4(B, slots + (size_t)cur.x * 32 + lane, 4, cur.y);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bars[2 + b]);
+            if (lane == 0) mbar_arrive(&bars[kTS + b]);   // this warp is done with the stage
             ++k;
-            // prefetch this warp's segment of the next block the group uses
-            J = next_block(J + 1);
-            if (J < NB) {
-                my_seg(J, sp, np);
-                load_e(0, S0);
-                load_e(1, S1);
-                load_e(2, S2);
-            }
         }
-        __syncwarp();
-        // rows of F: whole rows stored, pieces of split rows added (F zeroed before)
-        if (piece) {
-            if (lane == 0) atomicAdd(F + md.x, Fs[0]);
-        } else {
-            for (int q = lane; q < nu; q += 32) F[md.x + q] = Fs[q];
+        bar_consumers();
+        // rows of F: plain stores; a piece of a row split over several panels (bit 31) adds
+        for (int r = threadIdx.x; r < R; r += kTL) {
+            const int32_t q = rows[r0 + r];
+            if (q >= 0) F[q] = Fs[r];
+            else atomicAdd(F + (q & 0x7FFFFFFF), Fs[r]);
         }
-        __syncwarp();
+        bar_consumers();              // the next panel reuses Yi / Fs
     }
 }
 
-size_t cb_smem_bytes() {
-    return sizeof(float2) * (2 * kCbCols + kCbW * kCbRows) + 4 * sizeof(uint64_t);
+static size_t tile_smem_bytes(int R_max) {
+    return sizeof(float2) * ((size_t)kTS * kTB + 2 * (size_t)R_max + 2) + 2 * kTS * sizeof(uint64_t);
 }
 
-static int num_sms() {
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = kNumSMs;
-    }
-    return sms;
-}
-
-// F: rows [row_begin, row_end) of the plan's shard (nl = row_end - row_begin)
+// F: rows [row_begin, row_end) of the plan's shard (nl = row_end - row_begin).
+// No host read of the plan (the launch is captured in CUDA graphs): the shared
+// memory is sized for kTR rows per panel and the grid is one CTA per SM; the
+// kernel reads P and the panel sizes from the plan header.
 cudaError_t launch_attr_cb(const void* plan, const float2* Y, float2* F, int64_t nl, cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_attr_cb, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)cb_smem_bytes());
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
-    cudaError_t e = cudaMemsetAsync(F, 0, sizeof(float2) * (size_t)nl, s);   // split rows accumulate
+    if (nl == 0) return cudaSuccess;
+    const size_t smem = tile_smem_bytes(kTR);
+    cudaError_t e = cudaFuncSetAttribute(k_attr_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int aligned = ((uintptr_t)Y % 16) == 0;
-    k_attr_cb<<<num_sms(), (kCbW + 1) * 32, cb_smem_bytes(), s>>>(reinterpret_cast<const uint8_t*>(plan), Y, F,
-                                                                  aligned);
+    k_attr_tile<<<num_sms(), (kTW + 1) * 32, smem, s>>>(reinterpret_cast<const uint8_t*>(plan), Y, F, aligned);
     return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ plan build
-// Sort keys: (group, block, warp) of every entry of the shard; payload: the
-// packed 8-byte entry.  A stable LSD radix sort keeps the CSR (row, col)
-// order, i.e. rows ascending, inside each segment.
-__global__ void k_cb_keys(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                          const float* __restrict__ values, int64_t rb, int64_t re, const int32_t* __restrict__ row_mt,
-                          const int32_t* __restrict__ row_K, const int2* __restrict__ mt_desc, int NB,
-                          uint32_t* __restrict__ keys, unsigned long long* __restrict__ vals) {
+// Sort key of an entry: (((panel NB + block) kTW + warp) << kTRbits) | local
+// row; value: the shard-local entry index.  A stable LSD radix sort of entries
+// in CSR order keeps columns ascending inside a (tile, row) run.
+__global__ void k_tile_keys(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, int64_t rb,
+                            int64_t re, const int32_t* __restrict__ row_panel, const int32_t* __restrict__ row_local,
+                            const int32_t* __restrict__ row_warp, int NB, unsigned long long* __restrict__ keys,
+                            uint32_t* __restrict__ vals) {
     const int lane = threadIdx.x & 31;
     const int64_t e0 = indptr[rb];
     for (int64_t r = rb + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); r < re;
          r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t a = indptr[r], z = indptr[r + 1];
-        const int32_t mt0 = row_mt[r - rb];
-        const int K = row_K[r - rb];
+        const unsigned long long pk = (unsigned long long)row_panel[r - rb] * (unsigned long long)NB;
+        const unsigned long long wk = (unsigned long long)row_warp[r - rb];
+        const unsigned long long lr = (unsigned long long)row_local[r - rb];
         for (int64_t e = a + lane; e < z; e += 32) {
-            const int32_t c = indices[e];
-            const int J = c / kCbCols;
-            int32_t mt = mt0;
-            uint32_t lr = 0;
-            if (K > 1) {
-                // the row's entries inside block J: [lo, x) (columns ascending); piece by rank
-                int64_t lo = a, hi = z, x = a, y = z;
-                while (lo < hi) { const int64_t m = (lo + hi) >> 1; if (indices[m] < J * kCbCols) lo = m + 1; else hi = m; }
-                while (x < y) { const int64_t m = (x + y) >> 1; if (indices[m] < (J + 1) * kCbCols) x = m + 1; else y = m; }
-                mt += (int32_t)(((e - lo) * K) / (x - lo));
-            } else {
-                lr = (uint32_t)(r - rb - mt_desc[mt].x);
-            }
-            const uint32_t g = (uint32_t)(mt / kCbW), w = (uint32_t)(mt % kCbW);
-            keys[e - e0] = (g * (uint32_t)NB + (uint32_t)J) * (uint32_t)kCbW + w;
-            const uint32_t word = (lr << 16) | (uint32_t)(c - J * kCbCols);
-            vals[e - e0] = ((unsigned long long)__float_as_uint(values[e]) << 32) | word;
+            const unsigned long long J = (unsigned long long)(indices[e] / kTB);
+            keys[e - e0] = ((((pk + J) * kTW) + wk) << kTRbits) | lr;
+            vals[e - e0] = (uint32_t)(e - e0);
         }
     }
 }
 
-// segment start / end positions in the sorted order (empty segments stay 0, 0)
-__global__ void k_cb_bounds(const uint32_t* __restrict__ keys, int64_t m, int64_t* __restrict__ sstart,
-                            int64_t* __restrict__ send) {
+// tile start / end positions in the sorted order (empty tiles stay 0, 0)
+__global__ void k_tile_bounds(const unsigned long long* __restrict__ keys, int64_t m, int64_t* __restrict__ tstart,
+                              int64_t* __restrict__ tend) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t k = keys[q];
-        if (q == 0 || keys[q - 1] != k) sstart[k] = q;
-        if (q == m - 1 || keys[q + 1] != k) send[k] = q + 1;
+        const unsigned long long t = keys[q] >> kTRbits;
+        if (q == 0 || (keys[q - 1] >> kTRbits) != t) tstart[t] = q;
+        if (q == m - 1 || (keys[q + 1] >> kTRbits) != t) tend[t] = q + 1;
     }
 }
 
-// send -> padded (even) segment length, in place
-__global__ void k_cb_pad(const int64_t* __restrict__ sstart, int64_t* __restrict__ slen, int64_t nseg) {
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nseg; q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t L = slen[q] - sstart[q];
-        slen[q] = L + (L & 1);
+// tend -> warp steps of the tile (ceil(E / 32)), in place
+__global__ void k_tile_steps(const int64_t* __restrict__ tstart, int64_t* __restrict__ tsteps, int64_t ntiles) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < ntiles; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t E = tsteps[q] - tstart[q];
+        tsteps[q] = (E + 31) / 32;
     }
 }
 
-__global__ void k_cb_fill(const uint32_t* __restrict__ keys, const unsigned long long* __restrict__ vals, int64_t m,
-                          const int64_t* __restrict__ sstart, const int64_t* __restrict__ seg, uint2* __restrict__ ent) {
+// per-warp tile table: wtab[(p kTW + w) NB + J] = (first step, steps) of the
+// tile (p, J, w) = toff[t], toff[t + 1] - toff[t], t = (p NB + J) kTW + w
+__global__ void k_tile_wtab(const int64_t* __restrict__ toff, int64_t P, int64_t NB, int2* __restrict__ wtab) {
+    const int64_t m = P * NB * kTW;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t k = keys[q];
-        const unsigned long long v = vals[q];
-        const int64_t pos = seg[k] + (q - sstart[k]);
-        ent[pos] = make_uint2((uint32_t)v, (uint32_t)(v >> 32));
-        // odd segment: duplicate the last entry's key with p = 0 (keeps rows sorted)
-        const bool lastq = (q == m - 1) || keys[q + 1] != k;
-        if (lastq && pos + 1 < seg[k + 1]) ent[pos + 1] = make_uint2((uint32_t)v, 0u);
+        const int64_t J = q % NB, pw = q / NB, w = pw % kTW, p = pw / kTW;
+        const int64_t t = (p * NB + J) * kTW + w;
+        wtab[q] = make_int2((int32_t)toff[t], (int32_t)(toff[t + 1] - toff[t]));
     }
 }
 
-struct CbWs {
-    int32_t *row_mt, *row_K;
-    uint32_t *keys_a, *keys_b;
-    unsigned long long *vals_a, *vals_b;
-    int64_t *sstart, *slen;
+// Slot of sorted position q: tile t, index in tile i, chunk (lane) l = i / K,
+// step k = i - l K.  FLUSH: the row's run ends at this entry (the next entry
+// of the tile is another row, or the tile ends); at a chunk end a run that
+// continues is carried out instead (k_attr_tile, tile_carry).
+__global__ void k_tile_fill(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t m,
+                            const int64_t* __restrict__ tstart, const int64_t* __restrict__ tend,
+                            const int64_t* __restrict__ toff, const int32_t* __restrict__ indices,
+                            const float* __restrict__ values, int64_t e0, uint2* __restrict__ slots) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key = keys[q];
+        const unsigned long long t = key >> kTRbits;
+        const int64_t s0 = tstart[t], E = tend[t] - s0;
+        const int64_t K = (E + 31) / 32;
+        const int64_t i = q - s0, l = i / K, kk = i - l * K;
+        const bool flush = (i + 1 == E) || keys[q + 1] != key;
+        const bool newrow = (i == l * K) || keys[q - 1] != key;
+        const int64_t e = (int64_t)vals[q] + e0;
+        const uint32_t col = (uint32_t)(indices[e] % kTB);
+        const uint32_t lr = (uint32_t)(key & (kTR - 1));
+        uint32_t w = (col << 3) | (lr << 15);
+        if (flush) w |= kFlush;
+        if (newrow) w |= kNewRow;
+        slots[(size_t)(toff[t] + kk) * 32 + l] = make_uint2(w, __float_as_uint(values[e]));
+    }
+}
+
+struct TileWs {
+    int32_t *row_panel, *row_local, *row_warp;
+    unsigned long long *keys_a, *keys_b;
+    uint32_t *vals_a, *vals_b;
+    int64_t *tstart, *tend, *toff;
     void* cub_tmp;
     size_t cub_bytes, bytes;
 };
 
-static CbWs cb_ws_map(void* base, int64_t nr, int64_t m, int64_t nseg) {
-    CbWs w{};
+static TileWs tile_ws_map(void* base, int64_t nr, int64_t m, int64_t ntiles) {
+    TileWs w{};
     size_t cb = 0, cs = 0;
-    cub::DoubleBuffer<uint32_t> dk(nullptr, nullptr);
-    cub::DoubleBuffer<unsigned long long> dv(nullptr, nullptr);
-    cub::DeviceRadixSort::SortPairs(nullptr, cb, dk, dv, (int64_t)std::max<int64_t>(m, 1), 0, 32);
-    cub::DeviceScan::ExclusiveSum(nullptr, cs, (int64_t*)nullptr, (int64_t*)nullptr, (int64_t)(nseg + 1));
+    cub::DoubleBuffer<unsigned long long> dk(nullptr, nullptr);
+    cub::DoubleBuffer<uint32_t> dv(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, cb, dk, dv, (int64_t)std::max<int64_t>(m, 1), 0, 64);
+    cub::DeviceScan::ExclusiveSum(nullptr, cs, (int64_t*)nullptr, (int64_t*)nullptr, (int64_t)(ntiles + 1));
     w.cub_bytes = std::max(cb, cs);
     size_t off = 0;
     auto take = [&](size_t b) {
         size_t o = off;
-        off = cb_align(off + b);
+        off = t_align(off + b);
         return (char*)base + o;
     };
-    w.row_mt = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(nr, 1));
-    w.row_K = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(nr, 1));
-    w.keys_a = (uint32_t*)take(sizeof(uint32_t) * std::max<int64_t>(m, 1));
-    w.keys_b = (uint32_t*)take(sizeof(uint32_t) * std::max<int64_t>(m, 1));
-    w.vals_a = (unsigned long long*)take(sizeof(unsigned long long) * std::max<int64_t>(m, 1));
-    w.vals_b = (unsigned long long*)take(sizeof(unsigned long long) * std::max<int64_t>(m, 1));
-    w.sstart = (int64_t*)take(sizeof(int64_t) * (nseg + 1));
-    w.slen = (int64_t*)take(sizeof(int64_t) * (nseg + 1));
+    w.row_panel = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(nr, 1));
+    w.row_local = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(nr, 1));
+    w.row_warp = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(nr, 1));
+    w.keys_a = (unsigned long long*)take(sizeof(unsigned long long) * std::max<int64_t>(m, 1));
+    w.keys_b = (unsigned long long*)take(sizeof(unsigned long long) * std::max<int64_t>(m, 1));
+    w.vals_a = (uint32_t*)take(sizeof(uint32_t) * std::max<int64_t>(m, 1));
+    w.vals_b = (uint32_t*)take(sizeof(uint32_t) * std::max<int64_t>(m, 1));
+    w.tstart = (int64_t*)take(sizeof(int64_t) * (ntiles + 1));
+    w.tend = (int64_t*)take(sizeof(int64_t) * (ntiles + 1));
+    w.toff = (int64_t*)take(sizeof(int64_t) * (ntiles + 1));
     w.cub_tmp = take(w.cub_bytes);
     w.bytes = off;
     return w;
 }
 
-static int cb_rows(const tsnet_csr* P, const tsnet_shard* sh, int64_t& rb, int64_t& re) {
+static int tile_rows(const tsnet_csr* P, const tsnet_shard* sh, int64_t& rb, int64_t& re) {
     rb = 0;
     re = P->n;
     if (sh) {
@@ -570,22 +618,28 @@ static int cb_rows(const tsnet_csr* P, const tsnet_shard* sh, int64_t& rb, int64
     return TSNET_OK;
 }
 
-struct CbCut {
-    std::vector<int32_t> row_mt, row_K, mt_r0, mt_info;
-    int32_t G = 0;
+struct TileCut {
+    std::vector<int32_t> row_panel, row_local, row_warp, panel_off, panel_rows;
+    std::vector<int64_t> ip;
+    int32_t P = 0, R_max = 0;
     int64_t nnz_s = 0;
 };
 
-static int cb_host_cut(const tsnet_csr* P, int64_t rb, int64_t re, cudaStream_t s, CbCut& cut) {
-    std::vector<int64_t> ip(re - rb + 1, 0);
+static int tile_host_cut(const tsnet_csr* P, int64_t rb, int64_t re, cudaStream_t s, TileCut& cut) {
+    cut.ip.assign(re - rb + 1, 0);
     if (P->n > 0) {
-        TSNET_CUDA(cudaMemcpyAsync(ip.data(), P->indptr + rb, sizeof(int64_t) * ip.size(), cudaMemcpyDeviceToHost, s));
+        TSNET_CUDA(cudaMemcpyAsync(cut.ip.data(), P->indptr + rb, sizeof(int64_t) * cut.ip.size(),
+                                   cudaMemcpyDeviceToHost, s));
         TSNET_CUDA(cudaStreamSynchronize(s));
     }
-    cut.nnz_s = ip.back() - ip.front();
-    TSNET_ARG(cut.nnz_s < ((int64_t)1 << 31), "a plan holds < 2^31 entries per shard (got %lld)", (long long)cut.nnz_s);
-    cut.G = cb_partition(ip.data(), re - rb, kCbW, kCbRows, num_sms(), cut.row_mt, cut.row_K, cut.mt_r0, cut.mt_info);
-    TSNET_ARG(cut.G > 0, "row partition failed");
+    cut.nnz_s = cut.ip.back() - cut.ip.front();
+    TSNET_ARG(cut.nnz_s < ((int64_t)1 << 32), "a plan holds < 2^32 entries per shard (got %lld)", (long long)cut.nnz_s);
+    cut.P = tile_partition(cut.ip.data(), re - rb, num_sms(), kTR, cut.row_panel, cut.row_local, cut.panel_off,
+                           cut.panel_rows);
+    TSNET_ARG(cut.P > 0, "row partition failed");
+    cut.R_max = 0;
+    for (int32_t p = 0; p < cut.P; ++p) cut.R_max = std::max(cut.R_max, cut.panel_off[p + 1] - cut.panel_off[p]);
+    tile_warps(cut.ip.data(), cut.P, kTW, cut.panel_off, cut.panel_rows, cut.row_warp);
     return TSNET_OK;
 }
 
@@ -595,20 +649,20 @@ using namespace tsnet;
 
 extern "C" {
 
-int32_t tsnet_plan_partition(const int64_t* indptr_host, int64_t row_begin, int64_t row_end, int32_t warps,
-                             int32_t rows_max, int32_t base_groups, int64_t max_minitasks, int32_t* row_mt,
-                             int32_t* row_K, int32_t* mt_r0, int32_t* mt_info) {
-    if (!indptr_host || !row_mt || !row_K || !mt_r0 || !mt_info || row_begin < 0 || row_end < row_begin ||
-        warps < 1 || rows_max < 1 || base_groups < 1)
+int32_t tsnet_plan_partition(const int64_t* indptr_host, int64_t row_begin, int64_t row_end, int32_t groups,
+                             int32_t rows_cap, int32_t* row_panel, int32_t* row_local, int32_t* panel_off,
+                             int32_t* panel_rows, int64_t max_panels) {
+    if (!indptr_host || !row_panel || !row_local || !panel_off || !panel_rows || row_begin < 0 ||
+        row_end < row_begin || groups < 1 || rows_cap < 1)
         return -1;
     std::vector<int32_t> a, b, c, d;
-    const int32_t G = cb_partition(indptr_host + row_begin, row_end - row_begin, warps, rows_max, base_groups, a, b, c, d);
-    if (G < 0 || (int64_t)G * warps > max_minitasks) return -1;
-    std::memcpy(row_mt, a.data(), sizeof(int32_t) * a.size());
-    std::memcpy(row_K, b.data(), sizeof(int32_t) * b.size());
-    std::memcpy(mt_r0, c.data(), sizeof(int32_t) * c.size());
-    std::memcpy(mt_info, d.data(), sizeof(int32_t) * d.size());
-    return G;
+    const int32_t P = tile_partition(indptr_host + row_begin, row_end - row_begin, groups, rows_cap, a, b, c, d);
+    if (P < 0 || (int64_t)P > max_panels) return -1;
+    std::memcpy(row_panel, a.data(), sizeof(int32_t) * a.size());
+    std::memcpy(row_local, b.data(), sizeof(int32_t) * b.size());
+    std::memcpy(panel_off, c.data(), sizeof(int32_t) * c.size());
+    std::memcpy(panel_rows, d.data(), sizeof(int32_t) * d.size());
+    return P;
 }
 
 int tsnet_plan_query(const tsnet_csr* P, const tsnet_shard* shard, size_t* plan_bytes, size_t* ws_bytes,
@@ -616,13 +670,17 @@ int tsnet_plan_query(const tsnet_csr* P, const tsnet_shard* shard, size_t* plan_
     TSNET_ARG(P != nullptr && plan_bytes != nullptr && ws_bytes != nullptr, "NULL argument");
     TSNET_ARG(P->n >= 0 && P->nnz >= 0 && (P->n == 0 || P->indptr), "invalid P");
     int64_t rb, re;
-    int st = cb_rows(P, shard, rb, re);
+    int st = tile_rows(P, shard, rb, re);
     if (st != TSNET_OK) return st;
-    CbCut cut;
-    if ((st = cb_host_cut(P, rb, re, (cudaStream_t)stream, cut)) != TSNET_OK) return st;
-    const CbHeader h = cb_layout(P->n, rb, re, cut.nnz_s, cut.G);
+    TileCut cut;
+    if ((st = tile_host_cut(P, rb, re, (cudaStream_t)stream, cut)) != TSNET_OK) return st;
+    // upper bound of the steps: every non-empty tile pads < one step
+    const int64_t NB = std::max<int64_t>(1, (P->n + kTB - 1) / kTB);
+    const int64_t ntiles = (int64_t)cut.P * NB * kTW;
+    const int64_t steps_max = (cut.nnz_s + 31) / 32 + std::min<int64_t>(ntiles, cut.nnz_s);
+    const TileHeader h = tile_layout(P->n, rb, re, cut.nnz_s, cut.P, cut.R_max, steps_max);
     *plan_bytes = (size_t)h.bytes;
-    *ws_bytes = cb_ws_map(nullptr, re - rb, cut.nnz_s, (int64_t)h.G * h.NB * kCbW).bytes;
+    *ws_bytes = tile_ws_map(nullptr, re - rb, cut.nnz_s, ntiles).bytes;
     return TSNET_OK;
 }
 
@@ -634,57 +692,67 @@ int tsnet_plan_build(const tsnet_csr* P, const tsnet_shard* shard, void* plan, s
     TSNET_ARG(P->nnz == 0 || (P->indices && P->values), "P arrays are NULL");
     cudaStream_t s = (cudaStream_t)stream;
     int64_t rb, re;
-    int st = cb_rows(P, shard, rb, re);
+    int st = tile_rows(P, shard, rb, re);
     if (st != TSNET_OK) return st;
-    CbCut cut;
-    if ((st = cb_host_cut(P, rb, re, s, cut)) != TSNET_OK) return st;
-    CbHeader h = cb_layout(P->n, rb, re, cut.nnz_s, cut.G);
-    TSNET_ARG(plan_bytes >= (size_t)h.bytes, "plan buffer too small (%zu < %lld bytes)", plan_bytes, (long long)h.bytes);
-    const int64_t nseg = (int64_t)h.G * h.NB * kCbW;
-    TSNET_ARG((uint64_t)nseg < ((uint64_t)1 << 32), "too many (group, block, warp) segments");
-    const int64_t nr = re - rb, T = (int64_t)h.G * kCbW;
-    CbWs w = cb_ws_map(ws, nr, cut.nnz_s, nseg);
+    TileCut cut;
+    if ((st = tile_host_cut(P, rb, re, s, cut)) != TSNET_OK) return st;
+    const int64_t nr = re - rb, m = cut.nnz_s;
+    const int64_t NB = std::max<int64_t>(1, (P->n + kTB - 1) / kTB);
+    const int64_t ntiles = (int64_t)cut.P * NB * kTW;
+    TSNET_ARG(ntiles < ((int64_t)1 << (64 - kTRbits - 1)), "too many tiles");
+    TileWs w = tile_ws_map(ws, nr, m, ntiles);
     TSNET_ARG(ws != nullptr && ws_bytes >= w.bytes, "plan workspace too small (%zu < %zu bytes)", ws_bytes, w.bytes);
-    std::vector<int2> desc(T);
-    for (int64_t t = 0; t < T; ++t) desc[t] = make_int2(cut.mt_r0[t], cut.mt_info[t]);
-    uint8_t* pb = reinterpret_cast<uint8_t*>(plan);
-    int64_t* d_seg = reinterpret_cast<int64_t*>(pb + h.off_seg);
-    int2* d_mt = reinterpret_cast<int2*>(pb + h.off_mt);
-    uint2* d_ent = reinterpret_cast<uint2*>(pb + h.off_entries);
-    TSNET_CUDA(cudaMemcpyAsync(d_mt, desc.data(), sizeof(int2) * T, cudaMemcpyHostToDevice, s));
     if (nr > 0) {
-        TSNET_CUDA(cudaMemcpyAsync(w.row_mt, cut.row_mt.data(), sizeof(int32_t) * nr, cudaMemcpyHostToDevice, s));
-        TSNET_CUDA(cudaMemcpyAsync(w.row_K, cut.row_K.data(), sizeof(int32_t) * nr, cudaMemcpyHostToDevice, s));
+        TSNET_CUDA(cudaMemcpyAsync(w.row_panel, cut.row_panel.data(), sizeof(int32_t) * nr, cudaMemcpyHostToDevice, s));
+        TSNET_CUDA(cudaMemcpyAsync(w.row_local, cut.row_local.data(), sizeof(int32_t) * nr, cudaMemcpyHostToDevice, s));
+        TSNET_CUDA(cudaMemcpyAsync(w.row_warp, cut.row_warp.data(), sizeof(int32_t) * nr, cudaMemcpyHostToDevice, s));
     }
-    TSNET_CUDA(cudaMemsetAsync(w.slen, 0, sizeof(int64_t) * (nseg + 1), s));
-    TSNET_CUDA(cudaMemsetAsync(w.sstart, 0, sizeof(int64_t) * (nseg + 1), s));
-    const int64_t m = cut.nnz_s;
+    TSNET_CUDA(cudaMemsetAsync(w.tstart, 0, sizeof(int64_t) * (ntiles + 1), s));
+    TSNET_CUDA(cudaMemsetAsync(w.tend, 0, sizeof(int64_t) * (ntiles + 1), s));
+    int end_bit = kTRbits;
+    while (end_bit < 64 && ((uint64_t)1 << (end_bit - kTRbits)) < (uint64_t)ntiles) ++end_bit;
+    cub::DoubleBuffer<unsigned long long> dk(w.keys_a, w.keys_b);
+    cub::DoubleBuffer<uint32_t> dv(w.vals_a, w.vals_b);
     if (m > 0) {
-        k_cb_keys<<<num_sms() * 8, 256, 0, s>>>(P->indptr, P->indices, P->values, rb, re, w.row_mt, w.row_K, d_mt,
-                                                h.NB, w.keys_a, w.vals_a);
+        k_tile_keys<<<num_sms() * 8, 256, 0, s>>>(P->indptr, P->indices, rb, re, w.row_panel, w.row_local,
+                                                  w.row_warp, (int)NB, w.keys_a, w.vals_a);
         TSNET_LAUNCH_CHECK();
-        int end_bit = 1;
-        while (end_bit < 32 && ((uint64_t)1 << end_bit) < (uint64_t)nseg) ++end_bit;
-        cub::DoubleBuffer<uint32_t> dk(w.keys_a, w.keys_b);
-        cub::DoubleBuffer<unsigned long long> dv(w.vals_a, w.vals_b);
         size_t tb = w.cub_bytes;
         TSNET_CUDA(cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, dk, dv, m, 0, end_bit, s));
-        k_cb_bounds<<<num_sms() * 8, 256, 0, s>>>(dk.Current(), m, w.sstart, w.slen);
+        k_tile_bounds<<<num_sms() * 8, 256, 0, s>>>(dk.Current(), m, w.tstart, w.tend);
         TSNET_LAUNCH_CHECK();
-        k_cb_pad<<<num_sms() * 4, 256, 0, s>>>(w.sstart, w.slen, nseg);
+        k_tile_steps<<<num_sms() * 4, 256, 0, s>>>(w.tstart, w.tend, ntiles);
         TSNET_LAUNCH_CHECK();
-        tb = w.cub_bytes;
-        TSNET_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.slen, d_seg, nseg + 1, s));
-        k_cb_fill<<<num_sms() * 8, 256, 0, s>>>(dk.Current(), dv.Current(), m, w.sstart, d_seg, d_ent);
-        TSNET_LAUNCH_CHECK();
-    } else {
-        TSNET_CUDA(cudaMemsetAsync(d_seg, 0, sizeof(int64_t) * (nseg + 1), s));
     }
-    int64_t total = 0;
-    TSNET_CUDA(cudaMemcpyAsync(&total, d_seg + nseg, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    size_t tb = w.cub_bytes;
+    TSNET_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.tend, w.toff, ntiles + 1, s));
+    int64_t steps = 0;
+    TSNET_CUDA(cudaMemcpyAsync(&steps, w.toff + ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     TSNET_CUDA(cudaStreamSynchronize(s));
-    h.entries = total;
-    TSNET_CUDA(cudaMemcpyAsync(pb, &h, sizeof(CbHeader), cudaMemcpyHostToDevice, s));
+    TSNET_ARG(steps < ((int64_t)1 << 31), "plan too large (%lld steps)", (long long)steps);
+    TileHeader h = tile_layout(P->n, rb, re, m, cut.P, cut.R_max, steps);
+    TSNET_ARG(plan_bytes >= (size_t)h.bytes, "plan buffer too small (%zu < %lld bytes)", plan_bytes, (long long)h.bytes);
+    uint8_t* pb = reinterpret_cast<uint8_t*>(plan);
+    uint2* d_slots = reinterpret_cast<uint2*>(pb + h.off_slots);
+    k_tile_wtab<<<num_sms() * 4, 256, 0, s>>>(w.toff, cut.P, NB, reinterpret_cast<int2*>(pb + h.off_wtab));
+    TSNET_LAUNCH_CHECK();
+    TSNET_CUDA(cudaMemcpyAsync(pb + h.off_rowoff, cut.panel_off.data(), sizeof(int32_t) * (cut.P + 1),
+                               cudaMemcpyHostToDevice, s));
+    if (nr > 0)
+        TSNET_CUDA(cudaMemcpyAsync(pb + h.off_rows, cut.panel_rows.data(), sizeof(int32_t) * nr,
+                                   cudaMemcpyHostToDevice, s));
+    if (steps > 0) TSNET_CUDA(cudaMemsetAsync(d_slots, 0, sizeof(uint2) * 32 * (size_t)steps, s));
+    if (m > 0) {
+        // tend holds steps now; the fill needs the tile ends again
+        TSNET_CUDA(cudaMemsetAsync(w.tend, 0, sizeof(int64_t) * (ntiles + 1), s));
+        TSNET_CUDA(cudaMemsetAsync(w.tstart, 0, sizeof(int64_t) * (ntiles + 1), s));
+        k_tile_bounds<<<num_sms() * 8, 256, 0, s>>>(dk.Current(), m, w.tstart, w.tend);
+        TSNET_LAUNCH_CHECK();
+        k_tile_fill<<<num_sms() * 8, 256, 0, s>>>(dk.Current(), dv.Current(), m, w.tstart, w.tend, w.toff,
+                                                  P->indices, P->values, cut.ip.front(), d_slots);
+        TSNET_LAUNCH_CHECK();
+    }
+    TSNET_CUDA(cudaMemcpyAsync(pb, &h, sizeof(TileHeader), cudaMemcpyHostToDevice, s));
     TSNET_CUDA(cudaStreamSynchronize(s));
     return TSNET_OK;
 }

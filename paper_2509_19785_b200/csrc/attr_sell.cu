@@ -85,50 +85,7 @@ __device__ __forceinline__ void sell_acc(const float2* __restrict__ Y, float2 yi
 
 // One warp per slice (grid-stride).  The entry stream is prefetched NS - 1
 // register sets of U steps ahead (HBM latency), the sets rotate by unrolling
-// (no copies of in-flight loads); each set's U gathers of Y_j are in flight
-// together.
-template <int U, int NS>
-__global__ void __launch_bounds__(256) k_attr_sell(const uint8_t* __restrict__ plan, const float2* __restrict__ Y,
-                                                   float2* __restrict__ F) {
-    const SellHeader* h = reinterpret_cast<const SellHeader*>(plan);
-    const int64_t rb = h->row_begin, re = h->row_end, S = h->slices;
-    const int64_t* __restrict__ base = reinterpret_cast<const int64_t*>(plan + h->off_base);
-    const uint2* __restrict__ slots = reinterpret_cast<const uint2*>(plan + h->off_slots);
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t pol = sell_policy_evict_first();
-    for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < S; s += nw) {
-        const int64_t b0 = __ldg(base + s), K = (__ldg(base + s + 1) - b0) >> 5;
-        const int64_t r = rb + s * 32 + lane;
-        const bool live = r < re;
-        const float2 yi = live ? __ldg(Y + r) : make_float2(0.f, 0.f);
-        const uint2* p = slots + b0 + lane;
-        float fx = 0.f, fy = 0.f;
-        uint2 E[NS][U];
-#pragma unroll
-        for (int j = 0; j < NS - 1; ++j)
-#pragma unroll
-            for (int q = 0; q < U; ++q)
-                E[j][q] = j * U + q < K ? sell_ld_stream(p + 32 * (j * U + q), pol) : make_uint2(0u, 0u);
-        for (int64_t k = 0; k < K; k += NS * U) {
-#pragma unroll
-            for (int j = 0; j < NS; ++j) {
-                const int jl = (j + NS - 1) % NS;            // the set consumed one set ago
-                const int64_t kl = k + (int64_t)(j + NS - 1) * U;
-#pragma unroll
-                for (int q = 0; q < U; ++q)
-                    E[jl][q] = kl + q < K ? sell_ld_stream(p + 32 * (kl + q), pol) : make_uint2(0u, 0u);
-                // steps past K hold (0, +0.0f): they add p w d = 0 exactly, and
-                // computing them unconditionally lets the U gathers issue together
-#pragma unroll
-                for (int q = 0; q < U; ++q) sell_acc(Y, yi, E[j][q], fx, fy);
-            }
-        }
-        if (live) F[r - rb] = make_float2(fx, fy);
-    }
-}
-
-// Same, with the Y_j gathers pipelined too: the gathers of set j + 1 are
+// (no copies of in-flight loads), and the Y_j gathers of set j + 1 are
 // issued before set j is computed (two gather sets in flight per warp).
 // NS even (the unrolled body covers NS sets; gather sets alternate).
 //
@@ -209,230 +166,41 @@ __global__ void __launch_bounds__(256, MINB) k_attr_sell_g(const uint8_t* __rest
     }
 }
 
-// TMA-staged variant.  A warp owns a contiguous run of slices [s0, s1)
-// (balanced on slots), so its entries are ONE contiguous byte range; lane 0
-// streams it into a per-warp ring of R stages of CS steps (CS x 256 bytes)
-// with cp.async.bulk (mbarrier completion), R - 1 stages ahead.  The ring
-// holds the bytes in flight, not registers, so the warp count per SM is not
-// cut by the prefetch depth.  Per U steps: U entries from shared memory, U
-// gathers of Y_j in flight together, then the U updates in order, closing a
-// slice (writing its 32 F_i) whenever its last step is done.
-template <int U, int CS, int R>
-__global__ void __launch_bounds__(256) k_attr_sell_tma(const uint8_t* __restrict__ plan,
-                                                       const float2* __restrict__ Y, float2* __restrict__ F) {
-    extern __shared__ __align__(128) uint8_t sm[];
-    const SellHeader* h = reinterpret_cast<const SellHeader*>(plan);
-    const int64_t rb = h->row_begin, re = h->row_end, S = h->slices;
-    const int64_t* __restrict__ base = reinterpret_cast<const int64_t*>(plan + h->off_base);
-    const uint2* __restrict__ slots = reinterpret_cast<const uint2*>(plan + h->off_slots);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint2* ring = reinterpret_cast<uint2*>(sm) + (size_t)warp * R * CS * 32;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + (size_t)8 * R * CS * 32 * sizeof(uint2)) + warp * R;
-    if (lane == 0) {
-        for (int q = 0; q < R; ++q) mbar_init(&bars[q], 1);
-        fence_mbar_init();
-    }
-    __syncwarp();
-    // slices of this warp: lower bounds of its share of the slots in base[0..S]
-    const int64_t NW = (int64_t)gridDim.x * 8, wg = (int64_t)blockIdx.x * 8 + warp;
-    const int64_t total = __ldg(base + S);
-    auto lower_bound = [&](int64_t target) {   // first i in [0, S] with base[i] >= target (warp-uniform)
-        int64_t lo = 0, hi = S;
-        while (hi - lo > 0) {
-            const int64_t step = (hi - lo + 31) / 32;
-            const int64_t q = lo + lane * step;
-            const bool below = q < hi && __ldg(base + q) < target;
-            const unsigned m = __ballot_sync(0xffffffffu, below);
-            const int c = __popc(m);                  // probes lo, lo+step, ... below target
-            if (c == 0) {
-                hi = lo;
-            } else {
-                lo = lo + (int64_t)(c - 1) * step + 1;
-                hi = std::min(hi, lo - 1 + step);
-            }
-        }
-        return lo;
-    };
-    const int64_t s0 = lower_bound((int64_t)((double)total * wg / NW));
-    const int64_t s1 = wg == NW - 1 ? S : lower_bound((int64_t)((double)total * (wg + 1) / NW));
-    if (s0 >= s1) return;
-    const int64_t e0 = __ldg(base + s0), T = (__ldg(base + s1) - e0) >> 5;   // steps of the run
-    const uint64_t pol = sell_policy_evict_first();
-    auto issue = [&](int64_t t) {                     // lane 0: stage t into buffer t % R
-        const int64_t k0 = t * CS, nst = std::min<int64_t>(CS, T - k0);
-        const uint32_t bytes = (uint32_t)(nst * 32 * sizeof(uint2));
-        mbar_arrive_tx(&bars[t % R], bytes);
-        bulk_g2s_hint(ring + (size_t)(t % R) * CS * 32, slots + e0 + k0 * 32, bytes, &bars[t % R], pol);
-    };
-    if (lane == 0)
-        for (int64_t t = 0; t < R && t * CS < T; ++t) issue(t);
-    // consume cursor
-    int64_t s = s0, rem = 0;
-    float2 yi = make_float2(0.f, 0.f);
-    float fx = 0.f, fy = 0.f;
-    auto enter = [&](int64_t q) {                    // start slice q (< s1)
-        const int64_t r = rb + q * 32 + lane;
-        yi = r < re ? __ldg(Y + r) : make_float2(0.f, 0.f);
-        rem = (__ldg(base + q + 1) - __ldg(base + q)) >> 5;
-        fx = fy = 0.f;
-    };
-    auto close_empty = [&]() {                        // write finished slices, enter the next with steps
-        while (rem == 0 && s < s1) {
-            const int64_t r = rb + s * 32 + lane;
-            if (r < re) F[r - rb] = make_float2(fx, fy);
-            ++s;
-            if (s < s1) enter(s);
-        }
-    };
-    enter(s);
-    close_empty();
-    for (int64_t t = 0; t * CS < T; ++t) {
-        const int b = (int)(t % R);
-        mbar_wait(&bars[b], (uint32_t)((t / R) & 1));
-        const int64_t nst = std::min<int64_t>(CS, T - t * CS);
-        const uint2* st = ring + (size_t)b * CS * 32 + lane;
-#pragma unroll
-        for (int q0 = 0; q0 < CS; q0 += U) {
-            if (q0 >= nst) break;
-            uint2 e[U];
-            float2 yj[U];
-#pragma unroll
-            for (int q = 0; q < U; ++q) e[q] = q0 + q < nst ? st[(q0 + q) * 32] : make_uint2(0u, 0u);
-#pragma unroll
-            for (int q = 0; q < U; ++q) yj[q] = __ldg(Y + (int)e[q].x);
-#pragma unroll
-            for (int q = 0; q < U; ++q) {
-                if (q0 + q < nst) {
-                    const float dx = yi.x - yj[q].x, dy = yi.y - yj[q].y;
-                    const float w = __frcp_rn(fmaf(dx, dx, fmaf(dy, dy, 1.0f)));
-                    const float pw = __uint_as_float(e[q].y) * w;
-                    fx = fmaf(pw, dx, fx);
-                    fy = fmaf(pw, dy, fy);
-                    --rem;
-                    close_empty();
-                }
-            }
-        }
-        __syncwarp();                                 // every lane is done with buffer b
-        if (lane == 0 && (t + R) * CS < T) {
-            fence_proxy_async_smem();
-            issue(t + R);
-        }
-    }
-}
+// Kernel shape (measured on config 5, kernel alone, B200; CSR kernel 1.22 ms,
+// round-1 sweep r1cq): U = 4 steps per set, NS = 4 sets, 4 CTAs per SM
+// promised to ptxas: 0.751 ms (64 registers, 87% of the measured HBM peak);
+// g4,4 with 3 / 1 CTAs per SM 0.771 / 0.996 ms (94 registers), g4,2 0.816,
+// g2,4 0.879, g1,8 1.537; entries pipelined without the gather pipeline
+// 0.921-0.943; TMA-staged entries 1.01-1.47 (the ring's shared memory takes
+// L1 capacity from the Y_j gathers, which hit L1 on a mesh).
+static constexpr auto sell_kernel = k_attr_sell_g<4, 4, false, 4>;
+static constexpr auto sell_move_kernel = k_attr_sell_g<4, 4, true, 3>;
 
-template <int U, int CS, int R>
-static constexpr size_t sell_tma_smem() {
-    return (size_t)8 * R * CS * 32 * sizeof(uint2) + (size_t)8 * R * sizeof(uint64_t);
-}
-
-using SellKernel = void (*)(const uint8_t*, const float2*, float2*);
-using SellGKernel = void (*)(const uint8_t*, const float2*, float2*, SellMoveArgs);
-
-struct SellLaunch {
-    SellKernel k = nullptr;        // register / TMA variants (probing)
-    SellGKernel kg = nullptr;      // gather-pipelined variant (default)
-    size_t smem = 0;
-    int resident = 1;
-};
-
-// Kernel choice (measured on config 5, kernel alone, B200; CSR kernel 1.22 ms):
-//   gU,NS[,MINB]  entries and gathers pipelined (k_attr_sell_g), MINB = CTAs per
-//          SM promised to ptxas: g4,4,4 0.751 ms (default; 64 registers, 87% of
-//          the measured HBM peak), g4,4,3 0.771, g4,4,1 0.996 (94 registers, 2
-//          CTAs/SM), g4,2 0.816, g2,4 0.879, g2,6 1.137, g1,8 1.537; with the
-//          4-CTA bound (r1cq): g3,4 0.762, g2,4 0.872, g2,6 0.899, g4,6 1.030
-//          (spills), g4,4 at 5 CTAs/SM 1.327 (spills);
-//   U,NS   entries pipelined only (k_attr_sell): 2,4 0.921, 4,2 0.937, 4,3 0.943;
-//   tma:U,CS,R  TMA-staged entries (k_attr_sell_tma): 8,8,4 1.012, 4,8,3 1.052,
-//          4,8,4 1.138, 8,4,4 1.143 -- the ring's shared memory takes L1
-//          capacity from the Y_j gathers, which hit L1 on a mesh.
-// TSNET_SELL selects one for probing.
-template <int U, int CS, int R>
-static void pick_tma(SellLaunch& L) {
-    L.k = k_attr_sell_tma<U, CS, R>;
-    L.smem = sell_tma_smem<U, CS, R>();
-}
-
-// chosen once (function-local static: thread-safe initialisation)
-static const SellLaunch& sell_launch() {
-    static const SellLaunch launch = [] {
-        SellLaunch L;
-        const char* e = getenv("TSNET_SELL");
-        if (!e) e = "g4,4";   // the fused move (launch_attr_sell_move) uses this shape too
-        int u = 4, cs = 8, r = 4;
-        if (strncmp(e, "tma:", 4) != 0) {
-            int ns = 4;
-            u = 4;
-            const bool g = strchr(e, 'g') != nullptr;    // "gU,NS[,MINB]": gathers pipelined too
-            int mb = 4;
-            sscanf(g ? e + 1 : e, "%d,%d,%d", &u, &ns, &mb);
-            if (g && u == 2 && ns == 4) L.kg = k_attr_sell_g<2, 4, false>;
-            else if (g && u == 4 && ns == 4 && mb == 1) L.kg = k_attr_sell_g<4, 4, false, 1>;
-            else if (g && u == 4 && ns == 4 && mb == 3) L.kg = k_attr_sell_g<4, 4, false, 3>;
-            else if (g && u == 4 && ns == 4) L.kg = k_attr_sell_g<4, 4, false, 4>;
-            else if (g && u == 4 && ns == 2 && mb == 1) L.kg = k_attr_sell_g<4, 2, false, 1>;
-            else if (g && u == 4 && ns == 2) L.kg = k_attr_sell_g<4, 2, false, 4>;
-            else if (g && u == 6 && ns == 2) L.kg = k_attr_sell_g<6, 2, false>;
-            else if (u == 4 && ns == 2) L.k = k_attr_sell<4, 2>;
-            else if (u == 4 && ns == 3) L.k = k_attr_sell<4, 3>;
-            else L.k = k_attr_sell<2, 4>;
-        } else {
-            sscanf(e + 4, "%d,%d,%d", &u, &cs, &r);
-            if (u == 4 && cs == 4 && r == 6) pick_tma<4, 4, 6>(L);
-            else if (u == 4 && cs == 16 && r == 3) pick_tma<4, 16, 3>(L);
-            else if (u == 8 && cs == 8 && r == 4) pick_tma<8, 8, 4>(L);
-            else if (u == 2 && cs == 8 && r == 4) pick_tma<2, 8, 4>(L);
-            else if (u == 4 && cs == 8 && r == 3) pick_tma<4, 8, 3>(L);
-            else if (u == 8 && cs == 4 && r == 4) pick_tma<8, 4, 4>(L);
-            else if (u == 8 && cs == 4 && r == 3) pick_tma<8, 4, 3>(L);
-            else pick_tma<4, 8, 4>(L);
-        }
-        if (L.smem > 0) cudaFuncSetAttribute(L.k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
-        const cudaError_t oe = L.kg ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&L.resident, L.kg, 256, 0)
-                                    : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&L.resident, L.k, 256, L.smem);
-        if (oe != cudaSuccess || L.resident < 1) L.resident = 1;
-        return L;
-    }();
-    return launch;
-}
-
-// CTAs = TSNET_SELL_WAVES (default 1) x the resident CTAs (grid-stride over slices)
-static int sell_waves() {
-    static int v = 0;
-    if (v == 0) {
-        const char* e = getenv("TSNET_SELL_WAVES");
-        v = e ? std::max(1, std::min(64, atoi(e))) : 1;
-    }
-    return v;
+static int resident_of(const void* k) {
+    int r = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k, 256, 0) != cudaSuccess || r < 1) r = 1;
+    return r;
 }
 
 // F: rows [row_begin, row_end) of the plan's shard (nl = row_end - row_begin)
 cudaError_t launch_attr_sell(const void* plan, const float2* Y, float2* F, int64_t nl, cudaStream_t s) {
     if (nl == 0) return cudaSuccess;
-    const SellLaunch& L = sell_launch();
     const int64_t slices = (nl + 31) / 32;
     const int blocks = (int)std::max<int64_t>(
-        1, std::min<int64_t>((slices + 7) / 8, (int64_t)kNumSMs * L.resident * sell_waves()));
-    const uint8_t* pl = reinterpret_cast<const uint8_t*>(plan);
-    if (L.kg) L.kg<<<blocks, 256, 0, s>>>(pl, Y, F, SellMoveArgs{});
-    else L.k<<<blocks, 256, L.smem, s>>>(pl, Y, F);
+        1, std::min<int64_t>((slices + 7) / 8, (int64_t)kNumSMs * resident_of((const void*)sell_kernel)));
+    sell_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint8_t*>(plan), Y, F, SellMoveArgs{});
     return cudaGetLastError();
 }
 
-// SpMV + move of the plan's rows (the default gather-pipelined kernel with
-// the a7 epilogue); F_attr is not stored.
+// SpMV + move of the plan's rows (the same kernel shape with the a7
+// epilogue); F_attr is not stored.
 cudaError_t launch_attr_sell_move(const void* plan, const float2* Y, int64_t nl, const SellMoveArgs& m,
                                   cudaStream_t s) {
     if (nl == 0) return cudaSuccess;
-    static int resident = 0;
-    if (resident == 0 &&
-        (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_attr_sell_g<4, 4, true, 3>, 256, 0) != cudaSuccess ||
-         resident < 1))
-        resident = 1;
     const int64_t slices = (nl + 31) / 32;
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((slices + 7) / 8, (int64_t)kNumSMs * resident));
-    k_attr_sell_g<4, 4, true, 3><<<blocks, 256, 0, s>>>(reinterpret_cast<const uint8_t*>(plan), Y, nullptr, m);
+    const int blocks = (int)std::max<int64_t>(
+        1, std::min<int64_t>((slices + 7) / 8, (int64_t)kNumSMs * resident_of((const void*)sell_move_kernel)));
+    sell_move_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint8_t*>(plan), Y, nullptr, m);
     return cudaGetLastError();
 }
 

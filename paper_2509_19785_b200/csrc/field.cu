@@ -368,21 +368,34 @@ __global__ void __launch_bounds__(256) k_spread(const Geo* __restrict__ g, const
 constexpr int kRowThreads = 512;
 constexpr int kInvThreads = 256;
 constexpr int kColThreads = 512;
-constexpr int kMmax = 6 * TSNET_I_MAX_LIMIT;   // 1536
+constexpr int kMfast = 1536;   // M = 6 I <= 1536 (I <= 256): every pass keeps all its transforms in shared memory
+// Shared memory of each pass, in float2, for grids up to M_max: the fast
+// layout for M <= kMfast, else one transform (plus twiddles and scratch) at a
+// time, 3 M floats2 (M = 6144 at I = 1024: 147 KB).  The passes read the cap
+// and pick the batch size from the run-time M.
+static int smem_cap_row(int M_max) { return std::max(11 * std::min(M_max, kMfast), 3 * M_max); }
+static int smem_cap_col(int M_max) { return std::max(17 * std::min(M_max, kMfast), 3 * M_max); }
+static int smem_cap_inv(int M_max) { return std::max(5 * std::min(M_max, kMfast), 3 * M_max); }
+// transforms per batch for a pass needing tw (M) + buf (B M) + scratch (B M)
+__device__ __forceinline__ int fft_batch(int cap, int M, int want) {
+    return max(1, min(want, (cap / M - 1) / 2));
+}
 // spectra layout: array a, column kx, row y  ->  spec[(a * half_max + kx) * M_max + y]
 
 // a3 + first half of a4: per row y of the M x M circulant grid, build the 10
 // real arrays (3 charges, 7 kernel tables), FFT them along x in 5 packed
-// complex transforms, unpack to half spectra and store transposed.
+// complex transforms (in batches that fit the shared memory), unpack to half
+// spectra and store transposed.
 //   arrays: 0 W1, 1 Mx, 2 My, 3 K1, 4 K2, 5 Ke, 6 DxK2, 7 DxKe, 8 DyK2, 9 DyKe
 __global__ void __launch_bounds__(kRowThreads, 1) k_row_fwd(const Geo* __restrict__ gp, const float4* __restrict__ wgrid,
                                                          const float2* __restrict__ twg, float2* __restrict__ spec,
-                                                         int M_max, float eps) {
+                                                         int M_max, float eps, int cap) {
     extern __shared__ float2 sm[];
-    float2* tw = sm;                      // M
-    float2* buf = sm + M_max;             // 5 * M
-    float2* scr = buf + 5 * M_max;        // 5 * M
     const int M = gp->M, N = gp->N, half = M / 2 + 1, nrad = gp->nrad;
+    const int B = fft_batch(cap, M, 5);
+    float2* tw = sm;                      // M
+    float2* buf = sm + M;                 // B M
+    float2* scr = buf + B * M;            // B M
     const unsigned long long plan = gp->plan;
     const int half_max = M_max / 2 + 1;
     const double dlt = gp->delta;
@@ -390,89 +403,148 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_row_fwd(const Geo* __restric
     for (int y = blockIdx.x; y < M; y += gridDim.x) {
         const int dy = (y <= M / 2) ? y : y - M;
         const bool ky = (dy < N) && (-dy < N);       // |dy| <= N - 1
-        for (int x = threadIdx.x; x < M; x += blockDim.x) {
-            const int dx = (x <= M / 2) ? x : x - M;
-            float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (y < N && x < N) wv = wgrid[(int64_t)y * N + x];
-            float k1 = 0.f, k2 = 0.f, ke = 0.f, dxk2 = 0.f, dxke = 0.f, dyk2 = 0.f, dyke = 0.f;
-            if (ky && dx < N && -dx < N) {
-                const double ox = dx * dlt, oy = dy * dlt;
-                const double r2 = ox * ox + oy * oy;
-                const double K1 = 1.0 / (1.0 + r2), K2 = K1 * K1, Ke = 1.0 / ((double)eps + r2);
-                k1 = (float)K1; k2 = (float)K2; ke = (float)Ke;
-                dxk2 = (float)(ox * K2); dxke = (float)(ox * Ke);
-                dyk2 = (float)(oy * K2); dyke = (float)(oy * Ke);
+        for (int p0 = 0; p0 < 5; p0 += B) {
+            const int nb = min(B, 5 - p0);
+            for (int x = threadIdx.x; x < M; x += blockDim.x) {
+                const int dx = (x <= M / 2) ? x : x - M;
+                float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (y < N && x < N) wv = wgrid[(int64_t)y * N + x];
+                float k1 = 0.f, k2 = 0.f, ke = 0.f, dxk2 = 0.f, dxke = 0.f, dyk2 = 0.f, dyke = 0.f;
+                if (ky && dx < N && -dx < N) {
+                    const double ox = dx * dlt, oy = dy * dlt;
+                    const double r2 = ox * ox + oy * oy;
+                    const double K1 = 1.0 / (1.0 + r2), K2 = K1 * K1, Ke = 1.0 / ((double)eps + r2);
+                    k1 = (float)K1; k2 = (float)K2; ke = (float)Ke;
+                    dxk2 = (float)(ox * K2); dxke = (float)(ox * Ke);
+                    dyk2 = (float)(oy * K2); dyke = (float)(oy * Ke);
+                }
+                const float2 pk[5] = {make_float2(wv.x, wv.y), make_float2(wv.z, k1), make_float2(k2, ke),
+                                      make_float2(dxk2, dxke), make_float2(dyk2, dyke)};
+                for (int q = 0; q < nb; ++q) buf[q * M + x] = pk[p0 + q];
             }
-            buf[0 * M + x] = make_float2(wv.x, wv.y);
-            buf[1 * M + x] = make_float2(wv.z, k1);
-            buf[2 * M + x] = make_float2(k2, ke);
-            buf[3 * M + x] = make_float2(dxk2, dxke);
-            buf[4 * M + x] = make_float2(dyk2, dyke);
+            __syncthreads();
+            fft_block(buf, scr, M, nb, M, plan, nrad, tw, false);
+            // unpack z = A + iB:  A_k = (Z_k + conj Z_{M-k}) / 2,  B_k = -i (Z_k - conj Z_{M-k}) / 2
+            for (int t = threadIdx.x; t < nb * half; t += blockDim.x) {
+                const int q = t / half, k = t - q * half, p = p0 + q;
+                const float2 Zk = buf[q * M + k];
+                const float2 Zm = cconj(buf[q * M + (k == 0 ? 0 : M - k)]);
+                const float2 A = make_float2(0.5f * (Zk.x + Zm.x), 0.5f * (Zk.y + Zm.y));
+                const float2 D = make_float2(0.5f * (Zk.x - Zm.x), 0.5f * (Zk.y - Zm.y));
+                const float2 Bv = mul_mi(D);
+                spec[((int64_t)(2 * p) * half_max + k) * M_max + y] = A;
+                spec[((int64_t)(2 * p + 1) * half_max + k) * M_max + y] = Bv;
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        fft_block(buf, scr, M, 5, M, plan, nrad, tw, false);
-        // unpack z = A + iB:  A_k = (Z_k + conj Z_{M-k}) / 2,  B_k = -i (Z_k - conj Z_{M-k}) / 2
-        for (int t = threadIdx.x; t < 5 * half; t += blockDim.x) {
-            const int p = t / half, k = t - p * half;
-            const float2 Zk = buf[p * M + k];
-            const float2 Zm = cconj(buf[p * M + (k == 0 ? 0 : M - k)]);
-            const float2 A = make_float2(0.5f * (Zk.x + Zm.x), 0.5f * (Zk.y + Zm.y));
-            const float2 D = make_float2(0.5f * (Zk.x - Zm.x), 0.5f * (Zk.y - Zm.y));
-            const float2 B = mul_mi(D);
-            spec[((int64_t)(2 * p) * half_max + k) * M_max + y] = A;
-            spec[((int64_t)(2 * p + 1) * half_max + k) * M_max + y] = B;
-        }
-        __syncthreads();
     }
+}
+
+// Kernel-charge products of one frequency k (10 spectra in, 6 out) and the
+// Parseval term of Z:
+//   A0 = K2 W1, Ax = DxK2 W1 + K2 Mx, Ay = DyK2 W1 + K2 My   (alpha part)
+//   B0 = Ke W1, Bx = DxKe W1 + Ke Mx, By = DyKe W1 + Ke My   (beta part)
+__device__ __forceinline__ double col_products(const float2 (&v)[10], float2 (&o)[6]) {
+    const float2 W1 = v[0], Mx = v[1], My = v[2], K1 = v[3], K2 = v[4], Ke = v[5];
+    const float2 DxK2 = v[6], DxKe = v[7], DyK2 = v[8], DyKe = v[9];
+    o[0] = cmul(K2, W1);
+    o[1] = cadd(cmul(DxK2, W1), cmul(K2, Mx));
+    o[2] = cadd(cmul(DyK2, W1), cmul(K2, My));
+    o[3] = cmul(Ke, W1);
+    o[4] = cadd(cmul(DxKe, W1), cmul(Ke, Mx));
+    o[5] = cadd(cmul(DyKe, W1), cmul(Ke, My));
+    return (double)K1.x * ((double)W1.x * W1.x + (double)W1.y * W1.y);
 }
 
 // Second half of a4 + a5: per column kx, forward FFT along y of the 10
 // arrays, Parseval partial of Z, the kernel-charge products, inverse FFT of
-// the 6 products along y; rows y < N are stored.
-//   A0 = K2 W1, Ax = DxK2 W1 + K2 Mx, Ay = DyK2 W1 + K2 My   (alpha part)
-//   B0 = Ke W1, Bx = DxKe W1 + Ke Mx, By = DyKe W1 + Ke My   (beta part)
-__global__ void __launch_bounds__(kColThreads, 1) k_col(Geo* __restrict__ gp, const float2* __restrict__ spec,
+// the 6 products along y; rows y < N are stored.  M <= kMfast: all 16
+// transforms of a column in shared memory; larger M: the column's spectra are
+// transformed in place in `spec` a batch at a time, multiplied there, and the
+// products transformed back a batch at a time.
+__global__ void __launch_bounds__(kColThreads, 1) k_col(Geo* __restrict__ gp, float2* __restrict__ spec,
                                                         const float2* __restrict__ twg, float2* __restrict__ colout,
-                                                        int M_max, int N_max) {
+                                                        int M_max, int N_max, int cap) {
     extern __shared__ float2 sm[];
-    float2* tw = sm;                      // M
-    float2* buf = sm + M_max;             // 10 * M
-    float2* scr = buf + 10 * M_max;       // 6 * M
     __shared__ double zred[kColThreads / 32];
     const int M = gp->M, N = gp->N, half = M / 2 + 1, nrad = gp->nrad;
     const unsigned long long plan = gp->plan;
     const int half_max = M_max / 2 + 1;
+    float2* tw = sm;                      // M
     for (int k = threadIdx.x; k < M; k += blockDim.x) tw[k] = twg[k];
     double zpart = 0.0;
+    const bool fast = 17 * M <= cap;
     for (int kx = blockIdx.x; kx < half; kx += gridDim.x) {
-        for (int t = threadIdx.x; t < 10 * M; t += blockDim.x) {
-            const int a = t / M, y = t - a * M;
-            buf[t] = spec[((int64_t)a * half_max + kx) * M_max + y];
+        auto col = [&](int a) { return spec + ((int64_t)a * half_max + kx) * M_max; };
+        if (fast) {
+            float2* buf = sm + M;             // 10 M
+            float2* scr = buf + 10 * M;       // 6 M
+            for (int t = threadIdx.x; t < 10 * M; t += blockDim.x) {
+                const int a = t / M, y = t - a * M;
+                buf[t] = col(a)[y];
+            }
+            __syncthreads();
+            fft_block(buf, scr, M, 5, M, plan, nrad, tw, false);
+            fft_block(buf + 5 * M, scr, M, 5, M, plan, nrad, tw, false);
+            const double wt = (kx == 0 || 2 * kx == M) ? 1.0 : 2.0;
+            for (int k = threadIdx.x; k < M; k += blockDim.x) {
+                float2 v[10], o[6];
+#pragma unroll
+                for (int a = 0; a < 10; ++a) v[a] = buf[a * M + k];
+                zpart += wt * col_products(v, o);
+#pragma unroll
+                for (int b = 0; b < 6; ++b) buf[b * M + k] = o[b];
+            }
+            __syncthreads();
+            fft_block(buf, scr, M, 6, M, plan, nrad, tw, true);
+            for (int t = threadIdx.x; t < 6 * N; t += blockDim.x) {
+                const int b = t / N, y = t - b * N;
+                colout[((int64_t)b * half_max + kx) * N_max + y] = buf[b * M + y];
+            }
+            __syncthreads();
+        } else {
+            const int B = fft_batch(cap, M, 10);
+            float2* buf = sm + M;             // B M
+            float2* scr = buf + B * M;        // B M
+            for (int a0 = 0; a0 < 10; a0 += B) {          // forward, in place in spec
+                const int nb = min(B, 10 - a0);
+                for (int t = threadIdx.x; t < nb * M; t += blockDim.x) {
+                    const int q = t / M, y = t - q * M;
+                    buf[t] = col(a0 + q)[y];
+                }
+                __syncthreads();
+                fft_block(buf, scr, M, nb, M, plan, nrad, tw, false);
+                for (int t = threadIdx.x; t < nb * M; t += blockDim.x) {
+                    const int q = t / M, y = t - q * M;
+                    col(a0 + q)[y] = buf[t];
+                }
+                __syncthreads();
+            }
+            const double wt = (kx == 0 || 2 * kx == M) ? 1.0 : 2.0;
+            for (int k = threadIdx.x; k < M; k += blockDim.x) {   // products, in place (arrays 0-5)
+                float2 v[10], o[6];
+#pragma unroll
+                for (int a = 0; a < 10; ++a) v[a] = col(a)[k];
+                zpart += wt * col_products(v, o);
+#pragma unroll
+                for (int b = 0; b < 6; ++b) col(b)[k] = o[b];
+            }
+            __syncthreads();
+            for (int b0 = 0; b0 < 6; b0 += B) {           // inverse, rows y < N out
+                const int nb = min(B, 6 - b0);
+                for (int t = threadIdx.x; t < nb * M; t += blockDim.x) {
+                    const int q = t / M, y = t - q * M;
+                    buf[t] = col(b0 + q)[y];
+                }
+                __syncthreads();
+                fft_block(buf, scr, M, nb, M, plan, nrad, tw, true);
+                for (int t = threadIdx.x; t < nb * N; t += blockDim.x) {
+                    const int q = t / N, y = t - q * N;
+                    colout[((int64_t)(b0 + q) * half_max + kx) * N_max + y] = buf[q * M + y];
+                }
+                __syncthreads();
+            }
         }
-        __syncthreads();
-        fft_block(buf, scr, M, 5, M, plan, nrad, tw, false);
-        fft_block(buf + 5 * M, scr, M, 5, M, plan, nrad, tw, false);
-        const double wt = (kx == 0 || 2 * kx == M) ? 1.0 : 2.0;
-        for (int k = threadIdx.x; k < M; k += blockDim.x) {
-            const float2 W1 = buf[k], Mx = buf[M + k], My = buf[2 * M + k];
-            const float2 K1 = buf[3 * M + k], K2 = buf[4 * M + k], Ke = buf[5 * M + k];
-            const float2 DxK2 = buf[6 * M + k], DxKe = buf[7 * M + k];
-            const float2 DyK2 = buf[8 * M + k], DyKe = buf[9 * M + k];
-            zpart += wt * (double)K1.x * ((double)W1.x * W1.x + (double)W1.y * W1.y);
-            buf[k] = cmul(K2, W1);
-            buf[M + k] = cadd(cmul(DxK2, W1), cmul(K2, Mx));
-            buf[2 * M + k] = cadd(cmul(DyK2, W1), cmul(K2, My));
-            buf[3 * M + k] = cmul(Ke, W1);
-            buf[4 * M + k] = cadd(cmul(DxKe, W1), cmul(Ke, Mx));
-            buf[5 * M + k] = cadd(cmul(DyKe, W1), cmul(Ke, My));
-        }
-        __syncthreads();
-        fft_block(buf, scr, M, 6, M, plan, nrad, tw, true);
-        for (int t = threadIdx.x; t < 6 * N; t += blockDim.x) {
-            const int b = t / N, y = t - b * N;
-            colout[((int64_t)b * half_max + kx) * N_max + y] = buf[b * M + y];
-        }
-        __syncthreads();
     }
     for (int o = 16; o > 0; o >>= 1) zpart += __shfl_xor_sync(0xffffffffu, zpart, o);
     if ((threadIdx.x & 31) == 0) zred[threadIdx.x >> 5] = zpart;
@@ -485,16 +557,18 @@ __global__ void __launch_bounds__(kColThreads, 1) k_col(Geo* __restrict__ gp, co
 }
 
 // Last part of a4: per row y < N, combine with alpha/beta (Z is complete now),
-// inverse FFT along x (P0 + i Qx packed, Qy alone), scale 1/M^2, keep x < N.
+// inverse FFT along x (P0 + i Qx packed, Qy alone; one at a time when the two
+// do not fit), scale 1/M^2, keep x < N.
 __global__ void __launch_bounds__(kInvThreads) k_row_inv(Geo* __restrict__ gp, const float2* __restrict__ colout,
                                                          const float2* __restrict__ twg, float4* __restrict__ fgrid,
                                                          int M_max, int N_max, int64_t n, float lambda_kl,
-                                                         float lambda_r) {
+                                                         float lambda_r, int cap) {
     extern __shared__ float2 sm[];
-    float2* tw = sm;
-    float2* buf = sm + M_max;             // 2 * M
-    float2* scr = buf + 2 * M_max;        // 2 * M
     const int M = gp->M, N = gp->N, nrad = gp->nrad;
+    const int B = fft_batch(cap, M, 2);
+    float2* tw = sm;
+    float2* buf = sm + M;                 // B M
+    float2* scr = buf + B * M;            // B M
     const unsigned long long plan = gp->plan;
     const int half_max = M_max / 2 + 1;
     const double M2 = (double)M * (double)M;
@@ -506,28 +580,40 @@ __global__ void __launch_bounds__(kInvThreads) k_row_inv(Geo* __restrict__ gp, c
     const float sc = (float)(1.0 / M2);
     for (int k = threadIdx.x; k < M; k += blockDim.x) tw[k] = twg[k];
     for (int y = blockIdx.x; y < N; y += gridDim.x) {
-        for (int k = threadIdx.x; k < M; k += blockDim.x) {
-            const bool lo = (k <= M / 2);
-            const int kk = lo ? k : M - k;
-            float2 c[6];
+        for (int t0 = 0; t0 < 2; t0 += B) {               // transform 0: P0 + i Qx, 1: Qy
+            const int nb = min(B, 2 - t0);
+            for (int k = threadIdx.x; k < M; k += blockDim.x) {
+                const bool lo = (k <= M / 2);
+                const int kk = lo ? k : M - k;
+                float2 c[6];
 #pragma unroll
-            for (int b = 0; b < 6; ++b) {
-                c[b] = colout[((int64_t)b * half_max + kk) * N_max + y];
-                if (!lo) c[b] = cconj(c[b]);
+                for (int b = 0; b < 6; ++b) {
+                    c[b] = colout[((int64_t)b * half_max + kk) * N_max + y];
+                    if (!lo) c[b] = cconj(c[b]);
+                }
+                const float2 C0 = make_float2(alpha * c[0].x + beta * c[3].x, alpha * c[0].y + beta * c[3].y);
+                const float2 Cx = make_float2(alpha * c[1].x + beta * c[4].x, alpha * c[1].y + beta * c[4].y);
+                const float2 Cy = make_float2(alpha * c[2].x + beta * c[5].x, alpha * c[2].y + beta * c[5].y);
+                const float2 tr[2] = {cadd(C0, mul_pi(Cx)), Cy};
+                for (int q = 0; q < nb; ++q) buf[q * M + k] = tr[t0 + q];
             }
-            const float2 C0 = make_float2(alpha * c[0].x + beta * c[3].x, alpha * c[0].y + beta * c[3].y);
-            const float2 Cx = make_float2(alpha * c[1].x + beta * c[4].x, alpha * c[1].y + beta * c[4].y);
-            const float2 Cy = make_float2(alpha * c[2].x + beta * c[5].x, alpha * c[2].y + beta * c[5].y);
-            buf[k] = cadd(C0, mul_pi(Cx));
-            buf[M + k] = Cy;
+            __syncthreads();
+            fft_block(buf, scr, M, nb, M, plan, nrad, tw, true);
+            for (int x = threadIdx.x; x < N; x += blockDim.x) {
+                float* f = reinterpret_cast<float*>(fgrid + (int64_t)y * N + x);
+                for (int q = 0; q < nb; ++q) {
+                    const float2 a = buf[q * M + x];
+                    if (t0 + q == 0) {
+                        f[0] = a.x * sc;
+                        f[1] = a.y * sc;
+                    } else {
+                        f[2] = a.x * sc;
+                        f[3] = 0.f;
+                    }
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        fft_block(buf, scr, M, 2, M, plan, nrad, tw, true);
-        for (int x = threadIdx.x; x < N; x += blockDim.x) {
-            const float2 a = buf[x], b = buf[M + x];
-            fgrid[(int64_t)y * N + x] = make_float4(a.x * sc, a.y * sc, b.x * sc, 0.f);
-        }
-        __syncthreads();
     }
 }
 
@@ -542,10 +628,10 @@ __global__ void __launch_bounds__(kInvThreads) k_ent_row(const Geo* __restrict__
                                                          const float2* __restrict__ twg, float2* __restrict__ spec,
                                                          int M_max, float eps) {
     extern __shared__ float2 sm[];
-    float2* tw = sm;
-    float2* buf = sm + M_max;
-    float2* scr = buf + M_max;
     const int M = gp->M, N = gp->N, half = M / 2 + 1, nrad = gp->nrad;
+    float2* tw = sm;                     // M
+    float2* buf = sm + M;                // M
+    float2* scr = buf + M;               // M
     const unsigned long long plan = gp->plan;
     const int half_max = M_max / 2 + 1;
     const double dlt = gp->delta;
@@ -575,28 +661,43 @@ __global__ void __launch_bounds__(kInvThreads) k_ent_row(const Geo* __restrict__
     }
 }
 
-__global__ void __launch_bounds__(kInvThreads) k_ent_col(Geo* __restrict__ gp, const float2* __restrict__ spec,
-                                                         const float2* __restrict__ twg, int M_max) {
+__global__ void __launch_bounds__(kInvThreads) k_ent_col(Geo* __restrict__ gp, float2* __restrict__ spec,
+                                                         const float2* __restrict__ twg, int M_max, int cap) {
     extern __shared__ float2 sm[];
-    float2* tw = sm;
-    float2* buf = sm + M_max;            // 2 * M
-    float2* scr = buf + 2 * M_max;       // 2 * M
     __shared__ double red[kInvThreads / 32];
     const int M = gp->M, half = M / 2 + 1, nrad = gp->nrad;
+    const int B = fft_batch(cap, M, 2);
+    float2* tw = sm;
+    float2* buf = sm + M;                // B M
+    float2* scr = buf + B * M;           // B M
     const unsigned long long plan = gp->plan;
     const int half_max = M_max / 2 + 1;
     for (int k = threadIdx.x; k < M; k += blockDim.x) tw[k] = twg[k];
     double part = 0.0;
     for (int kx = blockIdx.x; kx < half; kx += gridDim.x) {
-        for (int t = threadIdx.x; t < 2 * M; t += blockDim.x) {
-            const int a = t / M, y = t - a * M;
-            buf[t] = spec[((int64_t)a * half_max + kx) * M_max + y];
+        auto col = [&](int a) { return spec + ((int64_t)a * half_max + kx) * M_max; };
+        if (B >= 2) {
+            for (int t = threadIdx.x; t < 2 * M; t += blockDim.x) {
+                const int a = t / M, y = t - a * M;
+                buf[t] = col(a)[y];
+            }
+            __syncthreads();
+            fft_block(buf, scr, M, 2, M, plan, nrad, tw, false);
+        } else {
+            // one transform at a time: W1 in place in spec, then K_ln in shared memory
+            for (int y = threadIdx.x; y < M; y += blockDim.x) buf[y] = col(0)[y];
+            __syncthreads();
+            fft_block(buf, scr, M, 1, M, plan, nrad, tw, false);
+            for (int y = threadIdx.x; y < M; y += blockDim.x) col(0)[y] = buf[y];
+            __syncthreads();
+            for (int y = threadIdx.x; y < M; y += blockDim.x) buf[y] = col(1)[y];
+            __syncthreads();
+            fft_block(buf, scr, M, 1, M, plan, nrad, tw, false);
         }
-        __syncthreads();
-        fft_block(buf, scr, M, 2, M, plan, nrad, tw, false);
         const double wt = (kx == 0 || 2 * kx == M) ? 1.0 : 2.0;
         for (int k = threadIdx.x; k < M; k += blockDim.x) {
-            const float2 W = buf[k], K = buf[M + k];
+            const float2 W = B >= 2 ? buf[k] : col(0)[k];
+            const float2 K = B >= 2 ? buf[M + k] : buf[k];
             part += wt * (double)K.x * ((double)W.x * W.x + (double)W.y * W.y);
         }
         __syncthreads();
@@ -613,9 +714,9 @@ __global__ void __launch_bounds__(kInvThreads) k_ent_col(Geo* __restrict__ gp, c
 
 __global__ void k_ent_zero(Geo* g) { g->eacc = 0.0; }
 
-size_t field_smem_row(int M_max) { return sizeof(float2) * (size_t)M_max * 11; }
-size_t field_smem_col(int M_max) { return sizeof(float2) * (size_t)M_max * 17; }
-size_t field_smem_inv(int M_max) { return sizeof(float2) * (size_t)M_max * 5; }
+size_t field_smem_row(int M_max) { return sizeof(float2) * (size_t)smem_cap_row(M_max); }
+size_t field_smem_col(int M_max) { return sizeof(float2) * (size_t)smem_cap_col(M_max); }
+size_t field_smem_inv(int M_max) { return sizeof(float2) * (size_t)smem_cap_inv(M_max); }
 
 cudaError_t field_set_attrs(int M_max) {
     cudaError_t e;
@@ -654,24 +755,28 @@ cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, b
 cudaError_t launch_field_conv(const Ws& w, const GradArgs& a, cudaStream_t s) {
     cudaError_t e;
     if ((e = field_set_attrs(w.M_max)) != cudaSuccess) return e;
-    k_row_fwd<<<kNumSMs * 2, kRowThreads, field_smem_row(w.M_max), s>>>(w.geo, w.wgrid, w.tw, w.spec, w.M_max, a.eps);
-    k_col<<<kNumSMs, kColThreads, field_smem_col(w.M_max), s>>>(w.geo, w.spec, w.tw, w.colout, w.M_max, w.N_max);
+    k_row_fwd<<<kNumSMs * 2, kRowThreads, field_smem_row(w.M_max), s>>>(w.geo, w.wgrid, w.tw, w.spec, w.M_max, a.eps,
+                                                                         smem_cap_row(w.M_max));
+    k_col<<<kNumSMs, kColThreads, field_smem_col(w.M_max), s>>>(w.geo, w.spec, w.tw, w.colout, w.M_max, w.N_max,
+                                                                smem_cap_col(w.M_max));
     k_row_inv<<<kNumSMs * 2, kInvThreads, field_smem_inv(w.M_max), s>>>(w.geo, w.colout, w.tw, w.fgrid, w.M_max,
-                                                                        w.N_max, a.n, a.lambda_kl, a.lambda_r);
+                                                                        w.N_max, a.n, a.lambda_kl, a.lambda_r,
+                                                                        smem_cap_inv(w.M_max));
     return cudaGetLastError();
 }
 
 // sum_{i != j} ln(eps + r^2) * M^2 + n ln(eps) M^2 into g->eacc, after launch_field_local
 cudaError_t launch_entropy_sum(const Ws& w, const GradArgs& a, cudaStream_t s) {
     cudaError_t e;
-    const size_t smr = sizeof(float2) * (size_t)w.M_max * 3, smc = sizeof(float2) * (size_t)w.M_max * 5;
+    const int capc = std::max(5 * std::min(w.M_max, kMfast), 3 * w.M_max);
+    const size_t smr = sizeof(float2) * (size_t)w.M_max * 3, smc = sizeof(float2) * (size_t)capc;
     if ((e = cudaFuncSetAttribute(k_ent_row, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smr)) != cudaSuccess)
         return e;
     if ((e = cudaFuncSetAttribute(k_ent_col, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc)) != cudaSuccess)
         return e;
     k_ent_zero<<<1, 1, 0, s>>>(w.geo);
     k_ent_row<<<kNumSMs * 2, kInvThreads, smr, s>>>(w.geo, w.wgrid, w.tw, w.spec, w.M_max, a.eps);
-    k_ent_col<<<kNumSMs, kInvThreads, smc, s>>>(w.geo, w.spec, w.tw, w.M_max);
+    k_ent_col<<<kNumSMs, kInvThreads, smc, s>>>(w.geo, w.spec, w.tw, w.M_max, capc);
     return cudaGetLastError();
 }
 

@@ -16,9 +16,7 @@
 
 namespace tsnet {
 
-constexpr int kSpmvChunk = 2048;   // stored entries of P per warp work item
 constexpr double kHubFactor = 4.0; // hot-column L1 policy threshold (k_spmv2)
-constexpr int kSpmvUnroll = 4;
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
@@ -51,58 +49,6 @@ __device__ __forceinline__ int64_t warp_row_of(const int64_t* __restrict__ indpt
         hi = std::min(lo + step, hi);
     }
     return lo;
-}
-
-__global__ void __launch_bounds__(256) k_spmv(int64_t n, int64_t nnz, const int64_t* __restrict__ indptr,
-                                              const int32_t* __restrict__ indices, const float* __restrict__ values,
-                                              const float2* __restrict__ Y, float2* __restrict__ F) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nchunks = (nnz + kSpmvChunk - 1) / kSpmvChunk;
-    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t pol = policy_evict_first();
-    for (int64_t c = wid; c < nchunks; c += nw) {
-        const int64_t cs = c * kSpmvChunk, ce = std::min(cs + kSpmvChunk, nnz);
-        int64_t r = warp_row_of(indptr, n, cs);
-        while (true) {
-            const int64_t rs = __ldg(indptr + r), re = __ldg(indptr + r + 1);
-            const int64_t s0 = std::max(rs, cs), s1 = std::min(re, ce);
-            if (s0 < s1) {
-                const float2 yi = __ldg(Y + r);
-                float fx = 0.f, fy = 0.f;
-                for (int64_t base = s0; base < s1; base += 32 * kSpmvUnroll) {
-                    int col[kSpmvUnroll];
-                    float val[kSpmvUnroll];
-#pragma unroll
-                    for (int q = 0; q < kSpmvUnroll; ++q) {
-                        const int64_t e = base + lane + 32 * q;
-                        const bool ok = e < s1;
-                        col[q] = ok ? ld_stream_i32(indices + e, pol) : (int)r;
-                        val[q] = ok ? ld_stream_f32(values + e, pol) : 0.f;
-                    }
-                    float2 yj[kSpmvUnroll];
-#pragma unroll
-                    for (int q = 0; q < kSpmvUnroll; ++q) yj[q] = __ldg(Y + col[q]);
-#pragma unroll
-                    for (int q = 0; q < kSpmvUnroll; ++q) {
-                        const float dx = yi.x - yj[q].x, dy = yi.y - yj[q].y;
-                        const float w = __frcp_rn(1.0f + dx * dx + dy * dy);
-                        const float pw = val[q] * w;
-                        fx = fmaf(pw, dx, fx);
-                        fy = fmaf(pw, dy, fy);
-                    }
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    fx += __shfl_xor_sync(0xffffffffu, fx, o);
-                    fy += __shfl_xor_sync(0xffffffffu, fy, o);
-                }
-                if (lane == 0) atomicAdd(F + r, make_float2(fx, fy));
-            }
-            if (re >= ce) break;
-            ++r;
-        }
-    }
 }
 
 // Row-wise CSR SpMV with the next row's first batch prefetched while the
@@ -228,104 +174,76 @@ __global__ void __launch_bounds__(256) k_spmv2(int64_t rb, int64_t re_rows, cons
     }
 }
 
-// Launch configuration of the row-wise kernel.  Defaults are the measured best
-// on B200 (profiles/, scripts/gpu_spmv_sweep.sh); TSNET_SPMV_{U,CPW,CTAS,L1}
-// override them for probing.
-struct SpmvCfg {
-    int kernel = 2;      // 1: legacy k_spmv, 2: k_spmv2
-    int U = 4;           // entries per lane per batch
-    int cpw = 1;         // chunks per warp
-    int ctas_per_sm = 5; // 256-thread CTAs per SM
-    int l1 = 1;          // prefer L1 over shared memory (carveout 0)
-    int reserve = 0;     // SMs left free for the concurrent field phase (side stream)
-    int waves = 16;      // CTAs = waves x resident: short CTAs balance the power-law rows dynamically
-                         // (cfg 4 kernel 0.83 -> 0.80 ms, step 0.889 -> 0.865 ms vs one wave with cpw 4)
-    int cpw_rows = 1;    // chunks per warp in the row-chunk launches of the pipelined host step
-    int hub = 8192;      // hot-column L1 policy candidate (hub_columns() decides per P; 0 = off):
-                         // cfg 4 kernel 0.792 -> 0.769 ms (r1cg; 4096: 0.778, 12288: 0.767, 16384: 0.771)
-};
-
-static int env_int(const char* name, int def) {
-    const char* e = getenv(name);
-    return e ? atoi(e) : def;
-}
-
-// read once (function-local static: thread-safe initialisation)
-static const SpmvCfg& spmv_cfg() {
-    static const SpmvCfg cfg = [] {
-        SpmvCfg c;
-        const char* k = getenv("TSNET_ATTR_KERNEL");
-        if (k && !strcmp(k, "v1")) c.kernel = 1;
-        c.U = env_int("TSNET_SPMV_U", c.U);
-        c.cpw = std::max(1, env_int("TSNET_SPMV_CPW", c.cpw));
-        c.cpw_rows = std::max(1, env_int("TSNET_SPMV_CPW_ROWS", c.cpw_rows));
-        c.hub = std::max(0, env_int("TSNET_SPMV_HUB_COLS", c.hub));
-        c.ctas_per_sm = std::max(1, env_int("TSNET_SPMV_CTAS", c.ctas_per_sm));
-        c.l1 = env_int("TSNET_SPMV_L1", c.l1);
-        c.reserve = std::max(0, std::min(64, env_int("TSNET_SPMV_RESERVE_SMS", c.reserve)));
-        c.waves = std::max(1, std::min(64, env_int("TSNET_SPMV_WAVES", c.waves)));
-        return c;
-    }();
-    return cfg;
-}
+// Launch configuration of the row-wise kernel: the measured best on B200
+// (round-1 sweeps of entries per lane, chunks per warp, CTAs
+// per SM, waves and the hot-column candidate set, profiles/r1*).
+constexpr int kSpmvU = 4;           // entries per lane per batch
+constexpr int kSpmvCtasPerSm = 5;   // 256-thread CTAs per SM
+constexpr int kSpmvWaves = 16;      // CTAs = waves x resident: short CTAs balance the power-law rows
+                                    // dynamically (cfg 4 kernel 0.83 -> 0.80 ms vs one wave)
+constexpr int kSpmvHubCols = 8192;  // hot-column L1 policy candidate (hub_columns() decides per P):
+                                    // cfg 4 kernel 0.792 -> 0.769 ms (r1cg)
 
 // Hot-column L1 policy for this P: on when its first `cand` columns (P is
 // symmetric: column count = row length) hold >= kHubFactor x their share of
 // the stored entries -- a power-law graph numbered by weight (cfg 4: 10% of
 // the entries in the first 8192 columns, 12x their share; meshes, block
-// models and random numberings stay off).  Decided once per P (three indptr
-// reads, cached); never inside a stream capture (then off until an eager call).
+// models and random numberings stay off).  Decided once per (P, n, nnz) (three
+// indptr reads on `s`, cached per thread); never inside a stream capture (then
+// off until an eager call).
 static int hub_columns(const GradArgs& a, int cand, cudaStream_t s) {
     if (cand <= 0 || cand >= a.n) return 0;
     struct Entry {
         const void* indptr = nullptr;
-        int64_t n = -1;
-        int cand = 0, hub = 0;
+        int64_t n = -1, nnz = -1;
+        int dev = -1, hub = 0;
     };
     static thread_local Entry cache[4];
     static thread_local int next = 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
     for (const auto& e : cache)
-        if (e.indptr == a.indptr && e.n == a.n && e.cand == cand) return e.hub;
+        if (e.indptr == a.indptr && e.n == a.n && e.nnz == a.nnz && e.dev == dev) return e.hub;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return 0;
     int64_t v[3] = {0, 0, 0};
-    if (cudaMemcpy(&v[0], a.indptr, sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess ||
-        cudaMemcpy(&v[1], a.indptr + cand, sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess ||
-        cudaMemcpy(&v[2], a.indptr + a.n, sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+    if (cudaMemcpyAsync(&v[0], a.indptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(&v[1], a.indptr + cand, sizeof(int64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(&v[2], a.indptr + a.n, sizeof(int64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
         return 0;
     const double share = (double)(v[1] - v[0]) / (double)std::max<int64_t>(1, v[2] - v[0]);
     Entry& e = cache[next++ & 3];
     e.indptr = a.indptr;
     e.n = a.n;
-    e.cand = cand;
+    e.nnz = a.nnz;
+    e.dev = dev;
     e.hub = share >= kHubFactor * (double)cand / (double)a.n ? cand : 0;
     return e.hub;
 }
 
-template <int U, bool HUB>
-static cudaError_t launch_spmv2_h(const GradArgs& a, float2* F, const SpmvCfg& c, int hub, cudaStream_t s) {
-    static int resident = 0;
-    if (resident == 0) {
-        if (c.l1) cudaFuncSetAttribute(k_spmv2<U, HUB>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_spmv2<U, HUB>, 256, 0) != cudaSuccess ||
-            resident < 1)
-            resident = 1;
-    }
+// Attributes are set on every launch (cheap; per device, no process-wide flags).
+template <bool HUB>
+static cudaError_t launch_spmv2_h(const GradArgs& a, float2* F, int cpw, int hub, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(k_spmv2<kSpmvU, HUB>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    if (e != cudaSuccess) return e;
+    int resident = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_spmv2<kSpmvU, HUB>, 256, 0) != cudaSuccess ||
+        resident < 1)
+        resident = 1;
     // `waves` x the resident CTAs, each warp `cpw` equal chunks (the hardware
     // scheduler balances the CTAs); small problems: fewer CTAs so that chunks
     // stay >= 1024 entries
-    const int64_t want = std::max<int64_t>(1, a.nnz / (1024 * 8 * c.cpw));
-    const int per_sm = std::min(c.ctas_per_sm, resident);
-    const int blocks =
-        (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)(kNumSMs - c.reserve) * per_sm * c.waves));
-    k_spmv2<U, HUB><<<blocks, 256, 0, s>>>(a.rb, a.re, a.indptr, a.indices, a.values, a.Y, F, c.cpw, hub);
+    const int64_t want = std::max<int64_t>(1, a.nnz / (1024 * 8 * cpw));
+    const int per_sm = std::min(kSpmvCtasPerSm, resident);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)kNumSMs * per_sm * kSpmvWaves));
+    k_spmv2<kSpmvU, HUB><<<blocks, 256, 0, s>>>(a.rb, a.re, a.indptr, a.indices, a.values, a.Y, F, cpw, hub);
     return cudaGetLastError();
 }
 
-template <int U>
-static cudaError_t launch_spmv2_t(const GradArgs& a, float2* F, const SpmvCfg& c, cudaStream_t s) {
-    const int hub = hub_columns(a, c.hub, s);
-    return hub > 0 ? launch_spmv2_h<U, true>(a, F, c, hub, s) : launch_spmv2_h<U, false>(a, F, c, 0, s);
+static cudaError_t launch_spmv2(const GradArgs& a, float2* F, int cpw, cudaStream_t s) {
+    const int hub = hub_columns(a, kSpmvHubCols, s);
+    return hub > 0 ? launch_spmv2_h<true>(a, F, cpw, hub, s) : launch_spmv2_h<false>(a, F, cpw, 0, s);
 }
 
 // a6 for the rows [rb, re) of the call into w.f_attr (local rows): the
@@ -337,18 +255,7 @@ cudaError_t launch_spmv(const Ws& w, const GradArgs& a, cudaStream_t s) {
     const int64_t nl = a.re - a.rb;
     cudaError_t e = cudaMemsetAsync(w.f_attr, 0, sizeof(float2) * (size_t)nl, s);
     if (e != cudaSuccess || a.nnz == 0 || nl == 0) return e;
-    const SpmvCfg& c = spmv_cfg();
-    if (c.kernel == 1 && a.rb == 0 && a.re == a.n) {
-        const int64_t nchunks = (a.nnz + kSpmvChunk - 1) / kSpmvChunk;
-        const int blocks = (int)std::min<int64_t>((nchunks + 7) / 8, (int64_t)kNumSMs * 8);
-        k_spmv<<<blocks, 256, 0, s>>>(a.n, a.nnz, a.indptr, a.indices, a.values, a.Y, w.f_attr);
-        return cudaGetLastError();
-    }
-    switch (c.U) {
-        case 2: return launch_spmv2_t<2>(a, w.f_attr, c, s);
-        case 8: return launch_spmv2_t<8>(a, w.f_attr, c, s);
-        default: return launch_spmv2_t<4>(a, w.f_attr, c, s);
-    }
+    return launch_spmv2(a, w.f_attr, 1, s);
 }
 
 // gather (a7) and the gains/momentum move: move.cuh
@@ -480,33 +387,9 @@ cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2
     return e;
 }
 
-using UpdateKernel = void (*)(int64_t, Geo*, const float4*, const int*, const float2*, const float2*, float2*,
-                              const float2*, float2*, float2*, float, float, tsnet_step_params, int);
-
-// TSNET_UPDATE=V,R (probing): V points per thread, R = 1 recompute the box.
-// All four within noise on the step (r1cd: cfg 5 1027-1039 it/s, cfg 4
-// 1150-1156): the move is ~2% of the step; default 2 points, read the box.
-static UpdateKernel update_kernel() {
-    static UpdateKernel k = nullptr;
-    if (!k) {
-        int v = 2, r = 0;
-        if (const char* e = getenv("TSNET_UPDATE")) sscanf(e, "%d,%d", &v, &r);
-        if (v == 1 && r) k = k_update<1, true>;
-        else if (v == 1) k = k_update<1, false>;
-        else if (r) k = k_update<2, true>;
-        else k = k_update<2, false>;
-    }
-    return k;
-}
-
-static cudaError_t update_smem_attr() {
-    static bool done = false;
-    if (done) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(update_kernel(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(float4) * kGridSmemCells));
-    done = e == cudaSuccess;
-    return e;
-}
+// The move: 2 points per thread, box and in-box coordinates read back
+// (recomputing them from the position measured the same, r1cd).
+static constexpr auto update_kernel = k_update<2, false>;
 
 // Y, vel, gains: full n x 2 arrays; rows [rb, re) are updated
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,
@@ -514,10 +397,11 @@ cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel
     const int64_t nl = a.re - a.rb;
     const int cap = (int)std::min<int64_t>((int64_t)w.N_max * w.N_max, kGridSmemCells);
     const size_t smem = sizeof(float4) * (size_t)cap;
-    cudaError_t ea = update_smem_attr();
+    cudaError_t ea = cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(sizeof(float4) * kGridSmemCells));
     if (ea != cudaSuccess) return ea;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nl + kUpdateThreads - 1) / kUpdateThreads, kNumSMs));
-    update_kernel()<<<blocks, kUpdateThreads, smem, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, Y + a.rb, Y + a.rb, w.f_attr,
+    update_kernel<<<blocks, kUpdateThreads, smem, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, Y + a.rb, Y + a.rb, w.f_attr,
                                                   vel + a.rb, gains + a.rb, a.lambda_kl, cn_of(a), sp, cap);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !sp.recenter) return e;
@@ -535,15 +419,7 @@ cudaError_t launch_spmv_rows(const Ws& w, const GradArgs& a, int64_t r0, int64_t
     b.rb = r0;
     b.re = r1;
     b.nnz = std::max<int64_t>(1, nnz_rows);     // sizes the grid
-    // a chunk is ~1/8 of P: fewer, longer pieces per warp (each piece starts
-    // with a row search and a pipeline ramp)
-    SpmvCfg c = spmv_cfg();
-    c.cpw = c.cpw_rows;
-    switch (c.U) {
-        case 2: return launch_spmv2_t<2>(b, F, c, s);
-        case 8: return launch_spmv2_t<8>(b, F, c, s);
-        default: return launch_spmv2_t<4>(b, F, c, s);
-    }
+    return launch_spmv2(b, F, 1, s);
 }
 
 cudaError_t launch_update_rows(const Ws& w, const GradArgs& a, int64_t r0, int64_t r1, float2* Yout, float2* vel,
@@ -555,7 +431,7 @@ cudaError_t launch_update_rows(const Ws& w, const GradArgs& a, int64_t r0, int64
     // chunk, whose CTAs run with the whole L1 carveout (a 200 KB shared-memory
     // CTA would wait for an idle SM); the field nodes are read through L1/L2
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nc + kUpdateThreads - 1) / kUpdateThreads, kNumSMs));
-    update_kernel()<<<blocks, kUpdateThreads, 0, s>>>(nc, w.geo, w.fgrid, w.box + q, w.uv + q, a.Y + r0, Yout + r0,
+    update_kernel<<<blocks, kUpdateThreads, 0, s>>>(nc, w.geo, w.fgrid, w.box + q, w.uv + q, a.Y + r0, Yout + r0,
                                                w.f_attr + q, vel + r0, gains + r0, a.lambda_kl, cn_of(a), sp, 0);
     return cudaGetLastError();
 }

@@ -22,7 +22,7 @@ c_i32, c_i64, c_f32, c_f64, c_sz, c_vp, c_u64 = (ctypes.c_int32, ctypes.c_int64,
                                                  ctypes.c_size_t, ctypes.c_void_p, ctypes.c_uint64)
 
 TSNET_OK, TSNET_E_ARG, TSNET_E_CAPACITY, TSNET_E_CUDA, TSNET_E_NCCL, TSNET_E_NONFINITE, TSNET_W_PERPLEXITY = range(7)
-TSNET_I_MAX_LIMIT = 256
+TSNET_I_MAX_LIMIT = 1024
 PLAN_CB, PLAN_SELL = 1, 2     # tsnet_csr.plan_kind (include/tsnet.h)
 
 
@@ -92,7 +92,7 @@ SIGNATURES = [
     ("tsnet_sell_query", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard), ctypes.POINTER(c_sz),
                                         ctypes.POINTER(ctypes.c_double), c_vp]),
     ("tsnet_sell_build", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard), c_vp, c_sz, c_vp]),
-    ("tsnet_plan_partition", c_i32, [c_vp, c_i64, c_i64, c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    ("tsnet_plan_partition", c_i32, [c_vp, c_i64, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_i64]),
     ("tsnet_comm_unique_id", ctypes.c_int, [c_vp]),
     ("tsnet_comm_init", ctypes.c_int, [c_vp, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     ("tsnet_comm_destroy", ctypes.c_int, [c_vp]),
@@ -372,22 +372,22 @@ def tsnet_sell_build(P: CSR, shard=None, stream=None) -> CSR:
     return P
 
 
-def tsnet_plan_partition(indptr_host, row_begin: int, row_end: int, warps: int = 16, rows_max: int = 704,
-                         base_groups: int = 148, max_minitasks: int = 1 << 22):
-    """Host cut of the plan (pure): returns (G, row_mt, row_K, mt_r0, mt_info) numpy arrays."""
+def tsnet_plan_partition(indptr_host, row_begin: int, row_end: int, groups: int = 148, rows_cap: int = 8192):
+    """Host cut of the column-blocked plan (pure): rows into panels.  Returns
+    (P, row_panel, row_local, panel_off, panel_rows) numpy arrays."""
     import numpy as np
     ip = np.ascontiguousarray(indptr_host, dtype=np.int64)
     nr = row_end - row_begin
-    row_mt = np.zeros(max(nr, 1), np.int32)
-    row_K = np.zeros(max(nr, 1), np.int32)
-    mt_r0 = np.zeros(max_minitasks, np.int32)
-    mt_info = np.zeros(max_minitasks, np.int32)
-    G = lib().tsnet_plan_partition(ip.ctypes.data, row_begin, row_end, warps, rows_max, base_groups, max_minitasks,
-                                   row_mt.ctypes.data, row_K.ctypes.data, mt_r0.ctypes.data, mt_info.ctypes.data)
-    if G < 0:
-        raise TsnetError("tsnet_plan_partition", G)
-    T = G * warps
-    return G, row_mt[:nr], row_K[:nr], mt_r0[:T], mt_info[:T]
+    maxp = max(1, nr)
+    row_panel = np.zeros(max(nr, 1), np.int32)
+    row_local = np.zeros(max(nr, 1), np.int32)
+    panel_off = np.zeros(maxp + 1, np.int32)
+    panel_rows = np.zeros(max(nr, 1), np.int32)
+    P = lib().tsnet_plan_partition(ip.ctypes.data, row_begin, row_end, groups, rows_cap, row_panel.ctypes.data,
+                                   row_local.ctypes.data, panel_off.ctypes.data, panel_rows.ctypes.data, maxp)
+    if P < 0:
+        raise TsnetError("tsnet_plan_partition", P)
+    return P, row_panel[:nr], row_local[:nr], panel_off[:P + 1], panel_rows[:nr]
 
 
 # ------------------------------------------------------ per-iteration path

@@ -41,19 +41,20 @@ def term_scale(r, Y, lam):
             + np.linalg.norm(lr * r["g_ent"]) + np.linalg.norm(lc / n * np.asarray(Y, np.float64)))
 
 
-def assert_grad_close(g, r, Y, lam, tol=GRAD_TOL):
-    """relL2(g, g_oracle) <= tol, the north-star bar.  Exception (DESIGN.md §8,
-    "conditioning"): where the exact gradient is a cancellation residual smaller
-    than 1e-3 of the terms it is assembled from (a machine-precision equilibrium,
-    e.g. p_ij = q_ij), an fp32 pipeline cannot resolve it; there the error must
-    stay within tol * 1e-2 of the term scale, i.e. at fp32 round-off of the terms."""
+def assert_grad_close(g, r, Y, lam, tol=GRAD_TOL, conditioned=False):
+    """relL2(g, g_oracle) <= tol, the north-star bar.  `conditioned` (only the
+    cases listed in tests/parity_cases.py, reading R28 of DESIGN.md, each with its
+    measured ||g|| / scale): the gradient is a cancellation residual far below the
+    terms, and the error is bounded by fp32 round-off of the terms instead,
+    err <= 1e-2 tol * scale."""
     err = np.linalg.norm(np.asarray(g, np.float64) - r["g"])
     gn = np.linalg.norm(r["g"])
-    scale = term_scale(r, Y, lam)
-    if gn >= 1e-3 * scale:
-        assert err <= tol * gn, f"relL2 {err / gn:.3e} > {tol}"
+    if conditioned:
+        scale = term_scale(r, Y, lam)
+        assert gn < 1e-3 * scale, "listed as conditioned but is not"
+        assert err <= 1e-2 * tol * scale, f"conditioned case: err/scale {err / scale:.3e}"
     else:
-        assert err <= 1e-2 * tol * scale, f"ill-conditioned case: err/scale {err / scale:.3e}"
+        assert err <= tol * gn, f"relL2 {err / gn:.3e} > {tol}"
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -187,7 +188,7 @@ def gpu_grad(P_dev, Y32, gp):
     return g.cpu().numpy(), float(Z.item()), fa.cpu().numpy(), ff.cpu().numpy(), st
 
 
-def oracle_grad(P, Y32, lam, h_max=0.25, I_min=20, I_max=256):
+def oracle_grad(P, Y32, lam, h_max=0.25, I_min=20, I_max=1024):
     return oracle.interp_gradient(Y32.astype(np.float64), P["indptr"], P["indices"], p32(P), *lam, eps=0.05,
                                   h_max=h_max, I_min=I_min, I_max=I_max)
 
@@ -266,26 +267,63 @@ def test_grad_parity_synthetic_layouts(cfg, lay, lam):
     assert relL2(g, r["g"]) <= GRAD_TOL, relL2(g, r["g"])
 
 
+def gpu_terms(P_dev, Y32):
+    """The GPU's own F_rep and g_ent: f_field with (lkl, lr) = (1, 0) is -4 F_rep,
+    with (0, 1) it is g_ent (tsnet_grad_parts)."""
+    ws = alloc_workspace(P_dev.n, P_dev.nnz, GradParams())
+    Yd = torch.from_numpy(Y32).cuda()
+    _, ff_rep, _ = tsnet_grad_parts(P_dev, Yd, GradParams(1.0, 0.0, 0.0), ws)
+    _, ff_ent, _ = tsnet_grad_parts(P_dev, Yd, GradParams(0.0, 0.0, 1.0), ws)
+    torch.cuda.synchronize()
+    return -ff_rep.cpu().numpy().astype(np.float64) / 4.0, ff_ent.cpu().numpy().astype(np.float64)
+
+
+def exact_terms(P, Y64):
+    """Exact (O4a) F_attr - F_rep and g_ent: the exact gradient with (lkl, lc, lr)
+    = (1, 0, 0) is 4 (F_attr - F_rep), with (0, 0, 1) it is g_ent."""
+    gkl, _ = oracle.exact_grad(Y64, P["indptr"], P["indices"], p32(P), 1.0, 0.0, 0.0)
+    gen, _ = oracle.exact_grad(Y64, P["indptr"], P["indices"], p32(P), 0.0, 0.0, 1.0)
+    F_attr = oracle.attr_sparse(Y64, P["indptr"], P["indices"], p32(P))
+    return F_attr - gkl / 4.0, gen
+
+
 @pytest.mark.parametrize("cfg", [1, 2])
 def test_grad_parity_oracle_trajectory(cfg):
     """Stage-A end (249), mid stage-B expansion (260) and converged stage-B (499)
-    layouts of the oracle's own run."""
+    layouts of the oracle's own run, both multiplier sets.  Per term at every
+    layout: F_attr <= 1e-5, f_field <= 1e-4, Z <= 1e-5 against the oracle's
+    parts; the GPU's F_rep and g_ent <= 2e-2 against the exact ones.  Total:
+    <= 1e-4 relL2 against the oracle and (stage B) <= 2e-2 against the exact
+    gradient, except the two cancellation cases of reading R28
+    (tests/parity_cases.py), bounded against the term scale instead."""
+    from parity_cases import CONDITIONED
     if cfg == 2:
         pytest.importorskip("scipy")
     P = oracle_P(cfg)
+    Pd = dev_P(P)
     for it, (Y, _, _) in sorted(oracle_layouts(cfg, TRAJ_ITERS).items()):
+        Y64 = Y.astype(np.float64)
+        Frep_ex, gent_ex = exact_terms(P, Y64)
+        Frep_g, gent_g = gpu_terms(Pd, Y)
+        assert relL2(Frep_g, Frep_ex) <= EXACT_TOL, (it, relL2(Frep_g, Frep_ex))
+        assert relL2(gent_g, gent_ex) <= EXACT_TOL, (it, relL2(gent_g, gent_ex))
         for lam in (STAGE_A, STAGE_B):
-            g, Z, _, _, st = gpu_grad(dev_P(P), Y, GradParams(*lam))
+            g, Z, fa, ff, st = gpu_grad(Pd, Y, GradParams(*lam))
             r = oracle_grad(P, Y, lam)
-            assert_grad_close(g, r, Y, lam)
+            lkl, lc, lr = lam
+            ff_o = -4.0 * lkl * r["F_rep"] + lr * r["g_ent"]
+            assert relL2(fa, r["F_attr"]) <= 1e-5, (it, lam, relL2(fa, r["F_attr"]))
+            assert relL2(ff, ff_o) <= GRAD_TOL, (it, lam, relL2(ff, ff_o))
+            assert abs(Z - r["Z"]) <= 1e-5 * r["Z"], (it, lam, Z, r["Z"])
+            cond = (cfg, it, lam) in CONDITIONED
+            assert_grad_close(g, r, Y, lam, conditioned=cond)
             if lam != STAGE_B:
                 continue
-            # interpolation vs the exact O(n^2) gradient (n <= 20k), stage-B multipliers.
-            ge, _ = oracle.exact_grad(Y.astype(np.float64), P["indptr"], P["indices"], p32(P), *lam)
-            if it == 499:
-                # 499 is an equilibrium of the INTERPOLATED dynamics: there g_interp ~ 0 by
-                # construction and relL2 vs exact is ~1 whatever h is (DESIGN.md §2, R18).
-                # The interpolation error is graded against the size of the terms instead.
+            # interpolation vs the exact O(n^2) gradient (n <= 20k), stage-B multipliers
+            ge, _ = oracle.exact_grad(Y64, P["indptr"], P["indices"], p32(P), *lam)
+            if cond:
+                # R28: the exact gradient is itself a residual of the same size as
+                # the terms' interpolation error (R18 restricted to this case)
                 err = np.linalg.norm(np.asarray(g, np.float64) - ge)
                 assert err <= EXACT_TOL * term_scale(r, Y, lam), (it, err / term_scale(r, Y, lam))
             else:
@@ -315,6 +353,103 @@ def test_grad_parity_full_size_config4():
     r = oracle_grad(Pnp, Y, STAGE_B)
     assert st["I"] == r["geo"]["I"]
     assert relL2(g, r["g"]) <= GRAD_TOL
+
+
+# ----------------------------------------- parity at the bench's own states
+def _gpu_trajectory_states(cfg, iters, plan="auto"):
+    """Run the bench path (GPU C0, attach_plan, runner.Layout with the O7
+    schedule, CUDA graphs) from the seeded init and snapshot the fp32 layout
+    before iteration `it` for it in iters.  SURVEY §8(c): parity is checked at
+    the GPU's own states, the oracle reading exactly those fp32 values."""
+    from paper_2509_19785_b200 import Layout, attach_plan
+    ip, ix = config_graph(cfg)
+    Pd = tsnet_build_P(*dev_graph(ip, ix), u=40.0, seed=0)["P"]
+    attach_plan(Pd, plan)
+    lay = Layout(Pd, torch.from_numpy(init_layout(Pd.n, 0)).cuda(), use_graphs=True)
+    out, it = {}, 0
+    for target in sorted(iters):
+        lay.run(target - it, start=it)
+        it = target
+        lay.sync()
+        out[target] = lay.Y.cpu().numpy().copy()
+    return Pd, out
+
+
+def _np_P(Pd):
+    return dict(indptr=Pd.indptr.cpu().numpy(), indices=Pd.indices.cpu().numpy(),
+                values=Pd.values.cpu().numpy().astype(np.float64))
+
+
+@pytest.mark.parametrize("plan", ["auto", "cb"])
+def test_grad_parity_bench_states_config4(plan):
+    """The timed window of bench.py (config 4, stage B): the full gradient at the
+    GPU's own layouts at iterations 260 and 999 (span 0.5-13, up to 1M points in
+    <= 2916 boxes) against the oracle O5 on exactly those fp32 positions; F_attr
+    <= 1e-5, Z <= 1e-5, gradient <= 1e-4 relL2.  Both SpMV layouts of P."""
+    Pd, states = _gpu_trajectory_states(4, (260, 999), plan)
+    Pn = _np_P(Pd)
+    for it, Y in states.items():
+        g, Z, fa, ff, st = gpu_grad(Pd, Y, GradParams(*STAGE_B))
+        r = oracle_grad(Pn, Y, STAGE_B)
+        assert st["I"] == r["geo"]["I"], (it, st["I"], r["geo"]["I"])
+        assert relL2(fa, r["F_attr"]) <= 1e-5, (it, relL2(fa, r["F_attr"]))
+        assert abs(Z - r["Z"]) <= 1e-5 * r["Z"], (it, Z, r["Z"])
+        assert relL2(g, r["g"]) <= GRAD_TOL, (it, relL2(g, r["g"]))
+
+
+def test_grad_parity_bench_states_config5():
+    """Config 5 (n = 4.1M, the scaling workload, sliced-ELL plan) at the GPU's own
+    layouts at iterations 260 and 999: F_attr and the gradient of three sampled
+    row blocks against the oracle (field from all 4.1M points), Z <= 1e-5."""
+    Pd, states = _gpu_trajectory_states(5, (260, 999), "auto")
+    n = Pd.n
+    pip = Pd.indptr.cpu().numpy()
+    for it, Y in states.items():
+        g, Z, fa, ff, st = gpu_grad(Pd, Y, GradParams(*STAGE_B))
+        fs = oracle.interp.field_state(Y.astype(np.float64))
+        assert st["I"] == fs["geo"]["I"]
+        assert abs(Z - fs["Z"]) <= 1e-5 * fs["Z"], (it, Z, fs["Z"])
+        for r0 in (0, n // 3, n - 3000):
+            B = 3000
+            fip, fix, fpv = _sub_csr(pip, Pd.indices, Pd.values, r0, B)
+            go = oracle.interp.gradient_rows(fs, Y.astype(np.float64), fip, fix, fpv, *STAGE_B, r0, B)
+            fo = oracle.attr_sparse_rows(Y.astype(np.float64), fip, fix, fpv, r0, B)
+            assert relL2(fa[r0:r0 + B], fo) <= 1e-5, (it, r0)
+            assert relL2(g[r0:r0 + B], go) <= GRAD_TOL, (it, r0, relL2(g[r0:r0 + B], go))
+
+
+def test_step_parity_teacher_forced_config2():
+    """SURVEY §8(c) step parity: the GPU state (Y, vel, gains) of its own config-2
+    run at iterations {0, 1, 5, 10, 250, 499}, one step on each side (GPU
+    tsnet_step; oracle O5 gradient + O6 move, the O7 multipliers of that
+    iteration); the state after the step <= 1e-4 relL2 (the move, vel), Y <=
+    1e-4 (at iteration 0 the move dwarfs the N(0, 1e-4^2) positions), gains equal
+    except where |g| < 1e-6 ||g||_inf (sign flips)."""
+    from paper_2509_19785_b200 import Layout
+    from paper_2509_19785_b200.runner import stage_params
+    P = oracle_P(2)
+    Pd = dev_P(P)
+    n = P["n"]
+    lay = Layout(Pd, torch.from_numpy(init_layout(n, 0)).cuda(), use_graphs=False)
+    it = 0
+    for target in (0, 1, 5, 10, 250, 499):
+        lay.run(target - it, start=it)
+        it = target
+        lay.sync()
+        Y, vel, gains = (a.cpu().numpy().copy() for a in (lay.Y, lay.vel, lay.gains))
+        stage = 0 if target < 250 else 1
+        gp, sp = stage_params(stage)
+        lam = (gp.lambda_kl, gp.lambda_c, gp.lambda_r)
+        Yd, Vd, Gd = (torch.from_numpy(a.copy()).cuda() for a in (Y, vel, gains))
+        tsnet_step(Pd, Yd, Vd, Gd, gp, sp, alloc_workspace(n, Pd.nnz, gp))
+        torch.cuda.synchronize()
+        r = oracle_grad(P, Y, lam)
+        Yo, Vo, Go = oracle.update_step(Y, vel, gains, r["g"], eta=sp.eta, mu=sp.momentum)
+        assert relL2(Vd.cpu().numpy(), Vo) <= GRAD_TOL, (target, relL2(Vd.cpu().numpy(), Vo))
+        assert relL2(Yd.cpu().numpy(), Yo) <= GRAD_TOL, (target, relL2(Yd.cpu().numpy(), Yo))
+        small = np.abs(r["g"]) < 1e-6 * np.abs(r["g"]).max()
+        same = np.isclose(Gd.cpu().numpy(), Go, rtol=1e-5)
+        assert np.all(same[~small]), (target, int((~same[~small]).sum()))
 
 
 # ---------------------------------------------------------------- steps
@@ -498,19 +633,21 @@ def test_edge_cases():
     g, Z, _, _, _ = gpu_grad(dev_P(P), Y, gp)
     r = oracle_grad(P, Y, STAGE_B)
     # p = q here: the KL part is an exact cancellation (4 F_attr = 4 F_rep)
-    assert_grad_close(g, r, Y, STAGE_B, tol=3e-4)
+    assert_grad_close(g, r, Y, STAGE_B)
     # coincident points (span floor 1e-12) and an empty P row
     P = dict(indptr=np.array([0, 1, 2, 2], np.int64), indices=np.array([1, 0], np.int32),
              values=np.array([0.5, 0.5]))
     Y = np.zeros((3, 2), np.float32)
     g, Z, _, _, st = gpu_grad(dev_P(P), Y, gp)
     assert np.all(np.isfinite(g)) and st["nonfinite"] == 0
-    # huge span -> I clamped at I_max (box width > h_max)
+    # huge span -> I clamped at I_max (box width > h_max); I_max = 64 keeps the
+    # oracle's grid small (the clamp rule is the same at any I_max)
     Pc = oracle_P(1)
     Y = uniform_layout(Pc["n"], 400.0, 9)
-    g, Z, _, _, st = gpu_grad(dev_P(Pc), Y, gp)
-    r = oracle_grad(Pc, Y, STAGE_B)
-    assert st["I"] == 256 and relL2(g, r["g"]) <= GRAD_TOL
+    gpc = GradParams(*STAGE_B, I_max=64)
+    g, Z, _, _, st = gpu_grad(dev_P(Pc), Y, gpc)
+    r = oracle_grad(Pc, Y, STAGE_B, I_max=64)
+    assert st["I"] == 64 and relL2(g, r["g"]) <= GRAD_TOL
     # non-finite input is flagged
     Yn = Y.copy()
     Yn[5, 0] = np.nan
@@ -521,6 +658,21 @@ def test_edge_cases():
     with pytest.raises(TsnetError):
         ws = alloc_workspace(Pc["n"], len(Pc["values"]), GradParams())
         tsnet_grad(dev_P(Pc), torch.from_numpy(Y).cuda(), bad, ws)
+
+
+@pytest.mark.parametrize("span,I", [(100.0, 400), (255.9, 1024)])
+def test_large_grids(span, I):
+    """Spans beyond 64 (I > 256, FFT size M = 6 I > 1536): the FFT passes run one
+    transform batch at a time through the spectra buffer (field.cu, reading R9's
+    I_max = 1024).  Gradient and Z against the oracle."""
+    P = oracle_P(1)
+    Y = uniform_layout(P["n"], span, 4)
+    g, Z, fa, ff, st = gpu_grad(dev_P(P), Y, GradParams(*STAGE_B))
+    r = oracle_grad(P, Y, STAGE_B)
+    assert st["I"] == r["geo"]["I"] == I and st["M"] == 6 * I
+    assert abs(Z - r["Z"]) <= 1e-5 * r["Z"]
+    assert relL2(ff, -4.0 * r["F_rep"] + 0.6 * r["g_ent"]) <= GRAD_TOL
+    assert relL2(g, r["g"]) <= GRAD_TOL, relL2(g, r["g"])
 
 
 @pytest.mark.parametrize("n", [1, 33, 1000, 4099])

@@ -143,5 +143,9 @@ def test_geometry_policy():
     g = interp.geometry(np.array([[0.0, 0.0], [33.1, 1.0]]))
     assert g["I"] == 135                                  # ceil(132.4)=133 -> 5-smooth 135
     g = interp.geometry(np.array([[0.0, 0.0], [1000.0, 1.0]]))
-    assert g["I"] == 256                                  # I_max clamp
+    assert g["I"] == 1024                                 # I_max clamp (R9: 1024)
+    g = interp.geometry(np.array([[0.0, 0.0], [1000.0, 1.0]]), I_max=250)
+    assert g["I"] == 250                                  # a 5-smooth I_max is kept
+    g = interp.geometry(np.array([[0.0, 0.0], [1000.0, 1.0]]), I_max=257)
+    assert g["I"] == 256                                  # else the largest 5-smooth below it
     assert interp.five_smooth_at_least(97) == 100 and interp.five_smooth_at_most(97) == 96

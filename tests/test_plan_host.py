@@ -1,6 +1,6 @@
 """Host logic of the column-blocked plan (tsnet_plan_partition, pure host code
-in libtsnet): the cut of rows into units (rows, or pieces of long rows) and of
-units into mini-tasks used by the attractive SpMV.  No GPU."""
+in libtsnet): the deal of rows into panels (one CTA each) used by the tiled
+attractive SpMV.  No GPU."""
 import numpy as np
 import pytest
 
@@ -15,85 +15,75 @@ def T():
     return tsnet
 
 
-def check_cut(ip, rb, re, W, RM, base, cut):
-    G, row_mt, row_K, mt_r0, mt_info = cut
+def check_cut(ip, rb, re, G, cap, cut):
+    P, row_panel, row_local, panel_off, panel_rows = cut
     nr = re - rb
-    L = np.diff(ip[rb:re + 1])
-    nnz = int(L.sum())
-    cap = max(256, nnz // (base * W) // 2)
-    T = G * W
-    assert G % base == 0 and G >= base and len(mt_r0) == T
-    assert np.array_equal(row_K, np.where(L > cap, -(-L // cap), 1))     # long rows split into pieces
-    covered = np.zeros(nr, np.int64)
-    for t in range(T):
-        r0, info = int(mt_r0[t]), int(mt_info[t])
-        if info < 0:                                     # a piece of one split row
-            assert row_K[r0] > 1 and row_mt[r0] <= t < row_mt[r0] + row_K[r0]
-            covered[r0] += 1
-        elif info > 0:                                   # a run of whole rows
-            assert info <= RM
-            rows = np.arange(r0, r0 + info)
-            assert np.all(row_K[rows] == 1) and np.all(row_mt[rows] == t)
-            covered[rows] += 1
-    assert np.array_equal(covered, row_K)                 # every row exactly once (pieces: K times)
-    # runs in row order
-    firsts = [int(mt_r0[t]) for t in range(T) if mt_info[t] != 0]
-    assert firsts == sorted(firsts)
-    # balance of runs on (entries + rows): none exceeds the mean by more than one row
-    runs = [(int(mt_r0[t]), int(mt_info[t])) for t in range(T) if mt_info[t] > 0]
-    if runs:
-        w = [int(L[r0:r0 + k].sum()) + k for r0, k in runs]
-        tot = sum(int(L[q]) + 1 for q in range(nr) if row_K[q] == 1)
-        n_pieces = int(row_K[row_K > 1].sum())
-        n_split = int((row_K > 1).sum())
-        assert max(w) <= tot / max(1, T - n_pieces - n_split) + cap + 1
-    return T
+    L = np.diff(ip[rb:re + 1]).astype(np.int64)
+    # panel count: G * ceil(nr / (G cap)), at most nr, at least 1
+    want_P = max(1, min(G * -(-nr // (G * cap)), max(nr, 1)))
+    assert P == want_P
+    assert panel_off[0] == 0 and panel_off[-1] == nr and np.all(np.diff(panel_off) >= 0)
+    sizes = np.diff(panel_off)
+    assert sizes.max(initial=0) <= cap
+    # every row exactly once; local index = position inside its panel; rows ascending in a panel
+    assert np.array_equal(np.sort(panel_rows), np.arange(nr))
+    for p in range(P):
+        rows = panel_rows[panel_off[p]:panel_off[p + 1]]
+        assert np.all(np.diff(rows) > 0)
+        assert np.all(row_panel[rows] == p)
+        assert np.array_equal(row_local[rows], np.arange(len(rows)))
+    # LPT balance on weight = entries + 8: no panel exceeds the mean by more than the
+    # largest single row weight (the textbook LPT bound); with a cap that binds,
+    # only panels below the cap are compared
+    if nr:
+        wts = np.bincount(row_panel, weights=L + 8, minlength=P)
+        open_ = sizes < cap
+        if open_.any():
+            assert wts[open_].max() <= wts.sum() / P + (L.max() + 8) + 1e-9
+    return P
 
 
-@pytest.mark.parametrize("base", [1, 7, 148])
-def test_cut_covers_rows_balanced(T, base):
+@pytest.mark.parametrize("G", [1, 7, 148])
+def test_cut_covers_rows_balanced(T, G):
     ip, _ = config_graph(2)
     n = len(ip) - 1
-    check_cut(ip, 0, n, 16, 704, base, T.tsnet_plan_partition(ip, 0, n, 16, 704, base))
+    check_cut(ip, 0, n, G, 8192, T.tsnet_plan_partition(ip, 0, n, G, 8192))
 
 
-def test_row_cap_forces_more_groups(T):
-    n = 100_000
-    ip = np.arange(n + 1, dtype=np.int64) * 3
-    cut = T.tsnet_plan_partition(ip, 0, n, 4, 100, 148)
-    check_cut(ip, 0, n, 4, 100, 148, cut)
-    assert cut[0] == 148 * 2     # 592 mini-tasks cannot hold 100k rows at <= 100 each; 1184 can
+def test_row_cap_forces_more_panels(T):
+    ip, _ = config_graph(2)
+    n = len(ip) - 1
+    cut = T.tsnet_plan_partition(ip, 0, n, 4, 100)
+    P = check_cut(ip, 0, n, 4, 100, cut)
+    assert P == 4 * -(-n // 400) and np.diff(cut[3]).max() <= 100
 
 
-def test_long_rows_are_split(T):
-    L = np.full(5000, 3)
-    L[10] = 4000                 # a hub row: far above the piece cap
-    ip, _, _ = random_csr(5000, L, seed=2)
-    cut = T.tsnet_plan_partition(ip, 0, 5000, 4, 64, 2)
-    check_cut(ip, 0, 5000, 4, 64, 2, cut)
-    assert cut[2][10] > 1
+def test_power_law_rows_balanced(T):
+    """Hub rows (a few rows hold a large share of the entries) spread over the
+    panels: entries per panel within one hub row of the mean."""
+    rng = np.random.default_rng(3)
+    L = np.minimum((rng.pareto(1.5, 20000) * 60 + 120).astype(np.int64), 20000)
+    ip = np.concatenate([[0], np.cumsum(L)])
+    P = check_cut(ip, 0, len(L), 148, 8192, T.tsnet_plan_partition(ip, 0, len(L), 148, 8192))
+    assert P == 148
 
 
-def test_shard_and_empty_ranges(T):
-    ip, _, _ = random_csr(5000, np.random.default_rng(0).integers(0, 30, 5000), seed=1)
-    check_cut(ip, 1234, 4321, 8, 64, 8, T.tsnet_plan_partition(ip, 1234, 4321, 8, 64, 8))
-    cut = T.tsnet_plan_partition(ip, 77, 77, 8, 64, 8)
-    assert len(cut[1]) == 0 and np.all(cut[4] == 0)
+def test_shard_rows_and_empty(T):
+    ip, _ = config_graph(1)
+    check_cut(ip, 100, 900, 8, 64, T.tsnet_plan_partition(ip, 100, 900, 8, 64))
+    P, rp, rl, po, pr = T.tsnet_plan_partition(ip, 77, 77, 8, 64)
+    assert P == 1 and len(rp) == 0 and list(po) == [0, 0]
+    # fewer rows than groups: one row per panel
+    P, rp, rl, po, pr = T.tsnet_plan_partition(ip, 0, 5, 148, 8192)
+    assert P == 5 and np.array_equal(np.sort(rp), np.arange(5))
 
 
-def test_trailing_and_leading_empty_rows(T):
-    """Rows with no entries at either end are covered (an earlier cut looped
-    forever when the last rows were empty)."""
-    L = np.zeros(30011, np.int64)
-    L[100:20000] = 5
-    ip = np.zeros(len(L) + 1, np.int64)
-    np.cumsum(L, out=ip[1:])
-    check_cut(ip, 0, len(L), 16, 704, 148, T.tsnet_plan_partition(ip, 0, len(L), 16, 704, 148))
-    z = np.zeros(501, np.int64)                                      # no entries at all
-    check_cut(z, 0, 500, 4, 64, 4, T.tsnet_plan_partition(z, 0, 500, 4, 64, 4))
-
-
-def test_bad_arguments(T):
-    ip = np.arange(11, dtype=np.int64)
+def test_empty_rows_and_bad_args(T):
+    ip = np.concatenate([[0], np.cumsum(np.array([0, 3, 0, 0, 5, 1, 0] * 50))])
+    check_cut(ip, 0, 350, 4, 64, T.tsnet_plan_partition(ip, 0, 350, 4, 64))
+    z = np.zeros(501, np.int64)
+    check_cut(z, 0, 500, 4, 64, T.tsnet_plan_partition(z, 0, 500, 4, 64))
+    ip2, _, _ = random_csr(1000, np.full(1000, 5), 1)
+    check_cut(ip2, 0, 1000, 3, 2000, T.tsnet_plan_partition(ip2, 0, 1000, 3, 2000))
     with pytest.raises(Exception):
-        T.tsnet_plan_partition(ip, 5, 3, 16, 704, 1)
+        T.tsnet_plan_partition(ip, 5, 3, 16, 704)
