@@ -89,6 +89,10 @@ typedef struct {
     float* values;           /* device, capacity */
     const void* plan;        /* device, tsnet_plan_build / tsnet_sell_build output, or NULL */
     int32_t plan_kind;       /* TSNET_PLAN_CB (or 0) / TSNET_PLAN_SELL; ignored without a plan */
+    int64_t plan_row_begin;  /* the rows [plan_row_begin, plan_row_end) the plan was built for (its
+                                shard; [0, n) without one); a call whose rows differ fails with
+                                TSNET_E_ARG.  Set by the caller with P->plan; ignored without a plan */
+    int64_t plan_row_end;
 } tsnet_csr;
 
 /* Cost multipliers and interpolation grid policy.
@@ -244,10 +248,15 @@ TSNET_API int tsnet_grad(const tsnet_csr* P, const float* Y, const tsnet_grad_pa
                float* grad, double* Z, void* ws, size_t ws_bytes, tsnet_stream_t stream);
 
 /* The attractive term alone (step a6, Eq. 6 first term):
- *   f_attr,i = sum_{j in row i} p_ij w_ij Delta_ij   (n x 2 fp32, device)
- * Uses P->plan when set (column-blocked kernel), else the row-wise CSR kernel.
- * Needs no workspace.  Async.  (Also the kernel bench.py times for the roofline.) */
-TSNET_API int tsnet_attr(const tsnet_csr* P, const float* Y, float* f_attr, tsnet_stream_t stream);
+ *   f_attr,i = sum_{j in row i} p_ij w_ij Delta_ij
+ * for the rows [row_begin, row_end) of `shard` (all n rows if NULL; only the row
+ * range of the shard is used): f_attr is (row_end - row_begin) x 2 fp32
+ * (device), row q = vertex row_begin + q.  Y is the full n x 2 layout.  Uses
+ * P->plan when set (its rows must be the shard's), else the row-wise CSR
+ * kernel.  Needs no workspace.  Async.  (Also the kernel bench.py times for the
+ * roofline.) */
+TSNET_API int tsnet_attr(const tsnet_csr* P, const float* Y, const tsnet_shard* shard, float* f_attr,
+                         tsnet_stream_t stream);
 
 /* Same evaluation, returning the parts separately (diagnostics / parity):
  *   f_attr  = F_attr (n x 2), f_field = -4 lambda_kl F_rep + lambda_r g_ent (n x 2),

@@ -19,14 +19,16 @@
 //     cp.async.bulk (TMA bulk copy, mbarrier completion) and prefetches the
 //     tile's entries into L2 (cp.async.bulk.prefetch.L2), kTS - 1 blocks
 //     ahead of the consumers;
-//   * warps: the rows of a panel are cut into kTW contiguous ranges of
-//     balanced entries, one per consumer warp, for the whole sweep -- a row is
-//     only ever touched by its warp, so warps need no barrier between blocks
-//     (each releases a ring stage on its own; the ring absorbs the drift);
-//   * per (panel, block, warp) tile the entries are sorted by (local row,
-//     column) and cut into 32 equal contiguous chunks, one per lane; slot
-//     (step k, lane l) = k-th entry of chunk l, so a warp's step is one
-//     coalesced 256-B load, and the tile is padded to whole steps (< 32
+//   * per (panel, block) tile the entries are sorted by (local row, column)
+//     and cut into kTW warp segments of equal size, each boundary moved to
+//     the nearest row boundary (within kSnap entries; a longer run is split
+//     and its row marked shared, "hub"), so every warp does the same work in
+//     every block whatever the row lengths (hub rows of 1e5 entries included);
+//     the warps meet at one named barrier per block (rows change owners
+//     between blocks);
+//   * a warp segment is cut into 32 equal contiguous chunks, one per lane;
+//     slot (step k, lane l) = k-th entry of chunk l, so a warp's step is one
+//     coalesced 256-B load, and the segment is padded to whole steps (< 32
 //     slots) with (0, p = 0) slots that add exactly 0;
 //   * a lane accumulates its run of equal rows in registers and adds it to
 //     the row's accumulator in shared memory when the run ends inside its
@@ -34,8 +36,8 @@
 //     continues past the chunk's end is carried out: after the tile the
 //     carries are summed per row across lanes (segmented warp scan, merge-path
 //     style) and added by one lane, after the row's own flush in program
-//     order -- no atomics anywhere (shared-memory float atomics are CAS loops
-//     on sm_100, and hub rows would serialise them);
+//     order; only the few shared rows use atomics (shared-memory float
+//     atomics are CAS loops on sm_100);
 // HBM bytes per launch: 8 per slot (stored entries + < 512 pads per tile) +
 // 4 per tile + 12 per row (row list, Y_i, F_i); Y blocks come from L2
 // (P x 8 n bytes of L2 reads).
@@ -52,21 +54,35 @@
 
 namespace tsnet {
 
-constexpr int kTB = 4096;            // points per column block (12-bit column in block)
-constexpr int kTS = 3;               // Y ring stages (3 x 32 KB)
-constexpr int kTPre = 4;             // blocks of entries prefetched into L2 ahead of the Y ring
-constexpr int kTW = 16;              // consumer warps per CTA (+1 producer warp)
+constexpr int kTB = 7168;            // points per column block (column * 8 < 2^16)
+constexpr int kTS = 2;               // Y ring stages (2 x 56 KB, double buffer)
+constexpr int kTPre = 3;             // blocks of entries prefetched into L2 ahead of the producer
+// probe builds only (scripts/tile_variants.sh): the slot-load cache policy
+#ifndef TILE_LDPOL
+#define TILE_LDPOL 0
+#endif
+#ifndef TILE_DIAG   // timing diagnostics only (wrong results): 1 no F read-modify-write, 2 Y_j from one address
+#define TILE_DIAG 0
+#endif
+constexpr int kTW = 15;              // consumer warps per CTA (+1 producer warp: 16 warps, <= 128 registers)
 constexpr int kTL = kTW * 32;        // consumer threads
-constexpr int kTR = 8192;            // max rows per panel (13-bit local row; 16 B of shared memory each)
+constexpr int kTR = 6912;            // max rows per panel (13-bit local row; 16 B of shared memory each)
 constexpr int kTRbits = 13;
-// slot word: column in block * 8 (bits 0-14, the byte offset of Y_j in the
-// ring stage) | local row (bits 15-27; * 8 = byte offset of Y_i and F_i) |
+constexpr unsigned long long kLocalMask = (1ull << kTRbits) - 1;
+// slot word: column in block * 8 (bits 0-15, the byte offset of Y_j in the
+// ring stage) | row slot (bits 16-28; * 8 = byte offset of Y_i and F_i) |
+// HUB (bit 29: the row is shared between warps; its flushes are atomic) |
 // NEWROW (bit 30: a run starts here) | FLUSH (bit 31: a run ends here).  Real
 // entries have p > 0 (C0 drops exact zeros); pads are (0, p = 0).
-constexpr uint32_t kColMask = 0x7FF8u, kRowMask = 0xFFF8u, kNewRow = 1u << 30, kFlush = 1u << 31;
-// byte offset of a dummy float2 from the Y_i array (Y_i[kTR], F_i[kTR], dummy):
-// lanes with nothing to read there all read it (one broadcast address)
-constexpr uint32_t kDummyFromYi = 2u * kTR * 8u, kDummyFromFs = kTR * 8u;
+constexpr uint32_t kColMask = 0xFFF8u, kRowMask = 0xFFF8u, kHub = 1u << 29, kNewRow = 1u << 30, kFlush = 1u << 31;
+constexpr int kRowShift = 13;        // (word >> kRowShift) & kRowMask = row slot * 8
+// Shared memory: Y_i[kTR] at 0, F_i[kTR] at kFsOff, a dummy float2 (lanes with
+// nothing to read there all read it: one broadcast address), the Y ring, the
+// mbarriers.  Row slot = swizzled local row (tile_slot): the rows a warp's
+// lanes touch at one step are spaced by about a run per chunk, so plain
+// indices would put them in a few banks.
+constexpr uint32_t kFsOff = kTR * 8u, kDummyOff = 2u * kTR * 8u, kRingOff = 2u * kTR * 8u + 16u;
+__host__ __device__ __forceinline__ uint32_t tile_slot(uint32_t r) { return r ^ ((r >> 4) & 15u); }
 constexpr uint64_t kTileMagic = 0x3654534e53545354ull;   // "TSTSNST6"
 
 struct TileHeader {
@@ -159,30 +175,16 @@ static int32_t tile_partition(const int64_t* ipr, int64_t nr, int32_t G, int32_t
     return P;
 }
 
-// The rows of each panel (in local order) cut into W contiguous ranges of
-// balanced entries: the row with local index l and e entries before it in the
-// panel (of E) goes to warp min(W - 1, floor(W (e + L_l / 2) / E)) -- its
-// midpoint decides, so ranges stay contiguous.  Pure host code.
-static void tile_warps(const int64_t* ipr, int32_t P, int32_t W, const std::vector<int32_t>& panel_off,
-                       const std::vector<int32_t>& panel_rows, std::vector<int32_t>& row_warp) {
-    row_warp.assign(panel_rows.size(), 0);
-    for (int32_t p = 0; p < P; ++p) {
-        int64_t E = 0;
-        for (int32_t l = panel_off[p]; l < panel_off[p + 1]; ++l) E += ipr[panel_rows[l] + 1] - ipr[panel_rows[l]];
-        int64_t e = 0;
-        for (int32_t l = panel_off[p]; l < panel_off[p + 1]; ++l) {
-            const int64_t q = panel_rows[l], L = ipr[q + 1] - ipr[q];
-            const double mid = (double)e + 0.5 * (double)L;
-            row_warp[q] = E > 0 ? (int32_t)std::min<double>(W - 1, std::floor((double)W * mid / (double)E)) : 0;
-            e += L;
-        }
-    }
-}
-
 // ------------------------------------------------------------------ kernel
 __device__ __forceinline__ uint2 ld_slot(const uint2* a) {
     uint2 v;
+#if TILE_LDPOL == 0
     asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(a));
+#elif TILE_LDPOL == 1
+    asm volatile("ld.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(a));
+#else
+    asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(a));
+#endif
     return v;
 }
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
@@ -194,10 +196,11 @@ struct TileSet {
     uint2 s[4];
 };
 
-// Four consecutive steps of this lane (steps >= K are pad slots: no load).
-__device__ __forceinline__ void load4(TileSet& S, const uint2* __restrict__ base, int k0, int K) {
+// Four consecutive steps of this lane from `at` (`left` steps remain in the
+// tile; steps past it are pad slots: no load).
+__device__ __forceinline__ void load4(TileSet& S, const uint2* at, int left) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) S.s[q] = (k0 + q < K) ? ld_slot(base + (size_t)(k0 + q) * 32) : make_uint2(0u, 0u);
+    for (int q = 0; q < 4; ++q) S.s[q] = (q < left) ? ld_slot(at + q * 32) : make_uint2(0u, 0u);
 }
 
 __device__ __forceinline__ float2 lds2(const char* base, uint32_t off) {
@@ -206,23 +209,28 @@ __device__ __forceinline__ float2 lds2(const char* base, uint32_t off) {
 
 // NQ consecutive entries of this lane: contribution p w (X_i - X_j), w = 1 /
 // (1 + r^2) (rcp.approx: 1 + r^2 >= 1, relative error <= 2^-22); pad slots
-// (p = 0) add exactly 0.  Y_i is read when a run starts (NEWROW) and kept in
-// registers; a run's sum goes to its row when it ends here (FLUSH).  All loads
-// of the NQ entries are issued first; lanes with nothing to read address one
-// dummy float2 (a broadcast), so bank conflicts come only from real reads.  The
-// flush values are formed in registers and the (distinct: a row is one run of
-// a lane) rows read-modified-written together.  kc = byte offset of the row of
-// the last real entry, cv = its run continues past the chunk (the carry-out
-// (ax, ay), possibly exactly 0, belongs to kc).
+// (word 0, p = 0) add exactly 0.  Y_i is read when a run starts (NEWROW) and
+// kept in registers; a run's sum goes to its row when it ends here (FLUSH).
+// All loads of the NQ entries are issued first; lanes with nothing to read
+// address the dummy (a broadcast), so bank conflicts come only from real reads.
+// The flush values are formed in registers and the (distinct: a row is one run
+// of a lane) rows read-modified-written together.  lastw = the slot word of the
+// lane's last real entry (a real word is never 0: the first entry of a run
+// carries NEWROW, later ones a column > 0).
 template <int NQ>
-__device__ __forceinline__ void tileq(const TileSet& S, const char* Ys, const char* Yi, char* Fs, float2& yi,
-                                      float& ax, float& ay, int& kc, bool& cv) {
+__device__ __forceinline__ void tileq(const TileSet& S, const char* sm, uint32_t ysoff, float2& yi, float& ax,
+                                      float& ay, uint32_t& lastw) {
     float2 yj[NQ], yl[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         const uint32_t w = S.s[q].x;
-        yj[q] = lds2(Ys, w & kColMask);
-        yl[q] = lds2(Yi, (w & kNewRow) ? ((w >> 12) & kRowMask) : kDummyFromYi);
+        const uint32_t ro = (w >> kRowShift) & kRowMask;
+#if TILE_DIAG == 2
+        yj[q] = lds2(sm, ysoff);
+#else
+        yj[q] = lds2(sm, ysoff + (w & kColMask));
+#endif
+        yl[q] = lds2(sm, (w & kNewRow) ? ro : kDummyOff);
     }
     float fx[NQ], fy[NQ];
 #pragma unroll
@@ -241,29 +249,58 @@ __device__ __forceinline__ void tileq(const TileSet& S, const char* Ys, const ch
         fy[q] = ay;
         ax = fl ? 0.f : ax;
         ay = fl ? 0.f : ay;
-        if (p != 0.f) {
-            kc = (int)((w >> 12) & kRowMask);
-            cv = !fl;
-        }
+        lastw = w ? w : lastw;
     }
+#if TILE_DIAG == 1
+    if (fx[0] == 1.2345f) *reinterpret_cast<float2*>(const_cast<char*>(sm) + kFsOff) = make_float2(fx[NQ - 1], fy[NQ - 1]);
+#else
+    // plain read-modify-write: rows owned by this lane in this block
     float2 v[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         const uint32_t w = S.s[q].x;
-        v[q] = lds2(Fs, ((int)w < 0) ? ((w >> 12) & kRowMask) : kDummyFromFs);
+        v[q] = lds2(sm, ((w & (kFlush | kHub)) == kFlush) ? kFsOff + ((w >> kRowShift) & kRowMask) : kDummyOff);
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
-        if ((int)S.s[q].x < 0)
-            *reinterpret_cast<float2*>(Fs + ((S.s[q].x >> 12) & kRowMask)) = make_float2(v[q].x + fx[q], v[q].y + fy[q]);
+        if ((S.s[q].x & (kFlush | kHub)) == kFlush)
+            *reinterpret_cast<float2*>(const_cast<char*>(sm) + kFsOff + ((S.s[q].x >> kRowShift) & kRowMask)) =
+                make_float2(v[q].x + fx[q], v[q].y + fy[q]);
+    // shared (hub) rows: atomic adds (rare: runs split between warps)
+    bool hf = false;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) hf |= (S.s[q].x & (kFlush | kHub)) == (kFlush | kHub);
+    if (__any_sync(0xffffffffu, hf)) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+            if ((S.s[q].x & (kFlush | kHub)) == (kFlush | kHub)) {
+                float* f = reinterpret_cast<float*>(const_cast<char*>(sm) + kFsOff + ((S.s[q].x >> kRowShift) & kRowMask));
+                atomicAdd(f, fx[q]);
+                atomicAdd(f + 1, fy[q]);
+            }
+    }
+#endif
 }
 
 // the last r = 1..3 steps of a tile (set S, statically indexed)
-__device__ __forceinline__ void tile_tail(const TileSet& S, int r, const char* Ys, const char* Yi, char* Fs, float2& yi,
-                                          float& ax, float& ay, int& kc, bool& cv) {
-    if (r == 3) tileq<3>(S, Ys, Yi, Fs, yi, ax, ay, kc, cv);
-    else if (r == 2) tileq<2>(S, Ys, Yi, Fs, yi, ax, ay, kc, cv);
-    else tileq<1>(S, Ys, Yi, Fs, yi, ax, ay, kc, cv);
+__device__ __forceinline__ void tile_tail(const TileSet& S, int r, const char* sm, uint32_t ysoff, float2& yi,
+                                          float& ax, float& ay, uint32_t& lastw) {
+    if (r == 3) tileq<3>(S, sm, ysoff, yi, ax, ay, lastw);
+    else if (r == 2) tileq<2>(S, sm, ysoff, yi, ax, ay, lastw);
+    else tileq<1>(S, sm, ysoff, yi, ax, ay, lastw);
+}
+
+// a carry-out sum into its row: plain for rows owned by this warp in this
+// block, atomic for shared (hub) rows
+__device__ __forceinline__ void carry_add(char* Fs, int kc, float ax, float ay, uint32_t hub) {
+    float2* f = reinterpret_cast<float2*>(Fs + kc);
+    if (hub) {
+        atomicAdd(&f->x, ax);
+        atomicAdd(&f->y, ay);
+    } else {
+        const float2 v = *f;
+        *f = make_float2(v.x + ax, v.y + ay);
+    }
 }
 
 // After a tile: carry-outs (ax, ay) of runs that continue into the next lane's
@@ -271,10 +308,12 @@ __device__ __forceinline__ void tile_tail(const TileSet& S, int r, const char* Y
 // run's lanes are consecutive: rows are sorted; every lane a run passes through
 // carries, so a row forms exactly one group) and add each sum once, by the last
 // lane of its group.  The row's own flush (by the lane where the run ends, in
-// this warp) happened earlier in program order.
-__device__ __forceinline__ void tile_carry(float ax, float ay, int kc, bool cv, char* Fs, int lane) {
+// this warp for an unshared row) happened earlier in program order; a shared
+// (hub) row, whose run continues into another warp, only ever gets atomic adds.
+__device__ __forceinline__ void tile_carry(float ax, float ay, uint32_t lastw, char* Fs, int lane) {
     const unsigned full = 0xffffffffu;
-    const bool nz = kc >= 0 && cv;
+    const int kc = (int)((lastw >> kRowShift) & kRowMask);
+    const bool nz = lastw != 0 && (int)lastw >= 0;   // a real last entry whose run does not end here
     const int kp = __shfl_up_sync(full, nz ? kc : -1, 1);
     if (__any_sync(full, nz && lane > 0 && kp == kc)) {
         // runs carried over more than one lane boundary: segmented inclusive
@@ -294,15 +333,9 @@ __device__ __forceinline__ void tile_carry(float ax, float ay, int kc, bool cv, 
             }
         }
         const int kn = __shfl_down_sync(full, key, 1);
-        if (nz && (lane == 31 || kn != key)) {
-            float2* f = reinterpret_cast<float2*>(Fs + kc);
-            const float2 v = *f;
-            *f = make_float2(v.x + ax, v.y + ay);
-        }
+        if (nz && (lane == 31 || kn != key)) carry_add(Fs, kc, ax, ay, lastw & kHub);
     } else if (nz) {
-        float2* f = reinterpret_cast<float2*>(Fs + kc);
-        const float2 v = *f;
-        *f = make_float2(v.x + ax, v.y + ay);
+        carry_add(Fs, kc, ax, ay, lastw & kHub);
     }
 }
 
@@ -327,12 +360,12 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
                                                                  const float2* __restrict__ Y, float2* __restrict__ F,
                                                                  int y_aligned) {
     extern __shared__ __align__(128) uint8_t t_smem[];
-    float2* ring = reinterpret_cast<float2*>(t_smem);                 // kTS x kTB
     const TileHeader* h = reinterpret_cast<const TileHeader*>(plan);
     const int P = h->P, NB = h->NB;
-    float2* Yi = ring + kTS * kTB;                                    // kTR
-    float2* Fs = Yi + kTR;                                            // kTR, then the dummy float2 (+ pad)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(Fs + kTR + 2);       // full[kTS], empty[kTS]
+    float2* Yi = reinterpret_cast<float2*>(t_smem);                   // kTR (swizzled row slots)
+    float2* Fs = reinterpret_cast<float2*>(t_smem + kFsOff);          // kTR
+    float2* ring = reinterpret_cast<float2*>(t_smem + kRingOff);      // kTS x kTB
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kTS * kTB);   // full[kTS], empty[kTS]
     const int64_t n = h->n, rb = h->row_begin;
     const int2* wtab = reinterpret_cast<const int2*>(plan + h->off_wtab);   // [(p kTW + w) NB + J] = (step, K)
     const int32_t* roff = reinterpret_cast<const int32_t*>(plan + h->off_rowoff);
@@ -343,18 +376,46 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTS; ++s) {
             mbar_init(&bars[s], 1);
-            mbar_init(&bars[kTS + s], kTW);
+            mbar_init(&bars[kTS + s], 1);
         }
-        Fs[kTR] = make_float2(0.f, 0.f);
+        *reinterpret_cast<float2*>(t_smem + kDummyOff) = make_float2(0.f, 0.f);
         fence_mbar_init();
     }
     __syncthreads();
 
     if (warp == kTW) {
-        // ---------------- producer: Y of every block, in order, for each panel
+        // ---------------- producer: Y of every block, in order, for each panel;
+        // the entries of block J + kTPre (all warps' tiles: one contiguous
+        // range) are prefetched into L2 before the ring wait for block J
         uint32_t k = 0;
+        const unsigned full = 0xffffffffu;
         for (int p = blockIdx.x; p < P; p += gridDim.x) {
+            // first step of block J (warp 0's tile) in lane J - J0 of bv / bn; the
+            // panel's end step for J = NB
+            const int2* w0 = wtab + (int64_t)p * kTW * NB;
+            const int2 lastt = w0[(int64_t)(kTW - 1) * NB + NB - 1];
+            const int pend = lastt.x + lastt.y;
+            auto start_of = [&](int J) { return J < NB ? __ldg(&w0[J].x) : pend; };
+            int bv = start_of(min(lane, NB)), bn = start_of(min(32 + lane, NB));
+            int B0 = 0;
+            auto block_start = [&](int J) {     // warp-uniform, J in [B0, B0 + 64)
+                const int v = (J - B0 < 32) ? bv : bn;
+                return __shfl_sync(full, v, (J - B0) & 31);
+            };
+            auto prefetch_block = [&](int J) {
+                if (J >= NB) return;
+                const int s0 = block_start(J), s1 = block_start(J + 1);
+                if (lane == 0 && s1 > s0) prefetch_l2(slots + (size_t)s0 * 32, (uint32_t)(s1 - s0) * 32u * 8u);
+            };
             for (int J = 0; J < NB; ++J) {
+                if (J + kTPre + 1 - B0 >= 64) {   // keep blocks [B0, B0 + 64) in bv / bn
+                    B0 += 32;
+                    bv = bn;
+                    bn = start_of(min(B0 + 32 + lane, NB));
+                }
+                if (J == 0)
+                    for (int q = 0; q < kTPre; ++q) prefetch_block(q);
+                prefetch_block(J + kTPre);
                 const int b = (int)(k % kTS);
                 float2* dst = ring + b * kTB;
                 if (k >= (uint32_t)kTS) mbar_wait(&bars[kTS + b], ((k / kTS) - 1) & 1);
@@ -381,15 +442,19 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
     }
 
     // ---------------- consumer warp `warp`: its tile of every block, lane = chunk
-    const char* Yib = reinterpret_cast<const char*>(Yi);
-    char* Fsb = reinterpret_cast<char*>(Fs);
+#if TILE_DIAG == 3
+    const long long t_start = clock64();
+    long long t_wait = 0;
+#endif
+    const char* sm = reinterpret_cast<const char*>(t_smem);
     const unsigned full = 0xffffffffu;
     uint32_t k = 0;
     for (int p = blockIdx.x; p < P; p += gridDim.x) {
         const int r0 = roff[p], R = roff[p + 1] - r0;
         for (int r = threadIdx.x; r < R; r += kTL) {
-            Yi[r] = Y[rb + (rows[r0 + r] & 0x7FFFFFFF)];
-            Fs[r] = make_float2(0.f, 0.f);
+            const uint32_t q = tile_slot((uint32_t)r);
+            Yi[q] = Y[rb + (rows[r0 + r] & 0x7FFFFFFF)];
+            Fs[q] = make_float2(0.f, 0.f);
         }
         bar_consumers();
         // this warp's (first step, steps) of blocks J0 .. J0 + 31 in tv (lane J - J0),
@@ -400,15 +465,11 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
             const int2 src = (J - J0 < 32) ? tv : tn;
             return make_int2(__shfl_sync(full, src.x, (J - J0) & 31), __shfl_sync(full, src.y, (J - J0) & 31));
         };
-        auto prefetch_tile = [&](int2 t) {     // the warp's entries of a later block into L2
-            if (lane == 0 && t.y > 0) prefetch_l2(slots + (size_t)t.x * 32, (uint32_t)t.y * 32u * (uint32_t)sizeof(uint2));
-        };
         int2 cur = tile_of(0, 0);
-        prefetch_tile(cur);
-        if (NB > 1) prefetch_tile(tile_of(1, 0));
-        TileSet A, B, C;
-        load4(A, slots + (size_t)cur.x * 32 + lane, 0, cur.y);
-        load4(B, slots + (size_t)cur.x * 32 + lane, 4, cur.y);
+        TileSet A, B, C, D, E;
+        const uint2* at = slots + (size_t)cur.x * 32 + lane;
+        load4(A, at, cur.y);
+        load4(B, at + 128, cur.y - 4);
         int J0 = 0;
         for (int J = 0; J < NB; ++J) {
             if (J - J0 == 32) {              // next 32 blocks
@@ -417,61 +478,79 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
                 tn = ld_tab(wt, J0 + 32 + lane, NB);
             }
             const int K = cur.y;
-            const uint2* base = slots + (size_t)cur.x * 32 + lane;
             const int2 nxt = (J + 1 < NB) ? tile_of(J + 1, J0) : make_int2(0, 0);
-            if (J + 2 < NB) prefetch_tile(tile_of(J + 2, J0));
+            // the next tile's first two groups, a whole tile ahead of their use
+            const uint2* atn = slots + (size_t)nxt.x * 32 + lane;
+            load4(D, atn, nxt.y);
+            load4(E, atn + 128, nxt.y - 4);
             const int b = (int)(k % kTS);
-            const char* Ys = reinterpret_cast<const char*>(ring + b * kTB);
+            const uint32_t ysoff = kRingOff + (uint32_t)b * (kTB * 8u);
+#if TILE_DIAG == 3
+            const long long tw0 = clock64();
+#endif
             while (!mbar_try_wait_hint(&bars[b], (k / kTS) & 1)) {
             }
+#if TILE_DIAG == 3
+            t_wait += clock64() - tw0;
+#endif
             if (K > 0) {
                 float ax = 0.f, ay = 0.f;
                 float2 yi = make_float2(0.f, 0.f);
-                int kc = -1;
-                bool cv = false;
+                uint32_t lastw = 0;
                 // three register sets rotated by unrolling, loads two groups ahead;
                 // the last 1-3 steps of the tile run exactly (no pad steps computed)
+                const uint2* ld = at + 256;          // step 8
 #pragma unroll 1
-                for (int k0 = 0;;) {
-                    load4(C, base, k0 + 8, K);
-                    if (K - k0 < 4) { tile_tail(A, K - k0, Ys, Yib, Fsb, yi, ax, ay, kc, cv); break; }
-                    tileq<4>(A, Ys, Yib, Fsb, yi, ax, ay, kc, cv);
-                    k0 += 4;
-                    if (k0 >= K) break;
-                    load4(A, base, k0 + 8, K);
-                    if (K - k0 < 4) { tile_tail(B, K - k0, Ys, Yib, Fsb, yi, ax, ay, kc, cv); break; }
-                    tileq<4>(B, Ys, Yib, Fsb, yi, ax, ay, kc, cv);
-                    k0 += 4;
-                    if (k0 >= K) break;
-                    load4(B, base, k0 + 8, K);
-                    if (K - k0 < 4) { tile_tail(C, K - k0, Ys, Yib, Fsb, yi, ax, ay, kc, cv); break; }
-                    tileq<4>(C, Ys, Yib, Fsb, yi, ax, ay, kc, cv);
-                    k0 += 4;
-                    if (k0 >= K) break;
+                for (int left = K;;) {
+                    load4(C, ld, left - 8);
+                    if (left < 4) { tile_tail(A, left, sm, ysoff, yi, ax, ay, lastw); break; }
+                    tileq<4>(A, sm, ysoff, yi, ax, ay, lastw);
+                    left -= 4;
+                    ld += 128;
+                    if (left <= 0) break;
+                    load4(A, ld, left - 8);
+                    if (left < 4) { tile_tail(B, left, sm, ysoff, yi, ax, ay, lastw); break; }
+                    tileq<4>(B, sm, ysoff, yi, ax, ay, lastw);
+                    left -= 4;
+                    ld += 128;
+                    if (left <= 0) break;
+                    load4(B, ld, left - 8);
+                    if (left < 4) { tile_tail(C, left, sm, ysoff, yi, ax, ay, lastw); break; }
+                    tileq<4>(C, sm, ysoff, yi, ax, ay, lastw);
+                    left -= 4;
+                    ld += 128;
+                    if (left <= 0) break;
                 }
-                tile_carry(ax, ay, kc, cv, Fsb, lane);
+                tile_carry(ax, ay, lastw, const_cast<char*>(sm) + kFsOff, lane);
             }
-            // every set is free here (loads past K are pads): the next tile's first groups
             cur = nxt;
-            load4(A, slots + (size_t)cur.x * 32 + lane, 0, cur.y);
-            load4(B, slots + (size_t)cur.x * 32 + lane, 4, cur.y);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bars[kTS + b]);   // this warp is done with the stage
+            at = atn;
+            A = D;
+            B = E;
+            // all warps done with block J: its ring stage is free, and no row is
+            // read-modified-written by two warps (rows change owners between blocks)
+            bar_consumers();
+            if (threadIdx.x == 0) mbar_arrive(&bars[kTS + b]);
             ++k;
         }
         bar_consumers();
         // rows of F: plain stores; a piece of a row split over several panels (bit 31) adds
         for (int r = threadIdx.x; r < R; r += kTL) {
             const int32_t q = rows[r0 + r];
-            if (q >= 0) F[q] = Fs[r];
-            else atomicAdd(F + (q & 0x7FFFFFFF), Fs[r]);
+            const float2 f = Fs[tile_slot((uint32_t)r)];
+            if (q >= 0) F[q] = f;
+            else atomicAdd(F + (q & 0x7FFFFFFF), f);
         }
         bar_consumers();              // the next panel reuses Yi / Fs
     }
+#if TILE_DIAG == 3
+    // timing probe: per (CTA, warp) total cycles and cycles waiting for Y (results overwritten)
+    if (lane == 0) F[blockIdx.x * kTW + warp] = make_float2((float)(clock64() - t_start), (float)t_wait);
+#endif
 }
 
-static size_t tile_smem_bytes(int R_max) {
-    return sizeof(float2) * ((size_t)kTS * kTB + 2 * (size_t)R_max + 2) + 2 * kTS * sizeof(uint64_t);
+static size_t tile_smem_bytes(int) {
+    return kRingOff + sizeof(float2) * (size_t)kTS * kTB + 2 * kTS * sizeof(uint64_t);
 }
 
 // F: rows [row_begin, row_end) of the plan's shard (nl = row_end - row_begin).
@@ -489,30 +568,28 @@ cudaError_t launch_attr_cb(const void* plan, const float2* Y, float2* F, int64_t
 }
 
 // ------------------------------------------------------------------ plan build
-// Sort key of an entry: (((panel NB + block) kTW + warp) << kTRbits) | local
-// row; value: the shard-local entry index.  A stable LSD radix sort of entries
-// in CSR order keeps columns ascending inside a (tile, row) run.
+// Sort key of an entry: ((panel NB + block) << kTRbits) | local row; value:
+// the shard-local entry index.  A stable LSD radix sort of entries in CSR order
+// keeps columns ascending inside a (block tile, row) run.
 __global__ void k_tile_keys(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, int64_t rb,
                             int64_t re, const int32_t* __restrict__ row_panel, const int32_t* __restrict__ row_local,
-                            const int32_t* __restrict__ row_warp, int NB, unsigned long long* __restrict__ keys,
-                            uint32_t* __restrict__ vals) {
+                            int NB, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
     const int lane = threadIdx.x & 31;
     const int64_t e0 = indptr[rb];
     for (int64_t r = rb + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); r < re;
          r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t a = indptr[r], z = indptr[r + 1];
         const unsigned long long pk = (unsigned long long)row_panel[r - rb] * (unsigned long long)NB;
-        const unsigned long long wk = (unsigned long long)row_warp[r - rb];
         const unsigned long long lr = (unsigned long long)row_local[r - rb];
         for (int64_t e = a + lane; e < z; e += 32) {
             const unsigned long long J = (unsigned long long)(indices[e] / kTB);
-            keys[e - e0] = ((((pk + J) * kTW) + wk) << kTRbits) | lr;
+            keys[e - e0] = ((pk + J) << kTRbits) | lr;
             vals[e - e0] = (uint32_t)(e - e0);
         }
     }
 }
 
-// tile start / end positions in the sorted order (empty tiles stay 0, 0)
+// block-tile start / end positions in the sorted order (empty tiles stay 0, 0)
 __global__ void k_tile_bounds(const unsigned long long* __restrict__ keys, int64_t m, int64_t* __restrict__ tstart,
                               int64_t* __restrict__ tend) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
@@ -522,61 +599,106 @@ __global__ void k_tile_bounds(const unsigned long long* __restrict__ keys, int64
     }
 }
 
-// tend -> warp steps of the tile (ceil(E / 32)), in place
-__global__ void k_tile_steps(const int64_t* __restrict__ tstart, int64_t* __restrict__ tsteps, int64_t ntiles) {
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < ntiles; q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t E = tsteps[q] - tstart[q];
-        tsteps[q] = (E + 31) / 32;
+constexpr int kSnap = 48;   // a warp boundary moves to a run boundary within this many entries
+
+// Per block tile (p, J): the row-sorted entries cut into kTW warp segments of
+// equal size, each boundary moved to the nearest run (row) boundary within
+// kSnap entries; a run longer than that is split between warps and its row
+// marked shared (hub: every flush of the row, in any block, is atomic).
+// seg[t (kTW + 1) + w] = first index of warp w's segment (seg[.. + kTW] = E);
+// steps[t kTW + w] = ceil(E_w / 32).
+__global__ void k_tile_segment(const unsigned long long* __restrict__ keys, const int64_t* __restrict__ tstart,
+                               const int64_t* __restrict__ tend, int64_t ntb, int NB,
+                               const int32_t* __restrict__ panel_off, int32_t* __restrict__ seg,
+                               int64_t* __restrict__ steps, int32_t* __restrict__ hub) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntb; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s0 = tstart[t], E = tend[t] - s0;
+        int32_t* sg = seg + t * (kTW + 1);
+        sg[0] = 0;
+        int64_t prev = 0;
+        for (int w = 1; w < kTW; ++w) {
+            const int64_t ideal = std::max<int64_t>(prev, E * w / kTW);
+            int64_t cut = -1;
+            for (int d = 0; d <= kSnap && cut < 0; ++d) {      // nearest q with a row change before q
+                const int64_t qa = ideal - d, qb = ideal + d;
+                if (qa >= prev && qa > 0 && qa < E && keys[s0 + qa - 1] != keys[s0 + qa]) cut = qa;
+                else if (qb < E && qb > 0 && qb >= prev && keys[s0 + qb - 1] != keys[s0 + qb]) cut = qb;
+            }
+            if (ideal <= 0 || ideal >= E) cut = std::min<int64_t>(std::max<int64_t>(ideal, prev), E);
+            if (cut < 0) {                                       // inside a long run: split it, shared row
+                cut = ideal;
+                const unsigned long long key = keys[s0 + cut];
+                const int64_t p = (int64_t)((key >> kTRbits) / (unsigned long long)NB);
+                atomicOr(&hub[panel_off[p] + (int32_t)(key & kLocalMask)], 1);
+            }
+            sg[w] = (int32_t)cut;
+            prev = cut;
+        }
+        sg[kTW] = (int32_t)E;
+        for (int w = 0; w < kTW; ++w) steps[t * kTW + w] = ((int64_t)sg[w + 1] - sg[w] + 31) / 32;
     }
 }
 
 // per-warp tile table: wtab[(p kTW + w) NB + J] = (first step, steps) of the
-// tile (p, J, w) = toff[t], toff[t + 1] - toff[t], t = (p NB + J) kTW + w
+// warp tile (p, J, w) = toff[u], toff[u + 1] - toff[u], u = (p NB + J) kTW + w
 __global__ void k_tile_wtab(const int64_t* __restrict__ toff, int64_t P, int64_t NB, int2* __restrict__ wtab) {
     const int64_t m = P * NB * kTW;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
         const int64_t J = q % NB, pw = q / NB, w = pw % kTW, p = pw / kTW;
-        const int64_t t = (p * NB + J) * kTW + w;
-        wtab[q] = make_int2((int32_t)toff[t], (int32_t)(toff[t + 1] - toff[t]));
+        const int64_t u = (p * NB + J) * kTW + w;
+        wtab[q] = make_int2((int32_t)toff[u], (int32_t)(toff[u + 1] - toff[u]));
     }
 }
 
-// Slot of sorted position q: tile t, index in tile i, chunk (lane) l = i / K,
-// step k = i - l K.  FLUSH: the row's run ends at this entry (the next entry
-// of the tile is another row, or the tile ends); at a chunk end a run that
-// continues is carried out instead (k_attr_tile, tile_carry).
+// Slot of sorted position q: block tile t, index i in the tile, warp w (its
+// segment holds i), index iw in the segment, chunk (lane) l = iw / K, step
+// k = iw - l K with K = the segment's steps.  FLUSH: the row's run ends at
+// this entry (the next entry of the tile is another row, or the tile ends);
+// at a chunk end a run that continues is carried out instead (tile_carry).
+// NEWROW: the first entry of a chunk or of a run.  HUB: the row is shared.
 __global__ void k_tile_fill(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t m,
                             const int64_t* __restrict__ tstart, const int64_t* __restrict__ tend,
-                            const int64_t* __restrict__ toff, const int32_t* __restrict__ indices,
-                            const float* __restrict__ values, int64_t e0, uint2* __restrict__ slots) {
+                            const int32_t* __restrict__ seg, const int64_t* __restrict__ toff, int NB,
+                            const int32_t* __restrict__ panel_off, const int32_t* __restrict__ hub,
+                            const int32_t* __restrict__ indices, const float* __restrict__ values, int64_t e0,
+                            uint2* __restrict__ slots) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long key = keys[q];
         const unsigned long long t = key >> kTRbits;
         const int64_t s0 = tstart[t], E = tend[t] - s0;
-        const int64_t K = (E + 31) / 32;
-        const int64_t i = q - s0, l = i / K, kk = i - l * K;
+        const int64_t i = q - s0;
+        const int32_t* sg = seg + t * (kTW + 1);
+        int w = 0;
+        while (w + 1 < kTW && sg[w + 1] <= i) ++w;
+        const int64_t u = (int64_t)t * kTW + w;
+        const int64_t K = toff[u + 1] - toff[u];
+        const int64_t iw = i - sg[w], l = iw / K, kk = iw - l * K;
         const bool flush = (i + 1 == E) || keys[q + 1] != key;
-        const bool newrow = (i == l * K) || keys[q - 1] != key;
+        const bool newrow = (kk == 0) || keys[q - 1] != key;
         const int64_t e = (int64_t)vals[q] + e0;
         const uint32_t col = (uint32_t)(indices[e] % kTB);
-        const uint32_t lr = (uint32_t)(key & (kTR - 1));
-        uint32_t w = (col << 3) | (lr << 15);
-        if (flush) w |= kFlush;
-        if (newrow) w |= kNewRow;
-        slots[(size_t)(toff[t] + kk) * 32 + l] = make_uint2(w, __float_as_uint(values[e]));
+        const uint32_t lr = (uint32_t)(key & kLocalMask);
+        const int64_t p = (int64_t)(t / (unsigned long long)NB);
+        uint32_t word = (col << 3) | (tile_slot(lr) << 16);
+        if (flush) word |= kFlush;
+        if (newrow) word |= kNewRow;
+        if (hub[panel_off[p] + (int32_t)lr]) word |= kHub;
+        slots[(size_t)(toff[u] + kk) * 32 + l] = make_uint2(word, __float_as_uint(values[e]));
     }
 }
 
 struct TileWs {
-    int32_t *row_panel, *row_local, *row_warp;
+    int32_t *row_panel, *row_local, *seg, *hub, *panel_off;
     unsigned long long *keys_a, *keys_b;
     uint32_t *vals_a, *vals_b;
-    int64_t *tstart, *tend, *toff;
+    int64_t *tstart, *tend, *steps, *toff;
     void* cub_tmp;
     size_t cub_bytes, bytes;
 };
 
-static TileWs tile_ws_map(void* base, int64_t nr, int64_t m, int64_t ntiles) {
+// ntb block tiles (P NB), ntiles = ntb kTW warp tiles
+static TileWs tile_ws_map(void* base, int64_t nr, int64_t m, int64_t ntb, int64_t P) {
+    const int64_t ntiles = ntb * kTW;
     TileWs w{};
     size_t cb = 0, cs = 0;
     cub::DoubleBuffer<unsigned long long> dk(nullptr, nullptr);
@@ -592,13 +714,16 @@ static TileWs tile_ws_map(void* base, int64_t nr, int64_t m, int64_t ntiles) {
     };
     w.row_panel = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(nr, 1));
     w.row_local = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(nr, 1));
-    w.row_warp = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(nr, 1));
+    w.seg = (int32_t*)take(sizeof(int32_t) * (size_t)(ntb * (kTW + 1)));
+    w.hub = (int32_t*)take(sizeof(int32_t) * std::max<int64_t>(nr, 1));
+    w.panel_off = (int32_t*)take(sizeof(int32_t) * (size_t)(P + 1));
     w.keys_a = (unsigned long long*)take(sizeof(unsigned long long) * std::max<int64_t>(m, 1));
     w.keys_b = (unsigned long long*)take(sizeof(unsigned long long) * std::max<int64_t>(m, 1));
     w.vals_a = (uint32_t*)take(sizeof(uint32_t) * std::max<int64_t>(m, 1));
     w.vals_b = (uint32_t*)take(sizeof(uint32_t) * std::max<int64_t>(m, 1));
-    w.tstart = (int64_t*)take(sizeof(int64_t) * (ntiles + 1));
-    w.tend = (int64_t*)take(sizeof(int64_t) * (ntiles + 1));
+    w.tstart = (int64_t*)take(sizeof(int64_t) * (ntb + 1));
+    w.tend = (int64_t*)take(sizeof(int64_t) * (ntb + 1));
+    w.steps = (int64_t*)take(sizeof(int64_t) * (ntiles + 1));
     w.toff = (int64_t*)take(sizeof(int64_t) * (ntiles + 1));
     w.cub_tmp = take(w.cub_bytes);
     w.bytes = off;
@@ -619,7 +744,7 @@ static int tile_rows(const tsnet_csr* P, const tsnet_shard* sh, int64_t& rb, int
 }
 
 struct TileCut {
-    std::vector<int32_t> row_panel, row_local, row_warp, panel_off, panel_rows;
+    std::vector<int32_t> row_panel, row_local, panel_off, panel_rows;
     std::vector<int64_t> ip;
     int32_t P = 0, R_max = 0;
     int64_t nnz_s = 0;
@@ -639,7 +764,6 @@ static int tile_host_cut(const tsnet_csr* P, int64_t rb, int64_t re, cudaStream_
     TSNET_ARG(cut.P > 0, "row partition failed");
     cut.R_max = 0;
     for (int32_t p = 0; p < cut.P; ++p) cut.R_max = std::max(cut.R_max, cut.panel_off[p + 1] - cut.panel_off[p]);
-    tile_warps(cut.ip.data(), cut.P, kTW, cut.panel_off, cut.panel_rows, cut.row_warp);
     return TSNET_OK;
 }
 
@@ -674,13 +798,13 @@ int tsnet_plan_query(const tsnet_csr* P, const tsnet_shard* shard, size_t* plan_
     if (st != TSNET_OK) return st;
     TileCut cut;
     if ((st = tile_host_cut(P, rb, re, (cudaStream_t)stream, cut)) != TSNET_OK) return st;
-    // upper bound of the steps: every non-empty tile pads < one step
+    // upper bound of the steps: every non-empty warp tile pads < one step
     const int64_t NB = std::max<int64_t>(1, (P->n + kTB - 1) / kTB);
-    const int64_t ntiles = (int64_t)cut.P * NB * kTW;
+    const int64_t ntb = (int64_t)cut.P * NB, ntiles = ntb * kTW;
     const int64_t steps_max = (cut.nnz_s + 31) / 32 + std::min<int64_t>(ntiles, cut.nnz_s);
     const TileHeader h = tile_layout(P->n, rb, re, cut.nnz_s, cut.P, cut.R_max, steps_max);
     *plan_bytes = (size_t)h.bytes;
-    *ws_bytes = tile_ws_map(nullptr, re - rb, cut.nnz_s, ntiles).bytes;
+    *ws_bytes = tile_ws_map(nullptr, re - rb, cut.nnz_s, ntb, cut.P).bytes;
     return TSNET_OK;
 }
 
@@ -698,34 +822,38 @@ int tsnet_plan_build(const tsnet_csr* P, const tsnet_shard* shard, void* plan, s
     if ((st = tile_host_cut(P, rb, re, s, cut)) != TSNET_OK) return st;
     const int64_t nr = re - rb, m = cut.nnz_s;
     const int64_t NB = std::max<int64_t>(1, (P->n + kTB - 1) / kTB);
-    const int64_t ntiles = (int64_t)cut.P * NB * kTW;
-    TSNET_ARG(ntiles < ((int64_t)1 << (64 - kTRbits - 1)), "too many tiles");
-    TileWs w = tile_ws_map(ws, nr, m, ntiles);
+    const int64_t ntb = (int64_t)cut.P * NB, ntiles = ntb * kTW;
+    TSNET_ARG(ntb < ((int64_t)1 << (64 - kTRbits - 1)), "too many tiles");
+    TileWs w = tile_ws_map(ws, nr, m, ntb, cut.P);
     TSNET_ARG(ws != nullptr && ws_bytes >= w.bytes, "plan workspace too small (%zu < %zu bytes)", ws_bytes, w.bytes);
     if (nr > 0) {
         TSNET_CUDA(cudaMemcpyAsync(w.row_panel, cut.row_panel.data(), sizeof(int32_t) * nr, cudaMemcpyHostToDevice, s));
         TSNET_CUDA(cudaMemcpyAsync(w.row_local, cut.row_local.data(), sizeof(int32_t) * nr, cudaMemcpyHostToDevice, s));
-        TSNET_CUDA(cudaMemcpyAsync(w.row_warp, cut.row_warp.data(), sizeof(int32_t) * nr, cudaMemcpyHostToDevice, s));
     }
-    TSNET_CUDA(cudaMemsetAsync(w.tstart, 0, sizeof(int64_t) * (ntiles + 1), s));
-    TSNET_CUDA(cudaMemsetAsync(w.tend, 0, sizeof(int64_t) * (ntiles + 1), s));
+    TSNET_CUDA(cudaMemcpyAsync(w.panel_off, cut.panel_off.data(), sizeof(int32_t) * (cut.P + 1), cudaMemcpyHostToDevice,
+                               s));
+    TSNET_CUDA(cudaMemsetAsync(w.hub, 0, sizeof(int32_t) * std::max<int64_t>(nr, 1), s));
+    TSNET_CUDA(cudaMemsetAsync(w.tstart, 0, sizeof(int64_t) * (ntb + 1), s));
+    TSNET_CUDA(cudaMemsetAsync(w.tend, 0, sizeof(int64_t) * (ntb + 1), s));
+    TSNET_CUDA(cudaMemsetAsync(w.steps, 0, sizeof(int64_t) * (ntiles + 1), s));
     int end_bit = kTRbits;
-    while (end_bit < 64 && ((uint64_t)1 << (end_bit - kTRbits)) < (uint64_t)ntiles) ++end_bit;
+    while (end_bit < 64 && ((uint64_t)1 << (end_bit - kTRbits)) < (uint64_t)ntb) ++end_bit;
     cub::DoubleBuffer<unsigned long long> dk(w.keys_a, w.keys_b);
     cub::DoubleBuffer<uint32_t> dv(w.vals_a, w.vals_b);
     if (m > 0) {
-        k_tile_keys<<<num_sms() * 8, 256, 0, s>>>(P->indptr, P->indices, rb, re, w.row_panel, w.row_local,
-                                                  w.row_warp, (int)NB, w.keys_a, w.vals_a);
+        k_tile_keys<<<num_sms() * 8, 256, 0, s>>>(P->indptr, P->indices, rb, re, w.row_panel, w.row_local, (int)NB,
+                                                  w.keys_a, w.vals_a);
         TSNET_LAUNCH_CHECK();
         size_t tb = w.cub_bytes;
         TSNET_CUDA(cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, dk, dv, m, 0, end_bit, s));
         k_tile_bounds<<<num_sms() * 8, 256, 0, s>>>(dk.Current(), m, w.tstart, w.tend);
         TSNET_LAUNCH_CHECK();
-        k_tile_steps<<<num_sms() * 4, 256, 0, s>>>(w.tstart, w.tend, ntiles);
-        TSNET_LAUNCH_CHECK();
     }
+    k_tile_segment<<<std::max<int64_t>(1, std::min<int64_t>((ntb + 255) / 256, num_sms() * 8)), 256, 0, s>>>(
+        dk.Current(), w.tstart, w.tend, ntb, (int)NB, w.panel_off, w.seg, w.steps, w.hub);
+    TSNET_LAUNCH_CHECK();
     size_t tb = w.cub_bytes;
-    TSNET_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.tend, w.toff, ntiles + 1, s));
+    TSNET_CUDA(cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.steps, w.toff, ntiles + 1, s));
     int64_t steps = 0;
     TSNET_CUDA(cudaMemcpyAsync(&steps, w.toff + ntiles, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     TSNET_CUDA(cudaStreamSynchronize(s));
@@ -743,13 +871,9 @@ int tsnet_plan_build(const tsnet_csr* P, const tsnet_shard* shard, void* plan, s
                                    cudaMemcpyHostToDevice, s));
     if (steps > 0) TSNET_CUDA(cudaMemsetAsync(d_slots, 0, sizeof(uint2) * 32 * (size_t)steps, s));
     if (m > 0) {
-        // tend holds steps now; the fill needs the tile ends again
-        TSNET_CUDA(cudaMemsetAsync(w.tend, 0, sizeof(int64_t) * (ntiles + 1), s));
-        TSNET_CUDA(cudaMemsetAsync(w.tstart, 0, sizeof(int64_t) * (ntiles + 1), s));
-        k_tile_bounds<<<num_sms() * 8, 256, 0, s>>>(dk.Current(), m, w.tstart, w.tend);
-        TSNET_LAUNCH_CHECK();
-        k_tile_fill<<<num_sms() * 8, 256, 0, s>>>(dk.Current(), dv.Current(), m, w.tstart, w.tend, w.toff,
-                                                  P->indices, P->values, cut.ip.front(), d_slots);
+        k_tile_fill<<<num_sms() * 8, 256, 0, s>>>(dk.Current(), dv.Current(), m, w.tstart, w.tend, w.seg, w.toff,
+                                                  (int)NB, w.panel_off, w.hub, P->indices, P->values, cut.ip.front(),
+                                                  d_slots);
         TSNET_LAUNCH_CHECK();
     }
     TSNET_CUDA(cudaMemcpyAsync(pb, &h, sizeof(TileHeader), cudaMemcpyHostToDevice, s));

@@ -174,7 +174,6 @@ __global__ void __launch_bounds__(256, MINB) k_attr_sell_g(const uint8_t* __rest
 // 0.921-0.943; TMA-staged entries 1.01-1.47 (the ring's shared memory takes
 // L1 capacity from the Y_j gathers, which hit L1 on a mesh).
 static constexpr auto sell_kernel = k_attr_sell_g<4, 4, false, 4>;
-static constexpr auto sell_move_kernel = k_attr_sell_g<4, 4, true, 3>;
 
 static int resident_of(const void* k) {
     int r = 0;
@@ -189,18 +188,6 @@ cudaError_t launch_attr_sell(const void* plan, const float2* Y, float2* F, int64
     const int blocks = (int)std::max<int64_t>(
         1, std::min<int64_t>((slices + 7) / 8, (int64_t)kNumSMs * resident_of((const void*)sell_kernel)));
     sell_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint8_t*>(plan), Y, F, SellMoveArgs{});
-    return cudaGetLastError();
-}
-
-// SpMV + move of the plan's rows (the same kernel shape with the a7
-// epilogue); F_attr is not stored.
-cudaError_t launch_attr_sell_move(const void* plan, const float2* Y, int64_t nl, const SellMoveArgs& m,
-                                  cudaStream_t s) {
-    if (nl == 0) return cudaSuccess;
-    const int64_t slices = (nl + 31) / 32;
-    const int blocks = (int)std::max<int64_t>(
-        1, std::min<int64_t>((slices + 7) / 8, (int64_t)kNumSMs * resident_of((const void*)sell_move_kernel)));
-    sell_move_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint8_t*>(plan), Y, nullptr, m);
     return cudaGetLastError();
 }
 

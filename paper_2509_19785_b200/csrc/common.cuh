@@ -169,8 +169,6 @@ struct SellMoveArgs {
     float lambda_kl, cn;
     tsnet_step_params sp;
 };
-cudaError_t launch_attr_sell_move(const void* plan, const float2* Y, int64_t nl, const SellMoveArgs& m,
-                                  cudaStream_t s);
 cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2* f_field, double* Z,
                             cudaStream_t s);
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,

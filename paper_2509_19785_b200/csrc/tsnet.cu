@@ -73,12 +73,24 @@ static int check_csr(const tsnet_csr* P) {
     return TSNET_OK;
 }
 
+// the call's rows [0, n) or the shard's; a plan must have been built for them
+static int check_rows(const tsnet_csr* P, const tsnet_shard* sh) {
+    const int64_t rb = sh ? sh->row_begin : 0, re = sh ? sh->row_end : P->n;
+    TSNET_ARG(0 <= rb && rb <= re && re <= P->n, "rows [%lld, %lld) outside [0, %lld)", (long long)rb, (long long)re,
+              (long long)P->n);
+    TSNET_ARG(P->plan == nullptr || (P->plan_row_begin == rb && P->plan_row_end == re),
+              "the plan of P holds rows [%lld, %lld), the call rows [%lld, %lld)", (long long)P->plan_row_begin,
+              (long long)P->plan_row_end, (long long)rb, (long long)re);
+    return TSNET_OK;
+}
+
 static int prepare(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp, const tsnet_shard* sh, void* ws,
                    size_t ws_bytes, Ws& w, GradArgs& a) {
     int st;
     if ((st = check_csr(P)) != TSNET_OK) return st;
     if ((st = check_grad_params(gp)) != TSNET_OK) return st;
     if ((st = check_shard(sh, P->n)) != TSNET_OK) return st;
+    if ((st = check_rows(P, sh)) != TSNET_OK) return st;
     TSNET_ARG(P->n == 0 || Y != nullptr, "Y is NULL");
     w = ws_map(ws, P->n, P->nnz, gp->I_max);
     TSNET_ARG(ws != nullptr && ws_bytes >= w.bytes, "workspace too small (%zu < %zu bytes)", ws_bytes, w.bytes);
@@ -108,7 +120,7 @@ static size_t grid_floats(const Ws& w) { return (size_t)4 * w.N_max * w.N_max; }
 // A second stream per (host thread, device) for the field phase, which is
 // independent of the attractive SpMV until the gather/update: the two chains
 // run concurrently (fork/join by events, so the pattern is also captured into
-// a CUDA graph as two branches).  TSNET_FIELD_STREAM=0 keeps one stream.
+// a CUDA graph as two branches).
 constexpr int kHostChunksMax = 16;
 
 struct SideStream {
@@ -117,19 +129,10 @@ struct SideStream {
     // priority: its moves gate the downloads); field: the field chain forked
     // beside the SpMV in a device step (normal priority: preempting the SpMV's
     // CTAs cost 1% there, r1cn)
-    cudaStream_t side = nullptr, field = nullptr, copy = nullptr, d2h = nullptr, spmv2 = nullptr;
+    cudaStream_t side = nullptr, field = nullptr, copy = nullptr, d2h = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr, copied = nullptr, y_in = nullptr, drained = nullptr, zeroed = nullptr;
     cudaEvent_t attr_done[kHostChunksMax] = {}, moved[kHostChunksMax] = {}, state_in[kHostChunksMax] = {};
 };
-
-static bool side_enabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TSNET_FIELD_STREAM");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v == 1;
-}
 
 static cudaError_t side_stream(SideStream*& out) {
     static thread_local SideStream ss[16];
@@ -140,20 +143,14 @@ static cudaError_t side_stream(SideStream*& out) {
     if (x.dev != dev) {
         // side (pipelined host step): the field chain is a row of short
         // dependent kernels; at the highest priority its CTAs go ahead of
-        // queued SpMV CTAs, so the first moves start early (TSNET_FIELD_PRIORITY=0:
-        // default priority); field (device step): default priority
-        // (TSNET_FIELD_PRIORITY=1: highest), both probing knobs
+        // queued SpMV CTAs, so the first moves start early; field (device
+        // step): default priority (the highest cost 1% there, r1cn)
         int lo = 0, hi = 0;
         if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return e;
-        const char* pe = getenv("TSNET_FIELD_PRIORITY");
-        const int prio = (pe && pe[0] == '0') ? lo : hi;
-        if ((e = cudaStreamCreateWithPriority(&x.side, cudaStreamNonBlocking, prio)) != cudaSuccess) return e;
-        if ((e = cudaStreamCreateWithPriority(&x.field, cudaStreamNonBlocking, pe && pe[0] == '1' ? hi : lo)) !=
-            cudaSuccess)
-            return e;
+        if ((e = cudaStreamCreateWithPriority(&x.side, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithPriority(&x.field, cudaStreamNonBlocking, lo)) != cudaSuccess) return e;
         if ((e = cudaStreamCreateWithFlags(&x.copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
         if ((e = cudaStreamCreateWithFlags(&x.d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
-        if ((e = cudaStreamCreateWithFlags(&x.spmv2, cudaStreamNonBlocking)) != cudaSuccess) return e;
         if ((e = cudaEventCreateWithFlags(&x.zeroed, cudaEventDisableTiming)) != cudaSuccess) return e;
         if ((e = cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
         if ((e = cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming)) != cudaSuccess) return e;
@@ -171,19 +168,6 @@ static cudaError_t side_stream(SideStream*& out) {
     return cudaSuccess;
 }
 
-// TSNET_FUSED_MOVE=1: with a sliced-ELL plan, run the field phase first and
-// fuse the move into the SpMV epilogue.  Off by default: measured 1015 vs
-// 1007 it/s on cfg 5 and 5577 vs 5965 it/s on cfg 3 -- the field phase then
-// no longer overlaps the SpMV, which costs about what k_update did.
-static bool fused_move_enabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TSNET_FUSED_MOVE");
-        v = (e && e[0] == '1') ? 1 : 0;
-    }
-    return v == 1;
-}
-
 static int eval_gradient_parts(const Ws& w, const GradArgs& a, const tsnet_shard* sh, cudaStream_t s) {
     int st;
     if ((st = check_comm(sh, a)) != TSNET_OK) return st;
@@ -191,22 +175,17 @@ static int eval_gradient_parts(const Ws& w, const GradArgs& a, const tsnet_shard
     SideStream* ss = nullptr;
     // the grid chain (field + its all-reduce) runs on the side stream, overlapped
     // with the SpMV (SURVEY §8(e) "chain G"); the Y all-gather stays on `s`
-    const bool fork = side_enabled();
-    if (fork) TSNET_CUDA(side_stream(ss));
-    cudaStream_t fs = fork ? ss->field : s;
-    if (fork) {
-        TSNET_CUDA(cudaEventRecord(ss->fork, s));
-        TSNET_CUDA(cudaStreamWaitEvent(fs, ss->fork, 0));
-    }
+    TSNET_CUDA(side_stream(ss));
+    cudaStream_t fs = ss->field;
+    TSNET_CUDA(cudaEventRecord(ss->fork, s));
+    TSNET_CUDA(cudaStreamWaitEvent(fs, ss->fork, 0));
     TSNET_CUDA(launch_field_local(w, a, fs, multi));
     if (multi && (st = comm_allreduce_grid(sh->comm, reinterpret_cast<float*>(w.wgrid), grid_floats(w), fs)) != TSNET_OK)
         return st;
     TSNET_CUDA(launch_field_conv(w, a, fs));
     TSNET_CUDA(launch_spmv(w, a, s));
-    if (fork) {
-        TSNET_CUDA(cudaEventRecord(ss->join, fs));
-        TSNET_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
-    }
+    TSNET_CUDA(cudaEventRecord(ss->join, fs));
+    TSNET_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
     return TSNET_OK;
 }
 
@@ -245,9 +224,10 @@ size_t tsnet_workspace_bytes(int64_t n, int64_t nnz, const tsnet_grad_params* gp
     return ws_map(nullptr, n, nnz, I_max).bytes;
 }
 
-int tsnet_attr(const tsnet_csr* P, const float* Y, float* f_attr, tsnet_stream_t stream) {
+int tsnet_attr(const tsnet_csr* P, const float* Y, const tsnet_shard* shard, float* f_attr, tsnet_stream_t stream) {
     int st;
     if ((st = check_csr(P)) != TSNET_OK) return st;
+    if ((st = check_rows(P, shard)) != TSNET_OK) return st;
     TSNET_ARG(P->n == 0 || (Y != nullptr && f_attr != nullptr), "Y or f_attr is NULL");
     if (P->n == 0) return TSNET_OK;
     Ws w{};
@@ -255,8 +235,8 @@ int tsnet_attr(const tsnet_csr* P, const float* Y, float* f_attr, tsnet_stream_t
     GradArgs a{};
     a.n = P->n;
     a.nnz = P->nnz;
-    a.rb = 0;
-    a.re = P->n;
+    a.rb = shard ? shard->row_begin : 0;
+    a.re = shard ? shard->row_end : P->n;
     a.indptr = P->indptr;
     a.indices = P->indices;
     a.values = P->values;
@@ -314,26 +294,6 @@ static int step_impl(const tsnet_csr* P, float* Y, float* vel, float* gains, con
     const bool multi = shard != nullptr && shard->comm != nullptr;
     TSNET_ARG(!multi || shard->bounds != nullptr, "a communicating shard needs shard->bounds to all-gather Y");
     if (a.n == 0) return TSNET_OK;
-    if (a.plan && a.plan_kind == TSNET_PLAN_SELL && !sp->recenter && fused_move_enabled()) {
-        // sliced-ELL plan: field phase first, then the SpMV with the move fused
-        // into its epilogue (no F_attr round trip, no k_update), new positions
-        // via w.ynext (the SpMV still gathers the old ones) copied back
-        if ((st = check_comm(shard, a)) != TSNET_OK) return st;
-        TSNET_CUDA(launch_field_local(w, a, s, multi));
-        if (multi && (st = comm_allreduce_grid(shard->comm, reinterpret_cast<float*>(w.wgrid), grid_floats(w), s)) !=
-                         TSNET_OK)
-            return st;
-        TSNET_CUDA(launch_field_conv(w, a, s));
-        if (before_update) TSNET_CUDA(cudaStreamWaitEvent(s, before_update, 0));
-        const int64_t nl = a.re - a.rb;
-        SellMoveArgs m{w.geo, w.fgrid, w.box, w.uv, w.ynext,
-                       reinterpret_cast<float2*>(vel) + a.rb, reinterpret_cast<float2*>(gains) + a.rb,
-                       a.lambda_kl, (float)((double)a.lambda_c / (double)a.n), *sp};
-        TSNET_CUDA(launch_attr_sell_move(a.plan, a.Y, nl, m, s));
-        TSNET_CUDA(cudaMemcpyAsync(Y + 2 * a.rb, w.ynext, sizeof(float2) * (size_t)nl, cudaMemcpyDeviceToDevice, s));
-        if (multi) return comm_allgather_rows(shard->comm, Y, shard->bounds, shard->world, s);
-        return TSNET_OK;
-    }
     if ((st = eval_gradient_parts(w, a, shard, s)) != TSNET_OK) return st;
     if (before_update) TSNET_CUDA(cudaStreamWaitEvent(s, before_update, 0));
     TSNET_CUDA(launch_update(w, a, reinterpret_cast<float2*>(Y), reinterpret_cast<float2*>(vel),
@@ -395,28 +355,11 @@ int tsnet_step_finish(const tsnet_csr* P, float* Y, float* vel, float* gains, co
 
 namespace tsnet {
 
-// TSNET_HOST_SPMV_STREAMS=2 alternates the chunks' SpMV over two streams
-// (probing; measured 821 vs 835 it/s e2e on cfg 4 for one stream: the
-// overlapping chunks delay the first moves more than the tails cost)
-static int host_spmv_streams() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TSNET_HOST_SPMV_STREAMS");
-        v = (e && e[0] == '2') ? 2 : 1;
-    }
-    return v;
-}
-
-// Row chunks of the pipelined host step (TSNET_HOST_CHUNKS, default 4; 1 = no pipeline):
-// measured on cfg 4 with the multi-wave SpMV, e2e 815 / 850 / 851 / 827 / 823 / 770 it/s for 2 / 3 / 4 / 5 / 6 / 8.
-static int host_chunks(int64_t n) {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TSNET_HOST_CHUNKS");
-        v = e ? std::max(1, std::min(kHostChunksMax, atoi(e))) : 4;
-    }
-    return n >= (int64_t)v * 16384 ? v : 1;
-}
+// Row chunks of the pipelined host step (1 = no pipeline): measured on cfg 4
+// with the multi-wave SpMV, e2e 815 / 850 / 851 / 827 / 823 / 770 it/s for
+// 2 / 3 / 4 / 5 / 6 / 8 chunks (r1bx).
+constexpr int kHostChunks = 4;
+static int host_chunks(int64_t n) { return n >= (int64_t)kHostChunks * 16384 ? kHostChunks : 1; }
 
 // Row cut of the pipelined host step: chunk c ends at the first row whose
 // indptr reaches nnz * (c + 1) / chunks (equal SpMV work per chunk).  Found by
@@ -465,41 +408,6 @@ static int chunk_rows(const tsnet_csr* P, int chunks, int64_t* cut, int64_t* cut
     return TSNET_OK;
 }
 
-// TSNET_HOST_TRACE=1: the pipelined host step records timing events at its
-// stage boundaries and prints them (ms after the call's first copy) to stderr.
-struct HostTrace {
-    bool on = false;
-    int k = 0;
-    cudaEvent_t ev[64] = {};
-    const char* name[64] = {};
-    int idx[64] = {};
-    void init() {
-        static int v = -1;
-        if (v < 0) v = getenv("TSNET_HOST_TRACE") ? 1 : 0;
-        on = v == 1;
-    }
-    void mark(const char* what, int i, cudaStream_t st) {
-        if (!on || k >= 64) return;
-        if (!ev[k]) cudaEventCreate(&ev[k]);
-        cudaEventRecord(ev[k], st);
-        name[k] = what;
-        idx[k++] = i;
-    }
-    void print() {
-        if (!on || k == 0) return;
-        cudaEventSynchronize(ev[k - 1]);
-        for (int q = 0; q < k; ++q) {
-            cudaEventSynchronize(ev[q]);
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, ev[0], ev[q]);
-            fprintf(stderr, "%s%s[%d] %.3f", q ? "  " : "trace ", name[q], idx[q], ms);
-        }
-        fprintf(stderr, "\n");
-        for (int q = 0; q < k; ++q) cudaEventDestroy(ev[q]);
-        k = 0;
-    }
-};
-
 // tsnet_step_host without recentring, shards or a plan: the host transfers of
 // the state overlap the attractive SpMV.  Rows are cut into `chunks` chunks.
 // Streams: `s` uploads Y, then runs the SpMV of chunk after chunk; `copy`
@@ -520,12 +428,8 @@ static int step_host_pipelined(const tsnet_csr* P, float* Y_host, float* vel_hos
     int st0 = chunk_rows(P, chunks, cut, cut_nnz);
     if (st0 != TSNET_OK) return st0;
     auto rows = [&](int c) { return cut[c]; };
-    HostTrace tr;
-    tr.init();
-    tr.mark("start", 0, s);
     TSNET_CUDA(cudaMemcpyAsync(dY, Y_host, b, cudaMemcpyHostToDevice, s));
     TSNET_CUDA(cudaEventRecord(ss->y_in, s));
-    tr.mark("y_in", 0, s);
     // vel/gains after Y (they share the host link; Y gates everything)
     TSNET_CUDA(cudaStreamWaitEvent(ss->copy, ss->y_in, 0));
     for (int k = 0; k < chunks; ++k) {   // in processing order (last chunk first, below)
@@ -534,7 +438,6 @@ static int step_host_pipelined(const tsnet_csr* P, float* Y_host, float* vel_hos
         TSNET_CUDA(cudaMemcpyAsync(dV + rows(c), vel_host + o, cb, cudaMemcpyHostToDevice, ss->copy));
         TSNET_CUDA(cudaMemcpyAsync(dG + rows(c), gains_host + o, cb, cudaMemcpyHostToDevice, ss->copy));
         TSNET_CUDA(cudaEventRecord(ss->state_in[c], ss->copy));
-        tr.mark("vg_in", c, ss->copy);
     }
     Ws w;
     GradArgs a;
@@ -544,41 +447,29 @@ static int step_host_pipelined(const tsnet_csr* P, float* Y_host, float* vel_hos
     TSNET_CUDA(cudaStreamWaitEvent(fs, ss->y_in, 0));
     TSNET_CUDA(launch_field_local(w, a, fs, false));
     TSNET_CUDA(launch_field_conv(w, a, fs));
-    tr.mark("field", 0, fs);
     TSNET_CUDA(cudaMemsetAsync(w.f_attr, 0, b, s));
-    // optionally the chunks' SpMV alternate between two streams, so that one
-    // chunk's last wave overlaps the next chunk's first
-    const bool two = host_spmv_streams() == 2;
-    if (two) {
-        TSNET_CUDA(cudaEventRecord(ss->zeroed, s));
-        TSNET_CUDA(cudaStreamWaitEvent(ss->spmv2, ss->zeroed, 0));
-    }
     // last chunk first: chunks have equal nnz, so the first rows (hubs of a
     // power-law graph) form the chunk with the fewest rows -- processed last,
     // its download is the short tail that nothing overlaps
     for (int k = 0; k < chunks; ++k) {
         const int c = chunks - 1 - k;
         const int64_t r0 = rows(c), r1 = rows(c + 1);
-        cudaStream_t sa = (two && (k & 1)) ? ss->spmv2 : s;
+        cudaStream_t sa = s;
         TSNET_CUDA(launch_spmv_rows(w, a, r0, r1, cut_nnz[c + 1] - cut_nnz[c], sa));
         TSNET_CUDA(cudaEventRecord(ss->attr_done[c], sa));
-        tr.mark("spmv", c, sa);
         TSNET_CUDA(cudaStreamWaitEvent(fs, ss->attr_done[c], 0));
         TSNET_CUDA(cudaStreamWaitEvent(fs, ss->state_in[c], 0));
         TSNET_CUDA(launch_update_rows(w, a, r0, r1, dYn, dV, dG, *sp, fs));
         TSNET_CUDA(cudaEventRecord(ss->moved[c], fs));
-        tr.mark("move", c, fs);
         TSNET_CUDA(cudaStreamWaitEvent(ss->d2h, ss->moved[c], 0));
         const size_t o = 2 * (size_t)r0, cb = sizeof(float2) * (size_t)(r1 - r0);
         TSNET_CUDA(cudaMemcpyAsync(Y_host + o, dYn + r0, cb, cudaMemcpyDeviceToHost, ss->d2h));
         TSNET_CUDA(cudaMemcpyAsync(vel_host + o, dV + r0, cb, cudaMemcpyDeviceToHost, ss->d2h));
         TSNET_CUDA(cudaMemcpyAsync(gains_host + o, dG + r0, cb, cudaMemcpyDeviceToHost, ss->d2h));
-        tr.mark("d2h", c, ss->d2h);
     }
     TSNET_CUDA(cudaEventRecord(ss->drained, ss->d2h));
     TSNET_CUDA(cudaStreamWaitEvent(s, ss->drained, 0));
     TSNET_CUDA(cudaStreamSynchronize(s));
-    tr.print();
     return TSNET_OK;
 }
 
@@ -607,7 +498,7 @@ int tsnet_step_host(const tsnet_csr* P, float* Y_host, float* vel_host, float* g
     TSNET_CUDA(cudaEventRecord(ss->fork, s));                  // after the previous work on s
     const int chunks = host_chunks(n);
     if (chunks > 1 && sp != nullptr && !sp->recenter && P->plan == nullptr && !sharded(shard, n) &&
-        (shard == nullptr || shard->comm == nullptr) && side_enabled()) {
+        (shard == nullptr || shard->comm == nullptr)) {
         TSNET_CUDA(cudaStreamWaitEvent(ss->side, ss->fork, 0));
         TSNET_CUDA(cudaStreamWaitEvent(ss->copy, ss->fork, 0));
         return step_host_pipelined(P, Y_host, vel_host, gains_host, gp, sp, ws, ws_bytes, s, ss, chunks, w0.state);

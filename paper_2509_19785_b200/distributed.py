@@ -45,8 +45,9 @@ class ShardedLayout:
         self.comm = tsnet_comm_init(uid, world, rank)
         self.shard = Shard(rank, world, bounds, self.comm)
         # the attractive SpMV reads the own rows of P (CSR), or a plan of them
-        # (attach_plan: "csr", "cb", "sell", "auto")
-        self.P = attach_plan(P, plan, self.shard)
+        # (attach_plan: "csr", "cb", "sell", "auto") attached to a shallow copy,
+        # so the caller's P keeps its own plan
+        self.P = attach_plan(P.without_plan(), plan, self.shard)
         self.Y = Y0.clone()
         self.vel = torch.zeros_like(self.Y)
         self.gains = torch.ones_like(self.Y)

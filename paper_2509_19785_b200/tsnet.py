@@ -32,7 +32,8 @@ class tsnet_graph(ctypes.Structure):
 
 class tsnet_csr(ctypes.Structure):
     _fields_ = [("n", c_i64), ("nnz", c_i64), ("capacity", c_i64), ("indptr", c_vp), ("indices", c_vp),
-                ("values", c_vp), ("plan", c_vp), ("plan_kind", c_i32)]
+                ("values", c_vp), ("plan", c_vp), ("plan_kind", c_i32), ("plan_row_begin", c_i64),
+                ("plan_row_end", c_i64)]
 
 
 class tsnet_grad_params(ctypes.Structure):
@@ -66,7 +67,7 @@ SIGNATURES = [
     ("tsnet_workspace_bytes", c_sz, [c_i64, c_i64, ctypes.POINTER(tsnet_grad_params), ctypes.POINTER(tsnet_shard)]),
     ("tsnet_grad", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, ctypes.POINTER(tsnet_grad_params),
                                   ctypes.POINTER(tsnet_shard), c_vp, c_vp, c_vp, c_sz, c_vp]),
-    ("tsnet_attr", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, c_vp, c_vp]),
+    ("tsnet_attr", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, ctypes.POINTER(tsnet_shard), c_vp, c_vp]),
     ("tsnet_grad_parts", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, ctypes.POINTER(tsnet_grad_params),
                                         ctypes.POINTER(tsnet_shard), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     ("tsnet_step", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, c_vp, c_vp, ctypes.POINTER(tsnet_grad_params),
@@ -200,13 +201,14 @@ class CSR:
         self.nnz = int(indices.numel()) if nnz is None else int(nnz)
         self.plan = None
         self.plan_kind = 0
+        self.plan_rows = (0, self.n)     # the rows the plan was built for (its shard)
 
     def c(self):
         return tsnet_csr(self.n, self.nnz, int(self.indices.numel()), self.indptr.data_ptr(),
                          self.indices.data_ptr() if self.indices.numel() else None,
                          self.values.data_ptr() if self.values.numel() else None,
                          self.plan.data_ptr() if self.plan is not None else None,
-                         self.plan_kind if self.plan is not None else 0)
+                         self.plan_kind if self.plan is not None else 0, self.plan_rows[0], self.plan_rows[1])
 
     def without_plan(self) -> "CSR":
         """Same P, CSR kernel (shares the tensors)."""
@@ -324,6 +326,7 @@ def tsnet_plan_build(P: CSR, shard=None, stream=None) -> CSR:
     del ws
     P.plan = plan
     P.plan_kind = PLAN_CB
+    P.plan_rows = (0, P.n) if shard is None else _shard_rows(shard)
     return P
 
 
@@ -369,6 +372,7 @@ def tsnet_sell_build(P: CSR, shard=None, stream=None) -> CSR:
                                                       _stream(stream)))
     P.plan = plan
     P.plan_kind = PLAN_SELL
+    P.plan_rows = (0, P.n) if shard is None else _shard_rows(shard)
     return P
 
 
@@ -428,12 +432,14 @@ def tsnet_grad_tree(P: CSR, Y: torch.Tensor, gp: GradParams, ws: torch.Tensor, t
     return grad, Z
 
 
-def tsnet_attr(P: CSR, Y: torch.Tensor, f_attr=None, stream=None):
-    """Attractive SpMV alone (a6)."""
+def tsnet_attr(P: CSR, Y: torch.Tensor, f_attr=None, shard=None, stream=None):
+    """Attractive SpMV alone (a6) for the shard's rows (all rows if None)."""
     _require_cuda(Y)
-    f_attr = torch.empty_like(Y) if f_attr is None else f_attr
+    if f_attr is None:
+        rb, re = (0, P.n) if shard is None else _shard_rows(shard)
+        f_attr = torch.empty((re - rb, 2), dtype=Y.dtype, device=Y.device)
     Pc = P.c()
-    _check("tsnet_attr", lib().tsnet_attr(ctypes.byref(Pc), _ptr(Y), _ptr(f_attr), _stream(stream)))
+    _check("tsnet_attr", lib().tsnet_attr(ctypes.byref(Pc), _ptr(Y), _shard(shard), _ptr(f_attr), _stream(stream)))
     return f_attr
 
 
@@ -500,6 +506,11 @@ class Shard:
 
     def c(self):
         return self._c
+
+
+def _shard_rows(shard):
+    s = shard.c() if isinstance(shard, Shard) else shard
+    return int(s.row_begin), int(s.row_end)
 
 
 def _shard(shard):

@@ -67,3 +67,13 @@ def test_short_window_takes_nearest(bench, tmp_path):
     t0 = (t + datetime.timedelta(seconds=0.21)).timestamp()
     r = s.stop(t0, t0 + 0.01)
     assert r["samples"] == 2 and r["reasons"] == []
+
+
+def test_window_starts(bench):
+    """Five timed windows of K iterations spread over stage B (250-999) after the
+    warm-up; as many as fit, at least one."""
+    s = bench.window_starts(250, 5, 20)
+    assert len(s) == 5 and s[0] == 255 and s[-1] + 20 <= 1000 and all(b - a >= 20 for a, b in zip(s, s[1:]))
+    s = bench.window_starts(250, 20, 200)
+    assert len(s) == 3 and s[0] == 270 and s[-1] + 200 <= 1000
+    assert bench.window_starts(250, 20, 1000) == [270]

@@ -64,7 +64,7 @@ def check(ip, ix, pv, Y, shard=None, y_offset_rows=0, plan="cb"):
     base[y_offset_rows:] = torch.from_numpy(Y)
     Yd = base[y_offset_rows:]
     F = torch.full((n, 2), float("nan"), dtype=torch.float32, device="cuda")
-    tsnet_attr(P, Yd, F)
+    tsnet_attr(P, Yd, F, shard=shard)
     torch.cuda.synchronize()
     got = F.cpu().numpy()[: re - rb].astype(np.float64)
     want = oracle.attr_sparse(Y.astype(np.float64), ip, ix, pv32)[rb:re]
@@ -92,7 +92,8 @@ def test_configs(cfg, plan):
 
 @pytest.mark.parametrize("plan", ["cb", "sell", "csr"])
 @pytest.mark.parametrize("n,kind", [(1, "single"), (7, "tiny"), (4095, "one_block_minus"), (4096, "one_block"),
-                                    (4097, "block_plus_one"), (8191, "two_blocks_minus"), (8192, "two_blocks"),
+                                    (4097, "block_plus_one"), (7167, "tile_block_minus"), (7168, "tile_block"),
+                                    (7169, "tile_block_plus"), (8191, "two_blocks_minus"), (8192, "two_blocks"),
                                     (8193, "block_plus_one"), (24577, "odd_tail"), (20011, "hub_and_empty"),
                                     (50000, "short_rows"), (30011, "many_empty")])
 def test_edge_patterns(n, kind, plan):
@@ -108,7 +109,7 @@ def test_edge_patterns(n, kind, plan):
         L = rng.integers(0, 4, n)
     if kind == "many_empty":
         L[rng.random(n) < 0.8] = 0
-    if kind in ("one_block", "two_blocks"):
+    if kind in ("one_block", "two_blocks", "tile_block"):
         L[0] = n                        # one row filling whole tiles: a run over many lanes (atomic pieces)
     ip, ix, pv = random_csr(n, L, seed=n)
     Y = uniform_layout(n, 10.0, 9)

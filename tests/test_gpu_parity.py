@@ -507,9 +507,7 @@ def test_step_host_equals_device_step(cfg, recenter):
 
 @pytest.mark.parametrize("cfg,stage,recenter", [(2, 0, 0), (2, 1, 0), (3, 1, 0), (2, 1, 1)])
 def test_step_sell_plan_equals_csr_step(cfg, stage, recenter):
-    """tsnet_step with a sliced-ELL plan equals the CSR step and the oracle's.
-    Run in a subprocess with TSNET_FUSED_MOVE=1 too (the move fused into the
-    SpMV epilogue; with recentring the separate move): see the next test."""
+    """tsnet_step with a sliced-ELL plan equals the CSR step and the oracle's."""
     P = oracle_P(cfg)
     n = P["n"]
     Y = clustered_layout(n, 20.0, 5, 1.5, 7)
@@ -539,19 +537,6 @@ def test_step_sell_plan_equals_csr_step(cfg, stage, recenter):
     r = oracle_grad(P, Y, lam)
     _, Vo, _ = oracle.update_step(Y, vel, gains, r["g"], eta=50.0, mu=mu)
     assert relL2(Vd.cpu().numpy(), Vo) <= GRAD_TOL
-
-
-def test_step_sell_fused_move_subprocess():
-    """The fused SpMV + move (TSNET_FUSED_MOVE=1, read once per process) passes
-    the sliced-ELL step tests."""
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, TSNET_FUSED_MOVE="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
-                        __file__ + "::test_step_sell_plan_equals_csr_step"], env=env, capture_output=True, text=True,
-                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
 def test_ten_iterations_config1():
