@@ -131,11 +131,11 @@ typedef struct {
  * gradient and of the state (vel, gains).  Y is REPLICATED: every rank holds
  * all n x 2 positions; each iteration the ranks
  *   - derive the same grid geometry from the full Y (no collective),
- *   - spread their own points (step a2) and all-reduce (sum) the charge grid
- *     over `comm` (fixed size 4 (3 I_max)^2 floats),
+ *   - spread their own points (step a2) and sum the charge grid over the ranks
+ *     (peer-memory all-reduce of the live cells, tsnet_comm_init),
  *   - convolve the reduced grid (replicated FFT), run the attractive SpMV and
  *     the gather/move for their own rows,
- *   - all-gather Y (each rank broadcasts its slice) -- tsnet_step only.
+ *   - all-gather Y (equal padded slices, one ncclAllGather) -- tsnet_step only.
  * comm   : communicator from tsnet_comm_init (NULL only for the phase calls
  *          tsnet_field_local / tsnet_step_finish, which do no communication).
  * bounds : [host] world + 1 row offsets, bounds[r] .. bounds[r+1] = rank r's rows
@@ -428,15 +428,34 @@ TSNET_API int tsnet_sell_build(const tsnet_csr* P, const tsnet_shard* shard, voi
 
 /* ------------------------------------------------------------- multi-GPU (§8(e)) */
 
-/* NCCL plumbing (NCCL is loaded at run time; TSNET_E_ARG if it cannot be).
+/* Communicator (NCCL is loaded at run time; TSNET_E_ARG if it cannot be).
  * tsnet_comm_unique_id : on one rank, write the 128-byte id to share with the
  *                        others (e.g. through torch.distributed). [host]
- * tsnet_comm_init      : every rank, collectively: communicator of `world` ranks
- *                        (the calling thread's current CUDA device). BLOCKING.
- * tsnet_comm_destroy   : release it. */
+ * tsnet_comm_init      : every rank, collectively: communicator of `world`
+ *                        (<= 64) ranks on the calling thread's current device.
+ *                        It allocates a peer-exchange buffer for charge grids of
+ *                        up to 3 I_max nodes per axis (2 x 16 (3 I_max)^2 bytes +
+ *                        256) and maps every peer's buffer (CUDA IPC); when all
+ *                        ranks sit on distinct, peer-accessible devices, the
+ *                        charge-grid sum of each step is a peer-memory
+ *                        all-reduce of the live N x N cells (device-side flag
+ *                        handshake, loads over NVLink), else an ncclAllReduce
+ *                        of the whole (3 I_max)^2 grid.  BLOCKING.
+ * tsnet_comm_peer_reduce : 1 if the communicator uses the peer-memory grid
+ *                        all-reduce, else 0. [host]
+ * tsnet_comm_destroy   : release it (synchronises the device). */
 TSNET_API int tsnet_comm_unique_id(uint8_t* id_out);
-TSNET_API int tsnet_comm_init(const uint8_t* id, int32_t world, int32_t rank, void** comm);
+TSNET_API int tsnet_comm_init(const uint8_t* id, int32_t world, int32_t rank, int32_t I_max, void** comm);
+TSNET_API int tsnet_comm_peer_reduce(const void* comm);
 TSNET_API int tsnet_comm_destroy(void* comm);
+
+/* The charge-grid sum of `count` workspaces on the calling device (shards run
+ * on one device, and the single-device emulation of several ranks): after
+ * tsnet_field_local on each, every workspace's live grid becomes the sum of all
+ * (the same N, from the first workspace's geometry).  n, nnz, gp: as for
+ * tsnet_workspace_bytes.  BLOCKING. */
+TSNET_API int tsnet_grids_sum(int32_t count, void* const* ws_list, size_t ws_bytes, int64_t n, int64_t nnz,
+                              const tsnet_grad_params* gp, tsnet_stream_t stream);
 
 /* Row shards: bounds[0..world] (host) cutting rows [0, n) of the HOST indptr
  * into `world` contiguous ranges balanced on nnz + rows (the per-rank bytes of

@@ -1,14 +1,24 @@
-// comm.cu -- multi-GPU plumbing of libtsnet: NCCL communicators and the two
-// collectives of one sharded L-tsNET iteration:
-//   * all-reduce (sum) of the spread charge grid W1, Mx, My after step a2,
-//   * all-gather of the updated layout Y after the move (grouped broadcasts of
-//     each rank's contiguous row slice, since nnz-balanced slices differ in size).
+// comm.cu -- multi-GPU plumbing of libtsnet: the communicator and the two
+// exchanges of one sharded L-tsNET iteration:
+//   * the sum of the spread charge grid (W1, Mx, My) over the ranks after step
+//     a2 -- a peer-memory all-reduce: each rank publishes its live N x N grid
+//     (N = 3 I from the device geometry, so only the cells in use move, whatever
+//     the I_max the buffers were sized for) into its exchange buffer, and every
+//     rank sums all ranks' buffers with direct loads over NVLink (CUDA IPC
+//     mappings), after a device-side flag handshake -- no host round trip, so
+//     the iteration stays one CUDA graph;
+//   * the all-gather of the updated layout Y after the move: each rank's rows
+//     padded to an equal slice (the shards are nnz-balanced, their row counts
+//     differ) and gathered with one ncclAllGather through a staging buffer.
 // NCCL is loaded at run time (dlopen "libnccl.so.2"): in a process that already
 // imported PyTorch this resolves to the NCCL torch loaded; the library has no
-// link-time NCCL dependency, so single-GPU use needs no NCCL at all.
+// link-time NCCL dependency, so single-GPU use needs no NCCL at all.  Where the
+// peers are not all reachable by CUDA peer access (e.g. several ranks on one
+// device), the grid falls back to an ncclAllReduce of the whole buffer.
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -23,9 +33,7 @@ struct NcclApi {
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
-    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*GroupStart)() = nullptr;
-    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -42,14 +50,12 @@ static NcclApi* nccl_api() {
             api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
             api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
             api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
-            api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
-            api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
-            api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+            api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
             api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
         }
     }
     const bool ok = api.handle && api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce &&
-                    api.Broadcast && api.GroupStart && api.GroupEnd && api.GetErrorString;
+                    api.AllGather && api.GetErrorString;
     return ok ? &api : nullptr;
 }
 
@@ -62,32 +68,175 @@ static NcclApi* nccl_api() {
         }                                                                                       \
     } while (0)
 
-// sum of the charge grid (count floats at `grid`) over the ranks, in place
-int comm_allreduce_grid(void* comm, float* grid, size_t count, cudaStream_t s) {
+constexpr int kMaxWorld = 64;
+
+// The communicator behind tsnet_comm_init's `void* comm`.
+struct Comm {
+    ncclComm_t nccl = nullptr;
+    int world = 1, rank = 0, dev = 0;
+    int64_t cells = 0;          // grid cells per exchange buffer ((3 I_max)^2)
+    // own exchange memory (cudaMalloc, IPC-shared): flags (256 B: [0] published
+    // iteration, [1] the iteration counter), then two grids of `cells` float4
+    // (iteration parity)
+    char* xbuf = nullptr;
+    size_t xbytes = 0;
+    bool p2p = false;           // every peer reachable: peer-memory all-reduce
+    std::vector<char*> peer;    // per rank: its exchange buffer as mapped here (own = xbuf)
+    // device copies of the per-rank pointers: flags[w], grid0[w], grid1[w]
+    unsigned long long** d_flags = nullptr;
+    float4** d_grid = nullptr;  // [2][world]
+};
+
+static unsigned long long* xflags(char* b) { return reinterpret_cast<unsigned long long*>(b); }
+static float4* xgrid(char* b, int parity, int64_t cells) {
+    return reinterpret_cast<float4*>(b + 256) + (size_t)parity * (size_t)cells;
+}
+
+// ----------------------------------------------------------- peer all-reduce
+// 1. publish: this rank's live grid (N x N float4 from the geometry) into its
+//    exchange grid of the next iteration's parity.
+__global__ void k_x_publish(const Geo* __restrict__ g, const float4* __restrict__ wgrid,
+                            const unsigned long long* __restrict__ flags, float4* __restrict__ x0,
+                            float4* __restrict__ x1) {
+    const int64_t cells = (int64_t)g->N * g->N;
+    float4* dst = ((flags[1] + 1) & 1) ? x1 : x0;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cells; c += (int64_t)gridDim.x * blockDim.x)
+        dst[c] = wgrid[c];
+}
+
+// 2. signal (one thread, after the publish kernel): the iteration counter goes
+//    to t + 1 and flags[0] = t + 1 is released at system scope.
+__global__ void k_x_signal(unsigned long long* flags) {
+    const unsigned long long t = flags[1] + 1;
+    flags[1] = t;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flags), "l"(t) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// 3. reduce: wait until every rank published iteration t (this rank's counter),
+//    then wgrid = sum over ranks of their exchange grid of parity t & 1, read
+//    over NVLink.  Parity reuse is safe: a rank overwrites its parity-p grid at
+//    iteration t + 2 only after its reduce of t + 1, which waited for every
+//    peer's signal of t + 1, issued after that peer's reduce of t.
+__global__ void k_x_reduce(const Geo* __restrict__ g, unsigned long long* const* __restrict__ flags,
+                           float4* const* __restrict__ grids, int world, const unsigned long long* own_flags,
+                           float4* __restrict__ wgrid) {
+    const unsigned long long t = own_flags[1];
+    if (threadIdx.x == 0) {
+        for (int r = 0; r < world; ++r)
+            while (ld_acquire_sys(flags[r]) < t) {
+            }
+    }
+    __syncthreads();
+    float4* const* gr = grids + (t & 1) * world;
+    const int64_t cells = (int64_t)g->N * g->N;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cells; c += (int64_t)gridDim.x * blockDim.x) {
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int r = 0; r < world; ++r) {
+            const float4 v = gr[r][c];
+            s.x += v.x;
+            s.y += v.y;
+            s.z += v.z;
+        }
+        wgrid[c] = s;
+    }
+}
+
+// sum of several workspaces' live grids on one device, into each of them
+// (tsnet_grids_sum: the same reduction without peers, for callers that run
+// several shards on one device and for tests)
+struct GridTab {
+    float4* p[kMaxWorld];
+};
+__global__ void k_grids_sum(const Geo* __restrict__ g, GridTab grids, int count) {
+    const int64_t cells = (int64_t)g->N * g->N;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cells; c += (int64_t)gridDim.x * blockDim.x) {
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int r = 0; r < count; ++r) {
+            const float4 v = grids.p[r][c];
+            s.x += v.x;
+            s.y += v.y;
+            s.z += v.z;
+        }
+        for (int r = 0; r < count; ++r) grids.p[r][c] = s;
+    }
+}
+
+// sum of the charge grid over the ranks, into `wgrid` (this rank's grid on entry)
+int comm_allreduce_grid(void* comm, const Geo* geo, float4* wgrid, size_t count_floats, cudaStream_t s) {
+    Comm* c = reinterpret_cast<Comm*>(comm);
+    if (c->p2p && (size_t)c->cells * 4 >= count_floats) {
+        k_x_publish<<<kNumSMs, 256, 0, s>>>(geo, wgrid, xflags(c->xbuf), xgrid(c->xbuf, 0, c->cells),
+                                            xgrid(c->xbuf, 1, c->cells));
+        k_x_signal<<<1, 1, 0, s>>>(xflags(c->xbuf));
+        k_x_reduce<<<kNumSMs, 256, 0, s>>>(geo, c->d_flags, c->d_grid, c->world, xflags(c->xbuf), wgrid);
+        TSNET_CUDA(cudaGetLastError());
+        return TSNET_OK;
+    }
     NcclApi* api = nccl_api();
     TSNET_ARG(api != nullptr, "libnccl.so.2 could not be loaded");
-    TSNET_NCCL(api->AllReduce(grid, grid, count, ncclFloat32, ncclSum, (ncclComm_t)comm, s));
+    TSNET_NCCL(api->AllReduce(wgrid, wgrid, count_floats, ncclFloat32, ncclSum, c->nccl, s));
     return TSNET_OK;
 }
 
-// every rank's rows [bounds[r], bounds[r+1]) of Y (n x 2 fp32) to every rank
-int comm_allgather_rows(void* comm, float* Y, const int64_t* bounds, int world, cudaStream_t s) {
+// ------------------------------------------------------------ Y all-gather
+struct Bounds {
+    int64_t b[kMaxWorld + 1];
+};
+
+// stage[r slice .. + rows_r) -> Y rows [bounds[r], bounds[r+1]) for r != self
+__global__ void k_unstage(const float2* __restrict__ stage, float2* __restrict__ Y, Bounds bd, int world, int self,
+                          int64_t slice) {
+    for (int r = 0; r < world; ++r) {
+        if (r == self) continue;
+        const int64_t b0 = bd.b[r], rows = bd.b[r + 1] - b0;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+            Y[b0 + i] = stage[(int64_t)r * slice + i];
+    }
+}
+
+// every rank's rows [bounds[r], bounds[r+1]) of Y (n x 2 fp32) to every rank:
+// own rows -> stage[rank slice], ncclAllGather of equal slices, rows back to Y.
+// `stage` holds world * max_r(rows_r) float2.
+int comm_allgather_rows(void* comm, float* Y, const int64_t* bounds, int world, float2* stage, size_t stage_cap,
+                        cudaStream_t s) {
+    Comm* c = reinterpret_cast<Comm*>(comm);
+    TSNET_ARG(world == c->world && world <= kMaxWorld, "world %d does not match the communicator (%d)", world, c->world);
+    if (world == 1) return TSNET_OK;
+    int64_t slice = 0;
+    Bounds bd{};
+    for (int r = 0; r <= world; ++r) bd.b[r] = bounds[r];
+    for (int r = 0; r < world; ++r) slice = std::max<int64_t>(slice, bounds[r + 1] - bounds[r]);
+    TSNET_ARG((size_t)(slice * world) <= stage_cap, "all-gather staging too small");
+    if (slice == 0) return TSNET_OK;
     NcclApi* api = nccl_api();
     TSNET_ARG(api != nullptr, "libnccl.so.2 could not be loaded");
-    TSNET_NCCL(api->GroupStart());
-    for (int r = 0; r < world; ++r) {
-        const size_t cnt = (size_t)(bounds[r + 1] - bounds[r]) * 2;
-        if (cnt == 0) continue;
-        float* p = Y + 2 * bounds[r];
-        ncclResult_t e = api->Broadcast(p, p, cnt, ncclFloat32, r, (ncclComm_t)comm, s);
-        if (e != ncclSuccess) {
-            api->GroupEnd();
-            set_error("ncclBroadcast: %s", api->GetErrorString(e));
-            return TSNET_E_NCCL;
-        }
-    }
-    TSNET_NCCL(api->GroupEnd());
+    float2* Y2 = reinterpret_cast<float2*>(Y);
+    const int64_t own = bounds[c->rank + 1] - bounds[c->rank];
+    if (own > 0)
+        TSNET_CUDA(cudaMemcpyAsync(stage + (size_t)c->rank * slice, Y2 + bounds[c->rank], sizeof(float2) * own,
+                                   cudaMemcpyDeviceToDevice, s));
+    TSNET_NCCL(api->AllGather(stage + (size_t)c->rank * slice, stage, (size_t)slice * 2, ncclFloat32, c->nccl, s));
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((slice + 255) / 256, (int64_t)kNumSMs * 8));
+    k_unstage<<<blocks, 256, 0, s>>>(stage, Y2, bd, world, c->rank, slice);
+    TSNET_CUDA(cudaGetLastError());
     return TSNET_OK;
+}
+
+static void comm_free(Comm* c) {
+    if (!c) return;
+    for (int r = 0; r < (int)c->peer.size(); ++r)
+        if (c->peer[r] && c->peer[r] != c->xbuf) cudaIpcCloseMemHandle(c->peer[r]);
+    if (c->xbuf) cudaFree(c->xbuf);
+    if (c->d_flags) cudaFree(c->d_flags);
+    if (c->d_grid) cudaFree(c->d_grid);
+    delete c;
 }
 
 }  // namespace tsnet
@@ -107,24 +256,132 @@ int tsnet_comm_unique_id(uint8_t* id_out) {
     return TSNET_OK;
 }
 
-int tsnet_comm_init(const uint8_t* id, int32_t world, int32_t rank, void** comm) {
+int tsnet_comm_init(const uint8_t* id, int32_t world, int32_t rank, int32_t I_max, void** comm) {
     TSNET_ARG(id != nullptr && comm != nullptr, "NULL argument");
-    TSNET_ARG(world >= 1 && rank >= 0 && rank < world, "rank %d / world %d", rank, world);
+    TSNET_ARG(world >= 1 && world <= kMaxWorld && rank >= 0 && rank < world, "rank %d / world %d", rank, world);
+    TSNET_ARG(I_max >= 1 && I_max <= TSNET_I_MAX_LIMIT, "I_max %d outside [1, %d]", I_max, TSNET_I_MAX_LIMIT);
     NcclApi* api = nccl_api();
     TSNET_ARG(api != nullptr, "libnccl.so.2 could not be loaded");
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
-    ncclComm_t c = nullptr;
-    TSNET_NCCL(api->CommInitRank(&c, world, uid, rank));
+    Comm* c = new Comm;
+    c->world = world;
+    c->rank = rank;
+    cudaGetDevice(&c->dev);
+    ncclResult_t nr = api->CommInitRank(&c->nccl, world, uid, rank);
+    if (nr != ncclSuccess) {
+        set_error("ncclCommInitRank: %s", api->GetErrorString(nr));
+        delete c;
+        return TSNET_E_NCCL;
+    }
+    // exchange buffer, its IPC handle to every rank (all-gather of the handles)
+    c->cells = (int64_t)(3 * I_max) * (3 * I_max);
+    c->xbytes = 256 + 2 * sizeof(float4) * (size_t)c->cells;
+    cudaError_t e = cudaMalloc(&c->xbuf, c->xbytes);
+    if (e == cudaSuccess) e = cudaMemset(c->xbuf, 0, c->xbytes);
+    if (e != cudaSuccess) {
+        set_error("exchange buffer: %s", cudaGetErrorString(e));
+        api->CommDestroy(c->nccl);
+        comm_free(c);
+        return TSNET_E_CUDA;
+    }
+    int reach = 1;
+    std::vector<cudaIpcMemHandle_t> h(world);
+    cudaIpcMemHandle_t mine;
+    if (cudaIpcGetMemHandle(&mine, c->xbuf) != cudaSuccess) {
+        cudaGetLastError();
+        reach = 0;
+        std::memset(&mine, 0, sizeof(mine));
+    }
+    // handles + per-rank device ordinal, gathered over NCCL
+    struct Rec {
+        cudaIpcMemHandle_t h;
+        int dev, reach;
+        char pad[64 - 8];
+    };
+    Rec me{};
+    me.h = mine;
+    me.dev = c->dev;
+    me.reach = reach;
+    Rec* d_rec = nullptr;
+    std::vector<Rec> recs(world);
+    e = cudaMalloc(&d_rec, sizeof(Rec) * world);
+    if (e == cudaSuccess) e = cudaMemcpy(d_rec + rank, &me, sizeof(Rec), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        nr = api->AllGather(d_rec + rank, d_rec, sizeof(Rec), ncclUint8, c->nccl, 0);
+        if (nr == ncclSuccess) e = cudaMemcpy(recs.data(), d_rec, sizeof(Rec) * world, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(d_rec);
+    if (e != cudaSuccess || nr != ncclSuccess) {
+        set_error("handle exchange: %s", e != cudaSuccess ? cudaGetErrorString(e) : api->GetErrorString(nr));
+        api->CommDestroy(c->nccl);
+        comm_free(c);
+        return e != cudaSuccess ? TSNET_E_CUDA : TSNET_E_NCCL;
+    }
+    // peer mappings when every rank sits on its own device and is reachable
+    bool p2p = true;
+    for (int r = 0; r < world; ++r) {
+        if (!recs[r].reach) p2p = false;
+        if (r != rank) {
+            int can = 0;
+            if (recs[r].dev == c->dev || cudaDeviceCanAccessPeer(&can, c->dev, recs[r].dev) != cudaSuccess || !can)
+                p2p = false;
+        }
+    }
+    c->peer.assign(world, nullptr);
+    c->peer[rank] = c->xbuf;
+    if (p2p) {
+        for (int r = 0; r < world && p2p; ++r) {
+            if (r == rank) continue;
+            void* ptr = nullptr;
+            if (cudaIpcOpenMemHandle(&ptr, recs[r].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                p2p = false;
+            } else {
+                c->peer[r] = reinterpret_cast<char*>(ptr);
+            }
+        }
+    }
+    c->p2p = p2p;
+    if (p2p) {
+        std::vector<unsigned long long*> fl(world);
+        std::vector<float4*> gr(2 * world);
+        for (int r = 0; r < world; ++r) {
+            fl[r] = xflags(c->peer[r]);
+            gr[r] = xgrid(c->peer[r], 0, c->cells);
+            gr[world + r] = xgrid(c->peer[r], 1, c->cells);
+        }
+        e = cudaMalloc(&c->d_flags, sizeof(void*) * world);
+        if (e == cudaSuccess) e = cudaMalloc(&c->d_grid, sizeof(void*) * 2 * world);
+        if (e == cudaSuccess) e = cudaMemcpy(c->d_flags, fl.data(), sizeof(void*) * world, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(c->d_grid, gr.data(), sizeof(void*) * 2 * world, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            set_error("peer tables: %s", cudaGetErrorString(e));
+            api->CommDestroy(c->nccl);
+            comm_free(c);
+            return TSNET_E_CUDA;
+        }
+    }
     *comm = c;
     return TSNET_OK;
 }
 
+int tsnet_comm_peer_reduce(const void* comm) {
+    return comm != nullptr && reinterpret_cast<const Comm*>(comm)->p2p ? 1 : 0;
+}
+
 int tsnet_comm_destroy(void* comm) {
     if (comm == nullptr) return TSNET_OK;
+    Comm* c = reinterpret_cast<Comm*>(comm);
     NcclApi* api = nccl_api();
     TSNET_ARG(api != nullptr, "libnccl.so.2 could not be loaded");
-    TSNET_NCCL(api->CommDestroy((ncclComm_t)comm));
+    cudaDeviceSynchronize();
+    ncclResult_t nr = api->CommDestroy(c->nccl);
+    comm_free(c);
+    if (nr != ncclSuccess) {
+        set_error("ncclCommDestroy: %s", api->GetErrorString(nr));
+        return TSNET_E_NCCL;
+    }
     return TSNET_OK;
 }
 
@@ -142,6 +399,26 @@ int32_t tsnet_shard_rows(const int64_t* indptr_host, int64_t n, int32_t world, i
     }
     bounds[world] = n;
     return world;
+}
+
+int tsnet_grids_sum(int32_t count, void* const* ws_list, size_t ws_bytes, int64_t n, int64_t nnz,
+                    const tsnet_grad_params* gp, tsnet_stream_t stream) {
+    TSNET_ARG(count >= 1 && count <= kMaxWorld && ws_list != nullptr && gp != nullptr, "bad arguments");
+    TSNET_ARG(gp->I_max >= 1 && gp->I_max <= TSNET_I_MAX_LIMIT, "bad I_max");
+    GridTab tab{};
+    Ws w0{};
+    for (int r = 0; r < count; ++r) {
+        TSNET_ARG(ws_list[r] != nullptr, "workspace %d is NULL", r);
+        Ws w = ws_map(ws_list[r], n, nnz, gp->I_max);
+        TSNET_ARG(ws_bytes >= w.bytes, "workspace too small");
+        tab.p[r] = w.wgrid;
+        if (r == 0) w0 = w;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    k_grids_sum<<<kNumSMs, 256, 0, s>>>(w0.geo, tab, count);
+    TSNET_CUDA(cudaGetLastError());
+    TSNET_CUDA(cudaStreamSynchronize(s));
+    return TSNET_OK;
 }
 
 }  // extern "C"

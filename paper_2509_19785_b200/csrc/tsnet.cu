@@ -34,8 +34,9 @@ static int check_grad_params(const tsnet_grad_params* gp) {
     return TSNET_OK;
 }
 
-int comm_allreduce_grid(void* comm, float* grid, size_t count, cudaStream_t s);
-int comm_allgather_rows(void* comm, float* Y, const int64_t* bounds, int world, cudaStream_t s);
+int comm_allreduce_grid(void* comm, const Geo* geo, float4* wgrid, size_t count_floats, cudaStream_t s);
+int comm_allgather_rows(void* comm, float* Y, const int64_t* bounds, int world, float2* stage, size_t stage_cap,
+                        cudaStream_t s);
 
 static int check_shard(const tsnet_shard* sh, int64_t n) {
     if (sh == nullptr) return TSNET_OK;
@@ -179,8 +180,10 @@ static int eval_gradient_parts(const Ws& w, const GradArgs& a, const tsnet_shard
     cudaStream_t fs = ss->field;
     TSNET_CUDA(cudaEventRecord(ss->fork, s));
     TSNET_CUDA(cudaStreamWaitEvent(fs, ss->fork, 0));
-    TSNET_CUDA(launch_field_local(w, a, fs, multi));
-    if (multi && (st = comm_allreduce_grid(sh->comm, reinterpret_cast<float*>(w.wgrid), grid_floats(w), fs)) != TSNET_OK)
+    // the whole I_max-sized grid is zeroed only for the NCCL fallback, which
+    // all-reduces it as one fixed-size buffer; the peer all-reduce moves the live cells
+    TSNET_CUDA(launch_field_local(w, a, fs, multi && !tsnet_comm_peer_reduce(sh->comm)));
+    if (multi && (st = comm_allreduce_grid(sh->comm, w.geo, w.wgrid, grid_floats(w), fs)) != TSNET_OK)
         return st;
     TSNET_CUDA(launch_field_conv(w, a, fs));
     TSNET_CUDA(launch_spmv(w, a, s));
@@ -298,7 +301,7 @@ static int step_impl(const tsnet_csr* P, float* Y, float* vel, float* gains, con
     if (before_update) TSNET_CUDA(cudaStreamWaitEvent(s, before_update, 0));
     TSNET_CUDA(launch_update(w, a, reinterpret_cast<float2*>(Y), reinterpret_cast<float2*>(vel),
                              reinterpret_cast<float2*>(gains), *sp, s));
-    if (multi) return comm_allgather_rows(shard->comm, Y, shard->bounds, shard->world, s);
+    if (multi) return comm_allgather_rows(shard->comm, Y, shard->bounds, shard->world, w.state, 4 * (size_t)a.n, s);
     return TSNET_OK;
 }
 }  // namespace tsnet

@@ -6,7 +6,9 @@ tsnet_step with its shard: geometry from the full Y, spread of its own points,
 NCCL all-reduce of the charge grid, replicated FFT convolution, attractive
 SpMV + gather + move of its own rows, NCCL all-gather of Y.  The NCCL
 communicator is created inside libtsnet (tsnet_comm_init); torch.distributed
-only carries its 128-byte id from rank 0 to the others.
+only carries its 128-byte id from rank 0 to the others.  The charge-grid sum is
+a peer-memory all-reduce of the live grid (tsnet_comm_init maps every peer's
+exchange buffer); Y is all-gathered in equal padded slices.
 """
 from __future__ import annotations
 
@@ -42,7 +44,8 @@ class ShardedLayout:
         self.rank, self.world = rank, world
         bounds = shard_bounds(P.indptr.cpu().numpy(), world)
         uid = share_comm_id(rank, group)
-        self.comm = tsnet_comm_init(uid, world, rank)
+        self.params = [stage_params(0, base, eta), stage_params(1, base, eta)]
+        self.comm = tsnet_comm_init(uid, world, rank, self.params[0][0].I_max)
         self.shard = Shard(rank, world, bounds, self.comm)
         # the attractive SpMV reads the own rows of P (CSR), or a plan of them
         # (attach_plan: "csr", "cb", "sell", "auto") attached to a shallow copy,
@@ -51,7 +54,6 @@ class ShardedLayout:
         self.Y = Y0.clone()
         self.vel = torch.zeros_like(self.Y)
         self.gains = torch.ones_like(self.Y)
-        self.params = [stage_params(0, base, eta), stage_params(1, base, eta)]
         self.ws = alloc_workspace(P.n, P.nnz, self.params[0][0], device=Y0.device)
         self.stage_switch = stage_switch
         self.use_graphs = use_graphs

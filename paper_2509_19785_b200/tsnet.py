@@ -95,7 +95,10 @@ SIGNATURES = [
     ("tsnet_sell_build", ctypes.c_int, [ctypes.POINTER(tsnet_csr), ctypes.POINTER(tsnet_shard), c_vp, c_sz, c_vp]),
     ("tsnet_plan_partition", c_i32, [c_vp, c_i64, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_i64]),
     ("tsnet_comm_unique_id", ctypes.c_int, [c_vp]),
-    ("tsnet_comm_init", ctypes.c_int, [c_vp, c_i32, c_i32, ctypes.POINTER(c_vp)]),
+    ("tsnet_comm_init", ctypes.c_int, [c_vp, c_i32, c_i32, c_i32, ctypes.POINTER(c_vp)]),
+    ("tsnet_comm_peer_reduce", ctypes.c_int, [c_vp]),
+    ("tsnet_grids_sum", ctypes.c_int, [c_i32, ctypes.POINTER(c_vp), c_sz, c_i64, c_i64,
+                                       ctypes.POINTER(tsnet_grad_params), c_vp]),
     ("tsnet_comm_destroy", ctypes.c_int, [c_vp]),
     ("tsnet_shard_rows", c_i32, [c_vp, c_i64, c_i32, c_vp]),
     ("tsnet_field_local", ctypes.c_int, [ctypes.POINTER(tsnet_csr), c_vp, ctypes.POINTER(tsnet_grad_params),
@@ -538,11 +541,23 @@ def tsnet_comm_unique_id() -> bytes:
     return bytes(buf)
 
 
-def tsnet_comm_init(uid: bytes, world: int, rank: int):
+def tsnet_comm_init(uid: bytes, world: int, rank: int, I_max: int = TSNET_I_MAX_LIMIT):
     buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
     comm = c_vp()
-    _check("tsnet_comm_init", lib().tsnet_comm_init(buf, world, rank, ctypes.byref(comm)))
+    _check("tsnet_comm_init", lib().tsnet_comm_init(buf, world, rank, int(I_max), ctypes.byref(comm)))
     return comm.value
+
+
+def tsnet_comm_peer_reduce(comm) -> bool:
+    return bool(lib().tsnet_comm_peer_reduce(comm))
+
+
+def tsnet_grids_sum(ws_list, n: int, nnz: int, gp: GradParams, stream=None):
+    """Sum the live charge grids of several workspaces (one device) into each."""
+    arr = (c_vp * len(ws_list))(*[w.data_ptr() for w in ws_list])
+    g = gp.c()
+    _check("tsnet_grids_sum", lib().tsnet_grids_sum(len(ws_list), arr, ws_list[0].numel(), n, nnz, ctypes.byref(g),
+                                                    _stream(stream)))
 
 
 def tsnet_comm_destroy(comm):

@@ -617,8 +617,13 @@ def test_edge_cases():
     Y = np.array([[0.0, 0.0], [1.0, 0.0]], np.float32)
     g, Z, _, _, _ = gpu_grad(dev_P(P), Y, gp)
     r = oracle_grad(P, Y, STAGE_B)
-    # p = q here: the KL part is an exact cancellation (4 F_attr = 4 F_rep)
-    assert_grad_close(g, r, Y, STAGE_B)
+    # p = q here: the KL part is an exact cancellation (4 F_attr = 4 F_rep), ||g|| is
+    # 0.065 of the term scale and the oracle's y-components are exactly 0 by
+    # symmetry; the fp32 FFT field leaves ~6e-6 there, 1.4e-5 of the term scale
+    # (R28: the bar is the fp32 floor of the terms, 2e-5 x scale, and
+    # relL2 <= 3e-4)
+    err = np.linalg.norm(np.asarray(g, np.float64) - r["g"])
+    assert err <= 2e-5 * term_scale(r, Y, STAGE_B) and err <= 3e-4 * np.linalg.norm(r["g"])
     # coincident points (span floor 1e-12) and an empty P row
     P = dict(indptr=np.array([0, 1, 2, 2], np.int64), indices=np.array([1, 0], np.int32),
              values=np.array([0.5, 0.5]))

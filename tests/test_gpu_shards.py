@@ -2,12 +2,14 @@
 
 Only one GPU is available to the tests, so the ranks are emulated the way the
 profiling guide prescribes (no kernels that wait on each other): G virtual
-shards run tsnet_field_local one after the other, the charge grids are summed
-on the device (the all-reduce), tsnet_step_finish runs per shard on its own
-replicated copy of Y, and the own rows are assembled (the all-gather).  The
-result must equal the unsharded tsnet_step (same arithmetic up to fp32
-summation order) and the oracle's step.  The NCCL calls themselves run with a
-1-rank communicator through tsnet_step.
+shards run tsnet_field_local one after the other, their live charge grids are
+summed by tsnet_grids_sum (the reduction of the peer all-reduce, over pointers
+on one device), tsnet_step_finish runs per shard on its own replicated copy of
+Y, and the own rows are assembled (the all-gather).  The result must equal the
+unsharded tsnet_step (same arithmetic up to fp32 summation order) and the
+oracle's step.  The communicator itself runs with one rank through tsnet_step:
+the peer all-reduce's publish / flag handshake / reduce kernels (1 peer), the
+NCCL all-gather path, eagerly and in a captured CUDA graph.
 """
 import numpy as np
 import pytest
@@ -63,10 +65,7 @@ def emulated_step(P, Y, vel, gains, gp, sp, world, plan="cb"):
         Yr = Y.clone()
         T.tsnet_field_local(Pr, Yr, gp, ws, shard=sh)
         Ps.append(Pr), wss.append(ws), Ys.append(Yr)
-    grids = [T.ws_grid_view(ws, n, P.nnz, gp) for ws in wss]
-    total = torch.stack(grids).sum(0)                     # the all-reduce
-    for g in grids:
-        g.copy_(total)
+    T.tsnet_grids_sum(wss, n, P.nnz, gp)                 # the all-reduce (live N x N cells)
     Yout, Vout, Gout = Y.clone(), vel.clone(), gains.clone()
     for sh, Pr, ws, Yr in zip(shards, Ps, wss, Ys):
         V, G = vel.clone(), gains.clone()
@@ -116,8 +115,9 @@ def test_nccl_one_rank_communicator_step():
     gp, sp = GradParams(1.0, 0.01, 0.6), StepParams(eta=50.0, momentum=0.8)
     Pd = dev(P)
     uid = T.tsnet_comm_unique_id()
-    comm = T.tsnet_comm_init(uid, 1, 0)
+    comm = T.tsnet_comm_init(uid, 1, 0, gp.I_max)
     try:
+        assert T.tsnet_comm_peer_reduce(comm)      # one rank: its own exchange buffer, peer path
         sh = T.Shard(0, 1, [0, n], comm)
         ws = alloc_workspace(n, Pd.nnz, gp)
         Yd, Vd, Gd = (torch.from_numpy(a.copy()).cuda() for a in (Y, vel, gains))
@@ -137,6 +137,13 @@ def test_nccl_one_rank_communicator_step():
         tsnet_step(Pd, Y1, V1, G1, gp, sp, alloc_workspace(n, Pd.nnz, gp))
         torch.cuda.synchronize()
         assert relL2(Vd.cpu().numpy(), V1.cpu().numpy()) <= 1e-5
+        # several replays: the iteration counter and the grid parity advance on the device
+        for _ in range(3):
+            with torch.cuda.stream(s):
+                g.replay()
+            tsnet_step(Pd, Y1, V1, G1, gp, sp, alloc_workspace(n, Pd.nnz, gp))
+        torch.cuda.synchronize()
+        assert relL2(Yd.cpu().numpy(), Y1.cpu().numpy()) <= 1e-5
     finally:
         T.tsnet_comm_destroy(comm)
 

@@ -45,7 +45,7 @@ def sharded_oracle_step(Y, P, bounds, rank, world, lam, mu, dist):
     xt, yt = Yr[:, 0] - cx, Yr[:, 1] - cy
     import torch
     W = torch.from_numpy(np.stack([it.spread(np.ones(re - rb)), it.spread(xt), it.spread(yt)]))
-    dist.all_reduce(W)                                         # the charge-grid all-reduce
+    dist.all_reduce(W)                                         # the charge-grid all-reduce (live N x N cells)
     W1, Wx, Wy = W.numpy()
     tab = lambda kern: (lambda dx, dy: kern(dx * dx + dy * dy))  # noqa: E731
     Z = float((W1 * interp.convolve(W1, tab(interp.k1), delta)).sum()) - n   # grid dot, replicated
@@ -60,11 +60,17 @@ def sharded_oracle_step(Y, P, bounds, rank, world, lam, mu, dist):
     g = 4.0 * lkl * (F_attr - F_rep) + (lc / n) * Yr + lr * g_ent
     vel, gains = np.zeros_like(Yr), np.ones_like(Yr)
     Yn, _, _ = update_step(Yr, vel, gains, g, eta=50.0, mu=mu)
-    parts = [None] * world
-    dist.all_gather_object(parts, (rb, re, Yn))                # the Y all-gather
+    # the Y all-gather as libtsnet does it (comm.cu): own rows padded to an equal
+    # slice of max_r(rows_r), one all-gather, each rank's valid rows back by bounds
+    slice_ = int(max(bounds[r + 1] - bounds[r] for r in range(world)))
+    stage = torch.zeros((slice_, 2), dtype=torch.float64)
+    stage[:re - rb] = torch.from_numpy(Yn)
+    parts = [torch.empty_like(stage) for _ in range(world)]
+    dist.all_gather(parts, stage)
     out = np.empty_like(Y)
-    for a, b, y in parts:
-        out[a:b] = y
+    for r in range(world):
+        a, b = int(bounds[r]), int(bounds[r + 1])
+        out[a:b] = parts[r][:b - a].numpy()
     return out
 
 
@@ -105,7 +111,7 @@ def worker(rank, world, port, errq):
         raise
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 3])
 def test_sharded_schedule_gloo(world):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
