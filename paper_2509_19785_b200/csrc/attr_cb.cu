@@ -650,6 +650,124 @@ __global__ void k_tile_wtab(const int64_t* __restrict__ toff, int64_t P, int64_t
     }
 }
 
+// Bank byte of sorted position q: Y_j bank pair (column mod 16) | Y_i / F_i
+// bank pair of the row slot << 4 (8-byte words: 16 bank pairs).
+__global__ void k_tile_banks(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t m,
+                             const int32_t* __restrict__ indices, int64_t e0, uint8_t* __restrict__ cb) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t col = (uint32_t)(indices[(int64_t)vals[q] + e0] % kTB);
+        const uint32_t sl = tile_slot((uint32_t)(keys[q] & kLocalMask));
+        cb[q] = (uint8_t)((col & 15u) | ((sl & 15u) << 4));
+    }
+}
+
+constexpr int kSchedMaxK = 64;   // chunks longer than this keep the row-sorted order
+
+__device__ __forceinline__ unsigned long long bits(int lo, int hi) {   // bits [lo, hi), 0 <= lo <= hi <= 64
+    const unsigned long long up = hi >= 64 ? ~0ull : ((1ull << hi) - 1);
+    return up & ~((1ull << lo) - 1);
+}
+
+// Per warp tile (one thread): the order in which each lane walks its chunk.
+// Any order keeps the arithmetic of a chunk (each row's entries form one run,
+// a run's entries are summed in registers) as long as a run's entries stay
+// consecutive and the run carried into the next chunk (if any) comes last.
+// Within those rules a greedy pass picks, step by step and lane by lane, the
+// entry whose shared-memory banks (Y_j, and Y_i / F_i where a run starts /
+// ends) are least used so far by the lanes of the same half-warp at that step
+// -- random gathers otherwise pile up ~3 deep per bank pair.  Output per
+// sorted position: step << 5 | lane | NEWROW << 30 | FLUSH << 31.
+__global__ void k_tile_schedule(const unsigned long long* __restrict__ keys, const uint8_t* __restrict__ cb,
+                                const int64_t* __restrict__ tstart, const int64_t* __restrict__ tend,
+                                const int32_t* __restrict__ seg, const int64_t* __restrict__ toff, int64_t ntiles,
+                                uint32_t* __restrict__ sched) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < ntiles; u += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = u / kTW, w = u % kTW;
+        const int32_t* sg = seg + t * (kTW + 1);
+        const int64_t base = tstart[t] + sg[w], tile_end = tend[t];
+        const int64_t E = sg[w + 1] - sg[w];
+        const int64_t K = toff[u + 1] - toff[u];
+        if (E == 0) continue;
+        auto key = [&](int64_t i) { return keys[base + i]; };
+        // does the entry after segment index i (in tile order) continue its row?
+        auto cont = [&](int64_t i) { return base + i + 1 < tile_end && keys[base + i + 1] == keys[base + i]; };
+        if (K > kSchedMaxK) {    // row-sorted order (flags as in the sorted list)
+            for (int64_t i = 0; i < E; ++i) {
+                const int64_t l = i / K, k = i - l * K;
+                const bool newrow = k == 0 || key(i - 1) != key(i);
+                sched[base + i] = (uint32_t)(k << 5) | (uint32_t)l | (newrow ? kNewRow : 0u) | (cont(i) ? 0u : kFlush);
+            }
+            continue;
+        }
+        unsigned long long done[32];
+        int8_t rs[32], re[32], tail[32];
+        for (int l = 0; l < 32; ++l) {
+            done[l] = 0ull;
+            rs[l] = re[l] = -1;
+            tail[l] = -1;
+            const int64_t a = l * K, b = std::min<int64_t>(a + K, E);
+            if (a < b && cont(b - 1)) {    // the chunk's last run goes on past it: it must come last
+                int64_t st = b - 1;
+                while (st > a && key(st - 1) == key(b - 1)) --st;
+                tail[l] = (int8_t)(st - a);
+            }
+        }
+        for (int64_t k = 0; k < K; ++k) {
+            uint8_t hy[2][16], hr[2][16];
+            for (int q = 0; q < 16; ++q) hy[0][q] = hy[1][q] = hr[0][q] = hr[1][q] = 0;
+            for (int l = 0; l < 32; ++l) {
+                const int64_t a = l * K, b = std::min<int64_t>(a + K, E);
+                if (a >= b) continue;
+                const int n = (int)(b - a);
+                if ((~done[l] & bits(0, n)) == 0) continue;
+                const int h = l >> 4;
+                int pick = -1;
+                bool newrow = false;
+                if (rs[l] >= 0 && (~done[l] & bits(rs[l], re[l])) != 0) {
+                    int best = 1 << 30;
+                    for (int i = rs[l]; i < re[l]; ++i) {
+                        if (done[l] >> i & 1) continue;
+                        const int c = hy[h][cb[base + a + i] & 15];
+                        if (c < best) { best = c; pick = i; }
+                    }
+                } else {
+                    // a new run: any remaining entry; the tail run only when nothing else is left
+                    const bool only_tail = tail[l] >= 0 && (~done[l] & bits(0, tail[l])) == 0;
+                    int best = 1 << 30;
+                    for (int i = 0; i < n; ++i) {
+                        if (done[l] >> i & 1) continue;
+                        if (tail[l] >= 0 && i >= tail[l] && !only_tail) continue;
+                        const uint8_t bb = cb[base + a + i];
+                        const bool single = (i == 0 || key(a + i - 1) != key(a + i)) &&
+                                            (i == n - 1 || key(a + i + 1) != key(a + i));
+                        const int c = 4 * hy[h][bb & 15] + 2 * hr[h][bb >> 4] * (single ? 2 : 1);
+                        if (c < best) { best = c; pick = i; }
+                    }
+                    int st = pick, en = pick + 1;
+                    while (st > 0 && key(a + st - 1) == key(a + pick)) --st;
+                    while (en < n && key(a + en) == key(a + pick)) ++en;
+                    rs[l] = (int8_t)st;
+                    re[l] = (int8_t)en;
+                    newrow = true;
+                }
+                done[l] |= 1ull << pick;
+                const uint8_t bb = cb[base + a + pick];
+                hy[h][bb & 15]++;
+                if (newrow) hr[h][bb >> 4]++;
+                const bool run_left = (~done[l] & bits(rs[l], re[l])) != 0;
+                bool flush = false;
+                if (!run_left) {
+                    // the run's part in this chunk is done: it ends here unless it goes on past the chunk
+                    flush = !(re[l] == n && cont(a + n - 1));
+                    if (flush) hr[h][bb >> 4]++;
+                    rs[l] = re[l] = -1;
+                }
+                sched[base + a + pick] = (uint32_t)(k << 5) | (uint32_t)l | (newrow ? kNewRow : 0u) | (flush ? kFlush : 0u);
+            }
+        }
+    }
+}
+
 // Slot of sorted position q: block tile t, index i in the tile, warp w (its
 // segment holds i), index iw in the segment, chunk (lane) l = iw / K, step
 // k = iw - l K with K = the segment's steps.  FLUSH: the row's run ends at
@@ -657,31 +775,26 @@ __global__ void k_tile_wtab(const int64_t* __restrict__ toff, int64_t P, int64_t
 // at a chunk end a run that continues is carried out instead (tile_carry).
 // NEWROW: the first entry of a chunk or of a run.  HUB: the row is shared.
 __global__ void k_tile_fill(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ vals, int64_t m,
-                            const int64_t* __restrict__ tstart, const int64_t* __restrict__ tend,
-                            const int32_t* __restrict__ seg, const int64_t* __restrict__ toff, int NB,
+                            const uint32_t* __restrict__ sched, const int64_t* __restrict__ toff,
+                            const int32_t* __restrict__ seg, const int64_t* __restrict__ tstart, int NB,
                             const int32_t* __restrict__ panel_off, const int32_t* __restrict__ hub,
                             const int32_t* __restrict__ indices, const float* __restrict__ values, int64_t e0,
                             uint2* __restrict__ slots) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long key = keys[q];
         const unsigned long long t = key >> kTRbits;
-        const int64_t s0 = tstart[t], E = tend[t] - s0;
-        const int64_t i = q - s0;
+        const int64_t i = q - tstart[t];
         const int32_t* sg = seg + t * (kTW + 1);
         int w = 0;
         while (w + 1 < kTW && sg[w + 1] <= i) ++w;
         const int64_t u = (int64_t)t * kTW + w;
-        const int64_t K = toff[u + 1] - toff[u];
-        const int64_t iw = i - sg[w], l = iw / K, kk = iw - l * K;
-        const bool flush = (i + 1 == E) || keys[q + 1] != key;
-        const bool newrow = (kk == 0) || keys[q - 1] != key;
+        const uint32_t sc = sched[q];
+        const int64_t l = sc & 31u, kk = (sc & ~(kNewRow | kFlush)) >> 5;
         const int64_t e = (int64_t)vals[q] + e0;
         const uint32_t col = (uint32_t)(indices[e] % kTB);
         const uint32_t lr = (uint32_t)(key & kLocalMask);
         const int64_t p = (int64_t)(t / (unsigned long long)NB);
-        uint32_t word = (col << 3) | (tile_slot(lr) << 16);
-        if (flush) word |= kFlush;
-        if (newrow) word |= kNewRow;
+        uint32_t word = (col << 3) | (tile_slot(lr) << 16) | (sc & (kNewRow | kFlush));
         if (hub[panel_off[p] + (int32_t)lr]) word |= kHub;
         slots[(size_t)(toff[u] + kk) * 32 + l] = make_uint2(word, __float_as_uint(values[e]));
     }
@@ -692,6 +805,8 @@ struct TileWs {
     unsigned long long *keys_a, *keys_b;
     uint32_t *vals_a, *vals_b;
     int64_t *tstart, *tend, *steps, *toff;
+    uint8_t* cb;
+    uint32_t* sched;
     void* cub_tmp;
     size_t cub_bytes, bytes;
 };
@@ -725,6 +840,8 @@ static TileWs tile_ws_map(void* base, int64_t nr, int64_t m, int64_t ntb, int64_
     w.tend = (int64_t*)take(sizeof(int64_t) * (ntb + 1));
     w.steps = (int64_t*)take(sizeof(int64_t) * (ntiles + 1));
     w.toff = (int64_t*)take(sizeof(int64_t) * (ntiles + 1));
+    w.cb = (uint8_t*)take(sizeof(uint8_t) * std::max<int64_t>(m, 1));
+    w.sched = (uint32_t*)take(sizeof(uint32_t) * std::max<int64_t>(m, 1));
     w.cub_tmp = take(w.cub_bytes);
     w.bytes = off;
     return w;
@@ -871,7 +988,12 @@ int tsnet_plan_build(const tsnet_csr* P, const tsnet_shard* shard, void* plan, s
                                    cudaMemcpyHostToDevice, s));
     if (steps > 0) TSNET_CUDA(cudaMemsetAsync(d_slots, 0, sizeof(uint2) * 32 * (size_t)steps, s));
     if (m > 0) {
-        k_tile_fill<<<num_sms() * 8, 256, 0, s>>>(dk.Current(), dv.Current(), m, w.tstart, w.tend, w.seg, w.toff,
+        k_tile_banks<<<num_sms() * 8, 256, 0, s>>>(dk.Current(), dv.Current(), m, P->indices, cut.ip.front(), w.cb);
+        TSNET_LAUNCH_CHECK();
+        k_tile_schedule<<<(int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 127) / 128, (int64_t)num_sms() * 16)),
+                          128, 0, s>>>(dk.Current(), w.cb, w.tstart, w.tend, w.seg, w.toff, ntiles, w.sched);
+        TSNET_LAUNCH_CHECK();
+        k_tile_fill<<<num_sms() * 8, 256, 0, s>>>(dk.Current(), dv.Current(), m, w.sched, w.toff, w.seg, w.tstart,
                                                   (int)NB, w.panel_off, w.hub, P->indices, P->values, cut.ip.front(),
                                                   d_slots);
         TSNET_LAUNCH_CHECK();
