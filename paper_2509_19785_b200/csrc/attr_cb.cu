@@ -56,7 +56,13 @@ namespace tsnet {
 
 constexpr int kTB = 7168;            // points per column block (column * 8 < 2^16)
 constexpr int kTS = 2;               // Y ring stages (2 x 56 KB, double buffer)
-constexpr int kTPre = 3;             // blocks of entries prefetched into L2 ahead of the producer
+#ifndef TILE_PREF
+#define TILE_PREF 1
+#endif
+#ifndef TILE_PREF_CHUNK    // bytes per bulk L2 prefetch instruction (0 = the whole block range in one)
+#define TILE_PREF_CHUNK 0
+#endif
+constexpr int kTPre = TILE_PREF;     // blocks of entries prefetched into L2 ahead of the producer
 // probe builds only (scripts/tile_variants.sh): the slot-load cache policy
 #ifndef TILE_LDPOL
 #define TILE_LDPOL 0
@@ -182,6 +188,8 @@ __device__ __forceinline__ uint2 ld_slot(const uint2* a) {
     asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(a));
 #elif TILE_LDPOL == 1
     asm volatile("ld.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(a));
+#elif TILE_LDPOL == 3
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(a));
 #else
     asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(a));
 #endif
@@ -405,7 +413,14 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
             auto prefetch_block = [&](int J) {
                 if (J >= NB) return;
                 const int s0 = block_start(J), s1 = block_start(J + 1);
+#if TILE_PREF_CHUNK > 0
+                // the range split over the producer's lanes, TILE_PREF_CHUNK bytes per instruction
+                const uint64_t b0 = (uint64_t)s0 * 256u, b1 = (uint64_t)s1 * 256u;
+                for (uint64_t o = b0 + (uint64_t)lane * TILE_PREF_CHUNK; o < b1; o += 32u * TILE_PREF_CHUNK)
+                    prefetch_l2(reinterpret_cast<const char*>(slots) + o, (uint32_t)std::min<uint64_t>(TILE_PREF_CHUNK, b1 - o));
+#else
                 if (lane == 0 && s1 > s0) prefetch_l2(slots + (size_t)s0 * 32, (uint32_t)(s1 - s0) * 32u * 8u);
+#endif
             };
             for (int J = 0; J < NB; ++J) {
                 if (J + kTPre + 1 - B0 >= 64) {   // keep blocks [B0, B0 + 64) in bv / bn

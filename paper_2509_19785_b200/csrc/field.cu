@@ -11,7 +11,9 @@
 //   a3/a4 k_row_fwd, k_col, k_row_inv   kernel tabulation + 2-D FFT convolution
 //                             (rows -> columns with products -> inverse rows)
 //   a5 Z by Parseval inside k_col (fp64 accumulation)
-// Output: fgrid[gy][gx] = (P0, Qx, Qy) with the combined kernel
+// Output: fgrid = (P0, Qx, Qy) per node, box-major (node (gx, gy) at
+// ((gy / 3) I + gx / 3) 9 + (gy % 3) 3 + gx % 3: the 9 nodes a point gathers are
+// one 144-byte run), with the combined kernel
 //   C = alpha K2 + beta K_e,  alpha = -4 lambda_kl / Z,  beta = -lambda_r / n^2,
 //   P0 = C * W1,  Qx = (D_x C) * W1 + C * M_x,  Qy = (D_y C) * W1 + C * M_y,
 // so that for a point in box (bx, by) with in-box coordinates (u_x, u_y):
@@ -564,7 +566,7 @@ __global__ void __launch_bounds__(kInvThreads) k_row_inv(Geo* __restrict__ gp, c
                                                          int M_max, int N_max, int64_t n, float lambda_kl,
                                                          float lambda_r, int cap) {
     extern __shared__ float2 sm[];
-    const int M = gp->M, N = gp->N, nrad = gp->nrad;
+    const int M = gp->M, N = gp->N, nrad = gp->nrad, I = gp->I;
     const int B = fft_batch(cap, M, 2);
     float2* tw = sm;
     float2* buf = sm + M;                 // B M
@@ -600,7 +602,8 @@ __global__ void __launch_bounds__(kInvThreads) k_row_inv(Geo* __restrict__ gp, c
             __syncthreads();
             fft_block(buf, scr, M, nb, M, plan, nrad, tw, true);
             for (int x = threadIdx.x; x < N; x += blockDim.x) {
-                float* f = reinterpret_cast<float*>(fgrid + (int64_t)y * N + x);
+                // box-major: the 9 nodes of box (x / 3, y / 3) are contiguous (144 B per box)
+                float* f = reinterpret_cast<float*>(fgrid + ((int64_t)(y / 3) * I + x / 3) * 9 + (y % 3) * 3 + x % 3);
                 for (int q = 0; q < nb; ++q) {
                     const float2 a = buf[q * M + x];
                     if (t0 + q == 0) {

@@ -280,16 +280,20 @@ __global__ void __launch_bounds__(256) k_grad_out(int64_t n, const Geo* __restri
 }
 
 // n = rows of this call (local; Y, vel, gains point at the first own row); cn = lambda_c / n_global.
-// When the field grid (N^2 float4) fits the dynamic shared memory of the launch
-// (grid_cap cells), each CTA stages it first: the 9 node gathers per point then
-// cost no L2 requests (they were ~9 sector requests per point).
+// SMEM: the field grid (N^2 float4) fits the launch's dynamic shared memory
+// (grid_cap cells) and each CTA stages it first -- the 9 node gathers per point
+// then cost no L2 requests; else (large grids, N > 113) the 144-byte box runs
+// of the box-major grid are read through L1 by a launch without shared memory
+// (the whole L1 caches the grid).  Both variants are launched each iteration
+// (N is only known on the device); the one that does not apply exits at once.
 constexpr int kUpdateThreads = 1024;
+constexpr int kUpdateThreadsG = 256;
 constexpr int kGridSmemCells = 12800;   // 200 KB of float4
 // V points per thread and iteration (their loads in flight together); RECOMPUTE:
 // the box and in-box coordinates from the position (as k_box_count) instead of
 // reading them back (12 B/point less traffic, some fp64 arithmetic more)
-template <int V, bool RECOMPUTE>
-__global__ void __launch_bounds__(kUpdateThreads, 1) k_update(int64_t n, Geo* __restrict__ gp,
+template <int V, bool RECOMPUTE, bool SMEM>
+__global__ void __launch_bounds__(SMEM ? kUpdateThreads : kUpdateThreadsG, SMEM ? 1 : 4) k_update(int64_t n, Geo* __restrict__ gp,
                                                               const float4* __restrict__ fgrid,
                                                               const int* __restrict__ box, const float2* __restrict__ uv,
                                                               const float2* Yin, float2* Yout,
@@ -300,8 +304,9 @@ __global__ void __launch_bounds__(kUpdateThreads, 1) k_update(int64_t n, Geo* __
     extern __shared__ float4 fsm[];
     const Geo g = *gp;
     const int cells = g.N * g.N;
+    if (SMEM != (cells <= grid_cap)) return;   // the other variant handles this grid size
     const float4* fg = fgrid;
-    if (cells <= grid_cap) {
+    if (SMEM) {
         for (int q = threadIdx.x; q < cells; q += blockDim.x) fsm[q] = __ldg(fgrid + q);
         __syncthreads();
         fg = fsm;
@@ -333,7 +338,7 @@ __global__ void __launch_bounds__(kUpdateThreads, 1) k_update(int64_t n, Geo* __
         for (int q = 0; q < V; ++q) {
             const int64_t i = i0 + q * stride;
             if (i >= n) break;
-            const float2 ff = gather_field(g, fg, b[q], u[q]);
+            const float2 ff = gather_field<!SMEM>(g, fg, b[q], u[q]);
             const float gx = fmaf(4.0f * lambda_kl, fa[q].x, ff.x) + cn * y[q].x;
             const float gy = fmaf(4.0f * lambda_kl, fa[q].y, ff.y) + cn * y[q].y;
             gains_move(gx, v[q].x, gn[q].x, y[q].x, sp);
@@ -389,7 +394,8 @@ cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2
 
 // The move: 2 points per thread, box and in-box coordinates read back
 // (recomputing them from the position measured the same, r1cd).
-static constexpr auto update_kernel = k_update<2, false>;
+static constexpr auto update_kernel = k_update<2, false, true>;
+static constexpr auto update_kernel_g = k_update<2, false, false>;
 
 // Y, vel, gains: full n x 2 arrays; rows [rb, re) are updated
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,
@@ -403,6 +409,10 @@ cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nl + kUpdateThreads - 1) / kUpdateThreads, kNumSMs));
     update_kernel<<<blocks, kUpdateThreads, smem, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, Y + a.rb, Y + a.rb, w.f_attr,
                                                   vel + a.rb, gains + a.rb, a.lambda_kl, cn_of(a), sp, cap);
+    const int blocks_g =
+        (int)std::max<int64_t>(1, std::min<int64_t>((nl + 2 * kUpdateThreadsG - 1) / (2 * kUpdateThreadsG), kNumSMs * 8));
+    update_kernel_g<<<blocks_g, kUpdateThreadsG, 0, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, Y + a.rb, Y + a.rb, w.f_attr,
+                                                         vel + a.rb, gains + a.rb, a.lambda_kl, cn_of(a), sp, cap);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !sp.recenter) return e;
     k_recenter<<<pts_blocks(a.n), 256, 0, s>>>(a.n, w.geo, Y);
@@ -430,8 +440,9 @@ cudaError_t launch_update_rows(const Ws& w, const GradArgs& a, int64_t r0, int64
     // no shared-memory grid here: this move runs beside the SpMV of the next
     // chunk, whose CTAs run with the whole L1 carveout (a 200 KB shared-memory
     // CTA would wait for an idle SM); the field nodes are read through L1/L2
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nc + kUpdateThreads - 1) / kUpdateThreads, kNumSMs));
-    update_kernel<<<blocks, kUpdateThreads, 0, s>>>(nc, w.geo, w.fgrid, w.box + q, w.uv + q, a.Y + r0, Yout + r0,
+    const int blocks =
+        (int)std::max<int64_t>(1, std::min<int64_t>((nc + 2 * kUpdateThreadsG - 1) / (2 * kUpdateThreadsG), kNumSMs * 8));
+    update_kernel_g<<<blocks, kUpdateThreadsG, 0, s>>>(nc, w.geo, w.fgrid, w.box + q, w.uv + q, a.Y + r0, Yout + r0,
                                                w.f_attr + q, vel + r0, gains + r0, a.lambda_kl, cn_of(a), sp, 0);
     return cudaGetLastError();
 }

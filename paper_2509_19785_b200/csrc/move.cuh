@@ -30,28 +30,30 @@ __device__ __forceinline__ void lagrange3u(float u, float (&L)[3]) {
 }
 
 // f_field_i = sum_{a,b} L_a(u_x) L_b(u_y) [ (X_i - t_ab) P0 + Q ],  X_i - t_ab = (u - s) h_b
+// The field grid is box-major (field.cu, k_row_inv): the 9 nodes of box b
+// are fgrid[9 b .. 9 b + 8], node (a, bb) at 9 b + 3 bb + a.
+template <bool GLOBAL = false>
 __device__ __forceinline__ float2 gather_field(const Geo& g, const float4* __restrict__ fgrid, int b, float2 u) {
-    const int I = g.I, N = g.N;
     const float h_b = (float)g.h_b;
-    // b / I by a float reciprocal: (b + 1/2) / I is >= 1/(2I) away from an
-    // integer, far more than the fp32 error for b < I^2 <= 768^2
-    const int by = __float2int_rz(((float)b + 0.5f) * __frcp_rn((float)I)), bx = b - by * I;
     float Lx[3], Ly[3];
     lagrange3u(u.x, Lx);
     lagrange3u(u.y, Ly);
     const float s[3] = {1.0f / 6.0f, 0.5f, 5.0f / 6.0f};
+    const float4* box = fgrid + (int64_t)b * 9;   // generic loads: fgrid may be the shared-memory copy
+    float4 f[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) f[q] = GLOBAL ? __ldg(box + q) : box[q];
     float fx = 0.f, fy = 0.f;
 #pragma unroll
     for (int bb = 0; bb < 3; ++bb) {
-        const float4* row = fgrid + (int64_t)(3 * by + bb) * N + 3 * bx;
         const float ey = (u.y - s[bb]) * h_b;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            const float4 f = row[a];   // generic load: fgrid may be the shared-memory copy
+            const float4 v = f[3 * bb + a];
             const float wgt = Lx[a] * Ly[bb];
             const float ex = (u.x - s[a]) * h_b;
-            fx = fmaf(wgt, fmaf(ex, f.x, f.y), fx);
-            fy = fmaf(wgt, fmaf(ey, f.x, f.z), fy);
+            fx = fmaf(wgt, fmaf(ex, v.x, v.y), fx);
+            fy = fmaf(wgt, fmaf(ey, v.x, v.z), fy);
         }
     }
     return make_float2(fx, fy);
