@@ -54,8 +54,14 @@
 
 namespace tsnet {
 
-constexpr int kTB = 7168;            // points per column block (column * 8 < 2^16)
-constexpr int kTS = 2;               // Y ring stages (2 x 56 KB, double buffer)
+#ifndef TILE_TB
+#define TILE_TB 8000
+#endif
+#ifndef TILE_TR
+#define TILE_TR 6464
+#endif
+constexpr int kTB = TILE_TB;         // points per column block (column * 8 < 2^16)
+constexpr int kTS = 2;               // Y ring stages (2 x 62.5 KB, double buffer)
 #ifndef TILE_PREF
 #define TILE_PREF 1
 #endif
@@ -72,7 +78,8 @@ constexpr int kTPre = TILE_PREF;     // blocks of entries prefetched into L2 ahe
 #endif
 constexpr int kTW = 15;              // consumer warps per CTA (+1 producer warp: 16 warps, <= 128 registers)
 constexpr int kTL = kTW * 32;        // consumer threads
-constexpr int kTR = 6912;            // max rows per panel (13-bit local row; 16 B of shared memory each)
+constexpr int kTR = TILE_TR;         // max rows per panel (13-bit local row; 16 B of shared memory each;
+                                     // a multiple of 16 for the row-slot swizzle; cfg 4 needs 6,408)
 constexpr int kTRbits = 13;
 constexpr unsigned long long kLocalMask = (1ull << kTRbits) - 1;
 // slot word: column in block * 8 (bits 0-15, the byte offset of Y_j in the
@@ -214,13 +221,27 @@ __device__ __forceinline__ void load4(TileSet& S, const uint2* at, int left) {
 __device__ __forceinline__ float2 lds2(const char* base, uint32_t off) {
     return *reinterpret_cast<const float2*>(base + off);
 }
+// a predicated 64-bit shared load (0 where p is false).  Lanes that are off take
+// no part in the access: a warp's active lanes are served together when they
+// fit one wavefront, and an unused lane reading a common dummy address instead
+// costs a wavefront more (measured, scripts/probes/lds_bank_probe{2,3}.cu).
+// volatile: kept in program order with the block barriers (rows of F change
+// owners between blocks).
+__device__ __forceinline__ float2 lds2_if(uint32_t sbase, uint32_t off, bool p) {
+    float2 v = make_float2(0.f, 0.f);
+    asm volatile(
+        "{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q ld.shared.v2.f32 {%0, %1}, [%3];\n}"
+        : "+f"(v.x), "+f"(v.y)
+        : "r"((uint32_t)p), "r"(sbase + off));
+    return v;
+}
 
 // NQ consecutive entries of this lane: contribution p w (X_i - X_j), w = 1 /
 // (1 + r^2) (rcp.approx: 1 + r^2 >= 1, relative error <= 2^-22); pad slots
 // (word 0, p = 0) add exactly 0.  Y_i is read when a run starts (NEWROW) and
 // kept in registers; a run's sum goes to its row when it ends here (FLUSH).
-// All loads of the NQ entries are issued first; lanes with nothing to read
-// address the dummy (a broadcast), so bank conflicts come only from real reads.
+// All loads of the NQ entries are issued first; Y_i and F_i loads are
+// predicated on NEWROW / FLUSH (lanes that are off add no bank conflicts).
 // The flush values are formed in registers and the (distinct: a row is one run
 // of a lane) rows read-modified-written together.  lastw = the slot word of the
 // lane's last real entry (a real word is never 0: the first entry of a run
@@ -228,6 +249,7 @@ __device__ __forceinline__ float2 lds2(const char* base, uint32_t off) {
 template <int NQ>
 __device__ __forceinline__ void tileq(const TileSet& S, const char* sm, uint32_t ysoff, float2& yi, float& ax,
                                       float& ay, uint32_t& lastw) {
+    const uint32_t sb = smem_u32(sm);
     float2 yj[NQ], yl[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -238,7 +260,7 @@ __device__ __forceinline__ void tileq(const TileSet& S, const char* sm, uint32_t
 #else
         yj[q] = lds2(sm, ysoff + (w & kColMask));
 #endif
-        yl[q] = lds2(sm, (w & kNewRow) ? ro : kDummyOff);
+        yl[q] = lds2_if(sb, ro, w & kNewRow);
     }
     float fx[NQ], fy[NQ];
 #pragma unroll
@@ -267,7 +289,7 @@ __device__ __forceinline__ void tileq(const TileSet& S, const char* sm, uint32_t
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         const uint32_t w = S.s[q].x;
-        v[q] = lds2(sm, ((w & (kFlush | kHub)) == kFlush) ? kFsOff + ((w >> kRowShift) & kRowMask) : kDummyOff);
+        v[q] = lds2_if(sb, kFsOff + ((w >> kRowShift) & kRowMask), (w & (kFlush | kHub)) == kFlush);
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
@@ -676,22 +698,38 @@ __global__ void k_tile_banks(const unsigned long long* __restrict__ keys, const 
     }
 }
 
-constexpr int kSchedMaxK = 64;   // chunks longer than this keep the row-sorted order
+constexpr int kSchedMaxK = 512;    // chunks longer than this keep the row-sorted order
+constexpr int kSchedW = kSchedMaxK / 64;
 
-__device__ __forceinline__ unsigned long long bits(int lo, int hi) {   // bits [lo, hi), 0 <= lo <= hi <= 64
-    const unsigned long long up = hi >= 64 ? ~0ull : ((1ull << hi) - 1);
-    return up & ~((1ull << lo) - 1);
-}
+// A lane's chunk as a set of entries not yet placed (bit i: chunk index i).
+struct ChunkSet {
+    unsigned long long w[kSchedW];
+    __device__ bool has(int i) const { return (w[i >> 6] >> (i & 63)) & 1ull; }
+    __device__ void take(int i) { w[i >> 6] &= ~(1ull << (i & 63)); }
+    __device__ int count(int lo, int hi) const {     // entries left in [lo, hi)
+        int c = 0;
+        for (int q = lo >> 6; q <= (hi - 1) >> 6 && lo < hi; ++q) {
+            unsigned long long m = w[q];
+            if (q == lo >> 6) m &= ~0ull << (lo & 63);
+            if (q == (hi - 1) >> 6 && (hi & 63)) m &= (1ull << (hi & 63)) - 1;
+            c += __popcll(m);
+        }
+        return c;
+    }
+};
 
 // Per warp tile (one thread): the order in which each lane walks its chunk.
 // Any order keeps the arithmetic of a chunk (each row's entries form one run,
 // a run's entries are summed in registers) as long as a run's entries stay
 // consecutive and the run carried into the next chunk (if any) comes last.
-// Within those rules a greedy pass picks, step by step and lane by lane, the
-// entry whose shared-memory banks (Y_j, and Y_i / F_i where a run starts /
-// ends) are least used so far by the lanes of the same half-warp at that step
-// -- random gathers otherwise pile up ~3 deep per bank pair.  Output per
-// sorted position: step << 5 | lane | NEWROW << 30 | FLUSH << 31.
+// Within those rules a greedy pass picks, step by step, an entry for every
+// lane whose shared-memory banks (Y_j, and Y_i / F_i where a run starts / ends)
+// are least used so far by the lanes of the same half-warp at that step (a
+// 64-bit shared access is served per half-warp: scripts/probes/) -- random
+// gathers otherwise pile up ~3 deep per bank pair.  The most constrained lanes
+// choose first: those with one entry to choose from, then those inside a run,
+// then those starting a run.  Output per sorted position: step << 5 | lane |
+// NEWROW << 30 | FLUSH << 31.
 __global__ void k_tile_schedule(const unsigned long long* __restrict__ keys, const uint8_t* __restrict__ cb,
                                 const int64_t* __restrict__ tstart, const int64_t* __restrict__ tend,
                                 const int32_t* __restrict__ seg, const int64_t* __restrict__ toff, int64_t ntiles,
@@ -714,71 +752,84 @@ __global__ void k_tile_schedule(const unsigned long long* __restrict__ keys, con
             }
             continue;
         }
-        unsigned long long done[32];
-        int8_t rs[32], re[32], tail[32];
+        ChunkSet left[32];
+        int16_t rs[32], re[32], tail[32], nleft[32];
         for (int l = 0; l < 32; ++l) {
-            done[l] = 0ull;
+            const int64_t a = l * K, b = std::min<int64_t>(a + K, E);
+            const int n = a < b ? (int)(b - a) : 0;
+            for (int q = 0; q < kSchedW; ++q) {
+                const int lo = q * 64;
+                left[l].w[q] = n <= lo ? 0ull : (n - lo >= 64 ? ~0ull : ((1ull << (n - lo)) - 1));
+            }
+            nleft[l] = (int16_t)n;
             rs[l] = re[l] = -1;
             tail[l] = -1;
-            const int64_t a = l * K, b = std::min<int64_t>(a + K, E);
-            if (a < b && cont(b - 1)) {    // the chunk's last run goes on past it: it must come last
+            if (n > 0 && cont(b - 1)) {    // the chunk's last run goes on past it: it must come last
                 int64_t st = b - 1;
                 while (st > a && key(st - 1) == key(b - 1)) --st;
-                tail[l] = (int8_t)(st - a);
+                tail[l] = (int16_t)(st - a);
             }
         }
         for (int64_t k = 0; k < K; ++k) {
             uint8_t hy[2][16], hr[2][16];
             for (int q = 0; q < 16; ++q) hy[0][q] = hy[1][q] = hr[0][q] = hr[1][q] = 0;
+            // class of each lane at this step: 0 one choice, 1 inside a run, 2 a new run, 3 done
+            uint8_t cls[32];
             for (int l = 0; l < 32; ++l) {
-                const int64_t a = l * K, b = std::min<int64_t>(a + K, E);
-                if (a >= b) continue;
-                const int n = (int)(b - a);
-                if ((~done[l] & bits(0, n)) == 0) continue;
-                const int h = l >> 4;
-                int pick = -1;
-                bool newrow = false;
-                if (rs[l] >= 0 && (~done[l] & bits(rs[l], re[l])) != 0) {
-                    int best = 1 << 30;
-                    for (int i = rs[l]; i < re[l]; ++i) {
-                        if (done[l] >> i & 1) continue;
-                        const int c = hy[h][cb[base + a + i] & 15];
-                        if (c < best) { best = c; pick = i; }
-                    }
-                } else {
-                    // a new run: any remaining entry; the tail run only when nothing else is left
-                    const bool only_tail = tail[l] >= 0 && (~done[l] & bits(0, tail[l])) == 0;
-                    int best = 1 << 30;
-                    for (int i = 0; i < n; ++i) {
-                        if (done[l] >> i & 1) continue;
-                        if (tail[l] >= 0 && i >= tail[l] && !only_tail) continue;
-                        const uint8_t bb = cb[base + a + i];
-                        const bool single = (i == 0 || key(a + i - 1) != key(a + i)) &&
-                                            (i == n - 1 || key(a + i + 1) != key(a + i));
-                        const int c = 4 * hy[h][bb & 15] + 2 * hr[h][bb >> 4] * (single ? 2 : 1);
-                        if (c < best) { best = c; pick = i; }
-                    }
-                    int st = pick, en = pick + 1;
-                    while (st > 0 && key(a + st - 1) == key(a + pick)) --st;
-                    while (en < n && key(a + en) == key(a + pick)) ++en;
-                    rs[l] = (int8_t)st;
-                    re[l] = (int8_t)en;
-                    newrow = true;
-                }
-                done[l] |= 1ull << pick;
-                const uint8_t bb = cb[base + a + pick];
-                hy[h][bb & 15]++;
-                if (newrow) hr[h][bb >> 4]++;
-                const bool run_left = (~done[l] & bits(rs[l], re[l])) != 0;
-                bool flush = false;
-                if (!run_left) {
-                    // the run's part in this chunk is done: it ends here unless it goes on past the chunk
-                    flush = !(re[l] == n && cont(a + n - 1));
-                    if (flush) hr[h][bb >> 4]++;
-                    rs[l] = re[l] = -1;
-                }
-                sched[base + a + pick] = (uint32_t)(k << 5) | (uint32_t)l | (newrow ? kNewRow : 0u) | (flush ? kFlush : 0u);
+                if (nleft[l] == 0) { cls[l] = 3; continue; }
+                const bool inrun = rs[l] >= 0 && left[l].count(rs[l], re[l]) > 0;
+                const int choices = inrun ? left[l].count(rs[l], re[l]) : nleft[l];
+                cls[l] = choices == 1 ? 0 : (inrun ? 1 : 2);
             }
+            for (int c = 0; c < 3; ++c)
+                for (int l = 0; l < 32; ++l) {
+                    if (cls[l] != c) continue;
+                    const int64_t a = l * K;
+                    const int n = (int)(std::min<int64_t>(a + K, E) - a);
+                    const int h = l >> 4;
+                    int pick = -1;
+                    bool newrow = false;
+                    if (rs[l] >= 0 && left[l].count(rs[l], re[l]) > 0) {
+                        int best = 1 << 30;
+                        for (int i = rs[l]; i < re[l]; ++i) {
+                            if (!left[l].has(i)) continue;
+                            const int cst = hy[h][cb[base + a + i] & 15];
+                            if (cst < best) { best = cst; pick = i; }
+                        }
+                    } else {
+                        // a new run: any remaining entry; the tail run only when nothing else is left
+                        const bool only_tail = tail[l] >= 0 && left[l].count(0, tail[l]) == 0;
+                        const int hi = (tail[l] >= 0 && !only_tail) ? tail[l] : n;
+                        int best = 1 << 30;
+                        for (int i = 0; i < hi; ++i) {
+                            if (!left[l].has(i)) continue;
+                            const uint8_t bb = cb[base + a + i];
+                            const bool single = (i == 0 || key(a + i - 1) != key(a + i)) &&
+                                                (i == n - 1 || key(a + i + 1) != key(a + i));
+                            const int cst = hy[h][bb & 15] + hr[h][bb >> 4] * (single ? 2 : 1);
+                            if (cst < best) { best = cst; pick = i; }
+                        }
+                        int st = pick, en = pick + 1;
+                        while (st > 0 && key(a + st - 1) == key(a + pick)) --st;
+                        while (en < n && key(a + en) == key(a + pick)) ++en;
+                        rs[l] = (int16_t)st;
+                        re[l] = (int16_t)en;
+                        newrow = true;
+                    }
+                    left[l].take(pick);
+                    --nleft[l];
+                    const uint8_t bb = cb[base + a + pick];
+                    hy[h][bb & 15]++;
+                    if (newrow) hr[h][bb >> 4]++;
+                    bool flush = false;
+                    if (left[l].count(rs[l], re[l]) == 0) {
+                        // the run's part in this chunk is done: it ends here unless it goes on past the chunk
+                        flush = !(re[l] == n && cont(a + n - 1));
+                        if (flush) hr[h][bb >> 4]++;
+                        rs[l] = re[l] = -1;
+                    }
+                    sched[base + a + pick] = (uint32_t)(k << 5) | (uint32_t)l | (newrow ? kNewRow : 0u) | (flush ? kFlush : 0u);
+                }
         }
     }
 }
