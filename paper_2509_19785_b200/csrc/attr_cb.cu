@@ -73,6 +73,9 @@ constexpr int kTPre = TILE_PREF;     // blocks of entries prefetched into L2 ahe
 #ifndef TILE_LDPOL
 #define TILE_LDPOL 0
 #endif
+#ifndef TILE_SETS   // probe builds: 4 = slot loads three groups ahead (four register sets)
+#define TILE_SETS 3
+#endif
 #ifndef TILE_DIAG   // timing diagnostics only (wrong results): 1 no F read-modify-write, 2 Y_j from one address
 #define TILE_DIAG 0
 #endif
@@ -221,19 +224,17 @@ __device__ __forceinline__ void load4(TileSet& S, const uint2* at, int left) {
 __device__ __forceinline__ float2 lds2(const char* base, uint32_t off) {
     return *reinterpret_cast<const float2*>(base + off);
 }
-// a predicated 64-bit shared load (0 where p is false).  Lanes that are off take
-// no part in the access: a warp's active lanes are served together when they
-// fit one wavefront, and an unused lane reading a common dummy address instead
-// costs a wavefront more (measured, scripts/probes/lds_bank_probe{2,3}.cu).
-// volatile: kept in program order with the block barriers (rows of F change
-// owners between blocks).
-__device__ __forceinline__ float2 lds2_if(uint32_t sbase, uint32_t off, bool p) {
-    float2 v = make_float2(0.f, 0.f);
+// a predicated 64-bit shared load (v kept where p is false).  Lanes that are
+// off take no part in the access: a warp's active lanes are served together
+// when they fit one wavefront, and an unused lane reading a common dummy
+// address instead costs a wavefront more (measured,
+// scripts/probes/lds_bank_probe{2,3,4}.cu).  volatile: kept in program order
+// with the block barriers (rows of F change owners between blocks).
+__device__ __forceinline__ void lds2_if(float2& v, uint32_t sbase, uint32_t off, bool p) {
     asm volatile(
         "{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q ld.shared.v2.f32 {%0, %1}, [%3];\n}"
         : "+f"(v.x), "+f"(v.y)
         : "r"((uint32_t)p), "r"(sbase + off));
-    return v;
 }
 
 // NQ consecutive entries of this lane: contribution p w (X_i - X_j), w = 1 /
@@ -260,7 +261,8 @@ __device__ __forceinline__ void tileq(const TileSet& S, const char* sm, uint32_t
 #else
         yj[q] = lds2(sm, ysoff + (w & kColMask));
 #endif
-        yl[q] = lds2_if(sb, ro, w & kNewRow);
+        yl[q] = make_float2(0.f, 0.f);
+        lds2_if(yl[q], sb, ro, w & kNewRow);
     }
     float fx[NQ], fy[NQ];
 #pragma unroll
@@ -289,7 +291,8 @@ __device__ __forceinline__ void tileq(const TileSet& S, const char* sm, uint32_t
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         const uint32_t w = S.s[q].x;
-        v[q] = lds2_if(sb, kFsOff + ((w >> kRowShift) & kRowMask), (w & (kFlush | kHub)) == kFlush);
+        v[q] = make_float2(0.f, 0.f);
+        lds2_if(v[q], sb, kFsOff + ((w >> kRowShift) & kRowMask), (w & (kFlush | kHub)) == kFlush);
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
@@ -534,6 +537,40 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
                 float ax = 0.f, ay = 0.f;
                 float2 yi = make_float2(0.f, 0.f);
                 uint32_t lastw = 0;
+#if TILE_SETS == 4
+                // four register sets rotated by unrolling, loads three groups ahead
+                const uint2* ld = at + 256;          // step 8
+                TileSet G;
+                load4(C, ld, K - 8);
+                ld += 128;
+#pragma unroll 1
+                for (int left = K;;) {
+                    load4(G, ld, left - 12);
+                    if (left < 4) { tile_tail(A, left, sm, ysoff, yi, ax, ay, lastw); break; }
+                    tileq<4>(A, sm, ysoff, yi, ax, ay, lastw);
+                    left -= 4;
+                    ld += 128;
+                    if (left <= 0) break;
+                    load4(A, ld, left - 12);
+                    if (left < 4) { tile_tail(B, left, sm, ysoff, yi, ax, ay, lastw); break; }
+                    tileq<4>(B, sm, ysoff, yi, ax, ay, lastw);
+                    left -= 4;
+                    ld += 128;
+                    if (left <= 0) break;
+                    load4(B, ld, left - 12);
+                    if (left < 4) { tile_tail(C, left, sm, ysoff, yi, ax, ay, lastw); break; }
+                    tileq<4>(C, sm, ysoff, yi, ax, ay, lastw);
+                    left -= 4;
+                    ld += 128;
+                    if (left <= 0) break;
+                    load4(C, ld, left - 12);
+                    if (left < 4) { tile_tail(G, left, sm, ysoff, yi, ax, ay, lastw); break; }
+                    tileq<4>(G, sm, ysoff, yi, ax, ay, lastw);
+                    left -= 4;
+                    ld += 128;
+                    if (left <= 0) break;
+                }
+#else
                 // three register sets rotated by unrolling, loads two groups ahead;
                 // the last 1-3 steps of the tile run exactly (no pad steps computed)
                 const uint2* ld = at + 256;          // step 8
@@ -558,6 +595,7 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
                     ld += 128;
                     if (left <= 0) break;
                 }
+#endif
                 tile_carry(ax, ay, lastw, const_cast<char*>(sm) + kFsOff, lane);
             }
             cur = nxt;
@@ -700,6 +738,12 @@ __global__ void k_tile_banks(const unsigned long long* __restrict__ keys, const 
 
 constexpr int kSchedMaxK = 512;    // chunks longer than this keep the row-sorted order
 constexpr int kSchedW = kSchedMaxK / 64;
+#ifndef SCHED_WY    // probe builds: weights of the Y_j and the Y_i / F_i bank counts
+#define SCHED_WY 1
+#endif
+#ifndef SCHED_WR
+#define SCHED_WR 2
+#endif
 
 // A lane's chunk as a set of entries not yet placed (bit i: chunk index i).
 struct ChunkSet {
@@ -806,7 +850,7 @@ __global__ void k_tile_schedule(const unsigned long long* __restrict__ keys, con
                             const uint8_t bb = cb[base + a + i];
                             const bool single = (i == 0 || key(a + i - 1) != key(a + i)) &&
                                                 (i == n - 1 || key(a + i + 1) != key(a + i));
-                            const int cst = hy[h][bb & 15] + hr[h][bb >> 4] * (single ? 2 : 1);
+                            const int cst = SCHED_WY * hy[h][bb & 15] + SCHED_WR * hr[h][bb >> 4] * (single ? 2 : 1);
                             if (cst < best) { best = cst; pick = i; }
                         }
                         int st = pick, en = pick + 1;

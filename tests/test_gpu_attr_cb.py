@@ -93,7 +93,8 @@ def test_configs(cfg, plan):
 @pytest.mark.parametrize("plan", ["cb", "sell", "csr"])
 @pytest.mark.parametrize("n,kind", [(1, "single"), (7, "tiny"), (4095, "one_block_minus"), (4096, "one_block"),
                                     (4097, "block_plus_one"), (7167, "tile_block_minus"), (7168, "tile_block"),
-                                    (7169, "tile_block_plus"), (8191, "two_blocks_minus"), (8192, "two_blocks"),
+                                    (7169, "tile_block_plus"), (7999, "y_block_minus"), (8000, "y_block"),
+                                    (8001, "y_block_plus"), (8191, "two_blocks_minus"), (8192, "two_blocks"),
                                     (8193, "block_plus_one"), (24577, "odd_tail"), (20011, "hub_and_empty"),
                                     (50000, "short_rows"), (30011, "many_empty")])
 def test_edge_patterns(n, kind, plan):
@@ -109,7 +110,7 @@ def test_edge_patterns(n, kind, plan):
         L = rng.integers(0, 4, n)
     if kind == "many_empty":
         L[rng.random(n) < 0.8] = 0
-    if kind in ("one_block", "two_blocks", "tile_block"):
+    if kind in ("one_block", "two_blocks", "tile_block", "y_block"):
         L[0] = n                        # one row filling whole tiles: a run over many lanes (atomic pieces)
     ip, ix, pv = random_csr(n, L, seed=n)
     Y = uniform_layout(n, 10.0, 9)
