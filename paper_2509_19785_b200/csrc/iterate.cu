@@ -263,16 +263,19 @@ cudaError_t launch_spmv(const Ws& w, const GradArgs& a, cudaStream_t s) {
 // mode 0: write grad; mode 1: write f_field (and F_attr stays in ws)
 // n = rows of this call (local); cn = lambda_c / n_global
 __global__ void __launch_bounds__(256) k_grad_out(int64_t n, const Geo* __restrict__ gp, const float4* __restrict__ fgrid,
-                                                  const int* __restrict__ box, const float2* __restrict__ uv,
                                                   const float2* __restrict__ Y, const float2* __restrict__ Fa,
                                                   float lambda_kl, float cn, float2* __restrict__ grad,
                                                   float2* __restrict__ f_field) {
     const Geo g = *gp;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const float2 ff = gather_field(g, fgrid, box[i], uv[i]);
+        const float2 y = Y[i];
+        int b;
+        float2 u;
+        box_of(y, g.lo_x, g.lo_y, g.h_b, g.I, b, u.x, u.y);
+        const float2 ff = gather_field(g, fgrid, b, u);
         if (f_field) f_field[i] = ff;
         if (grad) {
-            const float2 y = Y[i], fa = Fa[i];
+            const float2 fa = Fa[i];
             grad[i] = make_float2(fmaf(4.0f * lambda_kl, fa.x, ff.x) + cn * y.x,
                                   fmaf(4.0f * lambda_kl, fa.y, ff.y) + cn * y.y);
         }
@@ -384,7 +387,7 @@ static float cn_of(const GradArgs& a) { return (float)((double)a.lambda_c / (dou
 cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2* f_field, double* Z,
                             cudaStream_t s) {
     const int64_t nl = a.re - a.rb;
-    k_grad_out<<<pts_blocks(nl), 256, 0, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, a.Y + a.rb, w.f_attr, a.lambda_kl,
+    k_grad_out<<<pts_blocks(nl), 256, 0, s>>>(nl, w.geo, w.fgrid, a.Y + a.rb, w.f_attr, a.lambda_kl,
                                               cn_of(a), grad, f_field);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -392,10 +395,10 @@ cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2
     return e;
 }
 
-// The move: 2 points per thread, box and in-box coordinates read back
-// (recomputing them from the position measured the same, r1cd).
-static constexpr auto update_kernel = k_update<2, false, true>;
-static constexpr auto update_kernel_g = k_update<2, false, false>;
+// The move: 2 points per thread, box and in-box coordinates recomputed from
+// the position (the chunk-local spread, k_spread_local, does not store them).
+static constexpr auto update_kernel = k_update<2, true, true>;
+static constexpr auto update_kernel_g = k_update<2, true, false>;
 
 // Y, vel, gains: full n x 2 arrays; rows [rb, re) are updated
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,

@@ -1,0 +1,14 @@
+#!/bin/bash
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+for v in sortonly product loc4096; do
+  timeout 300 python scripts/step_variant_probe.py 5 600 $v >> gpurun_out/r3c_variants.log 2>&1
+  timeout 300 python scripts/step_variant_probe.py 4 990 $v >> gpurun_out/r3c_variants.log 2>&1
+  timeout 300 python scripts/step_variant_probe.py 5 100 $v >> gpurun_out/r3c_variants.log 2>&1
+done
+timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/r3c_launches5.csv python scripts/late_window_launches.py 5 600 3 > gpurun_out/r3c_ncu5.log 2>&1
+python scripts/ncu_summary.py launches gpurun_out/r3c_launches5.csv gpurun_out/r3c_launches5.txt
+timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/r3c_launches5a.csv python scripts/late_window_launches.py 5 100 3 > gpurun_out/r3c_ncu5a.log 2>&1
+python scripts/ncu_summary.py launches gpurun_out/r3c_launches5a.csv gpurun_out/r3c_launches5a.txt
