@@ -80,7 +80,6 @@ struct Ws {
     int* box_start;      // I_max^2 + 1
     int2* items;         // max_items (box, first point)
     float4* wgrid;       // N_max^2 spread charges (W1, Mx, My, 0), row-major [gy][gx]
-    float* spart;        // kNumSMs x 27 kLocalBoxes: private grids of k_spread_local
     float2* tw;          // M_max twiddles exp(-2 pi i k / M)
     float2* spec;        // 10 * (M_max/2+1) * M_max : forward row spectra, [a][kx][y]
     float2* colout;      // 6 * (M_max/2+1) * N_max  : after column pass, [b][kx][y]
@@ -94,10 +93,6 @@ struct Ws {
 };
 
 constexpr int kSpreadChunk = 256;   // points per spread work item
-#ifndef LOCAL_BOXES   // probe builds may move the switch between the two spread paths
-#define LOCAL_BOXES 1024
-#endif
-constexpr int kLocalBoxes = LOCAL_BOXES;   // grids of at most this many boxes: k_spread_local (field.cu)
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -129,7 +124,6 @@ inline Ws ws_map(void* base, int64_t n, int64_t nnz, int I_max) {
     w.box_start = (int*)take(sizeof(int) * nb);
     w.items = (int2*)take(sizeof(int2) * w.max_items);
     w.wgrid = (float4*)take(sizeof(float4) * (size_t)w.N_max * w.N_max);
-    w.spart = (float*)take(sizeof(float) * 27 * (size_t)kLocalBoxes * kNumSMs);
     w.tw = (float2*)take(sizeof(float2) * w.M_max);
     w.spec = (float2*)take(sizeof(float2) * 10 * half * (size_t)w.M_max);
     w.colout = (float2*)take(sizeof(float2) * 6 * half * (size_t)w.N_max);

@@ -8,8 +8,6 @@
 //   a1 k_box_count/k_box_scan/k_box_scatter  counting sort of points by box
 //   a2 k_spread               box-local charges W1 and local moments M_x, M_y (warp per
 //                             box chunk, register accumulation, 9 vector reds per warp)
-//   a1+a2 k_spread_local      both in one pass, chunk by chunk, for grids of at most
-//                             kLocalBoxes boxes (the sort kernels then return at once)
 //   a3/a4 k_row_fwd, k_col, k_row_inv   kernel tabulation + 2-D FFT convolution
 //                             (rows -> columns with products -> inverse rows)
 //   a5 Z by Parseval inside k_col (fp64 accumulation)
@@ -179,34 +177,17 @@ __global__ void k_prep(Geo* g, int* box_cnt, float4* wgrid, float2* tw) {
 // order of points inside a box is not deterministic (neither is the fp32
 // spread that follows).
 constexpr int kBoxSmem = 4096;     // counters (16 KB): I <= 64
-__device__ __forceinline__ bool use_local_spread(int I) { return I * I <= kLocalBoxes; }
 constexpr int kBoxPts = 8;         // points per thread
 constexpr int kBoxChunk = 256 * kBoxPts;
 
 // box_of (the box of a point and its in-box coordinates): move.cuh
 
-// rank of this lane's point among the points of the same box counted so far:
-// lanes with the same box (match.any) take one atomic for all of them -- a
-// layout whose consecutive points share boxes would otherwise serialise up to
-// 32 same-address atomics per instruction.  b < 0: no point (returns 0).
-__device__ __forceinline__ int rank_in_box(int* cnt, int b) {
-    const unsigned act = __activemask();
-    const unsigned peers = __match_any_sync(act, b);
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(peers) - 1;
-    int base = 0;
-    if (lane == leader && b >= 0) base = atomicAdd(&cnt[b], __popc(peers));
-    base = __shfl_sync(peers, base, leader);
-    return base + __popc(peers & ((1u << lane) - 1u));
-}
-
-__global__ void __launch_bounds__(256, 3) k_box_count(const float2* __restrict__ Y, int64_t n, const Geo* __restrict__ g,
+__global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__ Y, int64_t n, const Geo* __restrict__ g,
                                                    int* __restrict__ box_cnt, int* __restrict__ box,
                                                    int* __restrict__ rank, float2* __restrict__ uv) {
     __shared__ int hist[kBoxSmem];
     const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b;
     const int I = g->I;
-    if (use_local_spread(I)) return;
     const int nb = I * I;
     const bool local = nb <= kBoxSmem;
     const int64_t c0 = (int64_t)blockIdx.x * kBoxChunk + threadIdx.x;
@@ -226,12 +207,13 @@ __global__ void __launch_bounds__(256, 3) k_box_count(const float2* __restrict__
     for (int j = 0; j < kBoxPts; ++j) {
         const int64_t i = c0 + (int64_t)j * 256;
         bj[j] = -1;
+        rj[j] = 0;
         if (i < n) {
             float ux, uy;
             box_of(y[j], lo_x, lo_y, h_b, I, bj[j], ux, uy);
             uv[i] = make_float2(ux, uy);
+            rj[j] = atomicAdd(&cnt[bj[j]], 1);
         }
-        rj[j] = rank_in_box(cnt, bj[j]);
     }
     if (local) {
         __syncthreads();
@@ -255,7 +237,6 @@ __global__ void __launch_bounds__(256, 3) k_box_count(const float2* __restrict__
 // (one item per kSpreadChunk points of a box).  Single CTA of 1024 threads.
 __global__ void __launch_bounds__(1024) k_box_scan(Geo* g, const int* __restrict__ box_cnt, int* __restrict__ box_start,
                                                    int2* __restrict__ items, int64_t n) {
-    if (use_local_spread(g->I)) return;
     const int nb = g->I * g->I;
     const int T = blockDim.x;
     const int per = (nb + T - 1) / T;
@@ -296,11 +277,10 @@ __global__ void __launch_bounds__(1024) k_box_scan(Geo* g, const int* __restrict
 
 // 4 points per thread and iteration: their loads, then the box_start
 // gathers, then the stores, each in flight together
-__global__ void __launch_bounds__(256) k_box_scatter(const Geo* __restrict__ g, int64_t n, const int* __restrict__ box,
-                                                     const int* __restrict__ rank, const int* __restrict__ box_start,
-                                                     const float2* __restrict__ uv, float2* __restrict__ sorted_uv) {
+__global__ void __launch_bounds__(256) k_box_scatter(int64_t n, const int* __restrict__ box, const int* __restrict__ rank,
+                                                     const int* __restrict__ box_start, const float2* __restrict__ uv,
+                                                     float2* __restrict__ sorted_uv) {
     constexpr int V = 4;
-    if (use_local_spread(g->I)) return;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += V * stride) {
         int b[V], r[V], st[V];
@@ -332,7 +312,6 @@ __global__ void __launch_bounds__(256) k_spread(const Geo* __restrict__ g, const
                                                 const int* __restrict__ box_start,
                                                 const float2* __restrict__ sorted_uv, float4* __restrict__ wgrid) {
     const int nitems = g->nitems, I = g->I, N = g->N;
-    if (use_local_spread(I)) return;
     const float h_b = (float)g->h_b;
     const float s[3] = {1.0f / 6.0f, 0.5f, 5.0f / 6.0f};
     const int lane = threadIdx.x & 31;
@@ -384,203 +363,6 @@ __global__ void __launch_bounds__(256) k_spread(const Geo* __restrict__ g, const
             const int gx = 3 * bx + lane % 3, gy = 3 * by + lane / 3;
             red_add_v4(&wgrid[(int64_t)gy * N + gx], a0, a1 * h_b, a2 * h_b);
         }
-    }
-}
-
-// a1 + a2 in one pass for grids of at most kLocalBoxes boxes (I <= 32): a
-// persistent CTA per SM keeps a private copy of the charge grid in shared
-// memory (27 sums per box, box-major) and takes kLocChunk consecutive points
-// at a time: it sorts them by box in shared memory (counting sort: shared
-// histogram with one atomic per box and warp, block scan, scatter of the
-// in-box coordinates), then its warps walk the sorted chunk and add each box
-// segment to the private grid.  The private grids are written out once and
-// summed by k_spread_sum (no global atomics, no global sort: the layout is
-// read once).  Larger grids keep the global sort (k_box_count .. k_spread),
-// which returns at once here, and vice versa.
-constexpr int kLocThreads = 512;
-constexpr int kLocPts = 4;
-constexpr int kLocChunk = kLocThreads * kLocPts;
-constexpr int kLocSums = 27 * kLocalBoxes;     // floats of a private grid
-
-// 27 box-local sums of one point: W1, and the local moments before the h_b factor
-__device__ __forceinline__ void spread_point(float2 u, float (&acc)[27]) {
-    const float s[3] = {1.0f / 6.0f, 0.5f, 5.0f / 6.0f};
-    float Lx[3], Ly[3];
-    lagrange3(u.x, Lx);
-    lagrange3(u.y, Ly);
-#pragma unroll
-    for (int bb = 0; bb < 3; ++bb)
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const float w = Lx[a] * Ly[bb];
-            const int q = 3 * (3 * bb + a);
-            acc[q] += w;
-            acc[q + 1] += w * (s[a] - u.x);
-            acc[q + 2] += w * (s[bb] - u.y);
-        }
-}
-
-size_t spread_local_smem() { return sizeof(float) * (size_t)kLocSums; }
-
-__global__ void __launch_bounds__(kLocThreads, 1) k_spread_local(const float2* __restrict__ Y, int64_t n,
-                                                                  const Geo* __restrict__ g, float* __restrict__ part) {
-    extern __shared__ float grid3[];               // [box][27]
-    __shared__ int hist[kLocalBoxes + 1];          // counts, then starts (hist[nb] = points of the chunk)
-    __shared__ float2 suv[kLocChunk];              // in-box coordinates sorted by box
-    __shared__ int16_t sbox[kLocChunk];            // their boxes
-    __shared__ int wsum[kLocThreads / 32];
-    const int I = g->I;
-    if (!use_local_spread(I)) return;
-    const int nb = I * I;
-    const double lo_x = g->lo_x, lo_y = g->lo_y, h_bd = g->h_b;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int kPer = kLocalBoxes > kLocThreads ? (kLocalBoxes + kLocThreads - 1) / kLocThreads : 1;
-    for (int q = tid; q < 27 * nb; q += kLocThreads) grid3[q] = 0.f;
-    for (int64_t c0 = (int64_t)blockIdx.x * kLocChunk; c0 < n; c0 += (int64_t)gridDim.x * kLocChunk) {
-        for (int q = tid; q <= nb; q += kLocThreads) hist[q] = 0;
-        __syncthreads();
-        float2 y[kLocPts];
-#pragma unroll
-        for (int j = 0; j < kLocPts; ++j) {
-            const int64_t i = c0 + (int64_t)j * kLocThreads + tid;
-            y[j] = i < n ? Y[i] : make_float2(0.f, 0.f);
-        }
-        int bj[kLocPts], rj[kLocPts];
-        float2 uj[kLocPts];
-#pragma unroll
-        for (int j = 0; j < kLocPts; ++j) {
-            const int64_t i = c0 + (int64_t)j * kLocThreads + tid;
-            bj[j] = -1;
-            if (i < n) box_of(y[j], lo_x, lo_y, h_bd, I, bj[j], uj[j].x, uj[j].y);
-            rj[j] = rank_in_box(hist, bj[j]);
-        }
-        __syncthreads();
-        // exclusive scan of hist[0 .. nb) in place; hist[nb] = total
-        {
-            const int q0 = tid * kPer;
-            int loc[kPer], run = 0;
-#pragma unroll
-            for (int k = 0; k < kPer; ++k) {
-                loc[k] = (q0 + k < nb) ? hist[q0 + k] : 0;
-                run += loc[k];
-            }
-            int inc = run;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int v = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += v;
-            }
-            if (lane == 31) wsum[warp] = inc;
-            __syncthreads();
-            if (warp == 0) {
-                int v = lane < kLocThreads / 32 ? wsum[lane] : 0;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int u = __shfl_up_sync(0xffffffffu, v, o);
-                    if (lane >= o) v += u;
-                }
-                if (lane < kLocThreads / 32) wsum[lane] = v;   // inclusive warp totals
-            }
-            __syncthreads();
-            int st = inc - run + (warp > 0 ? wsum[warp - 1] : 0);
-#pragma unroll
-            for (int k = 0; k < kPer; ++k)
-                if (q0 + k < nb) {
-                    hist[q0 + k] = st;
-                    st += loc[k];
-                }
-            if (tid == kLocThreads - 1) hist[nb] = wsum[kLocThreads / 32 - 1];
-        }
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < kLocPts; ++j)
-            if (bj[j] >= 0) {
-                const int q = hist[bj[j]] + rj[j];
-                suv[q] = uj[j];
-                sbox[q] = (int16_t)bj[j];
-            }
-        __syncthreads();
-        // the sorted chunk in 16 contiguous warp ranges, 32 slots at a time: each
-        // lane's 27 sums, a segmented warp reduction by box, and the last lane of
-        // every box segment adds the segment to the private grid -- plain
-        // read-modify-writes, since a box's slots are contiguous: only the first
-        // and the last box of a warp range can be shared with a neighbouring
-        // range, and those two add atomically
-        {
-            const int total = hist[nb];
-            const int r0 = (int)((int64_t)total * warp / (kLocThreads / 32));
-            const int r1 = (int)((int64_t)total * (warp + 1) / (kLocThreads / 32));
-            const int bfirst = r0 < r1 ? sbox[r0] : -1, blast = r0 < r1 ? sbox[r1 - 1] : -1;
-            const bool shared_first = r0 < r1 && r0 > 0 && sbox[r0 - 1] == bfirst;
-            const bool shared_last = r0 < r1 && r1 < total && sbox[r1] == blast;
-            for (int w0 = r0; w0 < r1; w0 += 32) {
-                const int p = w0 + lane;
-                const bool ok = p < r1;
-                const int b = ok ? sbox[p] : -1 - lane;
-                float acc[27];
-#pragma unroll
-                for (int k = 0; k < 27; ++k) acc[k] = 0.f;
-                if (ok) spread_point(suv[p], acc);
-                // segmented inclusive scan (head flags) over the lanes
-                const int bp = __shfl_up_sync(0xffffffffu, b, 1);
-                bool head = lane == 0 || bp != b;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const bool uh = __shfl_up_sync(0xffffffffu, head, o);
-#pragma unroll
-                    for (int k = 0; k < 27; ++k) {
-                        const float v = __shfl_up_sync(0xffffffffu, acc[k], o);
-                        if (lane >= o && !head) acc[k] += v;
-                    }
-                    if (lane >= o) head = head || uh;
-                }
-                const int bn = __shfl_down_sync(0xffffffffu, b, 1);
-                if (ok && (lane == 31 || p + 1 == r1 || bn != b)) {
-                    float* gq = grid3 + 27 * b;
-                    if ((shared_first && b == bfirst) || (shared_last && b == blast)) {
-#pragma unroll
-                        for (int k = 0; k < 27; ++k) atomicAdd(gq + k, acc[k]);
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 27; ++k) gq[k] += acc[k];
-                    }
-                }
-                __syncwarp();
-            }
-        }
-        __syncthreads();    // hist / suv / items are reused by the next chunk
-    }
-    float* dst = part + (int64_t)blockIdx.x * kLocSums;
-    for (int q = tid; q < 27 * nb; q += kLocThreads) dst[q] = grid3[q];
-}
-
-// The private grids of the k_spread_local CTAs (nblk of them) summed into the
-// charge grid: (W1, h_b M_x, h_b M_y) per node.  Block = 32 sums x 8 groups of CTAs.
-__global__ void __launch_bounds__(256) k_spread_sum(const Geo* __restrict__ g, const float* __restrict__ part, int nblk,
-                                                    float4* __restrict__ wgrid) {
-    const int I = g->I;
-    if (!use_local_spread(I)) return;
-    const int nb = I * I, N = g->N;
-    const float h_b = (float)g->h_b;
-    __shared__ float red[8][33];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    for (int t0 = blockIdx.x * 32; t0 < 27 * nb; t0 += gridDim.x * 32) {
-        const int t = t0 + tx;
-        float s = 0.f;
-        if (t < 27 * nb) {
-#pragma unroll 4
-            for (int c = ty; c < nblk; c += 8) s += __ldg(part + (int64_t)c * kLocSums + t);
-        }
-        red[ty][tx] = s;
-        __syncthreads();
-        if (ty == 0 && t < 27 * nb) {
-            for (int k = 1; k < 8; ++k) s += red[k][tx];
-            const int b = t / 27, k = t % 27, node = k / 3, comp = k % 3;
-            const int bx = b % I, by = b / I;
-            float* dst = reinterpret_cast<float*>(&wgrid[(int64_t)(3 * by + node / 3) * N + 3 * bx + node % 3]);
-            dst[comp] = comp == 0 ? s : s * h_b;
-        }
-        __syncthreads();
     }
 }
 
@@ -944,7 +726,6 @@ cudaError_t field_set_attrs(int M_max) {
     if ((e = cudaFuncSetAttribute(k_row_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem_row(M_max))) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_col, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem_col(M_max))) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(k_row_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)field_smem_inv(M_max))) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(k_spread_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spread_local_smem())) != cudaSuccess) return e;
     return cudaSuccess;
 }
 
@@ -967,13 +748,8 @@ cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, b
     const int cb = (int)std::max<int64_t>(1, (nl + kBoxChunk - 1) / kBoxChunk);
     k_box_count<<<cb, 256, 0, s>>>(Yl, nl, w.geo, w.box_cnt, w.box, w.rank, w.uv);
     k_box_scan<<<1, 1024, 0, s>>>(w.geo, w.box_cnt, w.box_start, w.items, nl);
-    k_box_scatter<<<pbl, 256, 0, s>>>(w.geo, nl, w.box, w.rank, w.box_start, w.uv, w.sorted_uv);
+    k_box_scatter<<<pbl, 256, 0, s>>>(nl, w.box, w.rank, w.box_start, w.uv, w.sorted_uv);
     k_spread<<<kNumSMs * 8, 256, 0, s>>>(w.geo, w.items, w.box_start, w.sorted_uv, w.wgrid);
-    // grids of <= kLocalBoxes boxes (known on the device only): the four kernels
-    // above return at once and these sort and spread chunk by chunk
-    const int lc = (int)std::max<int64_t>(1, std::min<int64_t>((nl + kLocChunk - 1) / kLocChunk, (int64_t)kNumSMs));
-    k_spread_local<<<lc, kLocThreads, spread_local_smem(), s>>>(Yl, nl, w.geo, w.spart);
-    k_spread_sum<<<(kLocSums + 31) / 32, 256, 0, s>>>(w.geo, w.spart, lc, w.wgrid);
     return cudaGetLastError();
 }
 
