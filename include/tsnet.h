@@ -283,8 +283,8 @@ TSNET_API int tsnet_step(const tsnet_csr* P, float* Y, float* vel, float* gains,
  * (returns after the results are in the host buffers; work is ordered after
  * earlier work on `stream`).  Used for the end-to-end measurement of the
  * host-facing API.
- * Without recentring, shards or a plan (and n >= 8 * 16384), the rows are
- * processed in TSNET_HOST_CHUNKS (default 4) row chunks so that the download
+ * Without recentring, shards or a plan (and n >= 4 * 16384), the rows are
+ * processed in 4 row chunks so that the download
  * of a moved chunk overlaps the attractive SpMV of the next ones; the new
  * positions go to a separate workspace buffer until every chunk's SpMV has
  * read the old ones.  Results equal tsnet_step's up to fp32 summation order

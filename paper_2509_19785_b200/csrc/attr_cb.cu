@@ -60,38 +60,41 @@ namespace tsnet {
 #ifndef TILE_TR
 #define TILE_TR 6464
 #endif
-constexpr int kTB = TILE_TB;         // points per column block (column * 8 < 2^16)
+constexpr int kTB = TILE_TB;         // points per column block
 constexpr int kTS = 2;               // Y ring stages (2 x 62.5 KB, double buffer)
 #ifndef TILE_PREF
 #define TILE_PREF 1
-#endif
-#ifndef TILE_PREF_CHUNK    // bytes per bulk L2 prefetch instruction (0 = the whole block range in one)
-#define TILE_PREF_CHUNK 0
 #endif
 constexpr int kTPre = TILE_PREF;     // blocks of entries prefetched into L2 ahead of the producer
 // probe builds only (scripts/tile_variants.sh): the slot-load cache policy
 #ifndef TILE_LDPOL
 #define TILE_LDPOL 0
 #endif
-#ifndef TILE_SETS   // probe builds: 4 = slot loads three groups ahead (four register sets)
-#define TILE_SETS 3
-#endif
-#ifndef TILE_DIAG   // timing diagnostics only (wrong results): 1 no F read-modify-write, 2 Y_j from one address
+#ifndef TILE_DIAG   // timing diagnostics only (wrong results): 1 no F read-modify-write, 2 Y_j from one address,
+                    // 3/4 cycle counters, 5 no per-block barrier
 #define TILE_DIAG 0
 #endif
 constexpr int kTW = 15;              // consumer warps per CTA (+1 producer warp: 16 warps, <= 128 registers)
 constexpr int kTL = kTW * 32;        // consumer threads
-constexpr int kTR = TILE_TR;         // max rows per panel (13-bit local row; 16 B of shared memory each;
-                                     // a multiple of 16 for the row-slot swizzle; cfg 4 needs 6,408)
-constexpr int kTRbits = 13;
+constexpr int kTR = TILE_TR;         // max rows per panel (16 B of shared memory each; a multiple of 16
+                                     // for the row-slot swizzle)
+constexpr int kTRbits = 13;          // local row bits of the plan-build sort keys
 constexpr unsigned long long kLocalMask = (1ull << kTRbits) - 1;
-// slot word: column in block * 8 (bits 0-15, the byte offset of Y_j in the
-// ring stage) | row slot (bits 16-28; * 8 = byte offset of Y_i and F_i) |
-// HUB (bit 29: the row is shared between warps; its flushes are atomic) |
-// NEWROW (bit 30: a run starts here) | FLUSH (bit 31: a run ends here).  Real
-// entries have p > 0 (C0 drops exact zeros); pads are (0, p = 0).
-constexpr uint32_t kColMask = 0xFFF8u, kRowMask = 0xFFF8u, kHub = 1u << 29, kNewRow = 1u << 30, kFlush = 1u << 31;
-constexpr int kRowShift = 13;        // (word >> kRowShift) & kRowMask = row slot * 8
+constexpr int bits_for(int x) { return x <= 1 ? 0 : 1 + bits_for((x + 1) / 2); }
+constexpr int kColBits = bits_for(kTB);   // column in block
+constexpr int kSlotBits = bits_for(kTR);  // row slot
+static_assert(kTR % 16 == 0 && kTR <= (1 << kTRbits), "rows per panel");
+static_assert(kColBits + kSlotBits <= 26, "slot word: 3 + column + row-slot bits + 3 flags <= 32");
+// slot word: column in block * 8 (bits 0 .. 3 + kColBits: the byte offset of
+// Y_j in the ring stage) | row slot << (3 + kColBits) (the row-slot field
+// shifted right by kColBits is the byte offset of Y_i and F_i) | HUB (bit 29:
+// the row is shared between warps; its flushes are atomic) | NEWROW (bit 30: a
+// run starts here) | FLUSH (bit 31: a run ends here).  Real entries have p > 0
+// (C0 drops exact zeros); pads are (0, p = 0).
+constexpr uint32_t kColMask = ((1u << kColBits) - 1u) << 3;
+constexpr uint32_t kRowMask = ((1u << kSlotBits) - 1u) << 3;
+constexpr uint32_t kHub = 1u << 29, kNewRow = 1u << 30, kFlush = 1u << 31;
+constexpr int kRowShift = kColBits;  // (word >> kRowShift) & kRowMask = row slot * 8
 // Shared memory: Y_i[kTR] at 0, F_i[kTR] at kFsOff, a dummy float2 (lanes with
 // nothing to read there all read it: one broadcast address), the Y ring, the
 // mbarriers.  Row slot = swizzled local row (tile_slot): the rows a warp's
@@ -99,15 +102,28 @@ constexpr int kRowShift = 13;        // (word >> kRowShift) & kRowMask = row slo
 // indices would put them in a few banks.
 constexpr uint32_t kFsOff = kTR * 8u, kDummyOff = 2u * kTR * 8u, kRingOff = 2u * kTR * 8u + 16u;
 __host__ __device__ __forceinline__ uint32_t tile_slot(uint32_t r) { return r ^ ((r >> 4) & 15u); }
-constexpr uint64_t kTileMagic = 0x3654534e53545354ull;   // "TSTSNST6"
+// Panel p sweeps the column blocks rot, rot + 1, .., NB - 1, 0, .., rot - 1 with
+// rot = (p mod G) NB / G: the panels that run at the same time (one per CTA)
+// read different Y blocks, so the L2 is not hit by every SM for the same block.
+__host__ __device__ __forceinline__ int tile_rot(int p, int G, int NB) {
+    return (int)(((int64_t)(p % G) * NB) / G);
+}
+constexpr uint64_t kTileMagic = 0x3754534e53545354ull;   // "TSTSNST7"
 
 struct TileHeader {
     uint64_t magic;
     int64_t n, row_begin, row_end, nnz;
-    int32_t P, NB, R_max, pad;
+    int32_t P, NB, R_max, G;            // G: the CTAs the sweep rotations are spread over
     int64_t steps;                      // total warp steps (slots / 32)
     int64_t off_wtab, off_rowoff, off_rows, off_slots, bytes;
 };
+
+static int num_sms() {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = kNumSMs;
+    return sms;
+}
 
 static size_t t_align(size_t x) { return (x + 255) / 256 * 256; }
 
@@ -122,6 +138,7 @@ static TileHeader tile_layout(int64_t n, int64_t rb, int64_t re, int64_t nnz, in
     h.P = P;
     h.NB = (int32_t)std::max<int64_t>(1, (n + kTB - 1) / kTB);
     h.R_max = R_max;
+    h.G = std::max(1, num_sms());
     h.steps = steps;
     size_t off = t_align(sizeof(TileHeader));
     h.off_wtab = (int64_t)off;
@@ -134,13 +151,6 @@ static TileHeader tile_layout(int64_t n, int64_t rb, int64_t re, int64_t nnz, in
     off = t_align(off + sizeof(uint2) * 32 * (size_t)steps);
     h.bytes = (int64_t)off;
     return h;
-}
-
-static int num_sms() {
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = kNumSMs;
-    return sms;
 }
 
 // Host cut (pure).  ipr[q] = indptr[rb + q], q = 0 .. nr.  Panels:
@@ -405,7 +415,6 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
     const int32_t* rows = reinterpret_cast<const int32_t*>(plan + h->off_rows);
     const uint2* slots = reinterpret_cast<const uint2*>(plan + h->off_slots);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTS; ++s) {
             mbar_init(&bars[s], 1);
@@ -423,11 +432,14 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
         uint32_t k = 0;
         const unsigned full = 0xffffffffu;
         for (int p = blockIdx.x; p < P; p += gridDim.x) {
-            // first step of block J (warp 0's tile) in lane J - J0 of bv / bn; the
-            // panel's end step for J = NB
+            // The panel sweeps the column blocks from block rot (tile_rot): sweep
+            // position J is block jm(J).  wtab is in sweep order.  First step of
+            // the block at sweep position J (warp 0's tile) in lane J - B0 of bv / bn.
+            const int rot = tile_rot(p, h->G, NB);
+            auto jm = [&](int J) { return J + rot < NB ? J + rot : J + rot - NB; };
             const int2* w0 = wtab + (int64_t)p * kTW * NB;
-            const int2 lastt = w0[(int64_t)(kTW - 1) * NB + NB - 1];
-            const int pend = lastt.x + lastt.y;
+            const int2 lastt = w0[(int64_t)(kTW - 1) * NB + (NB - 1 - rot)];   // block NB - 1
+            const int pend = lastt.x + lastt.y;                               // the panel's end step
             auto start_of = [&](int J) { return J < NB ? __ldg(&w0[J].x) : pend; };
             int bv = start_of(min(lane, NB)), bn = start_of(min(32 + lane, NB));
             int B0 = 0;
@@ -435,38 +447,42 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
                 const int v = (J - B0 < 32) ? bv : bn;
                 return __shfl_sync(full, v, (J - B0) & 31);
             };
-            auto prefetch_block = [&](int J) {
+            auto prefetch_block = [&](int J) {  // the entries of the block at sweep position J
                 if (J >= NB) return;
-                const int s0 = block_start(J), s1 = block_start(J + 1);
-#if TILE_PREF_CHUNK > 0
-                // the range split over the producer's lanes, TILE_PREF_CHUNK bytes per instruction
-                const uint64_t b0 = (uint64_t)s0 * 256u, b1 = (uint64_t)s1 * 256u;
-                for (uint64_t o = b0 + (uint64_t)lane * TILE_PREF_CHUNK; o < b1; o += 32u * TILE_PREF_CHUNK)
-                    prefetch_l2(reinterpret_cast<const char*>(slots) + o, (uint32_t)std::min<uint64_t>(TILE_PREF_CHUNK, b1 - o));
-#else
+                const int s0 = block_start(J);
+                const int s1n = block_start(J + 1);   // the next sweep position's start (block jm(J) + 1)
+                const int s1 = jm(J) == NB - 1 ? pend : (J + 1 < NB ? s1n : __ldg(&w0[0].x));
                 if (lane == 0 && s1 > s0) prefetch_l2(slots + (size_t)s0 * 32, (uint32_t)(s1 - s0) * 32u * 8u);
-#endif
             };
             for (int J = 0; J < NB; ++J) {
-                if (J + kTPre + 1 - B0 >= 64) {   // keep blocks [B0, B0 + 64) in bv / bn
+                if (J + kTPre + 1 - B0 >= 64) {   // keep sweep positions [B0, B0 + 64) in bv / bn
                     B0 += 32;
                     bv = bn;
                     bn = start_of(min(B0 + 32 + lane, NB));
                 }
-                if (J == 0)
-                    for (int q = 0; q < kTPre; ++q) prefetch_block(q);
-                prefetch_block(J + kTPre);
+                if (kTPre >= 0) {
+                    if (J == 0)
+                        for (int q = 0; q < kTPre; ++q) prefetch_block(q);
+                    prefetch_block(J + kTPre);
+                }
                 const int b = (int)(k % kTS);
                 float2* dst = ring + b * kTB;
                 if (k >= (uint32_t)kTS) mbar_wait(&bars[kTS + b], ((k / kTS) - 1) & 1);
-                const int64_t lo = (int64_t)J * kTB;
+                const int64_t lo = (int64_t)jm(J) * kTB;
                 const int cnt = (int)std::min<int64_t>(kTB, n - lo);
                 if (y_aligned) {
                     const int even = cnt & ~1;
                     if (lane == 0) {
                         if (cnt & 1) dst[cnt - 1] = Y[lo + cnt - 1];
-                        mbar_arrive_tx(&bars[b], (uint32_t)(even * sizeof(float2)));
-                        if (even) bulk_g2s(dst, Y + lo, (uint32_t)(even * sizeof(float2)), &bars[b]);
+#if TILE_DIAG == 6      // timing probe (wrong results): half of every Y block
+                        const int ev = (even / 2) & ~1;
+#elif TILE_DIAG == 7    // timing probe (wrong results): no Y block loads
+                        const int ev = 0;
+#else
+                        const int ev = even;
+#endif
+                        mbar_arrive_tx(&bars[b], (uint32_t)(ev * sizeof(float2)));
+                        if (ev) bulk_g2s(dst, Y + lo, (uint32_t)(ev * sizeof(float2)), &bars[b]);
                     }
                 } else {
                     for (int q = lane; q < cnt; q += 32) dst[q] = Y[lo + q];
@@ -482,9 +498,9 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
     }
 
     // ---------------- consumer warp `warp`: its tile of every block, lane = chunk
-#if TILE_DIAG == 3
+#if TILE_DIAG >= 3
     const long long t_start = clock64();
-    long long t_wait = 0;
+    long long t_wait = 0, t_bar = 0;
 #endif
     const char* sm = reinterpret_cast<const char*>(t_smem);
     const unsigned full = 0xffffffffu;
@@ -525,52 +541,18 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
             load4(E, atn + 128, nxt.y - 4);
             const int b = (int)(k % kTS);
             const uint32_t ysoff = kRingOff + (uint32_t)b * (kTB * 8u);
-#if TILE_DIAG == 3
+#if TILE_DIAG >= 3
             const long long tw0 = clock64();
 #endif
             while (!mbar_try_wait_hint(&bars[b], (k / kTS) & 1)) {
             }
-#if TILE_DIAG == 3
+#if TILE_DIAG >= 3
             t_wait += clock64() - tw0;
 #endif
             if (K > 0) {
                 float ax = 0.f, ay = 0.f;
                 float2 yi = make_float2(0.f, 0.f);
                 uint32_t lastw = 0;
-#if TILE_SETS == 4
-                // four register sets rotated by unrolling, loads three groups ahead
-                const uint2* ld = at + 256;          // step 8
-                TileSet G;
-                load4(C, ld, K - 8);
-                ld += 128;
-#pragma unroll 1
-                for (int left = K;;) {
-                    load4(G, ld, left - 12);
-                    if (left < 4) { tile_tail(A, left, sm, ysoff, yi, ax, ay, lastw); break; }
-                    tileq<4>(A, sm, ysoff, yi, ax, ay, lastw);
-                    left -= 4;
-                    ld += 128;
-                    if (left <= 0) break;
-                    load4(A, ld, left - 12);
-                    if (left < 4) { tile_tail(B, left, sm, ysoff, yi, ax, ay, lastw); break; }
-                    tileq<4>(B, sm, ysoff, yi, ax, ay, lastw);
-                    left -= 4;
-                    ld += 128;
-                    if (left <= 0) break;
-                    load4(B, ld, left - 12);
-                    if (left < 4) { tile_tail(C, left, sm, ysoff, yi, ax, ay, lastw); break; }
-                    tileq<4>(C, sm, ysoff, yi, ax, ay, lastw);
-                    left -= 4;
-                    ld += 128;
-                    if (left <= 0) break;
-                    load4(C, ld, left - 12);
-                    if (left < 4) { tile_tail(G, left, sm, ysoff, yi, ax, ay, lastw); break; }
-                    tileq<4>(G, sm, ysoff, yi, ax, ay, lastw);
-                    left -= 4;
-                    ld += 128;
-                    if (left <= 0) break;
-                }
-#else
                 // three register sets rotated by unrolling, loads two groups ahead;
                 // the last 1-3 steps of the tile run exactly (no pad steps computed)
                 const uint2* ld = at + 256;          // step 8
@@ -595,7 +577,6 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
                     ld += 128;
                     if (left <= 0) break;
                 }
-#endif
                 tile_carry(ax, ay, lastw, const_cast<char*>(sm) + kFsOff, lane);
             }
             cur = nxt;
@@ -604,7 +585,15 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
             B = E;
             // all warps done with block J: its ring stage is free, and no row is
             // read-modified-written by two warps (rows change owners between blocks)
+#if TILE_DIAG == 4
+            const long long tb0 = clock64();
             bar_consumers();
+            t_bar += clock64() - tb0;
+#elif TILE_DIAG == 5
+            // timing probe (wrong results): no block barrier
+#else
+            bar_consumers();
+#endif
             if (threadIdx.x == 0) mbar_arrive(&bars[kTS + b]);
             ++k;
         }
@@ -613,14 +602,24 @@ __global__ void __launch_bounds__((kTW + 1) * 32, 1) k_attr_tile(const uint8_t* 
         for (int r = threadIdx.x; r < R; r += kTL) {
             const int32_t q = rows[r0 + r];
             const float2 f = Fs[tile_slot((uint32_t)r)];
+#if TILE_DIAG >= 3
+            if (f.x == 1.2345f) F[q & 0x7FFFFFFF] = f;   // timing probes: F holds the counters
+#else
             if (q >= 0) F[q] = f;
             else atomicAdd(F + (q & 0x7FFFFFFF), f);
+#endif
         }
         bar_consumers();              // the next panel reuses Yi / Fs
     }
 #if TILE_DIAG == 3
     // timing probe: per (CTA, warp) total cycles and cycles waiting for Y (results overwritten)
     if (lane == 0) F[blockIdx.x * kTW + warp] = make_float2((float)(clock64() - t_start), (float)t_wait);
+#elif TILE_DIAG == 4
+    // timing probe: per (CTA, warp) total cycles, cycles waiting for Y, cycles at the block barrier
+    if (lane == 0) {
+        F[2 * (blockIdx.x * kTW + warp)] = make_float2((float)(clock64() - t_start), (float)t_wait);
+        F[2 * (blockIdx.x * kTW + warp) + 1] = make_float2((float)t_bar, 0.f);
+    }
 #endif
 }
 
@@ -714,13 +713,15 @@ __global__ void k_tile_segment(const unsigned long long* __restrict__ keys, cons
     }
 }
 
-// per-warp tile table: wtab[(p kTW + w) NB + J] = (first step, steps) of the
-// warp tile (p, J, w) = toff[u], toff[u + 1] - toff[u], u = (p NB + J) kTW + w
-__global__ void k_tile_wtab(const int64_t* __restrict__ toff, int64_t P, int64_t NB, int2* __restrict__ wtab) {
+// per-warp tile table in sweep order: wtab[(p kTW + w) NB + J] = (first step,
+// steps) of the warp tile (p, jm, w), jm = (J + tile_rot(p)) mod NB: toff[u],
+// toff[u + 1] - toff[u], u = (p NB + jm) kTW + w
+__global__ void k_tile_wtab(const int64_t* __restrict__ toff, int64_t P, int64_t NB, int G, int2* __restrict__ wtab) {
     const int64_t m = P * NB * kTW;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < m; q += (int64_t)gridDim.x * blockDim.x) {
         const int64_t J = q % NB, pw = q / NB, w = pw % kTW, p = pw / kTW;
-        const int64_t u = (p * NB + J) * kTW + w;
+        const int64_t rot = tile_rot((int)p, G, (int)NB), jm = J + rot < NB ? J + rot : J + rot - NB;
+        const int64_t u = (p * NB + jm) * kTW + w;
         wtab[q] = make_int2((int32_t)toff[u], (int32_t)(toff[u + 1] - toff[u]));
     }
 }
@@ -904,7 +905,7 @@ __global__ void k_tile_fill(const unsigned long long* __restrict__ keys, const u
         const uint32_t col = (uint32_t)(indices[e] % kTB);
         const uint32_t lr = (uint32_t)(key & kLocalMask);
         const int64_t p = (int64_t)(t / (unsigned long long)NB);
-        uint32_t word = (col << 3) | (tile_slot(lr) << 16) | (sc & (kNewRow | kFlush));
+        uint32_t word = (col << 3) | (tile_slot(lr) << (3 + kColBits)) | (sc & (kNewRow | kFlush));
         if (hub[panel_off[p] + (int32_t)lr]) word |= kHub;
         slots[(size_t)(toff[u] + kk) * 32 + l] = make_uint2(word, __float_as_uint(values[e]));
     }
@@ -1089,7 +1090,7 @@ int tsnet_plan_build(const tsnet_csr* P, const tsnet_shard* shard, void* plan, s
     TSNET_ARG(plan_bytes >= (size_t)h.bytes, "plan buffer too small (%zu < %lld bytes)", plan_bytes, (long long)h.bytes);
     uint8_t* pb = reinterpret_cast<uint8_t*>(plan);
     uint2* d_slots = reinterpret_cast<uint2*>(pb + h.off_slots);
-    k_tile_wtab<<<num_sms() * 4, 256, 0, s>>>(w.toff, cut.P, NB, reinterpret_cast<int2*>(pb + h.off_wtab));
+    k_tile_wtab<<<num_sms() * 4, 256, 0, s>>>(w.toff, cut.P, NB, h.G, reinterpret_cast<int2*>(pb + h.off_wtab));
     TSNET_LAUNCH_CHECK();
     TSNET_CUDA(cudaMemcpyAsync(pb + h.off_rowoff, cut.panel_off.data(), sizeof(int32_t) * (cut.P + 1),
                                cudaMemcpyHostToDevice, s));

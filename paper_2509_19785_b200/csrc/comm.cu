@@ -37,23 +37,26 @@ struct NcclApi {
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
-static NcclApi* nccl_api() {
-    static NcclApi api;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-        if (h) {
-            api.handle = h;
-            api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
-            api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
-            api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
-            api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
-            api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
-            api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-        }
+// libnccl is loaded once per process (a function-local static: thread-safe
+// initialisation, C++11).
+static NcclApi load_nccl() {
+    NcclApi api;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+        api.handle = h;
+        api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+        api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+        api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+        api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+        api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+        api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
     }
+    return api;
+}
+
+static NcclApi* nccl_api() {
+    static NcclApi api = load_nccl();
     const bool ok = api.handle && api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce &&
                     api.AllGather && api.GetErrorString;
     return ok ? &api : nullptr;

@@ -366,10 +366,10 @@ static int host_chunks(int64_t n) { return n >= (int64_t)kHostChunks * 16384 ? k
 
 // Row cut of the pipelined host step: chunk c ends at the first row whose
 // indptr reaches nnz * (c + 1) / chunks (equal SpMV work per chunk).  Found by
-// binary search over the device indptr with single-entry reads, once per
+// binary search over the device indptr with single-entry reads on `s`, once per
 // (indptr, n, nnz, chunks) and cached; any cut is correct, the cut only
 // balances the pipeline.
-static int chunk_rows(const tsnet_csr* P, int chunks, int64_t* cut, int64_t* cut_nnz) {
+static int chunk_rows(const tsnet_csr* P, int chunks, int64_t* cut, int64_t* cut_nnz, cudaStream_t s) {
     struct Entry {
         const void* indptr = nullptr;
         int64_t n = -1, nnz = -1;
@@ -395,11 +395,13 @@ static int chunk_rows(const tsnet_csr* P, int chunks, int64_t* cut, int64_t* cut
         while (lo < hi) {
             const int64_t mid = lo + (hi - lo) / 2;
             int64_t v = 0;
-            TSNET_CUDA(cudaMemcpy(&v, P->indptr + mid, sizeof(int64_t), cudaMemcpyDeviceToHost));
+            TSNET_CUDA(cudaMemcpyAsync(&v, P->indptr + mid, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            TSNET_CUDA(cudaStreamSynchronize(s));
             if (v >= target) hi = mid; else lo = mid + 1;
         }
         cut[c] = std::max(lo, cut[c - 1]);
-        TSNET_CUDA(cudaMemcpy(&cut_nnz[c], P->indptr + cut[c], sizeof(int64_t), cudaMemcpyDeviceToHost));
+        TSNET_CUDA(cudaMemcpyAsync(&cut_nnz[c], P->indptr + cut[c], sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        TSNET_CUDA(cudaStreamSynchronize(s));
     }
     Entry& e = cache[next++ & 3];
     e.indptr = P->indptr;
@@ -428,7 +430,7 @@ static int step_host_pipelined(const tsnet_csr* P, float* Y_host, float* vel_hos
     float2* dYn = state + 3 * n;
     const size_t b = sizeof(float2) * (size_t)n;
     int64_t cut[kHostChunksMax + 1], cut_nnz[kHostChunksMax + 1];
-    int st0 = chunk_rows(P, chunks, cut, cut_nnz);
+    int st0 = chunk_rows(P, chunks, cut, cut_nnz, s);
     if (st0 != TSNET_OK) return st0;
     auto rows = [&](int c) { return cut[c]; };
     TSNET_CUDA(cudaMemcpyAsync(dY, Y_host, b, cudaMemcpyHostToDevice, s));
