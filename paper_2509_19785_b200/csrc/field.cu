@@ -4,8 +4,9 @@
 //
 // Steps, all device-driven (no host round trip):
 //   a0 k_bbox                 bounding box -> grid geometry (I, h_b, N = 3I, M = 6I, FFT plan)
-//   .. k_prep                 zero box counters and charge grid, twiddles of length M
-//   a1 k_box_count/k_box_scan/k_box_scatter  counting sort of points by box
+//   a1 k_box_count/k_box_scan/k_box_scatter  counting sort of points by box (the count
+//                             also zeroes the charge grid and writes the twiddles of length M;
+//                             the scan zeroes the box counters for the next iteration)
 //   a2 k_spread               box-local charges W1 and local moments M_x, M_y (warp per
 //                             box chunk, register accumulation, 9 vector reds per warp)
 //   a3/a4 k_row_fwd, k_col, k_row_inv   kernel tabulation + 2-D FFT convolution
@@ -47,17 +48,30 @@ __device__ __forceinline__ unsigned bb_key(float x) { return (unsigned)f2o(x) ^ 
 __device__ __forceinline__ float bb_val(unsigned u) { return o2f((int)(u ^ 0x80000000u)); }
 
 // a0: bounding box of Y and, in the last block, the grid geometry (R9).
+constexpr int kBBoxPts = 8;
 __global__ void __launch_bounds__(256) k_bbox(const float2* __restrict__ Y, int64_t n, Geo* g, float h_max,
                                               int I_min, int I_max) {
     float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
     bool bad = false;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        float2 y = Y[i];
-        bad |= !(isfinite(y.x) && isfinite(y.y));
-        mnx = fminf(mnx, y.x);
-        mny = fminf(mny, y.y);
-        mxx = fmaxf(mxx, y.x);
-        mxy = fmaxf(mxy, y.y);
+    // kBBoxPts points per thread and sweep, their loads in flight together (a
+    // grid of ~2 CTAs per SM: few blocks, so few same-address atomics below)
+    const int64_t sweep = (int64_t)gridDim.x * blockDim.x * kBBoxPts;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x * kBBoxPts + threadIdx.x; i0 < n; i0 += sweep) {
+        float2 y[kBBoxPts];
+#pragma unroll
+        for (int j = 0; j < kBBoxPts; ++j) {
+            const int64_t i = i0 + (int64_t)j * blockDim.x;
+            y[j] = i < n ? __ldg(Y + i) : make_float2(NAN, NAN);
+        }
+#pragma unroll
+        for (int j = 0; j < kBBoxPts; ++j) {
+            if (i0 + (int64_t)j * blockDim.x >= n) break;
+            bad |= !(isfinite(y[j].x) && isfinite(y[j].y));
+            mnx = fminf(mnx, y[j].x);
+            mny = fminf(mny, y[j].y);
+            mxx = fmaxf(mxx, y[j].x);
+            mxy = fmaxf(mxy, y[j].y);
+        }
     }
     for (int o = 16; o > 0; o >>= 1) {
         mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
@@ -146,25 +160,6 @@ __global__ void __launch_bounds__(256) k_bbox(const float2* __restrict__ Y, int6
     g->nrad = nr;
 }
 
-// Zero the box counters and the charge grid; twiddles w_M^k = exp(-2 pi i k / M).
-__global__ void k_prep(Geo* g, int* box_cnt, float4* wgrid, float2* tw) {
-    const int I = g->I, N = g->N, M = g->M;
-    const int64_t nb = (int64_t)I * I + 1, nn = (int64_t)N * N;
-    const int64_t tot = nb + nn + M;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
-        if (t < nb) {
-            box_cnt[t] = 0;
-        } else if (t < nb + nn) {
-            wgrid[t - nb] = make_float4(0.f, 0.f, 0.f, 0.f);
-        } else {
-            int k = (int)(t - nb - nn);
-            double s, c;
-            sincospi(-2.0 * (double)k / (double)M, &s, &c);
-            tw[k] = make_float2((float)c, (float)s);
-        }
-    }
-}
-
 // a1: box of every point (fp64 arithmetic, R16) and its rank inside the box.
 // Each CTA takes kBoxChunk consecutive points (kBoxPts per thread, loads of
 // all of them in flight together).  When the I^2 box counters fit in shared
@@ -182,13 +177,32 @@ constexpr int kBoxChunk = 256 * kBoxPts;
 
 // box_of (the box of a point and its in-box coordinates): move.cuh
 
+// The CTAs also zero the live charge grid (N^2 cells; every reader of the
+// previous iteration's grid has run) and write the twiddles of length M (what
+// a separate preparation kernel did); the box counters were zeroed by the
+// previous k_box_scan (or are zero in a fresh workspace).
 __global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__ Y, int64_t n, const Geo* __restrict__ g,
                                                    int* __restrict__ box_cnt, int* __restrict__ box,
-                                                   int* __restrict__ rank, float2* __restrict__ uv) {
+                                                   int* __restrict__ rank, float2* __restrict__ uv,
+                                                   float4* __restrict__ wgrid, float2* __restrict__ tw) {
     __shared__ int hist[kBoxSmem];
     const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b;
     const int I = g->I;
     const int nb = I * I;
+    {
+        const int N = g->N, M = g->M;
+        const int64_t nn = (int64_t)N * N, tot = nn + M;
+        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+            if (t < nn) {
+                wgrid[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+                const int k = (int)(t - nn);
+                double sn, cs;
+                sincospi(-2.0 * (double)k / (double)M, &sn, &cs);
+                tw[k] = make_float2((float)cs, (float)sn);
+            }
+        }
+    }
     const bool local = nb <= kBoxSmem;
     const int64_t c0 = (int64_t)blockIdx.x * kBoxChunk + threadIdx.x;
     if (local) {
@@ -235,7 +249,7 @@ __global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__
 
 // a1: exclusive scan of box counts -> box_start, and the spread work list
 // (one item per kSpreadChunk points of a box).  Single CTA of 1024 threads.
-__global__ void __launch_bounds__(1024) k_box_scan(Geo* g, const int* __restrict__ box_cnt, int* __restrict__ box_start,
+__global__ void __launch_bounds__(1024) k_box_scan(Geo* g, int* __restrict__ box_cnt, int* __restrict__ box_start,
                                                    int2* __restrict__ items, int64_t n) {
     const int nb = g->I * g->I;
     const int T = blockDim.x;
@@ -262,7 +276,8 @@ __global__ void __launch_bounds__(1024) k_box_scan(Geo* g, const int* __restrict
     int run = sc[threadIdx.x] - cs, irun = si[threadIdx.x] - is;
     int* item_start = reinterpret_cast<int*>(items);   // first spread item of each box
     for (int b = b0; b < b1; ++b) {
-        int c = box_cnt[b];
+        const int c = box_cnt[b];
+        box_cnt[b] = 0;                                // zero for the next iteration's count
         box_start[b] = run;
         item_start[b] = irun;
         run += c;
@@ -738,15 +753,15 @@ cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, b
     cudaError_t e;
     if ((e = field_set_attrs(w.M_max)) != cudaSuccess) return e;
     const int64_t n = a.n, nl = a.re - a.rb;
-    const int pb = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)kNumSMs * 8));
+    const int pb = (int)std::max<int64_t>(1, std::min<int64_t>((n + 256 * kBBoxPts - 1) / (256 * kBBoxPts),
+                                                                  (int64_t)kNumSMs * 2));
     const int pbl = (int)std::max<int64_t>(1, std::min<int64_t>((nl + 255) / 256, (int64_t)kNumSMs * 8));
     k_bbox<<<pb, 256, 0, s>>>(a.Y, n, w.geo, a.h_max, a.I_min, a.I_max);
     if (zero_all && (e = cudaMemsetAsync(w.wgrid, 0, sizeof(float4) * (size_t)w.N_max * w.N_max, s)) != cudaSuccess)
         return e;
-    k_prep<<<kNumSMs * 4, 256, 0, s>>>(w.geo, w.box_cnt, w.wgrid, w.tw);
     const float2* Yl = a.Y + a.rb;
-    const int cb = (int)std::max<int64_t>(1, (nl + kBoxChunk - 1) / kBoxChunk);
-    k_box_count<<<cb, 256, 0, s>>>(Yl, nl, w.geo, w.box_cnt, w.box, w.rank, w.uv);
+    const int cb = (int)std::max<int64_t>(kNumSMs, (nl + kBoxChunk - 1) / kBoxChunk);
+    k_box_count<<<cb, 256, 0, s>>>(Yl, nl, w.geo, w.box_cnt, w.box, w.rank, w.uv, w.wgrid, w.tw);
     k_box_scan<<<1, 1024, 0, s>>>(w.geo, w.box_cnt, w.box_start, w.items, nl);
     k_box_scatter<<<pbl, 256, 0, s>>>(nl, w.box, w.rank, w.box_start, w.uv, w.sorted_uv);
     k_spread<<<kNumSMs * 8, 256, 0, s>>>(w.geo, w.items, w.box_start, w.sorted_uv, w.wgrid);

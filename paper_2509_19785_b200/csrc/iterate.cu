@@ -13,6 +13,7 @@
 
 #include "common.cuh"
 #include "move.cuh"
+#include "ptx.cuh"
 
 namespace tsnet {
 
@@ -310,8 +311,19 @@ __global__ void __launch_bounds__(SMEM ? kUpdateThreads : kUpdateThreadsG, SMEM 
     if (SMEM != (cells <= grid_cap)) return;   // the other variant handles this grid size
     const float4* fg = fgrid;
     if (SMEM) {
-        for (int q = threadIdx.x; q < cells; q += blockDim.x) fsm[q] = __ldg(fgrid + q);
+        // the whole grid (N^2 float4, contiguous) in one TMA bulk copy
+        __shared__ __align__(8) uint64_t gbar;
+        if (threadIdx.x == 0) {
+            mbar_init(&gbar, 1);
+            fence_mbar_init();
+        }
         __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t bytes = (uint32_t)(sizeof(float4) * (size_t)cells);
+            mbar_arrive_tx(&gbar, bytes);
+            bulk_g2s(fsm, fgrid, bytes, &gbar);
+        }
+        mbar_wait(&gbar, 0);
         fg = fsm;
     }
     double sx = 0.0, sy = 0.0;

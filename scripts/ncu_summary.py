@@ -3,6 +3,7 @@
 
     python scripts/ncu_summary.py full <report.ncu-rep> <out.json>
     python scripts/ncu_summary.py launches <launches.csv> <out.txt>
+    python scripts/ncu_summary.py traffic <report.ncu-rep> <kernel> <out.json> <nnz> <n> <source> <limiter>
 
 `full`: key counters of every kernel in a `--set full` capture (DRAM bytes,
 L1/L2 throughput, occupancy, stall summary).  `launches`: per-kernel share of
@@ -67,5 +68,31 @@ def launches(path, out):
     print("\n".join(txt))
 
 
+def traffic(rep, kernel, out, nnz, n, source, limiter):
+    """Per-launch DRAM bytes of `kernel` from a --set full capture: the record
+    bench.py reads for roofline.traffic (profiles/<kernel>_dram_bytes_cfg<c>.json)."""
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--kernel-name", f"regex:{kernel}"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+    def get(k):
+        i = hdr.index(k)
+        return float(vals[i].replace(",", "")) * scale.get(units[i], 1)
+    rec = {"kernel": kernel, "source": source,
+           "dram_bytes_per_launch": get("dram__bytes_read.sum") + get("dram__bytes_write.sum"),
+           "dram_bytes_read": get("dram__bytes_read.sum"), "dram_bytes_write": get("dram__bytes_write.sum"),
+           "nnz": int(nnz), "n": int(n), "limiter": limiter,
+           "gpu_time_us_under_ncu": float(vals[hdr.index("gpu__time_duration.sum")].replace(",", "")) *
+           {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(units[hdr.index("gpu__time_duration.sum")], 1)}
+    with open(out, "w") as f:
+        json.dump(rec, f, indent=1)
+    print(json.dumps(rec, indent=1))
+
+
 if __name__ == "__main__":
-    {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    if sys.argv[1] == "traffic":
+        traffic(*sys.argv[2:9])
+    else:
+        {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2], sys.argv[3])
