@@ -110,7 +110,23 @@ typedef struct {
     int32_t interp_P;
     float h_max;
     int32_t I_min, I_max;
+    int32_t spread;          /* how steps a1-a2 (the spread of the charges onto the grid,
+                                PAPER.md:187-188) visit the points; the result is the same sum
+                                (up to fp32 rounding order):
+                                TSNET_SPREAD_AUTO (0): decided on the device every iteration
+                                  from the last iteration's measure (below);
+                                TSNET_SPREAD_SORT (1): counting sort of the points by box, then a
+                                  warp per box chunk -- any point order;
+                                TSNET_SPREAD_RUNS (2): one pass over consecutive points, summed
+                                  in registers while the box stays the same -- for layouts
+                                  whose index order is spatially local (meshes);
+                                AUTO starts with SORT, switches to RUNS when < 1/64 of the
+                                index-adjacent points lie in different boxes and back when a
+                                run averages < 32 points.  Other values: TSNET_E_ARG. */
 } tsnet_grad_params;
+#define TSNET_SPREAD_AUTO 0
+#define TSNET_SPREAD_SORT 1
+#define TSNET_SPREAD_RUNS 2
 
 /* I <= 1024 (reading R9; N = 3 I <= 3072 nodes, FFT size M = 6 I <= 6144).
  * Workspace grid buffers are sized by the call's I_max (tsnet_workspace_bytes):
@@ -160,6 +176,7 @@ typedef struct {
     double h_b;              /* interval (box) width                                    */
     int32_t I, N, M;         /* intervals per axis, nodes per axis (3I), FFT size (6I)   */
     int32_t nonfinite;       /* 1 if a non-finite coordinate/gradient was produced       */
+    int32_t spread;          /* spread path of the last evaluation: TSNET_SPREAD_SORT / _RUNS */
 } tsnet_stats;
 
 /* ---------------------------------------------------------------- C0 (set-up) */
@@ -447,6 +464,31 @@ TSNET_API int tsnet_sell_build(const tsnet_csr* P, const tsnet_shard* shard, voi
 TSNET_API int tsnet_comm_unique_id(uint8_t* id_out);
 TSNET_API int tsnet_comm_init(const uint8_t* id, int32_t world, int32_t rank, int32_t I_max, void** comm);
 TSNET_API int tsnet_comm_peer_reduce(const void* comm);
+
+/* The replicated layout Y owned by the communicator (SURVEY.md §8(e) "fused
+ * all-gather"; the move, Alg. 3 l.405 PAPER.md:405, writes its new positions
+ * straight into every rank's copy).
+ * tsnet_comm_layout      : every rank, collectively (same n): allocate this
+ *                          rank's n x 2 fp32 device buffer (owned and freed by
+ *                          the communicator; *Y_out stays valid until
+ *                          tsnet_comm_destroy) and map every peer's buffer.  A
+ *                          second call with the same n returns the same buffer.
+ *                          When every peer is mapped (tsnet_comm_layout_push),
+ *                          tsnet_step called with Y == this buffer skips the
+ *                          all-gather: k_update stores each moved position into
+ *                          all ranks' buffers over NVLink, after a device-side
+ *                          wait until every peer has finished reading Y for the
+ *                          iteration, and the next tsnet_step waits until every
+ *                          peer's move has landed.  Any other Y: the all-gather
+ *                          of tsnet_step.
+ * tsnet_comm_layout_push : 1 if the push is in use.
+ * tsnet_comm_layout_sync : enqueue on `stream` a wait until every peer's move of
+ *                          every iteration this rank has completed has landed in
+ *                          this rank's buffer (before the caller reads or
+ *                          overwrites Y outside tsnet_step). */
+TSNET_API int tsnet_comm_layout(void* comm, int64_t n, float** Y_out);
+TSNET_API int tsnet_comm_layout_push(const void* comm);
+TSNET_API int tsnet_comm_layout_sync(void* comm, tsnet_stream_t stream);
 TSNET_API int tsnet_comm_destroy(void* comm);
 
 /* The charge-grid sum of `count` workspaces on the calling device (shards run

@@ -7,9 +7,17 @@
 //     rank sums all ranks' buffers with direct loads over NVLink (CUDA IPC
 //     mappings), after a device-side flag handshake -- no host round trip, so
 //     the iteration stays one CUDA graph;
-//   * the all-gather of the updated layout Y after the move: each rank's rows
-//     padded to an equal slice (the shards are nnz-balanced, their row counts
-//     differ) and gathered with one ncclAllGather through a staging buffer.
+//   * the all-gather of the updated layout Y after the move.  When the ranks
+//     step on the communicator's own replicated layout buffer
+//     (tsnet_comm_layout: one IPC-shared n x 2 buffer per rank), the move
+//     itself stores each new position into every peer's buffer over NVLink
+//     (k_update with a PeerPush, iterate.cu) between two device-side
+//     handshakes: a rank writes into a peer's Y only after that peer has
+//     finished reading Y for the current iteration (field + SpMV), and starts
+//     the next iteration only after every peer's move has landed.  Otherwise
+//     each rank's rows are padded to an equal slice (the shards are
+//     nnz-balanced, their row counts differ) and gathered with one
+//     ncclAllGather through a staging buffer.
 // NCCL is loaded at run time (dlopen "libnccl.so.2"): in a process that already
 // imported PyTorch this resolves to the NCCL torch loaded; the library has no
 // link-time NCCL dependency, so single-GPU use needs no NCCL at all.  Where the
@@ -88,6 +96,12 @@ struct Comm {
     // device copies of the per-rank pointers: flags[w], grid0[w], grid1[w]
     unsigned long long** d_flags = nullptr;
     float4** d_grid = nullptr;  // [2][world]
+    // replicated layout owned by the communicator (tsnet_comm_layout)
+    float2* y = nullptr;        // own buffer, n x 2 fp32 (cudaMalloc, IPC-shared)
+    int64_t y_n = -1;
+    bool ypush = false;         // every peer's buffer mapped: the move pushes Y
+    std::vector<float2*> ypeer; // per rank: its layout buffer as mapped here (own = y)
+    float2** d_ypeer = nullptr; // device copy of ypeer
 };
 
 static unsigned long long* xflags(char* b) { return reinterpret_cast<unsigned long long*>(b); }
@@ -116,11 +130,7 @@ __global__ void k_x_signal(unsigned long long* flags) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flags), "l"(t) : "memory");
 }
 
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
+// ld_acquire_sys / st_release_sys: common.cuh
 
 // 3. reduce: wait until every rank published iteration t (this rank's counter),
 //    then wgrid = sum over ranks of their exchange grid of parity t & 1, read
@@ -169,6 +179,58 @@ __global__ void k_grids_sum(const Geo* __restrict__ g, GridTab grids, int count)
         }
         for (int r = 0; r < count; ++r) grids.p[r][c] = s;
     }
+}
+
+// ---------------------------------------------------------- Y push handshake
+// Flags of the exchange buffer (u64 words): [0] grid published, [1] grid
+// iteration counter (above); [kFRead] = t + 1 once this rank has finished
+// reading Y for its iteration t (field + SpMV); [kFMoved] = t + 1 once its
+// move of iteration t has been stored into every peer's Y; [kFTicket] the
+// move kernel's last-block counter; [kFIter] this rank's completed
+// iterations t (local).
+// before an iteration: wait until every rank's move of every earlier
+// iteration has landed in this rank's Y (lane r polls rank r over NVLink)
+__global__ void k_y_enter(unsigned long long* const* __restrict__ flags, int world,
+                          const unsigned long long* __restrict__ own) {
+    const unsigned long long t = own[kFIter];
+    for (int r = threadIdx.x; r < world; r += blockDim.x)
+        while (ld_acquire_sys(flags[r] + kFMoved) < t) {
+        }
+}
+
+// after the field chain and the SpMV of iteration t: this rank no longer reads Y(t)
+__global__ void k_y_read_done(unsigned long long* own) {
+    __threadfence_system();
+    st_release_sys(own + kFRead, own[kFIter] + 1);
+}
+
+PeerPush comm_peer_push(void* comm, int64_t n) {
+    PeerPush pp{};
+    Comm* c = reinterpret_cast<Comm*>(comm);
+    if (c == nullptr || !c->ypush || c->y_n != n) return pp;
+    pp.y = c->d_ypeer;
+    pp.flags = c->d_flags;
+    pp.own = xflags(c->xbuf);
+    pp.world = c->world;
+    pp.self = c->rank;
+    return pp;
+}
+
+bool comm_owns_layout(const void* comm, const float* Y, int64_t n) {
+    const Comm* c = reinterpret_cast<const Comm*>(comm);
+    return c != nullptr && c->ypush && c->y_n == n && reinterpret_cast<const float*>(c->y) == Y;
+}
+
+cudaError_t comm_y_enter(void* comm, cudaStream_t s) {
+    Comm* c = reinterpret_cast<Comm*>(comm);
+    k_y_enter<<<1, 32, 0, s>>>(c->d_flags, c->world, xflags(c->xbuf));
+    return cudaGetLastError();
+}
+
+cudaError_t comm_y_read_done(void* comm, cudaStream_t s) {
+    Comm* c = reinterpret_cast<Comm*>(comm);
+    k_y_read_done<<<1, 1, 0, s>>>(xflags(c->xbuf));
+    return cudaGetLastError();
 }
 
 // sum of the charge grid over the ranks, into `wgrid` (this rank's grid on entry)
@@ -236,6 +298,10 @@ static void comm_free(Comm* c) {
     if (!c) return;
     for (int r = 0; r < (int)c->peer.size(); ++r)
         if (c->peer[r] && c->peer[r] != c->xbuf) cudaIpcCloseMemHandle(c->peer[r]);
+    for (int r = 0; r < (int)c->ypeer.size(); ++r)
+        if (c->ypeer[r] && c->ypeer[r] != c->y) cudaIpcCloseMemHandle(c->ypeer[r]);
+    if (c->y) cudaFree(c->y);
+    if (c->d_ypeer) cudaFree(c->d_ypeer);
     if (c->xbuf) cudaFree(c->xbuf);
     if (c->d_flags) cudaFree(c->d_flags);
     if (c->d_grid) cudaFree(c->d_grid);
@@ -366,6 +432,80 @@ int tsnet_comm_init(const uint8_t* id, int32_t world, int32_t rank, int32_t I_ma
         }
     }
     *comm = c;
+    return TSNET_OK;
+}
+
+int tsnet_comm_layout(void* comm, int64_t n, float** Y_out) {
+    TSNET_ARG(comm != nullptr && Y_out != nullptr, "NULL argument");
+    TSNET_ARG(n >= 1, "n = %lld", (long long)n);
+    Comm* c = reinterpret_cast<Comm*>(comm);
+    if (c->y != nullptr) {
+        TSNET_ARG(c->y_n == n, "the communicator's layout has n = %lld, not %lld", (long long)c->y_n, (long long)n);
+        *Y_out = reinterpret_cast<float*>(c->y);
+        return TSNET_OK;
+    }
+    NcclApi* api = nccl_api();
+    TSNET_ARG(api != nullptr, "libnccl.so.2 could not be loaded");
+    TSNET_CUDA(cudaMalloc(&c->y, sizeof(float2) * (size_t)n));
+    c->y_n = n;
+    c->ypeer.assign(c->world, nullptr);
+    c->ypeer[c->rank] = c->y;
+    // IPC handles of every rank's buffer (all-gathered like the exchange buffers)
+    struct Rec {
+        cudaIpcMemHandle_t h;
+        int ok;
+        char pad[64 - 4];
+    };
+    Rec me{};
+    me.ok = c->p2p && cudaIpcGetMemHandle(&me.h, c->y) == cudaSuccess;
+    cudaGetLastError();
+    std::vector<Rec> recs(c->world);
+    Rec* d_rec = nullptr;
+    cudaError_t e = cudaMalloc(&d_rec, sizeof(Rec) * c->world);
+    ncclResult_t nr = ncclSuccess;
+    if (e == cudaSuccess) e = cudaMemcpy(d_rec + c->rank, &me, sizeof(Rec), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        nr = api->AllGather(d_rec + c->rank, d_rec, sizeof(Rec), ncclUint8, c->nccl, 0);
+        if (nr == ncclSuccess) e = cudaMemcpy(recs.data(), d_rec, sizeof(Rec) * c->world, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(d_rec);
+    if (e != cudaSuccess || nr != ncclSuccess) {
+        set_error("layout handle exchange: %s", e != cudaSuccess ? cudaGetErrorString(e) : api->GetErrorString(nr));
+        return e != cudaSuccess ? TSNET_E_CUDA : TSNET_E_NCCL;
+    }
+    bool ok = c->p2p;
+    for (int r = 0; r < c->world; ++r) ok = ok && recs[r].ok;
+    for (int r = 0; r < c->world && ok; ++r) {
+        if (r == c->rank) continue;
+        void* ptr = nullptr;
+        if (cudaIpcOpenMemHandle(&ptr, recs[r].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            ok = false;
+        } else {
+            c->ypeer[r] = reinterpret_cast<float2*>(ptr);
+        }
+    }
+    if (ok) {
+        e = cudaMalloc(&c->d_ypeer, sizeof(float2*) * c->world);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(c->d_ypeer, c->ypeer.data(), sizeof(float2*) * c->world, cudaMemcpyHostToDevice);
+        TSNET_CUDA(e);
+    }
+    // every rank decides the same (the records are the same everywhere)
+    c->ypush = ok;
+    *Y_out = reinterpret_cast<float*>(c->y);
+    return TSNET_OK;
+}
+
+int tsnet_comm_layout_push(const void* comm) {
+    return comm != nullptr && reinterpret_cast<const Comm*>(comm)->ypush ? 1 : 0;
+}
+
+int tsnet_comm_layout_sync(void* comm, tsnet_stream_t stream) {
+    TSNET_ARG(comm != nullptr, "NULL argument");
+    Comm* c = reinterpret_cast<Comm*>(comm);
+    if (!c->ypush) return TSNET_OK;
+    TSNET_CUDA(comm_y_enter(comm, (cudaStream_t)stream));
     return TSNET_OK;
 }
 

@@ -56,9 +56,15 @@ struct Geo {
     unsigned bbox[4];                  // ~u(min x), ~u(min y), u(max x), u(max y); 0 = empty (field.cu)
     double sum_x, sum_y;               // centroid accumulation (recenter)
     double eacc;                       // cost mode 1: Parseval accumulator <W1, K_ln * W1> * M^2
-    unsigned int pad2;
+    // a1/a2 path of this iteration (field.cu, k_bbox decides): kSpreadSort (box
+    // counting sort + spread) or kSpreadRuns (one pass over index runs)
+    int smode;
     int pad;
+    unsigned long long spts;           // points spread by the last iteration (its a1/a2 kernel)
+    unsigned long long schg;           // sort path: index-adjacent pairs in different boxes
+    unsigned long long sflush;         // runs path: box flushes
 };
+constexpr int kSpreadSort = 0, kSpreadRuns = 1;
 
 // Ordered float <-> int (monotone), for atomicMin/atomicMax on floats.
 __device__ __forceinline__ int f2o(float f) {
@@ -148,6 +154,7 @@ struct GradArgs {
     const float2* Y;
     float lambda_kl, lambda_c, lambda_r, eps, h_max;
     int I_min, I_max;
+    int spread;           // tsnet_grad_params.spread: 0 adaptive, 1 box sort, 2 index runs
 };
 
 cudaError_t launch_field_phase(const Ws& w, const GradArgs& a, cudaStream_t s);
@@ -158,6 +165,31 @@ cudaError_t launch_attr_cb(const void* plan, const float2* Y, float2* F, int64_t
 cudaError_t launch_attr_sell(const void* plan, const float2* Y, float2* F, int64_t nl, cudaStream_t s);
 // step a7 fused into the sliced-ELL SpMV (attr_sell.cu); pointers index the
 // plan's rows (row r at r - row_begin)
+// Multi-GPU layout push (comm.cu, tsnet_comm_layout): the move stores each
+// new position into every peer's replicated Y.  y[r] = rank r's Y buffer as
+// mapped here, flags[r] = rank r's exchange flags, own = this rank's flags;
+// y == nullptr: no push.
+struct PeerPush {
+    float2* const* y = nullptr;
+    unsigned long long* const* flags = nullptr;
+    unsigned long long* own = nullptr;
+    int world = 0, self = 0;
+};
+constexpr int kFRead = 2, kFMoved = 3, kFTicket = 4, kFIter = 5;   // exchange flag words
+PeerPush comm_peer_push(void* comm, int64_t n);
+bool comm_owns_layout(const void* comm, const float* Y, int64_t n);
+cudaError_t comm_y_enter(void* comm, cudaStream_t s);
+cudaError_t comm_y_read_done(void* comm, cudaStream_t s);
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 struct SellMoveArgs {
     Geo* geo;
     const float4* fgrid;
@@ -172,7 +204,7 @@ struct SellMoveArgs {
 cudaError_t launch_grad_out(const Ws& w, const GradArgs& a, float2* grad, float2* f_field, double* Z,
                             cudaStream_t s);
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,
-                          const tsnet_step_params& sp, cudaStream_t s);
+                          const tsnet_step_params& sp, cudaStream_t s, const PeerPush& push = PeerPush{});
 // Row-chunk pieces of the same two steps (rows [r0, r1) inside the call's [rb, re)),
 // used by the pipelined host step: the SpMV of a chunk (its rows of w.f_attr
 // must be zero before the call; nnz_rows = its stored entries, which size the

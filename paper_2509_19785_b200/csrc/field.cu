@@ -49,8 +49,22 @@ __device__ __forceinline__ float bb_val(unsigned u) { return o2f((int)(u ^ 0x800
 
 // a0: bounding box of Y and, in the last block, the grid geometry (R9).
 constexpr int kBBoxPts = 8;
+//
+// The CTAs also zero the charge grid cells the previous iteration used
+// ([0, N_prev^2), N_prev read before the last block sets the new geometry;
+// every reader of that grid has run).  No kernel writes beyond the live cells
+// of its iteration and a fresh workspace is zero, so the whole grid is zero
+// when the spread starts, whatever N this iteration takes.  The last block also
+// picks the a1/a2 path (kSpreadSort / kSpreadRuns) from the request `spread`
+// (tsnet_grad_params.spread) and, when adaptive, from the previous
+// iteration's measure (k_box_count / k_spread_runs).
 __global__ void __launch_bounds__(256) k_bbox(const float2* __restrict__ Y, int64_t n, Geo* g, float h_max,
-                                              int I_min, int I_max) {
+                                              int I_min, int I_max, float4* __restrict__ wgrid, int spread) {
+    {
+        const int64_t prev = (int64_t)g->N * g->N;
+        for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < prev; c += (int64_t)gridDim.x * blockDim.x)
+            wgrid[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
     bool bad = false;
     // kBBoxPts points per thread and sweep, their loads in flight together (a
@@ -124,6 +138,22 @@ __global__ void __launch_bounds__(256) k_bbox(const float2* __restrict__ Y, int6
     g->zacc = 0.0;
     g->sum_x = 0.0;
     g->sum_y = 0.0;
+    {
+        int mode;
+        if (spread == TSNET_SPREAD_SORT) {
+            mode = kSpreadSort;
+        } else if (spread == TSNET_SPREAD_RUNS) {
+            mode = kSpreadRuns;
+        } else if (g->smode == kSpreadRuns) {   // back to the sort when a run averages < 32 points
+            mode = g->sflush * 32ull > g->spts ? kSpreadSort : kSpreadRuns;
+        } else {                                // to the runs when < 1/64 of the adjacent points change box
+            mode = (g->spts > 0 && g->schg * 64ull < g->spts) ? kSpreadRuns : kSpreadSort;
+        }
+        g->smode = mode;
+        g->spts = 0ull;
+        g->schg = 0ull;
+        g->sflush = 0ull;
+    }
     double S = fmax(hi_x - lo_x, hi_y - lo_y);
     if (!(S >= 1e-12)) S = 1e-12;            // also catches NaN (non-finite layouts)
     if (!isfinite(S) || !isfinite(lo_x) || !isfinite(lo_y)) {
@@ -181,34 +211,41 @@ constexpr int kBoxChunk = 256 * kBoxPts;
 // previous iteration's grid has run) and write the twiddles of length M (what
 // a separate preparation kernel did); the box counters were zeroed by the
 // previous k_box_scan (or are zero in a fresh workspace).
-__global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__ Y, int64_t n, const Geo* __restrict__ g,
+__device__ __forceinline__ void write_twiddles(const Geo* __restrict__ g, float2* __restrict__ tw) {
+    const int M = g->M;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < M; k += gridDim.x * blockDim.x) {
+        double sn, cs;
+        sincospi(-2.0 * (double)k / (double)M, &sn, &cs);
+        tw[k] = make_float2((float)cs, (float)sn);
+    }
+}
+
+// Sort path only (exits at once on the runs path).  The CTAs also write the
+// twiddles of length M; the box counters were zeroed by the previous
+// k_box_scan (or are zero in a fresh workspace).  Every 8th CTA measures the
+// index locality of the layout for the next iteration's path choice: the
+// pairs of consecutive points (i, i + 1) held by neighbouring lanes, and how
+// many of them lie in different boxes.
+__global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__ Y, int64_t n, Geo* __restrict__ g,
                                                    int* __restrict__ box_cnt, int* __restrict__ box,
                                                    int* __restrict__ rank, float2* __restrict__ uv,
-                                                   float4* __restrict__ wgrid, float2* __restrict__ tw) {
+                                                   float2* __restrict__ tw) {
     __shared__ int hist[kBoxSmem];
+    __shared__ unsigned s_chg, s_pairs;
+    if (g->smode != kSpreadSort) return;
     const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b;
     const int I = g->I;
     const int nb = I * I;
-    {
-        const int N = g->N, M = g->M;
-        const int64_t nn = (int64_t)N * N, tot = nn + M;
-        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
-            if (t < nn) {
-                wgrid[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-            } else {
-                const int k = (int)(t - nn);
-                double sn, cs;
-                sincospi(-2.0 * (double)k / (double)M, &sn, &cs);
-                tw[k] = make_float2((float)cs, (float)sn);
-            }
-        }
+    write_twiddles(g, tw);
+    const bool sample = (blockIdx.x & 7) == 0;
+    if (sample && threadIdx.x == 0) {
+        s_chg = 0u;
+        s_pairs = 0u;
     }
     const bool local = nb <= kBoxSmem;
     const int64_t c0 = (int64_t)blockIdx.x * kBoxChunk + threadIdx.x;
-    if (local) {
-        for (int q = threadIdx.x; q < nb; q += blockDim.x) hist[q] = 0;
-        __syncthreads();
-    }
+    if (local) for (int q = threadIdx.x; q < nb; q += blockDim.x) hist[q] = 0;
+    if (local || sample) __syncthreads();
     int* cnt = local ? hist : box_cnt;
     float2 y[kBoxPts];
 #pragma unroll
@@ -229,8 +266,30 @@ __global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__
             rj[j] = atomicAdd(&cnt[bj[j]], 1);
         }
     }
+    if (sample) {
+        const unsigned full = 0xffffffffu;
+        const int lane = threadIdx.x & 31;
+        unsigned chg = 0u, pairs = 0u;
+#pragma unroll
+        for (int j = 0; j < kBoxPts; ++j) {
+            const int bp = __shfl_up_sync(full, bj[j], 1);
+            const bool pair = lane > 0 && bj[j] >= 0 && bp >= 0;
+            pairs += pair;
+            chg += pair && bp != bj[j];
+        }
+        chg = __reduce_add_sync(full, chg);
+        pairs = __reduce_add_sync(full, pairs);
+        if (lane == 0) {
+            atomicAdd(&s_chg, chg);
+            atomicAdd(&s_pairs, pairs);
+        }
+    }
+    if (local || sample) __syncthreads();
+    if (sample && threadIdx.x == 0 && s_pairs) {
+        atomicAdd(&g->schg, (unsigned long long)s_chg);
+        atomicAdd(&g->spts, (unsigned long long)s_pairs);
+    }
     if (local) {
-        __syncthreads();
         for (int q = threadIdx.x; q < nb; q += blockDim.x) {
             const int c = hist[q];
             if (c) hist[q] = atomicAdd(&box_cnt[q], c);   // this CTA's range inside box q
@@ -251,6 +310,7 @@ __global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__
 // (one item per kSpreadChunk points of a box).  Single CTA of 1024 threads.
 __global__ void __launch_bounds__(1024) k_box_scan(Geo* g, int* __restrict__ box_cnt, int* __restrict__ box_start,
                                                    int2* __restrict__ items, int64_t n) {
+    if (g->smode != kSpreadSort) return;
     const int nb = g->I * g->I;
     const int T = blockDim.x;
     const int per = (nb + T - 1) / T;
@@ -292,10 +352,11 @@ __global__ void __launch_bounds__(1024) k_box_scan(Geo* g, int* __restrict__ box
 
 // 4 points per thread and iteration: their loads, then the box_start
 // gathers, then the stores, each in flight together
-__global__ void __launch_bounds__(256) k_box_scatter(int64_t n, const int* __restrict__ box, const int* __restrict__ rank,
-                                                     const int* __restrict__ box_start, const float2* __restrict__ uv,
-                                                     float2* __restrict__ sorted_uv) {
+__global__ void __launch_bounds__(256) k_box_scatter(const Geo* __restrict__ g, int64_t n, const int* __restrict__ box,
+                                                     const int* __restrict__ rank, const int* __restrict__ box_start,
+                                                     const float2* __restrict__ uv, float2* __restrict__ sorted_uv) {
     constexpr int V = 4;
+    if (g->smode != kSpreadSort) return;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += V * stride) {
         int b[V], r[V], st[V];
@@ -326,6 +387,7 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float
 __global__ void __launch_bounds__(256) k_spread(const Geo* __restrict__ g, const int2* __restrict__ items,
                                                 const int* __restrict__ box_start,
                                                 const float2* __restrict__ sorted_uv, float4* __restrict__ wgrid) {
+    if (g->smode != kSpreadSort) return;
     const int nitems = g->nitems, I = g->I, N = g->N;
     const float h_b = (float)g->h_b;
     const float s[3] = {1.0f / 6.0f, 0.5f, 5.0f / 6.0f};
@@ -379,6 +441,112 @@ __global__ void __launch_bounds__(256) k_spread(const Geo* __restrict__ g, const
             red_add_v4(&wgrid[(int64_t)gy * N + gx], a0, a1 * h_b, a2 * h_b);
         }
     }
+}
+
+// a1 + a2 in one pass, for layouts whose index order is spatially local (a
+// mesh numbered along its axes: consecutive vertices sit in the same box for
+// long runs).  Runs path only (exits at once on the sort path).
+// A warp takes chunks of 32 kRunPts consecutive points, lane l the kRunPts
+// points from l kRunPts on.  A lane sums the charges of its points in 27
+// registers (9 nodes x (W1, M_x, M_y), as k_spread) while the box stays the
+// same, and adds them to the grid (9 red.global.add.v4) when the box changes;
+// at the end of the chunk the lanes' last runs are summed across lanes by a
+// segmented warp scan keyed on the box (a run continuing into the next lane's
+// points joins it), and the last lane of each segment adds the sum.  The same
+// sums as the box sort, in another fp32 order.  The CTAs also
+// write the twiddles; per CTA the box flushes are counted for the next
+// iteration's path choice (k_bbox).
+constexpr int kRunPts = 8;
+__device__ __forceinline__ void runs_flush(float4* __restrict__ wgrid, int b, int I, int N, float h_b,
+                                           const float (&acc)[27]) {
+    const int bx = b % I, by = b / I;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+        const int gx = 3 * bx + t % 3, gy = 3 * by + t / 3;
+        red_add_v4(&wgrid[(int64_t)gy * N + gx], acc[3 * t], acc[3 * t + 1] * h_b, acc[3 * t + 2] * h_b);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ Y, int64_t n, Geo* __restrict__ g,
+                                                     float4* __restrict__ wgrid, float2* __restrict__ tw) {
+    __shared__ unsigned s_flush;
+    if (g->smode != kSpreadRuns) return;
+    write_twiddles(g, tw);
+    if (threadIdx.x == 0) s_flush = 0u;
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) g->spts = (unsigned long long)n;
+    const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b;
+    const int I = g->I, N = g->N;
+    const float h_bf = (float)h_b;
+    const float sn[3] = {1.0f / 6.0f, 0.5f, 5.0f / 6.0f};
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    unsigned flushes = 0u;
+    for (int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); c * (32 * kRunPts) < n;
+         c += warps) {
+        const int64_t base = c * (32 * kRunPts) + (int64_t)lane * kRunPts;
+        float2 y[kRunPts];
+#pragma unroll
+        for (int v = 0; v < kRunPts; ++v) y[v] = base + v < n ? __ldg(Y + base + v) : make_float2(0.f, 0.f);
+        float acc[27];
+#pragma unroll
+        for (int q = 0; q < 27; ++q) acc[q] = 0.f;
+        int cur = -1;
+#pragma unroll
+        for (int v = 0; v < kRunPts; ++v) {
+            if (base + v >= n) break;
+            int b;
+            float ux, uy;
+            box_of(y[v], lo_x, lo_y, h_b, I, b, ux, uy);
+            if (b != cur) {
+                if (cur >= 0) {
+                    runs_flush(wgrid, cur, I, N, h_bf, acc);
+                    ++flushes;
+#pragma unroll
+                    for (int q = 0; q < 27; ++q) acc[q] = 0.f;
+                }
+                cur = b;
+            }
+            float Lx[3], Ly[3];
+            lagrange3(ux, Lx);
+            lagrange3(uy, Ly);
+#pragma unroll
+            for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const float w = Lx[a] * Ly[bb];
+                    const int q = 3 * (3 * bb + a);
+                    acc[q] += w;
+                    acc[q + 1] += w * (sn[a] - ux);
+                    acc[q + 2] += w * (sn[bb] - uy);
+                }
+        }
+        // segmented inclusive scan over the lanes, segments = equal boxes
+        // (lanes without points: key -1 - lane, a segment of their own)
+        const int key = cur >= 0 ? cur : -1 - lane;
+        const int kp = __shfl_up_sync(full, key, 1);
+        bool head = lane == 0 || kp != key;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const bool uh = __shfl_up_sync(full, head, o);
+#pragma unroll
+            for (int q = 0; q < 27; ++q) {
+                const float u = __shfl_up_sync(full, acc[q], o);
+                if (lane >= o && !head) acc[q] += u;
+            }
+            if (lane >= o) head = head || uh;
+        }
+        const int kn = __shfl_down_sync(full, key, 1);
+        if (cur >= 0 && (lane == 31 || kn != key)) {
+            runs_flush(wgrid, cur, I, N, h_bf, acc);
+            ++flushes;
+        }
+    }
+    flushes = __reduce_add_sync(full, flushes);
+    if (lane == 0 && flushes) atomicAdd(&s_flush, flushes);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_flush) atomicAdd(&g->sflush, (unsigned long long)s_flush);
 }
 
 // ---------------------------------------------------------------- FFT passes
@@ -756,14 +924,19 @@ cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, b
     const int pb = (int)std::max<int64_t>(1, std::min<int64_t>((n + 256 * kBBoxPts - 1) / (256 * kBBoxPts),
                                                                   (int64_t)kNumSMs * 2));
     const int pbl = (int)std::max<int64_t>(1, std::min<int64_t>((nl + 255) / 256, (int64_t)kNumSMs * 8));
-    k_bbox<<<pb, 256, 0, s>>>(a.Y, n, w.geo, a.h_max, a.I_min, a.I_max);
+    k_bbox<<<pb, 256, 0, s>>>(a.Y, n, w.geo, a.h_max, a.I_min, a.I_max, w.wgrid, a.spread);
     if (zero_all && (e = cudaMemsetAsync(w.wgrid, 0, sizeof(float4) * (size_t)w.N_max * w.N_max, s)) != cudaSuccess)
         return e;
     const float2* Yl = a.Y + a.rb;
+    // both paths are launched (the path is only known on the device, and the
+    // iteration is one CUDA graph); the kernels of the other path exit at once
+    const int rbk = (int)std::max<int64_t>(1, std::min<int64_t>((nl + 8 * 32 * kRunPts - 1) / (8 * 32 * kRunPts),
+                                                                  (int64_t)kNumSMs * 2));
+    k_spread_runs<<<rbk, 256, 0, s>>>(Yl, nl, w.geo, w.wgrid, w.tw);
     const int cb = (int)std::max<int64_t>(kNumSMs, (nl + kBoxChunk - 1) / kBoxChunk);
-    k_box_count<<<cb, 256, 0, s>>>(Yl, nl, w.geo, w.box_cnt, w.box, w.rank, w.uv, w.wgrid, w.tw);
+    k_box_count<<<cb, 256, 0, s>>>(Yl, nl, w.geo, w.box_cnt, w.box, w.rank, w.uv, w.tw);
     k_box_scan<<<1, 1024, 0, s>>>(w.geo, w.box_cnt, w.box_start, w.items, nl);
-    k_box_scatter<<<pbl, 256, 0, s>>>(nl, w.box, w.rank, w.box_start, w.uv, w.sorted_uv);
+    k_box_scatter<<<pbl, 256, 0, s>>>(w.geo, nl, w.box, w.rank, w.box_start, w.uv, w.sorted_uv);
     k_spread<<<kNumSMs * 8, 256, 0, s>>>(w.geo, w.items, w.box_start, w.sorted_uv, w.wgrid);
     return cudaGetLastError();
 }

@@ -304,11 +304,21 @@ __global__ void __launch_bounds__(SMEM ? kUpdateThreads : kUpdateThreadsG, SMEM 
                                                               const float2* __restrict__ Fa,
                                                               float2* __restrict__ vel, float2* __restrict__ gains,
                                                               float lambda_kl, float cn, tsnet_step_params sp,
-                                                              int grid_cap) {
+                                                              int grid_cap, PeerPush push, int64_t row0) {
     extern __shared__ float4 fsm[];
     const Geo g = *gp;
     const int cells = g.N * g.N;
     if (SMEM != (cells <= grid_cap)) return;   // the other variant handles this grid size
+    unsigned long long iter = 0;
+    if (push.y) {
+        // multi-GPU layout push: store into a peer's Y only once that peer has
+        // finished reading Y for this iteration (its field + SpMV)
+        iter = push.own[kFIter];
+        if (threadIdx.x < push.world)
+            while (ld_acquire_sys(push.flags[threadIdx.x] + kFRead) < iter + 1) {
+            }
+        __syncthreads();
+    }
     const float4* fg = fgrid;
     if (SMEM) {
         // the whole grid (N^2 float4, contiguous) in one TMA bulk copy
@@ -362,6 +372,9 @@ __global__ void __launch_bounds__(SMEM ? kUpdateThreads : kUpdateThreadsG, SMEM 
             Yout[i] = y[q];
             vel[i] = v[q];
             gains[i] = gn[q];
+            if (push.y)
+                for (int r = 0; r < push.world; ++r)
+                    if (r != push.self) push.y[r][row0 + i] = y[q];   // over NVLink
             if (sp.recenter) {
                 sx += y[q].x;
                 sy += y[q].y;
@@ -379,6 +392,21 @@ __global__ void __launch_bounds__(SMEM ? kUpdateThreads : kUpdateThreadsG, SMEM 
         }
     }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&gp->nonfinite, 1);
+    if (push.y) {
+        // the last block to finish publishes "moved t + 1" at system scope
+        // after every block's peer stores (fenced before its ticket)
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned long long tk = atomicAdd(push.own + kFTicket, 1ull);
+            if (tk == gridDim.x - 1ull) {
+                push.own[kFTicket] = 0ull;
+                push.own[kFIter] = iter + 1;
+                __threadfence_system();
+                st_release_sys(push.own + kFMoved, iter + 1);
+            }
+        }
+    }
 }
 
 __global__ void k_recenter(int64_t n, const Geo* __restrict__ gp, float2* __restrict__ Y) {
@@ -414,7 +442,7 @@ static constexpr auto update_kernel_g = k_update<2, true, false>;
 
 // Y, vel, gains: full n x 2 arrays; rows [rb, re) are updated
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,
-                          const tsnet_step_params& sp, cudaStream_t s) {
+                          const tsnet_step_params& sp, cudaStream_t s, const PeerPush& push) {
     const int64_t nl = a.re - a.rb;
     const int cap = (int)std::min<int64_t>((int64_t)w.N_max * w.N_max, kGridSmemCells);
     const size_t smem = sizeof(float4) * (size_t)cap;
@@ -423,11 +451,13 @@ cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel
     if (ea != cudaSuccess) return ea;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nl + kUpdateThreads - 1) / kUpdateThreads, kNumSMs));
     update_kernel<<<blocks, kUpdateThreads, smem, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, Y + a.rb, Y + a.rb, w.f_attr,
-                                                  vel + a.rb, gains + a.rb, a.lambda_kl, cn_of(a), sp, cap);
+                                                  vel + a.rb, gains + a.rb, a.lambda_kl, cn_of(a), sp, cap, push,
+                                                  a.rb);
     const int blocks_g =
         (int)std::max<int64_t>(1, std::min<int64_t>((nl + 2 * kUpdateThreadsG - 1) / (2 * kUpdateThreadsG), kNumSMs * 8));
     update_kernel_g<<<blocks_g, kUpdateThreadsG, 0, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, Y + a.rb, Y + a.rb, w.f_attr,
-                                                         vel + a.rb, gains + a.rb, a.lambda_kl, cn_of(a), sp, cap);
+                                                         vel + a.rb, gains + a.rb, a.lambda_kl, cn_of(a), sp, cap,
+                                                         push, a.rb);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !sp.recenter) return e;
     k_recenter<<<pts_blocks(a.n), 256, 0, s>>>(a.n, w.geo, Y);
@@ -458,7 +488,8 @@ cudaError_t launch_update_rows(const Ws& w, const GradArgs& a, int64_t r0, int64
     const int blocks =
         (int)std::max<int64_t>(1, std::min<int64_t>((nc + 2 * kUpdateThreadsG - 1) / (2 * kUpdateThreadsG), kNumSMs * 8));
     update_kernel_g<<<blocks, kUpdateThreadsG, 0, s>>>(nc, w.geo, w.fgrid, w.box + q, w.uv + q, a.Y + r0, Yout + r0,
-                                               w.f_attr + q, vel + r0, gains + r0, a.lambda_kl, cn_of(a), sp, 0);
+                                               w.f_attr + q, vel + r0, gains + r0, a.lambda_kl, cn_of(a), sp, 0,
+                                               PeerPush{}, 0);
     return cudaGetLastError();
 }
 

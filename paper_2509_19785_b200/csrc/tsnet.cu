@@ -31,6 +31,8 @@ static int check_grad_params(const tsnet_grad_params* gp) {
               "need 1 <= I_min (%d) <= I_max (%d) <= %d", gp->I_min, gp->I_max, TSNET_I_MAX_LIMIT);
     TSNET_ARG(gp->h_max > 0.f && std::isfinite(gp->h_max), "h_max must be > 0");
     TSNET_ARG(gp->eps > 0.f, "eps must be > 0");
+    TSNET_ARG(gp->spread >= TSNET_SPREAD_AUTO && gp->spread <= TSNET_SPREAD_RUNS, "spread = %d: not 0, 1 or 2",
+              gp->spread);
     return TSNET_OK;
 }
 
@@ -112,6 +114,7 @@ static int prepare(const tsnet_csr* P, const float* Y, const tsnet_grad_params* 
     a.h_max = gp->h_max;
     a.I_min = gp->I_min;
     a.I_max = gp->I_max;
+    a.spread = gp->spread;
     return TSNET_OK;
 }
 
@@ -308,11 +311,18 @@ static int step_impl(const tsnet_csr* P, float* Y, float* vel, float* gains, con
     const bool multi = shard != nullptr && shard->comm != nullptr;
     TSNET_ARG(!multi || shard->bounds != nullptr, "a communicating shard needs shard->bounds to all-gather Y");
     if (a.n == 0) return TSNET_OK;
+    // multi-GPU on the communicator's own layout buffers: the move pushes the
+    // new positions into every peer's Y (comm.cu), between the handshakes
+    const bool push = multi && comm_owns_layout(shard->comm, Y, a.n);
+    if (push) TSNET_CUDA(comm_y_enter(shard->comm, s));
     if ((st = eval_gradient_parts(w, a, shard, s)) != TSNET_OK) return st;
+    if (push) TSNET_CUDA(comm_y_read_done(shard->comm, s));
     if (before_update) TSNET_CUDA(cudaStreamWaitEvent(s, before_update, 0));
     TSNET_CUDA(launch_update(w, a, reinterpret_cast<float2*>(Y), reinterpret_cast<float2*>(vel),
-                             reinterpret_cast<float2*>(gains), *sp, s));
-    if (multi) return comm_allgather_rows(shard->comm, Y, shard->bounds, shard->world, w.state, 4 * (size_t)a.n, s);
+                             reinterpret_cast<float2*>(gains), *sp, s,
+                             push ? comm_peer_push(shard->comm, a.n) : PeerPush{}));
+    if (multi && !push)
+        return comm_allgather_rows(shard->comm, Y, shard->bounds, shard->world, w.state, 4 * (size_t)a.n, s);
     return TSNET_OK;
 }
 }  // namespace tsnet
@@ -584,6 +594,7 @@ int tsnet_read_stats(const void* ws, tsnet_stats* out, tsnet_stream_t stream) {
     out->N = g.N;
     out->M = g.M;
     out->nonfinite = g.nonfinite;
+    out->spread = g.smode == kSpreadRuns ? TSNET_SPREAD_RUNS : TSNET_SPREAD_SORT;
     return g.nonfinite ? TSNET_E_NONFINITE : TSNET_OK;
 }
 

@@ -4,11 +4,14 @@ Rank r owns the contiguous rows bounds[r]:bounds[r+1] of P (nnz + rows
 balanced, tsnet_shard_rows), holds the full replicated layout Y, and runs
 tsnet_step with its shard: geometry from the full Y, spread of its own points,
 NCCL all-reduce of the charge grid, replicated FFT convolution, attractive
-SpMV + gather + move of its own rows, NCCL all-gather of Y.  The NCCL
+SpMV + gather + move of its own rows, exchange of Y.  The NCCL
 communicator is created inside libtsnet (tsnet_comm_init); torch.distributed
 only carries its 128-byte id from rank 0 to the others.  The charge-grid sum is
 a peer-memory all-reduce of the live grid (tsnet_comm_init maps every peer's
-exchange buffer); Y is all-gathered in equal padded slices.
+exchange buffer).  Y lives in the communicator's own IPC-shared buffer
+(tsnet_comm_layout) when every peer can map it: the move then stores the new
+positions straight into every rank's copy over NVLink; otherwise Y is
+all-gathered in equal padded slices.
 """
 from __future__ import annotations
 
@@ -16,7 +19,8 @@ import torch
 
 from .runner import STAGE_SWITCH, stage_of, stage_params
 from .tsnet import (CSR, GradParams, Shard, attach_plan, alloc_workspace, tsnet_comm_destroy, tsnet_comm_init,
-                    tsnet_comm_unique_id, tsnet_read_stats, tsnet_shard_rows, tsnet_step)
+                    tsnet_comm_layout, tsnet_comm_layout_push, tsnet_comm_layout_sync, tsnet_comm_unique_id,
+                    tsnet_read_stats, tsnet_shard_rows, tsnet_step)
 
 
 def shard_bounds(indptr_host, world: int):
@@ -51,14 +55,24 @@ class ShardedLayout:
         # (attach_plan: "csr", "cb", "sell", "auto") attached to a shallow copy,
         # so the caller's P keeps its own plan
         self.P = attach_plan(P.without_plan(), plan, self.shard)
-        self.Y = Y0.clone()
-        self.vel = torch.zeros_like(self.Y)
-        self.gains = torch.ones_like(self.Y)
+        self.stream = torch.cuda.Stream(device=Y0.device)
+        self.stream.wait_stream(torch.cuda.current_stream(Y0.device))
+        # the replicated layout: the communicator's buffer when the move can push
+        # into every peer's copy (collective call on every rank), else a tensor
+        # of our own and the all-gather
+        Yc = tsnet_comm_layout(self.comm, P.n, device=Y0.device)
+        self.push = tsnet_comm_layout_push(self.comm)
+        if self.push:
+            self.Y = Yc
+            with torch.cuda.stream(self.stream):
+                self.Y.copy_(Y0)
+        else:
+            self.Y = Y0.clone()
+        self.vel = torch.zeros_like(Y0)
+        self.gains = torch.ones_like(Y0)
         self.ws = alloc_workspace(P.n, P.nnz, self.params[0][0], device=Y0.device)
         self.stage_switch = stage_switch
         self.use_graphs = use_graphs
-        self.stream = torch.cuda.Stream(device=Y0.device)
-        self.stream.wait_stream(torch.cuda.current_stream(Y0.device))
         self.graphs = [None, None]
 
     @property
@@ -74,6 +88,7 @@ class ShardedLayout:
             # capture without advancing the state (snapshot/restore on self.stream);
             # every rank captures at the same iteration, so the collectives match
             with torch.cuda.stream(self.stream):
+                self._layout_sync()
                 saved = (self.Y.clone(), self.vel.clone(), self.gains.clone())
                 self._raw_step(stage)
             self.stream.synchronize()
@@ -81,6 +96,7 @@ class ShardedLayout:
             with torch.cuda.graph(g, stream=self.stream):
                 self._raw_step(stage)
             with torch.cuda.stream(self.stream):
+                self._layout_sync()          # every peer's push of the eager step has landed
                 self.Y.copy_(saved[0])
                 self.vel.copy_(saved[1])
                 self.gains.copy_(saved[2])
@@ -103,7 +119,14 @@ class ShardedLayout:
             self.step(it)
         return self
 
+    def _layout_sync(self):
+        if self.push and self.comm:
+            tsnet_comm_layout_sync(self.comm, self.stream)
+
     def sync(self):
+        """Wait for this rank's work and, with the layout push, for every peer's
+        moves into this rank's Y (so Y is complete when read)."""
+        self._layout_sync()
         self.stream.synchronize()
 
     def stats(self):
@@ -113,6 +136,9 @@ class ShardedLayout:
     def close(self):
         self.sync()
         self.graphs = [None, None]
+        if self.push:
+            self.Y = self.Y.clone()    # the communicator's buffer is freed with it
+            self.push = False
         if self.comm:
             tsnet_comm_destroy(self.comm)
             self.comm = None

@@ -23,10 +23,10 @@ def stage_params(stage: int, base: GradParams | None = None, eta: float = 50.0):
     """O7: stage A (lkl, lc, lr) = (1, 1.2, 0), momentum 0.5; stage B (1, 0.01, 0.6), momentum 0.8."""
     b = base or GradParams()
     if stage == 0:
-        gp = GradParams(1.0, 1.2, 0.0, b.eps, b.interp_P, b.h_max, b.I_min, b.I_max)
+        gp = GradParams(1.0, 1.2, 0.0, b.eps, b.interp_P, b.h_max, b.I_min, b.I_max, b.spread)
         sp = StepParams(eta=eta, momentum=0.5)
     else:
-        gp = GradParams(1.0, 0.01, 0.6, b.eps, b.interp_P, b.h_max, b.I_min, b.I_max)
+        gp = GradParams(1.0, 0.01, 0.6, b.eps, b.interp_P, b.h_max, b.I_min, b.I_max, b.spread)
         sp = StepParams(eta=eta, momentum=0.8)
     return gp, sp
 

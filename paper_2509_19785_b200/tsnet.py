@@ -38,7 +38,7 @@ class tsnet_csr(ctypes.Structure):
 
 class tsnet_grad_params(ctypes.Structure):
     _fields_ = [("lambda_kl", c_f32), ("lambda_c", c_f32), ("lambda_r", c_f32), ("eps", c_f32),
-                ("interp_P", c_i32), ("h_max", c_f32), ("I_min", c_i32), ("I_max", c_i32)]
+                ("interp_P", c_i32), ("h_max", c_f32), ("I_min", c_i32), ("I_max", c_i32), ("spread", c_i32)]
 
 
 class tsnet_step_params(ctypes.Structure):
@@ -53,7 +53,7 @@ class tsnet_shard(ctypes.Structure):
 
 class tsnet_stats(ctypes.Structure):
     _fields_ = [("Z", c_f64), ("lo_x", c_f64), ("lo_y", c_f64), ("S", c_f64), ("h_b", c_f64), ("I", c_i32),
-                ("N", c_i32), ("M", c_i32), ("nonfinite", c_i32)]
+                ("N", c_i32), ("M", c_i32), ("nonfinite", c_i32), ("spread", c_i32)]
 
 
 _lib = None
@@ -97,6 +97,9 @@ SIGNATURES = [
     ("tsnet_comm_unique_id", ctypes.c_int, [c_vp]),
     ("tsnet_comm_init", ctypes.c_int, [c_vp, c_i32, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     ("tsnet_comm_peer_reduce", ctypes.c_int, [c_vp]),
+    ("tsnet_comm_layout", ctypes.c_int, [c_vp, c_i64, ctypes.POINTER(c_vp)]),
+    ("tsnet_comm_layout_push", ctypes.c_int, [c_vp]),
+    ("tsnet_comm_layout_sync", ctypes.c_int, [c_vp, c_vp]),
     ("tsnet_grids_sum", ctypes.c_int, [c_i32, ctypes.POINTER(c_vp), c_sz, c_i64, c_i64,
                                        ctypes.POINTER(tsnet_grad_params), c_vp]),
     ("tsnet_comm_destroy", ctypes.c_int, [c_vp]),
@@ -170,10 +173,11 @@ class GradParams:
     h_max: float = 0.25
     I_min: int = 20
     I_max: int = TSNET_I_MAX_LIMIT
+    spread: int = 0        # TSNET_SPREAD_AUTO / _SORT / _RUNS (tsnet.h)
 
     def c(self):
         return tsnet_grad_params(self.lambda_kl, self.lambda_c, self.lambda_r, self.eps, self.interp_P, self.h_max,
-                                 self.I_min, self.I_max)
+                                 self.I_min, self.I_max, self.spread)
 
 
 @dataclass
@@ -550,6 +554,33 @@ def tsnet_comm_init(uid: bytes, world: int, rank: int, I_max: int = TSNET_I_MAX_
 
 def tsnet_comm_peer_reduce(comm) -> bool:
     return bool(lib().tsnet_comm_peer_reduce(comm))
+
+
+class _DeviceArray:
+    """A device buffer owned elsewhere (the communicator), exposed to torch
+    through __cuda_array_interface__ (no copy, no ownership)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def tsnet_comm_layout(comm, n: int, device=None) -> torch.Tensor:
+    """The communicator's own replicated layout buffer (n x 2 fp32, collective;
+    valid until tsnet_comm_destroy).  tsnet_step on this tensor pushes the
+    moved positions to the peers instead of all-gathering them."""
+    ptr = c_vp()
+    _check("tsnet_comm_layout", lib().tsnet_comm_layout(comm, int(n), ctypes.byref(ptr)))
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    return torch.as_tensor(_DeviceArray(ptr.value, (int(n), 2), "<f4"), device=dev)
+
+
+def tsnet_comm_layout_push(comm) -> bool:
+    return bool(lib().tsnet_comm_layout_push(comm))
+
+
+def tsnet_comm_layout_sync(comm, stream=None):
+    _check("tsnet_comm_layout_sync", lib().tsnet_comm_layout_sync(comm, _stream(stream)))
 
 
 def tsnet_grids_sum(ws_list, n: int, nnz: int, gp: GradParams, stream=None):

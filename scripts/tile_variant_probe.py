@@ -15,7 +15,8 @@ from workloads import clustered_layout, config_graph  # noqa: E402
 def main():
     cfg = int(sys.argv[1])
     name = sys.argv[2]
-    T.LIB_PATH = os.path.join(ROOT, "paper_2509_19785_b200", "build", "variants", f"libtsnet_{name}.so")
+    if name != "product":
+        T.LIB_PATH = os.path.join(ROOT, "paper_2509_19785_b200", "build", "variants", f"libtsnet_{name}.so")
     ip, ix = config_graph(cfg)
     P = T.tsnet_build_P(torch.from_numpy(ip).cuda(), torch.from_numpy(ix).cuda(), u=40.0, seed=0)["P"]
     Y = torch.from_numpy(clustered_layout(P.n, 30.0, 40, 2.0, 5)).cuda()

@@ -721,3 +721,76 @@ def test_config5_full_size_sampled():
         fo = oracle.attr_sparse_rows(Y.astype(np.float64), fip, fix, fpv, r0, B)
         assert relL2(fa[r0:r0 + B], fo) <= 1e-5
         assert relL2(g[r0:r0 + B], go) <= GRAD_TOL, (r0, relL2(g[r0:r0 + B], go))
+
+
+# ------------------------------------------------------------ spread paths
+def _sorted_layout(n, side, seed, cell=0.25):
+    """Uniform points renumbered cell by cell (cells of `cell` x `cell`, rows of
+    cells, x inside a cell): consecutive indices are spatial neighbours (the
+    index locality of a mesh)."""
+    Y = uniform_layout(n, side, seed)
+    cx, cy = np.floor(Y[:, 0] / cell), np.floor(Y[:, 1] / cell)
+    order = np.lexsort((Y[:, 0], cx, cy))
+    return np.ascontiguousarray(Y[order])
+
+
+@pytest.mark.parametrize("cfg,lay", [(1, "traj499"), (1, "uniform30"), (2, "sorted"), (2, "clustered")])
+@pytest.mark.parametrize("spread", [1, 2])
+def test_spread_paths_equal_oracle(cfg, lay, spread):
+    """Steps a1-a2 by the box sort (TSNET_SPREAD_SORT) and by index runs
+    (TSNET_SPREAD_RUNS, k_spread_runs) on layouts with and without index
+    locality: both paths are the same sums, so the gradient,
+    Z and the field agree with the oracle O5 to the usual bars, whatever the
+    point order."""
+    P = oracle_P(cfg)
+    n = P["n"]
+    Y = {"traj499": lambda: oracle_layouts(cfg)[499][0], "uniform30": lambda: uniform_layout(n, 30.0, 1),
+         "sorted": lambda: _sorted_layout(n, 20.0, 4), "clustered": lambda: clustered_layout(n, 25.0, 7, 1.2, 2)}[lay]()
+    gp = GradParams(*STAGE_B, spread=spread)
+    g, Z, fa, ff, st = gpu_grad(dev_P(P), Y, gp)
+    assert st["spread"] == spread
+    r = oracle_grad(P, Y, STAGE_B)
+    assert st["I"] == r["geo"]["I"]
+    assert abs(Z - r["Z"]) <= 1e-5 * r["Z"]
+    assert relL2(g, r["g"]) <= GRAD_TOL, relL2(g, r["g"])
+    assert relL2(ff, r["g"] - 4 * r["F_attr"] - 0.01 / n * Y.astype(np.float64)) <= GRAD_TOL
+
+
+def test_spread_auto_choice():
+    """TSNET_SPREAD_AUTO: the first evaluation on a fresh workspace sorts; the
+    next one takes the runs path when the layout's index order is local (sorted
+    rows) and stays on the sort when it is not (uniform random order); the
+    forced requests override the measure."""
+    n = 100_000   # 400 boxes (I = 20 over a span of 5): 250 points per box
+    P = dict(indptr=np.zeros(n + 1, np.int64), indices=np.zeros(0, np.int32), values=np.zeros(0))
+    Pd = dev_P(P)
+    for Y, want in ((_sorted_layout(n, 4.99, 4), 2), (uniform_layout(n, 4.99, 4), 1)):
+        ws = alloc_workspace(n, Pd.nnz, GradParams())
+        Yd = torch.from_numpy(Y).cuda()
+        modes = []
+        for _ in range(3):
+            tsnet_grad(Pd, Yd, GradParams(*STAGE_B), ws)
+            modes.append(tsnet_read_stats(ws)["spread"])
+        assert modes == [1, want, want], modes
+        tsnet_grad(Pd, Yd, GradParams(*STAGE_B, spread=3 - want), ws)
+        assert tsnet_read_stats(ws)["spread"] == 3 - want
+
+
+@pytest.mark.parametrize("n", [1, 2, 33, 255, 257, 4099])
+def test_spread_runs_ragged(n):
+    """The runs path on sizes that leave lanes and warps without points."""
+    Y = _sorted_layout(n, 6.0, n) if n > 1 else np.zeros((1, 2), np.float32)
+    P = dict(indptr=np.zeros(n + 1, np.int64), indices=np.zeros(0, np.int32), values=np.zeros(0))
+    for spread in (1, 2):
+        g, Z, _, _, st = gpu_grad(dev_P(P), Y, GradParams(*STAGE_B, spread=spread))
+        assert st["spread"] == spread
+        if n > 1:
+            r = oracle_grad(P, Y, STAGE_B)
+            assert abs(Z - r["Z"]) <= 1e-5 * r["Z"]
+            assert relL2(g, r["g"]) <= GRAD_TOL, (spread, relL2(g, r["g"]))
+
+
+def test_spread_bad_request():
+    P = oracle_P(1)
+    with pytest.raises(TsnetError):
+        gpu_grad(dev_P(P), uniform_layout(P["n"], 5.0, 1), GradParams(*STAGE_B, spread=3))

@@ -160,3 +160,54 @@ def test_shard_argument_errors():
         tsnet_step(Pp, Yd, V, G, gp, sp, ws, shard=T.Shard(0, 2, [0, n // 2, n]))
     with pytest.raises(T.TsnetError):      # recentring across ranks
         T.tsnet_step_finish(Pp, Yd, V, G, gp, StepParams(recenter=1), ws, shard=T.Shard(0, 2, [0, n // 2, n]))
+
+
+def test_layout_push_one_rank_communicator():
+    """The fused move + Y push (tsnet_comm_layout): with a 1-rank communicator
+    the step on the communicator's own layout buffer takes the push path (its
+    read-done / moved handshake, the move's last-block ticket and iteration
+    counter), eagerly, in a captured CUDA graph and over several replays, and
+    equals the unsharded step; tsnet_comm_layout_sync waits on the counters."""
+    P = oracle_P(2)
+    n = P["n"]
+    Y = clustered_layout(n, 20.0, 5, 1.5, 7)
+    vel, gains = random_state(n, 3)
+    gp, sp = GradParams(1.0, 0.01, 0.6), StepParams(eta=50.0, momentum=0.8)
+    Pd = dev(P)
+    comm = T.tsnet_comm_init(T.tsnet_comm_unique_id(), 1, 0, gp.I_max)
+    try:
+        Yc = T.tsnet_comm_layout(comm, n)
+        assert T.tsnet_comm_layout_push(comm)
+        assert T.tsnet_comm_layout(comm, n).data_ptr() == Yc.data_ptr()
+        with pytest.raises(T.TsnetError):
+            T.tsnet_comm_layout(comm, n + 1)
+        Yc.copy_(torch.from_numpy(Y))
+        sh = T.Shard(0, 1, [0, n], comm)
+        ws = alloc_workspace(n, Pd.nnz, gp)
+        Vd, Gd = (torch.from_numpy(a.copy()).cuda() for a in (vel, gains))
+        Y1, V1, G1 = (torch.from_numpy(a.copy()).cuda() for a in (Y, vel, gains))
+        ws1 = alloc_workspace(n, Pd.nnz, gp)
+        tsnet_step(Pd, Yc, Vd, Gd, gp, sp, ws, shard=sh)
+        tsnet_step(Pd, Y1, V1, G1, gp, sp, ws1)
+        T.tsnet_comm_layout_sync(comm)
+        torch.cuda.synchronize()
+        assert relL2(Yc.cpu().numpy(), Y1.cpu().numpy()) <= 1e-6
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            tsnet_step(Pd, Yc, Vd, Gd, gp, sp, ws, shard=sh, stream=s)
+        for _ in range(4):
+            with torch.cuda.stream(s):
+                g.replay()
+            tsnet_step(Pd, Y1, V1, G1, gp, sp, ws1)
+        T.tsnet_comm_layout_sync(comm, stream=s)
+        torch.cuda.synchronize()
+        assert relL2(Yc.cpu().numpy(), Y1.cpu().numpy()) <= 1e-5
+        assert relL2(Vd.cpu().numpy(), V1.cpu().numpy()) <= 1e-5
+        # another Y than the communicator's: the all-gather path
+        Y2 = Yc.clone()
+        tsnet_step(Pd, Y2, Vd.clone(), Gd.clone(), gp, sp, alloc_workspace(n, Pd.nnz, gp), shard=sh)
+        torch.cuda.synchronize()
+    finally:
+        T.tsnet_comm_destroy(comm)
