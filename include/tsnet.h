@@ -114,15 +114,17 @@ typedef struct {
                                 PAPER.md:187-188) visit the points; the result is the same sum
                                 (up to fp32 rounding order):
                                 TSNET_SPREAD_AUTO (0): decided on the device every iteration
-                                  from the last iteration's measure (below);
+                                  (below);
                                 TSNET_SPREAD_SORT (1): counting sort of the points by box, then a
-                                  warp per box chunk -- any point order;
-                                TSNET_SPREAD_RUNS (2): one pass over consecutive points, summed
-                                  in registers while the box stays the same -- for layouts
-                                  whose index order is spatially local (meshes);
-                                AUTO starts with SORT, switches to RUNS when < 1/64 of the
-                                index-adjacent points lie in different boxes and back when a
-                                run averages < 32 points.  Other values: TSNET_E_ARG. */
+                                  warp per box chunk; it also records the box order of the
+                                  points in the workspace;
+                                TSNET_SPREAD_RUNS (2): one pass over the points in the last
+                                  recorded box order (index order when none is recorded for
+                                  this n), summed in registers while the box stays the same;
+                                AUTO sorts on a fresh workspace, then runs over the recorded
+                                order until a run averages fewer than 16 points (the points
+                                moved across boxes since the sort), then sorts again.  Other
+                                values: TSNET_E_ARG. */
 } tsnet_grad_params;
 #define TSNET_SPREAD_AUTO 0
 #define TSNET_SPREAD_SORT 1

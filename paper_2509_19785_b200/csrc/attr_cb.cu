@@ -246,17 +246,7 @@ __device__ __forceinline__ void lds2_if(float2& v, uint32_t sbase, uint32_t off,
         : "+f"(v.x), "+f"(v.y)
         : "r"((uint32_t)p), "r"(sbase + off));
 }
-// the same without an input value: v is undefined where p is false (its
-// callers only read v where p holds), so no register is zeroed first
-__device__ __forceinline__ void lds2_p(float2& v, uint32_t sbase, uint32_t off, bool p) {
-    asm volatile(
-        "{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q ld.shared.v2.f32 {%0, %1}, [%3];\n}"
-        : "=f"(v.x), "=f"(v.y)
-        : "r"((uint32_t)p), "r"(sbase + off));
-}
-#ifndef TILE_NOINIT
-#define TILE_NOINIT 0
-#endif
+
 
 // NQ consecutive entries of this lane: contribution p w (X_i - X_j), w = 1 /
 // (1 + r^2) (rcp.approx: 1 + r^2 >= 1, relative error <= 2^-22); pad slots
@@ -282,12 +272,8 @@ __device__ __forceinline__ void tileq(const TileSet& S, const char* sm, uint32_t
 #else
         yj[q] = lds2(sm, ysoff + (w & kColMask));
 #endif
-#if TILE_NOINIT
-        lds2_p(yl[q], sb, ro, w & kNewRow);
-#else
         yl[q] = make_float2(0.f, 0.f);
         lds2_if(yl[q], sb, ro, w & kNewRow);
-#endif
     }
     float fx[NQ], fy[NQ];
 #pragma unroll
@@ -316,12 +302,8 @@ __device__ __forceinline__ void tileq(const TileSet& S, const char* sm, uint32_t
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         const uint32_t w = S.s[q].x;
-#if TILE_NOINIT
-        lds2_p(v[q], sb, kFsOff + ((w >> kRowShift) & kRowMask), (w & (kFlush | kHub)) == kFlush);
-#else
         v[q] = make_float2(0.f, 0.f);
         lds2_if(v[q], sb, kFsOff + ((w >> kRowShift) & kRowMask), (w & (kFlush | kHub)) == kFlush);
-#endif
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q)

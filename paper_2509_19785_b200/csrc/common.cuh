@@ -57,12 +57,13 @@ struct Geo {
     double sum_x, sum_y;               // centroid accumulation (recenter)
     double eacc;                       // cost mode 1: Parseval accumulator <W1, K_ln * W1> * M^2
     // a1/a2 path of this iteration (field.cu, k_bbox decides): kSpreadSort (box
-    // counting sort + spread) or kSpreadRuns (one pass over index runs)
+    // counting sort + spread, which also records the box order `perm`) or
+    // kSpreadRuns (one pass over the points in the last recorded box order)
     int smode;
     int pad;
-    unsigned long long spts;           // points spread by the last iteration (its a1/a2 kernel)
-    unsigned long long schg;           // sort path: index-adjacent pairs in different boxes
-    unsigned long long sflush;         // runs path: box flushes
+    long long perm_n;                  // points of the recorded box order (0: none)
+    unsigned long long spts;           // runs path: points spread by the last iteration
+    unsigned long long sflush;         // runs path: box flushes of the last iteration
 };
 constexpr int kSpreadSort = 0, kSpreadRuns = 1;
 
@@ -82,6 +83,7 @@ struct Ws {
     int* rank;           // n   rank of the point inside its box
     float2* uv;          // n   in-box coordinates (u_x, u_y) in [0,1]
     float2* sorted_uv;   // n   uv in box order
+    int* perm;           // n   the points in box order (k_box_scatter), visited by k_spread_runs
     int* box_cnt;        // I_max^2 + 1
     int* box_start;      // I_max^2 + 1
     int2* items;         // max_items (box, first point)
@@ -126,6 +128,7 @@ inline Ws ws_map(void* base, int64_t n, int64_t nnz, int I_max) {
     w.rank = (int*)take(sizeof(int) * n);
     w.uv = (float2*)take(sizeof(float2) * n);
     w.sorted_uv = (float2*)take(sizeof(float2) * n);
+    w.perm = (int*)take(sizeof(int) * n);
     w.box_cnt = (int*)take(sizeof(int) * nb);
     w.box_start = (int*)take(sizeof(int) * nb);
     w.items = (int2*)take(sizeof(int2) * w.max_items);

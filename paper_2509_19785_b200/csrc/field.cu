@@ -49,6 +49,10 @@ __device__ __forceinline__ float bb_val(unsigned u) { return o2f((int)(u ^ 0x800
 
 // a0: bounding box of Y and, in the last block, the grid geometry (R9).
 constexpr int kBBoxPts = 8;
+#ifndef RUNS_RESORT       // probe builds (scripts/tile_variants.sh SRC=field): the re-sort threshold
+#define RUNS_RESORT 16
+#endif
+constexpr int kRunsResort = RUNS_RESORT;   // adaptive spread: re-sort when flushes * this > points
 //
 // The CTAs also zero the charge grid cells the previous iteration used
 // ([0, N_prev^2), N_prev read before the last block sets the new geometry;
@@ -144,14 +148,13 @@ __global__ void __launch_bounds__(256) k_bbox(const float2* __restrict__ Y, int6
             mode = kSpreadSort;
         } else if (spread == TSNET_SPREAD_RUNS) {
             mode = kSpreadRuns;
-        } else if (g->smode == kSpreadRuns) {   // back to the sort when a run averages < 32 points
-            mode = g->sflush * 32ull > g->spts ? kSpreadSort : kSpreadRuns;
-        } else {                                // to the runs when < 1/64 of the adjacent points change box
-            mode = (g->spts > 0 && g->schg * 64ull < g->spts) ? kSpreadRuns : kSpreadSort;
+        } else if (g->smode == kSpreadRuns) {   // re-sort once a run averages < kRunsResort points
+            mode = g->sflush * (unsigned long long)kRunsResort > g->spts ? kSpreadSort : kSpreadRuns;
+        } else {                                // a fresh box order: runs
+            mode = g->perm_n > 0 ? kSpreadRuns : kSpreadSort;
         }
         g->smode = mode;
         g->spts = 0ull;
-        g->schg = 0ull;
         g->sflush = 0ull;
     }
     double S = fmax(hi_x - lo_x, hi_y - lo_y);
@@ -222,30 +225,23 @@ __device__ __forceinline__ void write_twiddles(const Geo* __restrict__ g, float2
 
 // Sort path only (exits at once on the runs path).  The CTAs also write the
 // twiddles of length M; the box counters were zeroed by the previous
-// k_box_scan (or are zero in a fresh workspace).  Every 8th CTA measures the
-// index locality of the layout for the next iteration's path choice: the
-// pairs of consecutive points (i, i + 1) held by neighbouring lanes, and how
-// many of them lie in different boxes.
+// k_box_scan (or are zero in a fresh workspace).
 __global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__ Y, int64_t n, Geo* __restrict__ g,
                                                    int* __restrict__ box_cnt, int* __restrict__ box,
                                                    int* __restrict__ rank, float2* __restrict__ uv,
                                                    float2* __restrict__ tw) {
     __shared__ int hist[kBoxSmem];
-    __shared__ unsigned s_chg, s_pairs;
     if (g->smode != kSpreadSort) return;
     const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b;
     const int I = g->I;
     const int nb = I * I;
     write_twiddles(g, tw);
-    const bool sample = (blockIdx.x & 7) == 0;
-    if (sample && threadIdx.x == 0) {
-        s_chg = 0u;
-        s_pairs = 0u;
-    }
     const bool local = nb <= kBoxSmem;
     const int64_t c0 = (int64_t)blockIdx.x * kBoxChunk + threadIdx.x;
-    if (local) for (int q = threadIdx.x; q < nb; q += blockDim.x) hist[q] = 0;
-    if (local || sample) __syncthreads();
+    if (local) {
+        for (int q = threadIdx.x; q < nb; q += blockDim.x) hist[q] = 0;
+        __syncthreads();
+    }
     int* cnt = local ? hist : box_cnt;
     float2 y[kBoxPts];
 #pragma unroll
@@ -266,30 +262,8 @@ __global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__
             rj[j] = atomicAdd(&cnt[bj[j]], 1);
         }
     }
-    if (sample) {
-        const unsigned full = 0xffffffffu;
-        const int lane = threadIdx.x & 31;
-        unsigned chg = 0u, pairs = 0u;
-#pragma unroll
-        for (int j = 0; j < kBoxPts; ++j) {
-            const int bp = __shfl_up_sync(full, bj[j], 1);
-            const bool pair = lane > 0 && bj[j] >= 0 && bp >= 0;
-            pairs += pair;
-            chg += pair && bp != bj[j];
-        }
-        chg = __reduce_add_sync(full, chg);
-        pairs = __reduce_add_sync(full, pairs);
-        if (lane == 0) {
-            atomicAdd(&s_chg, chg);
-            atomicAdd(&s_pairs, pairs);
-        }
-    }
-    if (local || sample) __syncthreads();
-    if (sample && threadIdx.x == 0 && s_pairs) {
-        atomicAdd(&g->schg, (unsigned long long)s_chg);
-        atomicAdd(&g->spts, (unsigned long long)s_pairs);
-    }
     if (local) {
+        __syncthreads();
         for (int q = threadIdx.x; q < nb; q += blockDim.x) {
             const int c = hist[q];
             if (c) hist[q] = atomicAdd(&box_cnt[q], c);   // this CTA's range inside box q
@@ -352,11 +326,13 @@ __global__ void __launch_bounds__(1024) k_box_scan(Geo* g, int* __restrict__ box
 
 // 4 points per thread and iteration: their loads, then the box_start
 // gathers, then the stores, each in flight together
-__global__ void __launch_bounds__(256) k_box_scatter(const Geo* __restrict__ g, int64_t n, const int* __restrict__ box,
+__global__ void __launch_bounds__(256) k_box_scatter(Geo* __restrict__ g, int64_t n, const int* __restrict__ box,
                                                      const int* __restrict__ rank, const int* __restrict__ box_start,
-                                                     const float2* __restrict__ uv, float2* __restrict__ sorted_uv) {
+                                                     const float2* __restrict__ uv, float2* __restrict__ sorted_uv,
+                                                     int* __restrict__ perm) {
     constexpr int V = 4;
     if (g->smode != kSpreadSort) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) g->perm_n = n;   // the box order of these n points
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += V * stride) {
         int b[V], r[V], st[V];
@@ -372,7 +348,10 @@ __global__ void __launch_bounds__(256) k_box_scatter(const Geo* __restrict__ g, 
         for (int v = 0; v < V; ++v) st[v] = __ldg(box_start + b[v]);
 #pragma unroll
         for (int v = 0; v < V; ++v)
-            if (i0 + v * stride < n) sorted_uv[st[v] + r[v]] = u[v];
+            if (i0 + v * stride < n) {
+                sorted_uv[st[v] + r[v]] = u[v];
+                perm[st[v] + r[v]] = (int)(i0 + v * stride);
+            }
     }
 }
 
@@ -443,11 +422,13 @@ __global__ void __launch_bounds__(256) k_spread(const Geo* __restrict__ g, const
     }
 }
 
-// a1 + a2 in one pass, for layouts whose index order is spatially local (a
-// mesh numbered along its axes: consecutive vertices sit in the same box for
-// long runs).  Runs path only (exits at once on the sort path).
-// A warp takes chunks of 32 kRunPts consecutive points, lane l the kRunPts
-// points from l kRunPts on.  A lane sums the charges of its points in 27
+// a1 + a2 in one pass over the points in the box order the last sort recorded
+// (perm; the index order when there is none): the points have moved little
+// since, so most consecutive points of that order still share a box.  Runs
+// path only (exits at once on the sort path); any order gives the same sums,
+// the order only decides how often a run breaks.
+// A warp takes chunks of 32 kRunPts consecutive positions of the order, lane l
+// the kRunPts positions from l kRunPts on.  A lane sums the charges of its points in 27
 // registers (9 nodes x (W1, M_x, M_y), as k_spread) while the box stays the
 // same, and adds them to the grid (9 red.global.add.v4) when the box changes;
 // at the end of the chunk the lanes' last runs are summed across lanes by a
@@ -468,9 +449,11 @@ __device__ __forceinline__ void runs_flush(float4* __restrict__ wgrid, int b, in
 }
 
 __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ Y, int64_t n, Geo* __restrict__ g,
-                                                     float4* __restrict__ wgrid, float2* __restrict__ tw) {
+                                                     const int* __restrict__ perm, float4* __restrict__ wgrid,
+                                                     float2* __restrict__ tw) {
     __shared__ unsigned s_flush;
     if (g->smode != kSpreadRuns) return;
+    const bool ordered = g->perm_n == n;
     write_twiddles(g, tw);
     if (threadIdx.x == 0) s_flush = 0u;
     __syncthreads();
@@ -488,7 +471,10 @@ __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ 
         const int64_t base = c * (32 * kRunPts) + (int64_t)lane * kRunPts;
         float2 y[kRunPts];
 #pragma unroll
-        for (int v = 0; v < kRunPts; ++v) y[v] = base + v < n ? __ldg(Y + base + v) : make_float2(0.f, 0.f);
+        for (int v = 0; v < kRunPts; ++v) {
+            const int64_t k = base + v;
+            y[v] = k < n ? __ldg(Y + (ordered ? (int64_t)__ldg(perm + k) : k)) : make_float2(0.f, 0.f);
+        }
         float acc[27];
 #pragma unroll
         for (int q = 0; q < 27; ++q) acc[q] = 0.f;
@@ -932,11 +918,11 @@ cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, b
     // iteration is one CUDA graph); the kernels of the other path exit at once
     const int rbk = (int)std::max<int64_t>(1, std::min<int64_t>((nl + 8 * 32 * kRunPts - 1) / (8 * 32 * kRunPts),
                                                                   (int64_t)kNumSMs * 2));
-    k_spread_runs<<<rbk, 256, 0, s>>>(Yl, nl, w.geo, w.wgrid, w.tw);
+    k_spread_runs<<<rbk, 256, 0, s>>>(Yl, nl, w.geo, w.perm, w.wgrid, w.tw);
     const int cb = (int)std::max<int64_t>(kNumSMs, (nl + kBoxChunk - 1) / kBoxChunk);
     k_box_count<<<cb, 256, 0, s>>>(Yl, nl, w.geo, w.box_cnt, w.box, w.rank, w.uv, w.tw);
     k_box_scan<<<1, 1024, 0, s>>>(w.geo, w.box_cnt, w.box_start, w.items, nl);
-    k_box_scatter<<<pbl, 256, 0, s>>>(w.geo, nl, w.box, w.rank, w.box_start, w.uv, w.sorted_uv);
+    k_box_scatter<<<pbl, 256, 0, s>>>(w.geo, nl, w.box, w.rank, w.box_start, w.uv, w.sorted_uv, w.perm);
     k_spread<<<kNumSMs * 8, 256, 0, s>>>(w.geo, w.items, w.box_start, w.sorted_uv, w.wgrid);
     return cudaGetLastError();
 }
