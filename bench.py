@@ -233,15 +233,15 @@ def choose_plan(P, shard, stream):
     if Q.plan is not None and Q.plan_kind == PLAN_SELL:
         return Q, {"choice": "sliced ELL (pads <= 1.3 slots per entry)"}
     Y = torch.randn((P.n, 2), device=P.indptr.device) * 3.0
-    F = torch.empty_like(Y)
+    F = tsnet_attr(Q, Y, shard=shard, stream=stream)      # this rank's rows
 
     def t(Pk):
         for _ in range(2):
-            tsnet_attr(Pk, Y, F, stream=stream)
+            tsnet_attr(Pk, Y, F, shard=shard, stream=stream)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(5):
-            tsnet_attr(Pk, Y, F, stream=stream)
+            tsnet_attr(Pk, Y, F, shard=shard, stream=stream)
         e1.record(stream)
         e1.synchronize()
         return e0.elapsed_time(e1) / 5
@@ -279,7 +279,14 @@ def run_ours(args, rank, world, local_rank):
     if world > 1 or args.sharded:
         # row shards + NCCL communicator (+ the plan of the own rows) (set-up, untimed)
         from paper_2509_19785_b200.distributed import ShardedLayout
-        lay = ShardedLayout(P, Y0, rank, world, plan=args.plan)
+        if args.plan == "auto":      # the same timed choice as one GPU, on this rank's rows
+            def pick(Pc, sh, st):
+                nonlocal plan_info
+                Pk, plan_info = choose_plan(Pc, sh, st)
+                return Pk
+            lay = ShardedLayout(P, Y0, rank, world, plan=pick)
+        else:
+            lay = ShardedLayout(P, Y0, rank, world, plan=args.plan)
         shard = lay.shard
         rb, re = lay.rows
     else:

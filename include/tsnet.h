@@ -179,6 +179,8 @@ typedef struct {
     int32_t I, N, M;         /* intervals per axis, nodes per axis (3I), FFT size (6I)   */
     int32_t nonfinite;       /* 1 if a non-finite coordinate/gradient was produced       */
     int32_t spread;          /* spread path of the last evaluation: TSNET_SPREAD_SORT / _RUNS */
+    int64_t spread_points;   /* runs path: points of the last evaluation (0 after a sort)   */
+    int64_t spread_flushes;  /* runs path: box runs it summed (flushes to the grid)         */
 } tsnet_stats;
 
 /* ---------------------------------------------------------------- C0 (set-up) */

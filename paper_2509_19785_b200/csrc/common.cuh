@@ -60,6 +60,8 @@ struct Geo {
     // counting sort + spread, which also records the box order `perm`) or
     // kSpreadRuns (one pass over the points in the last recorded box order)
     int smode;
+    int sruns;                         // consecutive runs-path iterations so far
+    int sskip;                         // sorts still to do before the runs path is tried again
     int pad;
     long long perm_n;                  // points of the recorded box order (0: none)
     unsigned long long spts;           // runs path: points spread by the last iteration

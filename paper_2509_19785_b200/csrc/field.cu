@@ -53,6 +53,7 @@ constexpr int kBBoxPts = 8;
 #define RUNS_RESORT 16
 #endif
 constexpr int kRunsResort = RUNS_RESORT;   // adaptive spread: re-sort when flushes * this > points
+constexpr int kRunsBackoff = 8;            // sorts before retrying the runs after a failed first run
 //
 // The CTAs also zero the charge grid cells the previous iteration used
 // ([0, N_prev^2), N_prev read before the last block sets the new geometry;
@@ -150,9 +151,16 @@ __global__ void __launch_bounds__(256) k_bbox(const float2* __restrict__ Y, int6
             mode = kSpreadRuns;
         } else if (g->smode == kSpreadRuns) {   // re-sort once a run averages < kRunsResort points
             mode = g->sflush * (unsigned long long)kRunsResort > g->spts ? kSpreadSort : kSpreadRuns;
+            // the order was already too stale one iteration after a sort (the
+            // layout moves fast): sort for the next kRunsBackoff iterations
+            if (mode == kSpreadSort && g->sruns <= 1) g->sskip = kRunsBackoff;
+        } else if (g->sskip > 0) {
+            --g->sskip;
+            mode = kSpreadSort;
         } else {                                // a fresh box order: runs
             mode = g->perm_n > 0 ? kSpreadRuns : kSpreadSort;
         }
+        g->sruns = mode == kSpreadRuns ? g->sruns + 1 : 0;
         g->smode = mode;
         g->spts = 0ull;
         g->sflush = 0ull;
@@ -448,6 +456,24 @@ __device__ __forceinline__ void runs_flush(float4* __restrict__ wgrid, int b, in
     }
 }
 
+// the charges of one point on the 9 nodes of its box b
+__device__ __forceinline__ void runs_point(float4* __restrict__ wgrid, int b, int I, int N, float h_b, float ux,
+                                           float uy) {
+    const float sn[3] = {1.0f / 6.0f, 0.5f, 5.0f / 6.0f};
+    float Lx[3], Ly[3];
+    lagrange3(ux, Lx);
+    lagrange3(uy, Ly);
+    const int bx = b % I, by = b / I;
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float w = Lx[a] * Ly[bb];
+            red_add_v4(&wgrid[(int64_t)(3 * by + bb) * N + 3 * bx + a], w, w * (sn[a] - ux) * h_b,
+                       w * (sn[bb] - uy) * h_b);
+        }
+}
+
 __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ Y, int64_t n, Geo* __restrict__ g,
                                                      const int* __restrict__ perm, float4* __restrict__ wgrid,
                                                      float2* __restrict__ tw) {
@@ -478,14 +504,27 @@ __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ 
         float acc[27];
 #pragma unroll
         for (int q = 0; q < 27; ++q) acc[q] = 0.f;
+        int bv[kRunPts];
+        float uxv[kRunPts], uyv[kRunPts];
+#pragma unroll
+        for (int v = 0; v < kRunPts; ++v) {
+            bv[v] = -1;
+            if (base + v < n) box_of(y[v], lo_x, lo_y, h_b, I, bv[v], uxv[v], uyv[v]);
+        }
         int cur = -1;
 #pragma unroll
         for (int v = 0; v < kRunPts; ++v) {
-            if (base + v >= n) break;
-            int b;
-            float ux, uy;
-            box_of(y[v], lo_x, lo_y, h_b, I, b, ux, uy);
+            const int b = bv[v];
+            if (b < 0) break;
+            const float ux = uxv[v], uy = uyv[v];
             if (b != cur) {
+                if (cur >= 0 && v + 1 < kRunPts && bv[v + 1] == cur) {
+                    // a stray (it left the run's box since the sort; the run goes
+                    // on after it): its 9 nodes directly, the run unbroken
+                    runs_point(wgrid, b, I, N, h_bf, ux, uy);
+                    ++flushes;
+                    continue;
+                }
                 if (cur >= 0) {
                     runs_flush(wgrid, cur, I, N, h_bf, acc);
                     ++flushes;

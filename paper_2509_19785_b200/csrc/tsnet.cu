@@ -595,6 +595,8 @@ int tsnet_read_stats(const void* ws, tsnet_stats* out, tsnet_stream_t stream) {
     out->M = g.M;
     out->nonfinite = g.nonfinite;
     out->spread = g.smode == kSpreadRuns ? TSNET_SPREAD_RUNS : TSNET_SPREAD_SORT;
+    out->spread_points = (int64_t)g.spts;
+    out->spread_flushes = (int64_t)g.sflush;
     return g.nonfinite ? TSNET_E_NONFINITE : TSNET_OK;
 }
 

@@ -51,12 +51,16 @@ class ShardedLayout:
         self.params = [stage_params(0, base, eta), stage_params(1, base, eta)]
         self.comm = tsnet_comm_init(uid, world, rank, self.params[0][0].I_max)
         self.shard = Shard(rank, world, bounds, self.comm)
-        # the attractive SpMV reads the own rows of P (CSR), or a plan of them
-        # (attach_plan: "csr", "cb", "sell", "auto") attached to a shallow copy,
-        # so the caller's P keeps its own plan
-        self.P = attach_plan(P.without_plan(), plan, self.shard)
         self.stream = torch.cuda.Stream(device=Y0.device)
         self.stream.wait_stream(torch.cuda.current_stream(Y0.device))
+        # the attractive SpMV reads the own rows of P (CSR), or a plan of them
+        # (attach_plan: "csr", "cb", "sell", "auto"; or a callable
+        # (P, shard, stream) -> P with a plan, e.g. bench.choose_plan) attached
+        # to a shallow copy, so the caller's P keeps its own plan
+        if callable(plan):
+            self.P = plan(P.without_plan(), self.shard, self.stream)
+        else:
+            self.P = attach_plan(P.without_plan(), plan, self.shard)
         # the replicated layout: the communicator's buffer when the move can push
         # into every peer's copy (collective call on every rank), else a tensor
         # of our own and the all-gather

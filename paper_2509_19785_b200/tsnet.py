@@ -53,7 +53,8 @@ class tsnet_shard(ctypes.Structure):
 
 class tsnet_stats(ctypes.Structure):
     _fields_ = [("Z", c_f64), ("lo_x", c_f64), ("lo_y", c_f64), ("S", c_f64), ("h_b", c_f64), ("I", c_i32),
-                ("N", c_i32), ("M", c_i32), ("nonfinite", c_i32), ("spread", c_i32)]
+                ("N", c_i32), ("M", c_i32), ("nonfinite", c_i32), ("spread", c_i32), ("spread_points", c_i64),
+                ("spread_flushes", c_i64)]
 
 
 _lib = None

@@ -29,6 +29,11 @@ st = tsnet_read_stats(lay.ws, stream=lay.stream)
 print("plan", info, "N", st["N"], "span", st["S"], flush=True)
 lay.use_graphs = False
 torch.cuda.profiler.start()
-lay.run(reps, start=start)
+for r in range(reps):
+    lay.run(1, start=start + r)
+    if len(sys.argv) > 4:      # per-iteration spread path and its measure
+        st = tsnet_read_stats(lay.ws, stream=lay.stream)
+        print("iter", start + r, "spread", st["spread"], "points", st["spread_points"], "flushes",
+              st["spread_flushes"], "N", st["N"], flush=True)
 lay.sync()
 torch.cuda.profiler.stop()
