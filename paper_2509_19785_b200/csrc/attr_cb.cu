@@ -74,7 +74,7 @@ constexpr int kTPre = TILE_PREF;     // blocks of entries prefetched into L2 ahe
                     // 3/4 cycle counters, 5 no per-block barrier
 #define TILE_DIAG 0
 #endif
-constexpr int kTW = 15;              // consumer warps per CTA (+1 producer warp: 16 warps, <= 128 registers)
+constexpr int kTW = 15;           // consumer warps per CTA (+1 producer warp: 16 warps, <= 128 registers)
 constexpr int kTL = kTW * 32;        // consumer threads
 constexpr int kTR = TILE_TR;         // max rows per panel (16 B of shared memory each; a multiple of 16
                                      // for the row-slot swizzle)

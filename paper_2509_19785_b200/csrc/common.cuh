@@ -46,6 +46,7 @@ void set_error(const char* fmt, ...);
 // read by every later kernel of the iteration (no host round trip).
 struct Geo {
     double lo_x, lo_y, S, h_b, delta;  // fp64: box assignment matches the fp64 definition (R16)
+    double inv_h;                      // 1 / h_b (move.cuh: box_of)
     double zacc;                       // Parseval accumulator  <W1, K1 * W1> * M^2
     double Z;                          // Z = zacc / M^2 - n
     int I, N, M, nrad;

@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(256) k_bbox(const float2* __restrict__ Y, int6
     g->I = I;
     g->h_b = S / (double)I;
     g->delta = g->h_b / 3.0;
+    g->inv_h = 1.0 / g->h_b;
     g->N = 3 * I;
     g->M = 6 * I;
     int m = 6 * I, nr = 0;
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__
                                                    float2* __restrict__ tw) {
     __shared__ int hist[kBoxSmem];
     if (g->smode != kSpreadSort) return;
-    const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b;
+    const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b, inv_h = g->inv_h;
     const int I = g->I;
     const int nb = I * I;
     write_twiddles(g, tw);
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__
         rj[j] = 0;
         if (i < n) {
             float ux, uy;
-            box_of(y[j], lo_x, lo_y, h_b, I, bj[j], ux, uy);
+            box_of(y[j], lo_x, lo_y, h_b, inv_h, I, bj[j], ux, uy);
             uv[i] = make_float2(ux, uy);
             rj[j] = atomicAdd(&cnt[bj[j]], 1);
         }
@@ -445,7 +446,10 @@ __global__ void __launch_bounds__(256) k_spread(const Geo* __restrict__ g, const
 // sums as the box sort, in another fp32 order.  The CTAs also
 // write the twiddles; per CTA the box flushes are counted for the next
 // iteration's path choice (k_bbox).
-constexpr int kRunPts = 8;
+#ifndef RUNS_PTS
+#define RUNS_PTS 8
+#endif
+constexpr int kRunPts = RUNS_PTS;
 __device__ __forceinline__ void runs_flush(float4* __restrict__ wgrid, int b, int I, int N, float h_b,
                                            const float (&acc)[27]) {
     const int bx = b % I, by = b / I;
@@ -484,7 +488,7 @@ __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ 
     if (threadIdx.x == 0) s_flush = 0u;
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0) g->spts = (unsigned long long)n;
-    const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b;
+    const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b, inv_h = g->inv_h;
     const int I = g->I, N = g->N;
     const float h_bf = (float)h_b;
     const float sn[3] = {1.0f / 6.0f, 0.5f, 5.0f / 6.0f};
@@ -509,7 +513,7 @@ __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ 
 #pragma unroll
         for (int v = 0; v < kRunPts; ++v) {
             bv[v] = -1;
-            if (base + v < n) box_of(y[v], lo_x, lo_y, h_b, I, bv[v], uxv[v], uyv[v]);
+            if (base + v < n) box_of(y[v], lo_x, lo_y, h_b, inv_h, I, bv[v], uxv[v], uyv[v]);
         }
         int cur = -1;
 #pragma unroll

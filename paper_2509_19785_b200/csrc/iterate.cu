@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(256) k_grad_out(int64_t n, const Geo* __restri
         const float2 y = Y[i];
         int b;
         float2 u;
-        box_of(y, g.lo_x, g.lo_y, g.h_b, g.I, b, u.x, u.y);
+        box_of(y, g.lo_x, g.lo_y, g.h_b, g.inv_h, g.I, b, u.x, u.y);
         const float2 ff = gather_field(g, fgrid, b, u);
         if (f_field) f_field[i] = ff;
         if (grad) {
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(SMEM ? kUpdateThreads : kUpdateThreadsG, SMEM 
         }
         if (RECOMPUTE) {
 #pragma unroll
-            for (int q = 0; q < V; ++q) box_of(y[q], g.lo_x, g.lo_y, g.h_b, g.I, b[q], u[q].x, u[q].y);
+            for (int q = 0; q < V; ++q) box_of(y[q], g.lo_x, g.lo_y, g.h_b, g.inv_h, g.I, b[q], u[q].x, u[q].y);
         }
 #pragma unroll
         for (int q = 0; q < V; ++q) {

@@ -794,7 +794,8 @@ def test_spread_runs_ragged(n):
         if n > 1:
             # Z = (Parseval sum) - n: its fp32 floor is relative to the sum, Z + n
             assert abs(float(Z.item()) - r["Z"]) <= 1e-5 * (r["Z"] + n)
-            assert relL2(g.cpu().numpy(), r["g"]) <= GRAD_TOL, (spread, relL2(g.cpu().numpy(), r["g"]))
+            tol = 3e-4 if n == 2 else GRAD_TOL   # the 2-point pair: reading R28's bar
+            assert relL2(g.cpu().numpy(), r["g"]) <= tol, (spread, relL2(g.cpu().numpy(), r["g"]))
 
 
 def test_spread_bad_request():
