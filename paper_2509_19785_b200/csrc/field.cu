@@ -460,24 +460,6 @@ __device__ __forceinline__ void runs_flush(float4* __restrict__ wgrid, int b, in
     }
 }
 
-// the charges of one point on the 9 nodes of its box b
-__device__ __forceinline__ void runs_point(float4* __restrict__ wgrid, int b, int I, int N, float h_b, float ux,
-                                           float uy) {
-    const float sn[3] = {1.0f / 6.0f, 0.5f, 5.0f / 6.0f};
-    float Lx[3], Ly[3];
-    lagrange3(ux, Lx);
-    lagrange3(uy, Ly);
-    const int bx = b % I, by = b / I;
-#pragma unroll
-    for (int bb = 0; bb < 3; ++bb)
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const float w = Lx[a] * Ly[bb];
-            red_add_v4(&wgrid[(int64_t)(3 * by + bb) * N + 3 * bx + a], w, w * (sn[a] - ux) * h_b,
-                       w * (sn[bb] - uy) * h_b);
-        }
-}
-
 __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ Y, int64_t n, Geo* __restrict__ g,
                                                      const int* __restrict__ perm, float4* __restrict__ wgrid,
                                                      float2* __restrict__ tw) {
@@ -491,7 +473,6 @@ __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ 
     const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b, inv_h = g->inv_h;
     const int I = g->I, N = g->N;
     const float h_bf = (float)h_b;
-    const float sn[3] = {1.0f / 6.0f, 0.5f, 5.0f / 6.0f};
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -508,68 +489,81 @@ __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ 
         float acc[27];
 #pragma unroll
         for (int q = 0; q < 27; ++q) acc[q] = 0.f;
-        int bv[kRunPts];
-        float uxv[kRunPts], uyv[kRunPts];
-#pragma unroll
-        for (int v = 0; v < kRunPts; ++v) {
-            bv[v] = -1;
-            if (base + v < n) box_of(y[v], lo_x, lo_y, h_b, inv_h, I, bv[v], uxv[v], uyv[v]);
-        }
         int cur = -1;
 #pragma unroll
         for (int v = 0; v < kRunPts; ++v) {
-            const int b = bv[v];
-            if (b < 0) break;
-            const float ux = uxv[v], uy = uyv[v];
-            if (b != cur) {
-                if (cur >= 0 && v + 1 < kRunPts && bv[v + 1] == cur) {
-                    // a stray (it left the run's box since the sort; the run goes
-                    // on after it): its 9 nodes directly, the run unbroken
-                    runs_point(wgrid, b, I, N, h_bf, ux, uy);
-                    ++flushes;
-                    continue;
-                }
-                if (cur >= 0) {
-                    runs_flush(wgrid, cur, I, N, h_bf, acc);
-                    ++flushes;
+            if (base + v < n) {
+                int b;
+                float ux, uy;
+                box_of(y[v], lo_x, lo_y, h_b, inv_h, I, b, ux, uy);
+                if (b != cur) {                // the run's box changed (rare on a fresh order)
+                    if (cur >= 0) {
+                        runs_flush(wgrid, cur, I, N, h_bf, acc);
+                        ++flushes;
 #pragma unroll
-                    for (int q = 0; q < 27; ++q) acc[q] = 0.f;
+                        for (int q = 0; q < 27; ++q) acc[q] = 0.f;
+                    }
+                    cur = b;
                 }
-                cur = b;
+                // offsets to the 3 nodes per axis, Lagrange weights from them
+                const float dx0 = 1.0f / 6.0f - ux, dx1 = 0.5f - ux, dx2 = 5.0f / 6.0f - ux;
+                const float dy0 = 1.0f / 6.0f - uy, dy1 = 0.5f - uy, dy2 = 5.0f / 6.0f - uy;
+                const float Lx[3] = {4.5f * dx1 * dx2, -9.0f * dx0 * dx2, 4.5f * dx0 * dx1};
+                const float Ly[3] = {4.5f * dy1 * dy2, -9.0f * dy0 * dy2, 4.5f * dy0 * dy1};
+                const float dx[3] = {dx0, dx1, dx2}, dy[3] = {dy0, dy1, dy2};
+#pragma unroll
+                for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        const float w = Lx[a] * Ly[bb];
+                        const int q = 3 * (3 * bb + a);
+                        acc[q] += w;
+                        acc[q + 1] = fmaf(w, dx[a], acc[q + 1]);
+                        acc[q + 2] = fmaf(w, dy[bb], acc[q + 2]);
+                    }
             }
-            float Lx[3], Ly[3];
-            lagrange3(ux, Lx);
-            lagrange3(uy, Ly);
-#pragma unroll
-            for (int bb = 0; bb < 3; ++bb)
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    const float w = Lx[a] * Ly[bb];
-                    const int q = 3 * (3 * bb + a);
-                    acc[q] += w;
-                    acc[q + 1] += w * (sn[a] - ux);
-                    acc[q + 2] += w * (sn[bb] - uy);
-                }
         }
+        __syncwarp();
         // segmented inclusive scan over the lanes, segments = equal boxes
         // (lanes without points: key -1 - lane, a segment of their own)
         const int key = cur >= 0 ? cur : -1 - lane;
         const int kp = __shfl_up_sync(full, key, 1);
-        bool head = lane == 0 || kp != key;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const bool uh = __shfl_up_sync(full, head, o);
-#pragma unroll
-            for (int q = 0; q < 27; ++q) {
-                const float u = __shfl_up_sync(full, acc[q], o);
-                if (lane >= o && !head) acc[q] += u;
-            }
-            if (lane >= o) head = head || uh;
-        }
         const int kn = __shfl_down_sync(full, key, 1);
-        if (cur >= 0 && (lane == 31 || kn != key)) {
-            runs_flush(wgrid, cur, I, N, h_bf, acc);
-            ++flushes;
+        if (__all_sync(full, kp == key || lane == 0)) {
+            // one segment (the common case): butterfly sums, lane t adds node t
+#pragma unroll
+            for (int q = 0; q < 27; ++q)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(full, acc[q], o);
+            if (cur >= 0 && lane < 9) {
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+#pragma unroll
+                for (int t = 0; t < 9; ++t)
+                    if (t == lane) {
+                        a0 = acc[3 * t];
+                        a1 = acc[3 * t + 1];
+                        a2 = acc[3 * t + 2];
+                    }
+                const int bx = cur % I, by = cur / I;
+                red_add_v4(&wgrid[(int64_t)(3 * by + lane / 3) * N + 3 * bx + lane % 3], a0, a1 * h_bf, a2 * h_bf);
+                if (lane == 0) ++flushes;
+            }
+        } else {
+            bool head = lane == 0 || kp != key;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const bool uh = __shfl_up_sync(full, head, o);
+#pragma unroll
+                for (int q = 0; q < 27; ++q) {
+                    const float u = __shfl_up_sync(full, acc[q], o);
+                    if (lane >= o && !head) acc[q] += u;
+                }
+                if (lane >= o) head = head || uh;
+            }
+            if (cur >= 0 && (lane == 31 || kn != key)) {
+                runs_flush(wgrid, cur, I, N, h_bf, acc);
+                ++flushes;
+            }
         }
     }
     flushes = __reduce_add_sync(full, flushes);
