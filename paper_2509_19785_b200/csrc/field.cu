@@ -460,14 +460,38 @@ __device__ __forceinline__ void runs_flush(float4* __restrict__ wgrid, int b, in
     }
 }
 
+// the charges of one point on the 9 nodes of its box b
+__device__ __forceinline__ void runs_point(float4* __restrict__ wgrid, int b, int I, int N, float h_b, float ux,
+                                           float uy) {
+    const float dx[3] = {1.0f / 6.0f - ux, 0.5f - ux, 5.0f / 6.0f - ux};
+    const float dy[3] = {1.0f / 6.0f - uy, 0.5f - uy, 5.0f / 6.0f - uy};
+    const float Lx[3] = {4.5f * dx[1] * dx[2], -9.0f * dx[0] * dx[2], 4.5f * dx[0] * dx[1]};
+    const float Ly[3] = {4.5f * dy[1] * dy[2], -9.0f * dy[0] * dy[2], 4.5f * dy[0] * dy[1]};
+    const int bx = b % I, by = b / I;
+#pragma unroll
+    for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float w = Lx[a] * Ly[bb];
+            red_add_v4(&wgrid[(int64_t)(3 * by + bb) * N + 3 * bx + a], w, w * dx[a] * h_b, w * dy[bb] * h_b);
+        }
+}
+
+constexpr int kStrayCap = 2048;   // per CTA (16 B each)
+
 __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ Y, int64_t n, Geo* __restrict__ g,
                                                      const int* __restrict__ perm, float4* __restrict__ wgrid,
                                                      float2* __restrict__ tw) {
     __shared__ unsigned s_flush;
+    __shared__ int s_nstray;
+    __shared__ int4 s_stray[kStrayCap];    // (box, u_x, u_y) of points outside their lane's run
     if (g->smode != kSpreadRuns) return;
     const bool ordered = g->perm_n == n;
     write_twiddles(g, tw);
-    if (threadIdx.x == 0) s_flush = 0u;
+    if (threadIdx.x == 0) {
+        s_flush = 0u;
+        s_nstray = 0;
+    }
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0) g->spts = (unsigned long long)n;
     const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b, inv_h = g->inv_h;
@@ -496,15 +520,21 @@ __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ 
                 int b;
                 float ux, uy;
                 box_of(y[v], lo_x, lo_y, h_b, inv_h, I, b, ux, uy);
-                if (b != cur) {                // the run's box changed (rare on a fresh order)
-                    if (cur >= 0) {
-                        runs_flush(wgrid, cur, I, N, h_bf, acc);
-                        ++flushes;
-#pragma unroll
-                        for (int q = 0; q < 27; ++q) acc[q] = 0.f;
-                    }
-                    cur = b;
+                if (cur < 0) cur = b;          // the lane's run: the box of its first point
+                bool stray = b != cur;
+                if (stray) {
+                    // a point outside the run (it crossed a box boundary since
+                    // the sort, or the order moves on to the next box): kept for
+                    // the CTA's stray pass below, so the warp does not diverge
+                    // into a flush here
+                    ++flushes;
+                    const int slot = atomicAdd(&s_nstray, 1);
+                    if (slot < kStrayCap) s_stray[slot] = make_int4(b, __float_as_int(ux), __float_as_int(uy), 0);
+                    else runs_point(wgrid, b, I, N, h_bf, ux, uy);
+                    ux = 0.5f;                 // contributes nothing to the run below
+                    uy = 0.5f;
                 }
+                const float keep = stray ? 0.f : 1.f;
                 // offsets to the 3 nodes per axis, Lagrange weights from them
                 const float dx0 = 1.0f / 6.0f - ux, dx1 = 0.5f - ux, dx2 = 5.0f / 6.0f - ux;
                 const float dy0 = 1.0f / 6.0f - uy, dy1 = 0.5f - uy, dy2 = 5.0f / 6.0f - uy;
@@ -515,7 +545,7 @@ __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ 
                 for (int bb = 0; bb < 3; ++bb)
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
-                        const float w = Lx[a] * Ly[bb];
+                        const float w = Lx[a] * (Ly[bb] * keep);
                         const int q = 3 * (3 * bb + a);
                         acc[q] += w;
                         acc[q + 1] = fmaf(w, dx[a], acc[q + 1]);
@@ -569,6 +599,12 @@ __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ 
     flushes = __reduce_add_sync(full, flushes);
     if (lane == 0 && flushes) atomicAdd(&s_flush, flushes);
     __syncthreads();
+    // the strays, one per thread
+    const int ns = min(s_nstray, kStrayCap);
+    for (int t = threadIdx.x; t < ns; t += blockDim.x) {
+        const int4 e = s_stray[t];
+        runs_point(wgrid, e.x, I, N, h_bf, __int_as_float(e.y), __int_as_float(e.z));
+    }
     if (threadIdx.x == 0 && s_flush) atomicAdd(&g->sflush, (unsigned long long)s_flush);
 }
 
