@@ -15,10 +15,13 @@ namespace tsnet {
 // |r| <= I <= 1024, so the box (its floor) is the quotient's unless r lies
 // within kBoxGuard of an integer -- then the quotient itself decides.
 constexpr double kBoxGuard = 1e-10;
+// out of line, so that the (rarely taken) exact division is a branch and not
+// computed for every point and selected
+static __device__ __noinline__ double box_coord_exact(double d, double h_b) { return d / h_b; }
 __device__ __forceinline__ double box_coord(double d, double h_b, double inv_h) {
     double r = d * inv_h;
     const double f = floor(r);
-    if (r - f < kBoxGuard || f + 1.0 - r < kBoxGuard) r = d / h_b;
+    if (r - f < kBoxGuard || f + 1.0 - r < kBoxGuard) r = box_coord_exact(d, h_b);
     return r;
 }
 __device__ __forceinline__ void box_of(float2 y, double lo_x, double lo_y, double h_b, double inv_h, int I, int& b,
