@@ -115,12 +115,14 @@ typedef struct {
                                 (up to fp32 rounding order):
                                 TSNET_SPREAD_AUTO (0): decided on the device every iteration
                                   (below);
-                                TSNET_SPREAD_SORT (1): counting sort of the points by box, then a
-                                  warp per box chunk; it also records the box order of the
-                                  points in the workspace;
-                                TSNET_SPREAD_RUNS (2): one pass over the points in the last
-                                  recorded box order (index order when none is recorded for
-                                  this n), summed in registers while the box stays the same;
+                                TSNET_SPREAD_SORT (1): counting sort of the points by box (the
+                                  box order is recorded in the workspace), then one pass over
+                                  the points in that order, summed in registers while the box
+                                  stays the same;
+                                TSNET_SPREAD_RUNS (2): the same pass over the last recorded
+                                  box order, without the sort (index order when none is
+                                  recorded for this n); points that left their box since are
+                                  summed one by one;
                                 AUTO sorts on a fresh workspace, then runs over the recorded
                                 order until a run averages fewer than 16 points (the points
                                 moved across boxes since the sort), then sorts again.  Other

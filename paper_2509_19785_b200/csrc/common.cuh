@@ -51,7 +51,7 @@ struct Geo {
     double Z;                          // Z = zacc / M^2 - n
     int I, N, M, nrad;
     unsigned long long plan;           // FFT plan for length M: stage s radix = ((plan >> 2s) & 3) + 2
-    int nitems;                        // spread work items
+    int pad0;
     int nonfinite;
     unsigned int ticket;               // last-block-done counter of the bbox kernel
     unsigned bbox[4];                  // ~u(min x), ~u(min y), u(max x), u(max y); 0 = empty (field.cu)
@@ -84,12 +84,9 @@ struct Ws {
     float2* f_field;     // n (grad_parts only)
     int* box;            // n   box id of each point
     int* rank;           // n   rank of the point inside its box
-    float2* uv;          // n   in-box coordinates (u_x, u_y) in [0,1]
-    float2* sorted_uv;   // n   uv in box order
     int* perm;           // n   the points in box order (k_box_scatter), visited by k_spread_runs
     int* box_cnt;        // I_max^2 + 1
     int* box_start;      // I_max^2 + 1
-    int2* items;         // max_items (box, first point)
     float4* wgrid;       // N_max^2 spread charges (W1, Mx, My, 0), row-major [gy][gx]
     float2* tw;          // M_max twiddles exp(-2 pi i k / M)
     float2* spec;        // 10 * (M_max/2+1) * M_max : forward row spectra, [a][kx][y]
@@ -99,11 +96,10 @@ struct Ws {
     float2* ynext;       // n   : new positions of the fused SpMV + move (sliced-ELL plan)
     double* cost;        // scratch for tsnet_cost (4 doubles)
     int64_t n, nnz;
-    int I_max, N_max, M_max, max_items;
+    int I_max, N_max, M_max;
     size_t bytes;
 };
 
-constexpr int kSpreadChunk = 256;   // points per spread work item
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -115,7 +111,6 @@ inline Ws ws_map(void* base, int64_t n, int64_t nnz, int I_max) {
     w.I_max = I_max;
     w.N_max = 3 * I_max;
     w.M_max = 6 * I_max;
-    w.max_items = (int)((n + kSpreadChunk - 1) / kSpreadChunk + (int64_t)I_max * I_max + 1);
     const int64_t nb = (int64_t)I_max * I_max + 1;
     const int64_t half = w.M_max / 2 + 1;
     size_t off = 0;
@@ -129,12 +124,9 @@ inline Ws ws_map(void* base, int64_t n, int64_t nnz, int I_max) {
     w.f_field = (float2*)take(sizeof(float2) * n);
     w.box = (int*)take(sizeof(int) * n);
     w.rank = (int*)take(sizeof(int) * n);
-    w.uv = (float2*)take(sizeof(float2) * n);
-    w.sorted_uv = (float2*)take(sizeof(float2) * n);
     w.perm = (int*)take(sizeof(int) * n);
     w.box_cnt = (int*)take(sizeof(int) * nb);
     w.box_start = (int*)take(sizeof(int) * nb);
-    w.items = (int2*)take(sizeof(int2) * w.max_items);
     w.wgrid = (float4*)take(sizeof(float4) * (size_t)w.N_max * w.N_max);
     w.tw = (float2*)take(sizeof(float2) * w.M_max);
     w.spec = (float2*)take(sizeof(float2) * 10 * half * (size_t)w.M_max);

@@ -4,11 +4,12 @@
 //
 // Steps, all device-driven (no host round trip):
 //   a0 k_bbox                 bounding box -> grid geometry (I, h_b, N = 3I, M = 6I, FFT plan)
-//   a1 k_box_count/k_box_scan/k_box_scatter  counting sort of points by box (the count
-//                             also zeroes the charge grid and writes the twiddles of length M;
-//                             the scan zeroes the box counters for the next iteration)
-//   a2 k_spread               box-local charges W1 and local moments M_x, M_y (warp per
-//                             box chunk, register accumulation, 9 vector reds per warp)
+//   a1 k_box_count/k_box_scan/k_box_scatter  counting sort of the points by box into
+//                             the box order `perm` (the scan zeroes the box counters for
+//                             the next iteration); run only on the sort path
+//   a2 k_spread_runs          box-local charges W1 and local moments M_x, M_y over the
+//                             points in box order (register runs, 9 vector reds per run);
+//                             also writes the twiddles of length M
 //   a3/a4 k_row_fwd, k_col, k_row_inv   kernel tabulation + 2-D FFT convolution
 //                             (rows -> columns with products -> inverse rows)
 //   a5 Z by Parseval inside k_col (fp64 accumulation)
@@ -233,18 +234,16 @@ __device__ __forceinline__ void write_twiddles(const Geo* __restrict__ g, float2
 }
 
 // Sort path only (exits at once on the runs path).  The CTAs also write the
-// twiddles of length M; the box counters were zeroed by the previous
-// k_box_scan (or are zero in a fresh workspace).
+// box counters were zeroed by the previous k_box_scan (or are zero in a fresh
+// workspace).
 __global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__ Y, int64_t n, Geo* __restrict__ g,
                                                    int* __restrict__ box_cnt, int* __restrict__ box,
-                                                   int* __restrict__ rank, float2* __restrict__ uv,
-                                                   float2* __restrict__ tw) {
+                                                   int* __restrict__ rank) {
     __shared__ int hist[kBoxSmem];
     if (g->smode != kSpreadSort) return;
     const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b, inv_h = g->inv_h;
     const int I = g->I;
     const int nb = I * I;
-    write_twiddles(g, tw);
     const bool local = nb <= kBoxSmem;
     const int64_t c0 = (int64_t)blockIdx.x * kBoxChunk + threadIdx.x;
     if (local) {
@@ -267,7 +266,6 @@ __global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__
         if (i < n) {
             float ux, uy;
             box_of(y[j], lo_x, lo_y, h_b, inv_h, I, bj[j], ux, uy);
-            uv[i] = make_float2(ux, uy);
             rj[j] = atomicAdd(&cnt[bj[j]], 1);
         }
     }
@@ -289,55 +287,40 @@ __global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__
     }
 }
 
-// a1: exclusive scan of box counts -> box_start, and the spread work list
-// (one item per kSpreadChunk points of a box).  Single CTA of 1024 threads.
+// a1: exclusive scan of box counts -> box_start.  Single CTA of 1024 threads.
 __global__ void __launch_bounds__(1024) k_box_scan(Geo* g, int* __restrict__ box_cnt, int* __restrict__ box_start,
-                                                   int2* __restrict__ items, int64_t n) {
+                                                   int64_t n) {
     if (g->smode != kSpreadSort) return;
     const int nb = g->I * g->I;
     const int T = blockDim.x;
     const int per = (nb + T - 1) / T;
     const int b0 = threadIdx.x * per, b1 = min(nb, b0 + per);
-    int cs = 0, is = 0;
-    for (int b = b0; b < b1; ++b) {
-        int c = box_cnt[b];
-        cs += c;
-        is += (c + kSpreadChunk - 1) / kSpreadChunk;
-    }
-    __shared__ int sc[1024], si[1024];
+    int cs = 0;
+    for (int b = b0; b < b1; ++b) cs += box_cnt[b];
+    __shared__ int sc[1024];
     sc[threadIdx.x] = cs;
-    si[threadIdx.x] = is;
     __syncthreads();
     for (int o = 1; o < T; o <<= 1) {            // Hillis-Steele inclusive scan
-        int a = threadIdx.x >= o ? sc[threadIdx.x - o] : 0;
-        int c = threadIdx.x >= o ? si[threadIdx.x - o] : 0;
+        const int a = threadIdx.x >= o ? sc[threadIdx.x - o] : 0;
         __syncthreads();
         sc[threadIdx.x] += a;
-        si[threadIdx.x] += c;
         __syncthreads();
     }
-    int run = sc[threadIdx.x] - cs, irun = si[threadIdx.x] - is;
-    int* item_start = reinterpret_cast<int*>(items);   // first spread item of each box
+    int run = sc[threadIdx.x] - cs;
     for (int b = b0; b < b1; ++b) {
         const int c = box_cnt[b];
         box_cnt[b] = 0;                                // zero for the next iteration's count
         box_start[b] = run;
-        item_start[b] = irun;
         run += c;
-        irun += (c + kSpreadChunk - 1) / kSpreadChunk;
     }
-    if (threadIdx.x == T - 1) {
-        box_start[nb] = (int)n;
-        item_start[nb] = si[T - 1];
-        g->nitems = si[T - 1];
-    }
+    if (threadIdx.x == T - 1) box_start[nb] = (int)n;
 }
 
-// 4 points per thread and iteration: their loads, then the box_start
-// gathers, then the stores, each in flight together
+// the box order of the points: perm[box_start[b] + rank] = i.  4 points per
+// thread and iteration: their loads, then the box_start gathers, then the
+// stores, each in flight together
 __global__ void __launch_bounds__(256) k_box_scatter(Geo* __restrict__ g, int64_t n, const int* __restrict__ box,
                                                      const int* __restrict__ rank, const int* __restrict__ box_start,
-                                                     const float2* __restrict__ uv, float2* __restrict__ sorted_uv,
                                                      int* __restrict__ perm) {
     constexpr int V = 4;
     if (g->smode != kSpreadSort) return;
@@ -345,22 +328,17 @@ __global__ void __launch_bounds__(256) k_box_scatter(Geo* __restrict__ g, int64_
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += V * stride) {
         int b[V], r[V], st[V];
-        float2 u[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const int64_t i = i0 + v * stride;
             b[v] = i < n ? box[i] : 0;
             r[v] = i < n ? rank[i] : 0;
-            u[v] = i < n ? uv[i] : make_float2(0.f, 0.f);
         }
 #pragma unroll
         for (int v = 0; v < V; ++v) st[v] = __ldg(box_start + b[v]);
 #pragma unroll
         for (int v = 0; v < V; ++v)
-            if (i0 + v * stride < n) {
-                sorted_uv[st[v] + r[v]] = u[v];
-                perm[st[v] + r[v]] = (int)(i0 + v * stride);
-            }
+            if (i0 + v * stride < n) perm[st[v] + r[v]] = (int)(i0 + v * stride);
     }
 }
 
@@ -369,76 +347,16 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float
                  : "memory");
 }
 
-// a2: spread.  One warp per item = up to kSpreadChunk points of one box.
-//   W1[g]  = sum_i L_g(X_i)
-//   M_x[g] = sum_i L_g(X_i) (t_gx - x_i) = h_b sum_i L_g (s_a - u_x)   (local moments)
-__global__ void __launch_bounds__(256) k_spread(const Geo* __restrict__ g, const int2* __restrict__ items,
-                                                const int* __restrict__ box_start,
-                                                const float2* __restrict__ sorted_uv, float4* __restrict__ wgrid) {
-    if (g->smode != kSpreadSort) return;
-    const int nitems = g->nitems, I = g->I, N = g->N;
-    const float h_b = (float)g->h_b;
-    const float s[3] = {1.0f / 6.0f, 0.5f, 5.0f / 6.0f};
-    const int lane = threadIdx.x & 31;
-    const int wpb = blockDim.x >> 5;
-    const int* item_start = reinterpret_cast<const int*>(items);
-    const int nb = I * I;
-    for (int it = blockIdx.x * wpb + (threadIdx.x >> 5); it < nitems; it += gridDim.x * wpb) {
-        // box of this item: largest b with item_start[b] <= it (32-ary warp search)
-        int lo = 0, hi = nb;
-        while (hi - lo > 1) {
-            const int step = (hi - lo + 31) / 32;
-            const int p = lo + lane * step;
-            const unsigned m = __ballot_sync(0xffffffffu, p < hi && item_start[p] <= it);
-            lo += (31 - __clz(m)) * step;
-            hi = min(lo + step, hi);
-        }
-        const int b = lo;
-        const int2 item = make_int2(b, box_start[b] + (it - item_start[b]) * kSpreadChunk);
-        const int end = min(item.y + kSpreadChunk, box_start[b + 1]);
-        float acc[27];
-#pragma unroll
-        for (int q = 0; q < 27; ++q) acc[q] = 0.f;
-        for (int p = item.y + lane; p < end; p += 32) {
-            const float2 u = sorted_uv[p];
-            float Lx[3], Ly[3];
-            lagrange3(u.x, Lx);
-            lagrange3(u.y, Ly);
-#pragma unroll
-            for (int bb = 0; bb < 3; ++bb)
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    const float w = Lx[a] * Ly[bb];
-                    const int q = 3 * (3 * bb + a);
-                    acc[q] += w;
-                    acc[q + 1] += w * (s[a] - u.x);
-                    acc[q + 2] += w * (s[bb] - u.y);
-                }
-        }
-#pragma unroll
-        for (int q = 0; q < 27; ++q)
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
-        if (lane < 9) {
-            float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-#pragma unroll
-            for (int q = 0; q < 9; ++q)
-                if (q == lane) { a0 = acc[3 * q]; a1 = acc[3 * q + 1]; a2 = acc[3 * q + 2]; }
-            const int bx = b % I, by = b / I;
-            const int gx = 3 * bx + lane % 3, gy = 3 * by + lane / 3;
-            red_add_v4(&wgrid[(int64_t)gy * N + gx], a0, a1 * h_b, a2 * h_b);
-        }
-    }
-}
-
 // a1 + a2 in one pass over the points in the box order the last sort recorded
 // (perm; the index order when there is none): the points have moved little
-// since, so most consecutive points of that order still share a box.  Runs
-// path only (exits at once on the sort path); any order gives the same sums,
-// the order only decides how often a run breaks.
+// since, so most consecutive points of that order still share a box.  Any
+// order gives the same sums; the order only decides how often a run breaks.
+// Every iteration: on the sort path right after the sort (a fresh order: a run
+// only ends where the box does), on the runs path over an order a few
+// iterations old.
 // A warp takes chunks of 32 kRunPts consecutive positions of the order, lane l
 // the kRunPts positions from l kRunPts on.  A lane sums the charges of its points in 27
-// registers (9 nodes x (W1, M_x, M_y), as k_spread) while the box stays the
+// registers (9 nodes x (W1, M_x, M_y)) while the box stays the
 // same, and adds them to the grid (9 red.global.add.v4) when the box changes;
 // at the end of the chunk the lanes' last runs are summed across lanes by a
 // segmented warp scan keyed on the box (a run continuing into the next lane's
@@ -485,7 +403,6 @@ __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ 
     __shared__ unsigned s_flush;
     __shared__ int s_nstray;
     __shared__ int4 s_stray[kStrayCap];    // (box, u_x, u_y) of points outside their lane's run
-    if (g->smode != kSpreadRuns) return;
     const bool ordered = g->perm_n == n;
     write_twiddles(g, tw);
     if (threadIdx.x == 0) {
@@ -504,12 +421,19 @@ __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ 
     for (int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); c * (32 * kRunPts) < n;
          c += warps) {
         const int64_t base = c * (32 * kRunPts) + (int64_t)lane * kRunPts;
+        // all kRunPts order entries, then all kRunPts gathers, in flight together
+        // (branch-free: positions past n read the last point and are masked below)
+        int64_t idx[kRunPts];
+        if (ordered) {
+#pragma unroll
+            for (int v = 0; v < kRunPts; ++v) idx[v] = __ldg(perm + min(base + v, n - 1));
+        } else {
+#pragma unroll
+            for (int v = 0; v < kRunPts; ++v) idx[v] = min(base + v, n - 1);
+        }
         float2 y[kRunPts];
 #pragma unroll
-        for (int v = 0; v < kRunPts; ++v) {
-            const int64_t k = base + v;
-            y[v] = k < n ? __ldg(Y + (ordered ? (int64_t)__ldg(perm + k) : k)) : make_float2(0.f, 0.f);
-        }
+        for (int v = 0; v < kRunPts; ++v) y[v] = __ldg(Y + idx[v]);
         float acc[27];
 #pragma unroll
         for (int q = 0; q < 27; ++q) acc[q] = 0.f;
@@ -987,16 +911,16 @@ cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, b
     if (zero_all && (e = cudaMemsetAsync(w.wgrid, 0, sizeof(float4) * (size_t)w.N_max * w.N_max, s)) != cudaSuccess)
         return e;
     const float2* Yl = a.Y + a.rb;
-    // both paths are launched (the path is only known on the device, and the
-    // iteration is one CUDA graph); the kernels of the other path exit at once
+    // the sort's kernels are launched every iteration (the path is only known
+    // on the device, and the iteration is one CUDA graph) and exit at once on
+    // the runs path
+    const int cb = (int)std::max<int64_t>(kNumSMs, (nl + kBoxChunk - 1) / kBoxChunk);
+    k_box_count<<<cb, 256, 0, s>>>(Yl, nl, w.geo, w.box_cnt, w.box, w.rank);
+    k_box_scan<<<1, 1024, 0, s>>>(w.geo, w.box_cnt, w.box_start, nl);
+    k_box_scatter<<<pbl, 256, 0, s>>>(w.geo, nl, w.box, w.rank, w.box_start, w.perm);
     const int rbk = (int)std::max<int64_t>(1, std::min<int64_t>((nl + 8 * 32 * kRunPts - 1) / (8 * 32 * kRunPts),
                                                                   (int64_t)kNumSMs * 2));
     k_spread_runs<<<rbk, 256, 0, s>>>(Yl, nl, w.geo, w.perm, w.wgrid, w.tw);
-    const int cb = (int)std::max<int64_t>(kNumSMs, (nl + kBoxChunk - 1) / kBoxChunk);
-    k_box_count<<<cb, 256, 0, s>>>(Yl, nl, w.geo, w.box_cnt, w.box, w.rank, w.uv, w.tw);
-    k_box_scan<<<1, 1024, 0, s>>>(w.geo, w.box_cnt, w.box_start, w.items, nl);
-    k_box_scatter<<<pbl, 256, 0, s>>>(w.geo, nl, w.box, w.rank, w.box_start, w.uv, w.sorted_uv, w.perm);
-    k_spread<<<kNumSMs * 8, 256, 0, s>>>(w.geo, w.items, w.box_start, w.sorted_uv, w.wgrid);
     return cudaGetLastError();
 }
 

@@ -450,12 +450,12 @@ cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel
                                           (int)(sizeof(float4) * kGridSmemCells));
     if (ea != cudaSuccess) return ea;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nl + kUpdateThreads - 1) / kUpdateThreads, kNumSMs));
-    update_kernel<<<blocks, kUpdateThreads, smem, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, Y + a.rb, Y + a.rb, w.f_attr,
+    update_kernel<<<blocks, kUpdateThreads, smem, s>>>(nl, w.geo, w.fgrid, w.box, nullptr, Y + a.rb, Y + a.rb, w.f_attr,
                                                   vel + a.rb, gains + a.rb, a.lambda_kl, cn_of(a), sp, cap, push,
                                                   a.rb);
     const int blocks_g =
         (int)std::max<int64_t>(1, std::min<int64_t>((nl + 2 * kUpdateThreadsG - 1) / (2 * kUpdateThreadsG), kNumSMs * 8));
-    update_kernel_g<<<blocks_g, kUpdateThreadsG, 0, s>>>(nl, w.geo, w.fgrid, w.box, w.uv, Y + a.rb, Y + a.rb, w.f_attr,
+    update_kernel_g<<<blocks_g, kUpdateThreadsG, 0, s>>>(nl, w.geo, w.fgrid, w.box, nullptr, Y + a.rb, Y + a.rb, w.f_attr,
                                                          vel + a.rb, gains + a.rb, a.lambda_kl, cn_of(a), sp, cap,
                                                          push, a.rb);
     cudaError_t e = cudaGetLastError();
@@ -487,7 +487,7 @@ cudaError_t launch_update_rows(const Ws& w, const GradArgs& a, int64_t r0, int64
     // CTA would wait for an idle SM); the field nodes are read through L1/L2
     const int blocks =
         (int)std::max<int64_t>(1, std::min<int64_t>((nc + 2 * kUpdateThreadsG - 1) / (2 * kUpdateThreadsG), kNumSMs * 8));
-    update_kernel_g<<<blocks, kUpdateThreadsG, 0, s>>>(nc, w.geo, w.fgrid, w.box + q, w.uv + q, a.Y + r0, Yout + r0,
+    update_kernel_g<<<blocks, kUpdateThreadsG, 0, s>>>(nc, w.geo, w.fgrid, w.box + q, nullptr, a.Y + r0, Yout + r0,
                                                w.f_attr + q, vel + r0, gains + r0, a.lambda_kl, cn_of(a), sp, 0,
                                                PeerPush{}, 0);
     return cudaGetLastError();

@@ -17,6 +17,6 @@ for st in 600 900; do
     timeout 300 python scripts/step_variant_probe.py 4 $st product 50 graph $sp >> gpurun_out/${T}_variants.log 2>&1
   done
 done
-timeout 600 python -m pytest tests/test_gpu_parity.py -q --timeout 900 -p no:cacheprovider -k "spread" > gpurun_out/${T}_pytest.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -q --timeout 900 -p no:cacheprovider -k "spread or bench_states or ragged or edge or synthetic or trajectory" > gpurun_out/${T}_pytest.log 2>&1
 echo "pytest exit $?" >> gpurun_out/${T}_pytest.log
 echo done
