@@ -397,7 +397,7 @@ __device__ __forceinline__ void runs_point(float4* __restrict__ wgrid, int b, in
 
 constexpr int kStrayCap = 2048;   // per CTA (16 B each)
 
-__global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ Y, int64_t n, Geo* __restrict__ g,
+__global__ void __launch_bounds__(256, 3) k_spread_runs(const float2* __restrict__ Y, int64_t n, Geo* __restrict__ g,
                                                      const int* __restrict__ perm, float4* __restrict__ wgrid,
                                                      float2* __restrict__ tw) {
     __shared__ unsigned s_flush;
@@ -423,13 +423,13 @@ __global__ void __launch_bounds__(256) k_spread_runs(const float2* __restrict__ 
         const int64_t base = c * (32 * kRunPts) + (int64_t)lane * kRunPts;
         // all kRunPts order entries, then all kRunPts gathers, in flight together
         // (branch-free: positions past n read the last point and are masked below)
-        int64_t idx[kRunPts];
+        int idx[kRunPts];
         if (ordered) {
 #pragma unroll
             for (int v = 0; v < kRunPts; ++v) idx[v] = __ldg(perm + min(base + v, n - 1));
         } else {
 #pragma unroll
-            for (int v = 0; v < kRunPts; ++v) idx[v] = min(base + v, n - 1);
+            for (int v = 0; v < kRunPts; ++v) idx[v] = (int)min(base + v, n - 1);
         }
         float2 y[kRunPts];
 #pragma unroll
@@ -919,7 +919,7 @@ cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, b
     k_box_scan<<<1, 1024, 0, s>>>(w.geo, w.box_cnt, w.box_start, nl);
     k_box_scatter<<<pbl, 256, 0, s>>>(w.geo, nl, w.box, w.rank, w.box_start, w.perm);
     const int rbk = (int)std::max<int64_t>(1, std::min<int64_t>((nl + 8 * 32 * kRunPts - 1) / (8 * 32 * kRunPts),
-                                                                  (int64_t)kNumSMs * 2));
+                                                                  (int64_t)kNumSMs * 3));
     k_spread_runs<<<rbk, 256, 0, s>>>(Yl, nl, w.geo, w.perm, w.wgrid, w.tw);
     return cudaGetLastError();
 }

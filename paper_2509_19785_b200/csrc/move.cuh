@@ -18,21 +18,27 @@ constexpr double kBoxGuard = 1e-10;
 // out of line, so that the (rarely taken) exact division is a branch and not
 // computed for every point and selected
 static __device__ __noinline__ double box_coord_exact(double d, double h_b) { return d / h_b; }
-__device__ __forceinline__ double box_coord(double d, double h_b, double inv_h) {
+// one axis: the interval b in [0, I) and the coordinate u in it
+__device__ __forceinline__ void box_axis(float y, double lo, double h_b, double inv_h, int I, int& b, float& u) {
+    const double d = (double)y - lo;          // exact: both are fp32 values
     double r = d * inv_h;
-    const double f = floor(r);
-    if (r - f < kBoxGuard || f + 1.0 - r < kBoxGuard) r = box_coord_exact(d, h_b);
-    return r;
+    double f = floor(r);
+    double t = r - f;
+    if (fabs(t - 0.5) > 0.5 - kBoxGuard) {    // within kBoxGuard of a boundary: the quotient decides
+        r = box_coord_exact(d, h_b);
+        f = floor(r);
+        t = r - f;
+    }
+    const int bi = (int)f;
+    b = min(max(bi, 0), I - 1);
+    u = (float)t;
+    if (b != bi) u = (float)(r - (double)b);  // clamped (a point on the far edge)
 }
 __device__ __forceinline__ void box_of(float2 y, double lo_x, double lo_y, double h_b, double inv_h, int I, int& b,
                                        float& ux, float& uy) {
-    double rx = box_coord((double)y.x - lo_x, h_b, inv_h);
-    double ry = box_coord((double)y.y - lo_y, h_b, inv_h);
-    double fx = floor(rx), fy = floor(ry);
-    int bx = (int)fmin(fmax(fx, 0.0), (double)(I - 1));
-    int by = (int)fmin(fmax(fy, 0.0), (double)(I - 1));
-    ux = (float)(rx - (double)bx);
-    uy = (float)(ry - (double)by);
+    int bx, by;
+    box_axis(y.x, lo_x, h_b, inv_h, I, bx, ux);
+    box_axis(y.y, lo_y, h_b, inv_h, I, by, uy);
     b = by * I + bx;
 }
 
