@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) k_bbox(const float2* __restrict__ Y, int6
     float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
     bool bad = false;
     // kBBoxPts points per thread and sweep, their loads in flight together (a
-    // grid of ~2 CTAs per SM: few blocks, so few same-address atomics below)
+    // grid of 4 CTAs per SM: 4 same-address atomics per CTA below)
     const int64_t sweep = (int64_t)gridDim.x * blockDim.x * kBBoxPts;
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x * kBBoxPts + threadIdx.x; i0 < n; i0 += sweep) {
         float2 y[kBBoxPts];
@@ -905,7 +905,7 @@ cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, b
     if ((e = field_set_attrs(w.M_max)) != cudaSuccess) return e;
     const int64_t n = a.n, nl = a.re - a.rb;
     const int pb = (int)std::max<int64_t>(1, std::min<int64_t>((n + 256 * kBBoxPts - 1) / (256 * kBBoxPts),
-                                                                  (int64_t)kNumSMs * 2));
+                                                                  (int64_t)kNumSMs * 4));
     const int pbl = (int)std::max<int64_t>(1, std::min<int64_t>((nl + 255) / 256, (int64_t)kNumSMs * 8));
     k_bbox<<<pb, 256, 0, s>>>(a.Y, n, w.geo, a.h_max, a.I_min, a.I_max, w.wgrid, a.spread);
     if (zero_all && (e = cudaMemsetAsync(w.wgrid, 0, sizeof(float4) * (size_t)w.N_max * w.N_max, s)) != cudaSuccess)
