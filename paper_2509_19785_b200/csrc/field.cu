@@ -568,9 +568,16 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_row_fwd(const Geo* __restric
     const int half_max = M_max / 2 + 1;
     const double dlt = gp->delta;
     for (int k = threadIdx.x; k < M; k += blockDim.x) tw[k] = twg[k];
-    for (int y = blockIdx.x; y < M; y += gridDim.x) {
-        const int dy = (y <= M / 2) ? y : y - M;
-        const bool ky = (dy < N) && (-dy < N);       // |dy| <= N - 1
+    // Rows y < N only (M = 2N): the charges are zero in rows y >= N, and the
+    // kernel tables there are those of row M - y mirrored in dy -- even (K1,
+    // K2, K_e, D_x K2, D_x K_e: the same row spectrum) or odd (D_y K2, D_y K_e:
+    // negated) -- so the spectra of rows N+1 .. M-1 are written from rows
+    // M-y without their FFTs; row N (|dy| = N) is zero.
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < 10 * half; t += gridDim.x * blockDim.x)
+        spec[((int64_t)(t / half) * half_max + t % half) * M_max + N] = make_float2(0.f, 0.f);
+    for (int y = blockIdx.x; y < N; y += gridDim.x) {
+        const int dy = y;
+        const bool ky = true;                        // |dy| <= N - 1
         for (int p0 = 0; p0 < 5; p0 += B) {
             const int nb = min(B, 5 - p0);
             for (int x = threadIdx.x; x < M; x += blockDim.x) {
@@ -602,6 +609,14 @@ __global__ void __launch_bounds__(kRowThreads, 1) k_row_fwd(const Geo* __restric
                 const float2 Bv = mul_mi(D);
                 spec[((int64_t)(2 * p) * half_max + k) * M_max + y] = A;
                 spec[((int64_t)(2 * p + 1) * half_max + k) * M_max + y] = Bv;
+                if (y > 0) {
+                    // row M - y: arrays 0-2 (charges) zero, 3-7 even, 8-9 odd in dy
+                    const int a0 = 2 * p, a1 = 2 * p + 1;
+                    const float s0 = a0 <= 2 ? 0.f : (a0 >= 8 ? -1.f : 1.f);
+                    const float s1 = a1 <= 2 ? 0.f : (a1 >= 8 ? -1.f : 1.f);
+                    spec[((int64_t)a0 * half_max + k) * M_max + (M - y)] = make_float2(s0 * A.x, s0 * A.y);
+                    spec[((int64_t)a1 * half_max + k) * M_max + (M - y)] = make_float2(s1 * Bv.x, s1 * Bv.y);
+                }
             }
             __syncthreads();
         }
