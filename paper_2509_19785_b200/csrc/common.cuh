@@ -63,7 +63,7 @@ struct Geo {
     int smode;
     int sruns;                         // consecutive runs-path iterations so far
     int sskip;                         // sorts still to do before the runs path is tried again
-    int pad;
+    int sfail;                         // consecutive failed first runs (the backoff doubles)
     long long perm_n;                  // points of the recorded box order (0: none)
     unsigned long long spts;           // runs path: points spread by the last iteration
     unsigned long long sflush;         // runs path: box flushes of the last iteration

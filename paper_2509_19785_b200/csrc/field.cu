@@ -54,7 +54,7 @@ constexpr int kBBoxPts = 8;
 #define RUNS_RESORT 16
 #endif
 constexpr int kRunsResort = RUNS_RESORT;   // adaptive spread: re-sort when flushes * this > points
-constexpr int kRunsBackoff = 8;            // sorts before retrying the runs after a failed first run
+constexpr int kRunsBackoff = 8;            // sorts before retrying the runs after a failed first run (doubling)
 //
 // The CTAs also zero the charge grid cells the previous iteration used
 // ([0, N_prev^2), N_prev read before the last block sets the new geometry;
@@ -153,8 +153,14 @@ __global__ void __launch_bounds__(256) k_bbox(const float2* __restrict__ Y, int6
         } else if (g->smode == kSpreadRuns) {   // re-sort once a run averages < kRunsResort points
             mode = g->sflush * (unsigned long long)kRunsResort > g->spts ? kSpreadSort : kSpreadRuns;
             // the order was already too stale one iteration after a sort (the
-            // layout moves fast): sort for the next kRunsBackoff iterations
-            if (mode == kSpreadSort && g->sruns <= 1) g->sskip = kRunsBackoff;
+            // layout moves fast): sort for the next kRunsBackoff iterations,
+            // twice as many after each further failed first run (up to 8x)
+            if (mode == kSpreadSort && g->sruns <= 1) {
+                g->sfail = min(g->sfail + 1, 4);
+                g->sskip = kRunsBackoff << (g->sfail - 1);
+            } else if (mode == kSpreadRuns) {
+                g->sfail = 0;
+            }
         } else if (g->sskip > 0) {
             --g->sskip;
             mode = kSpreadSort;

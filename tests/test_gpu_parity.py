@@ -807,13 +807,14 @@ def test_spread_bad_request():
 def test_spread_auto_backoff():
     """When the first run after a sort already breaks (the layout moves faster
     than the recorded order can follow), TSNET_SPREAD_AUTO sorts for the next
-    8 iterations before it tries the runs again."""
+    8 iterations before it tries the runs again, 16 after a second failure."""
     n = 100_000
     P = dict(indptr=np.zeros(n + 1, np.int64), indices=np.zeros(0, np.int32), values=np.zeros(0))
     Pd = dev_P(P)
     ws = alloc_workspace(n, Pd.nnz, GradParams())
     modes = []
-    for seed in range(12):      # a new random layout every call: every run breaks
+    for seed in range(30):      # a new random layout every call: every run breaks
         tsnet_grad(Pd, torch.from_numpy(uniform_layout(n, 4.99, 10 + seed)).cuda(), GradParams(*STAGE_B), ws)
         modes.append(tsnet_read_stats(ws)["spread"])
-    assert modes == [1, 2] + [1] * 9 + [2], modes
+    # sort, a failed run, 1 + 8 sorts, a failed run, 1 + 16 sorts, a run
+    assert modes == [1, 2] + [1] * 9 + [2] + [1] * 17 + [2], modes
