@@ -818,3 +818,24 @@ def test_spread_auto_backoff():
         modes.append(tsnet_read_stats(ws)["spread"])
     # sort, a failed run, 1 + 8 sorts, a failed run, 1 + 16 sorts, a run
     assert modes == [1, 2] + [1] * 9 + [2] + [1] * 17 + [2], modes
+
+
+def test_spread_runs_stray_overflow():
+    """The run pass over a stale order where nearly every point is a stray
+    (the order of another layout): more strays per CTA than its shared list
+    holds (2048), so the overflow is summed inline.  Same field and Z as the
+    sort path on the same layout (both checked against the oracle above)."""
+    n = 1_500_000
+    P = dict(indptr=np.zeros(n + 1, np.int64), indices=np.zeros(0, np.int32), values=np.zeros(0))
+    Pd = dev_P(P)
+    ws = alloc_workspace(n, Pd.nnz, GradParams())
+    A = torch.from_numpy(uniform_layout(n, 4.99, 21)).cuda()
+    B = torch.from_numpy(uniform_layout(n, 4.99, 22)).cuda()
+    tsnet_grad(Pd, A, GradParams(*STAGE_B, spread=1), ws)                  # records A's box order
+    g_runs, Z_runs = tsnet_grad(Pd, B, GradParams(*STAGE_B, spread=2), ws)
+    st = tsnet_read_stats(ws)
+    assert st["spread"] == 2 and st["spread_flushes"] > n // 2, st         # nearly all points strays
+    g_sort, Z_sort = tsnet_grad(Pd, B, GradParams(*STAGE_B, spread=1), alloc_workspace(n, Pd.nnz, GradParams()))
+    torch.cuda.synchronize()
+    assert abs(float(Z_runs.item()) - float(Z_sort.item())) <= 1e-6 * float(Z_sort.item())
+    assert relL2(g_runs.cpu().numpy(), g_sort.cpu().numpy()) <= 1e-5
