@@ -418,13 +418,33 @@ def test_grad_parity_bench_states_config5():
             assert relL2(g[r0:r0 + B], go) <= GRAD_TOL, (it, r0, relL2(g[r0:r0 + B], go))
 
 
+def assert_gains_follow(Gd, Y, vel, gains, g_gpu, g_oracle, sp):
+    """The gains update (reading R12) is an integer-like decision, sign(g) vs
+    sign(v), taken on each side in its own precision.  Both sides take it here
+    from the GPU's fp32 gradient (g_gpu: the same kernels on the same state,
+    evaluated once more; the fp32 atomics make two evaluations differ by
+    round-off, so components within 1e-5 ||g||_inf of zero are left out): the
+    GPU's gains must equal the oracle's move (O6) applied to that gradient,
+    and wherever the fp32 and fp64 gradients agree in sign, the oracle's own
+    gains."""
+    _, _, Gg = oracle.update_step(Y, vel, gains, np.asarray(g_gpu, np.float64), eta=sp.eta, mu=sp.momentum)
+    Gd = Gd.cpu().numpy()
+    band = np.abs(g_gpu) <= 1e-5 * np.abs(g_gpu).max()
+    ok = np.isclose(Gd, Gg, rtol=1e-6, atol=0) | band
+    assert np.all(ok), int((~ok).sum())
+    _, _, Go = oracle.update_step(Y, vel, gains, g_oracle, eta=sp.eta, mu=sp.momentum)
+    agree = (np.sign(np.asarray(g_gpu, np.float64)) == np.sign(g_oracle)) & ~band
+    assert np.all(np.isclose(Gd, Go, rtol=1e-5)[agree])
+    return int((~agree).sum())
+
+
 def test_step_parity_teacher_forced_config2():
     """SURVEY §8(c) step parity: the GPU state (Y, vel, gains) of its own config-2
     run at iterations {0, 1, 5, 10, 250, 499}, one step on each side (GPU
     tsnet_step; oracle O5 gradient + O6 move, the O7 multipliers of that
     iteration); the state after the step <= 1e-4 relL2 (the move, vel), Y <=
-    1e-4 (at iteration 0 the move dwarfs the N(0, 1e-4^2) positions), gains equal
-    except where |g| < 1e-6 ||g||_inf (sign flips)."""
+    1e-4 (at iteration 0 the move dwarfs the N(0, 1e-4^2) positions); the gains
+    decision checked by assert_gains_follow."""
     from paper_2509_19785_b200 import Layout
     from paper_2509_19785_b200.runner import stage_params
     P = oracle_P(2)
@@ -441,15 +461,18 @@ def test_step_parity_teacher_forced_config2():
         gp, sp = stage_params(stage)
         lam = (gp.lambda_kl, gp.lambda_c, gp.lambda_r)
         Yd, Vd, Gd = (torch.from_numpy(a.copy()).cuda() for a in (Y, vel, gains))
-        tsnet_step(Pd, Yd, Vd, Gd, gp, sp, alloc_workspace(n, Pd.nnz, gp))
+        ws = alloc_workspace(n, Pd.nnz, gp)
+        g_gpu, _ = tsnet_grad(Pd, Yd, gp, ws)           # the gradient the step uses (same kernels)
+        g_gpu = g_gpu.cpu().numpy()
+        tsnet_step(Pd, Yd, Vd, Gd, gp, sp, ws)
         torch.cuda.synchronize()
         r = oracle_grad(P, Y, lam)
         Yo, Vo, Go = oracle.update_step(Y, vel, gains, r["g"], eta=sp.eta, mu=sp.momentum)
+        assert relL2(g_gpu, r["g"]) <= GRAD_TOL, (target, relL2(g_gpu, r["g"]))
         assert relL2(Vd.cpu().numpy(), Vo) <= GRAD_TOL, (target, relL2(Vd.cpu().numpy(), Vo))
         assert relL2(Yd.cpu().numpy(), Yo) <= GRAD_TOL, (target, relL2(Yd.cpu().numpy(), Yo))
-        small = np.abs(r["g"]) < 1e-6 * np.abs(r["g"]).max()
-        same = np.isclose(Gd.cpu().numpy(), Go, rtol=1e-5)
-        assert np.all(same[~small]), (target, int((~same[~small]).sum()))
+        flips = assert_gains_follow(Gd, Y, vel, gains, g_gpu, r["g"], sp)
+        assert flips <= 1e-3 * g_gpu.size, (target, flips)
 
 
 # ---------------------------------------------------------------- steps
@@ -465,6 +488,8 @@ def test_step_parity_common_state(stage):
     Pd = dev_P(P)
     ws = alloc_workspace(n, Pd.nnz, gp)
     Yd, Vd, Gd = (torch.from_numpy(a.copy()).cuda() for a in (Y, vel, gains))
+    g_gpu, _ = tsnet_grad(Pd, Yd, gp, ws)
+    g_gpu = g_gpu.cpu().numpy()
     tsnet_step(Pd, Yd, Vd, Gd, gp, sp, ws)
     torch.cuda.synchronize()
     r = oracle_grad(P, Y, lam)
@@ -472,8 +497,7 @@ def test_step_parity_common_state(stage):
     assert relL2(Vd.cpu().numpy(), Vo) <= GRAD_TOL
     # positions: Y + v rounded to fp32 on the GPU; the move itself is checked via vel
     assert relL2(Yd.cpu().numpy(), Yo) <= 1e-6
-    small = np.abs(r["g"]) < 1e-6 * np.abs(r["g"]).max()
-    assert np.array_equal(np.isclose(Gd.cpu().numpy(), Go, rtol=1e-5)[~small], np.ones((~small).sum(), bool))
+    assert assert_gains_follow(Gd, Y, vel, gains, g_gpu, r["g"], sp) <= 1e-3 * g_gpu.size
 
 
 @pytest.mark.parametrize("cfg,recenter", [(3, 0), (3, 1), (2, 0)])
