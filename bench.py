@@ -34,8 +34,9 @@ import numpy as np  # noqa: E402
 
 METRIC = "tsNET gradient iterations/sec at n=1M (1/2/4/8 B200); % of HBM roofline"
 UNIT = "iterations/s"
-KERNELS_PER_STEP = 11   # kernels tsnet_step launches: field.cu 8, attractive SpMV 1, the move 2 (the
-                        # shared-memory and the L1 variant; the one not matching the grid size exits at once)
+KERNELS_PER_STEP = 11   # kernels tsnet_step launches: field.cu 8 (bbox, the box sort's 3, which exit at
+                        # once on the runs path, the run pass, 3 FFT passes), attractive SpMV 1, the move 2
+                        # (the shared-memory and the L1 variant; the one not matching the grid size exits at once)
 CONFIG_DESC = {
     1: "cfg1 2-D grid 32x32 (n=1024), u=40",
     2: "cfg2 RGG n=20,000 mean degree 8 (LCC), u=40",
