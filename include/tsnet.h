@@ -155,7 +155,9 @@ typedef struct {
  *     (peer-memory all-reduce of the live cells, tsnet_comm_init),
  *   - convolve the reduced grid (replicated FFT), run the attractive SpMV and
  *     the gather/move for their own rows,
- *   - all-gather Y (equal padded slices, one ncclAllGather) -- tsnet_step only.
+ *   - exchange Y -- tsnet_step only: pushed by the move into every rank's copy
+ *     when Y is the communicator's layout buffer (tsnet_comm_layout), else
+ *     all-gathered (equal padded slices, one ncclAllGather).
  * comm   : communicator from tsnet_comm_init (NULL only for the phase calls
  *          tsnet_field_local / tsnet_step_finish, which do no communication).
  * bounds : [host] world + 1 row offsets, bounds[r] .. bounds[r+1] = rank r's rows
@@ -292,8 +294,12 @@ TSNET_API int tsnet_grad_parts(const tsnet_csr* P, const float* Y, const tsnet_g
  * One full iteration: gradient at Y (as tsnet_grad) followed by the
  * momentum/gains move ("Move each vertex v in the direction of
  * dC/dv"; reading R12), in place on Y, vel, gains (n x 2 fp32 each).
- * Sharded: rows [row_begin, row_end) of vel/gains are updated, and Y is
- * all-gathered over shard->comm before the call returns (stream order).
+ * Sharded: rows [row_begin, row_end) of vel/gains are updated, and every
+ * rank's new rows reach every rank's Y: on the communicator's layout buffer
+ * (tsnet_comm_layout) the move stores them into the peers' copies and the next
+ * tsnet_step waits until every peer's have landed (tsnet_comm_layout_sync
+ * before reading Y outside tsnet_step); on any other Y they are all-gathered
+ * over shard->comm before the call returns (stream order).
  */
 TSNET_API int tsnet_step(const tsnet_csr* P, float* Y, float* vel, float* gains, const tsnet_grad_params* gp,
                const tsnet_step_params* sp, const tsnet_shard* shard, void* ws, size_t ws_bytes,
@@ -519,7 +525,7 @@ TSNET_API int32_t tsnet_shard_rows(const int64_t* indptr_host, int64_t n, int32_
  * tsnet_step_finish : steps a3-a7 from the (summed) grid in ws: convolution, Z,
  *                     attractive SpMV and gather + move of the own rows of Y,
  *                     vel, gains (full n x 2 arrays).  No communication.
- * tsnet_step = field_local + all-reduce(grid) + step_finish + all-gather(Y). */
+ * tsnet_step = field_local + all-reduce(grid) + step_finish + exchange of Y. */
 TSNET_API int tsnet_field_local(const tsnet_csr* P, const float* Y, const tsnet_grad_params* gp,
                                 const tsnet_shard* shard, void* ws, size_t ws_bytes, tsnet_stream_t stream);
 TSNET_API int tsnet_ws_grid(int64_t n, int64_t nnz, const tsnet_grad_params* gp, size_t* offset_bytes,
