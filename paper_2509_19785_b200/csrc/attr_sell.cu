@@ -175,16 +175,10 @@ __global__ void __launch_bounds__(256, MINB) k_attr_sell_g(const uint8_t* __rest
 // L1 capacity from the Y_j gathers, which hit L1 on a mesh).
 static constexpr auto sell_kernel = k_attr_sell_g<4, 4, false, 4>;
 
-// probe builds only (scripts/tile_variants.sh): CTAs per SM of the launch
-// (0: all that fit)
-#ifndef TSNET_SELL_CTAS
-#define TSNET_SELL_CTAS 0
-#endif
-
 static int resident_of(const void* k) {
     int r = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k, 256, 0) != cudaSuccess || r < 1) r = 1;
-    return TSNET_SELL_CTAS > 0 ? std::min(r, TSNET_SELL_CTAS) : r;
+    return r;
 }
 
 // F: rows [row_begin, row_end) of the plan's shard (nl = row_end - row_begin)

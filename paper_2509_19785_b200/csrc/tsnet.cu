@@ -126,15 +126,6 @@ static size_t grid_floats(const Ws& w) { return (size_t)4 * w.N_max * w.N_max; }
 // run concurrently (fork/join by events, so the pattern is also captured into
 // a CUDA graph as two branches).
 constexpr int kHostChunksMax = 16;
-// probe builds only (scripts/tile_variants.sh SRC=tsnet): priority of the
-// device step's field stream (0: lowest, 1: highest) and whether the SpMV is
-// enqueued before the field chain
-#ifndef TSNET_FIELD_PRIO
-#define TSNET_FIELD_PRIO 0
-#endif
-#ifndef TSNET_SPMV_FIRST
-#define TSNET_SPMV_FIRST 0
-#endif
 
 struct SideStream {
     int dev = -1;
@@ -161,8 +152,7 @@ static cudaError_t side_stream(SideStream*& out) {
         int lo = 0, hi = 0;
         if ((e = cudaDeviceGetStreamPriorityRange(&lo, &hi)) != cudaSuccess) return e;
         if ((e = cudaStreamCreateWithPriority(&x.side, cudaStreamNonBlocking, hi)) != cudaSuccess) return e;
-        if ((e = cudaStreamCreateWithPriority(&x.field, cudaStreamNonBlocking, TSNET_FIELD_PRIO ? hi : lo)) != cudaSuccess)
-            return e;
+        if ((e = cudaStreamCreateWithPriority(&x.field, cudaStreamNonBlocking, lo)) != cudaSuccess) return e;
         if ((e = cudaStreamCreateWithFlags(&x.copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
         if ((e = cudaStreamCreateWithFlags(&x.d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
         if ((e = cudaEventCreateWithFlags(&x.zeroed, cudaEventDisableTiming)) != cudaSuccess) return e;
@@ -193,14 +183,13 @@ static int eval_gradient_parts(const Ws& w, const GradArgs& a, const tsnet_shard
     cudaStream_t fs = ss->field;
     TSNET_CUDA(cudaEventRecord(ss->fork, s));
     TSNET_CUDA(cudaStreamWaitEvent(fs, ss->fork, 0));
-    if (TSNET_SPMV_FIRST) TSNET_CUDA(launch_spmv(w, a, s));
     // the whole I_max-sized grid is zeroed only for the NCCL fallback, which
     // all-reduces it as one fixed-size buffer; the peer all-reduce moves the live cells
     TSNET_CUDA(launch_field_local(w, a, fs, multi && !tsnet_comm_peer_reduce(sh->comm)));
     if (multi && (st = comm_allreduce_grid(sh->comm, w.geo, w.wgrid, grid_floats(w), fs)) != TSNET_OK)
         return st;
     TSNET_CUDA(launch_field_conv(w, a, fs));
-    if (!TSNET_SPMV_FIRST) TSNET_CUDA(launch_spmv(w, a, s));
+    TSNET_CUDA(launch_spmv(w, a, s));
     TSNET_CUDA(cudaEventRecord(ss->join, fs));
     TSNET_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
     return TSNET_OK;
