@@ -403,7 +403,10 @@ __device__ __forceinline__ void runs_point(float4* __restrict__ wgrid, int b, in
 
 constexpr int kStrayCap = 2048;   // per CTA (16 B each)
 
-__global__ void __launch_bounds__(256, 3) k_spread_runs(const float2* __restrict__ Y, int64_t n, Geo* __restrict__ g,
+#ifndef RUNS_MINB
+#define RUNS_MINB 3
+#endif
+__global__ void __launch_bounds__(256, RUNS_MINB) k_spread_runs(const float2* __restrict__ Y, int64_t n, Geo* __restrict__ g,
                                                      const int* __restrict__ perm, float4* __restrict__ wgrid,
                                                      float2* __restrict__ tw) {
     __shared__ unsigned s_flush;
@@ -940,7 +943,7 @@ cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, b
     k_box_scan<<<1, 1024, 0, s>>>(w.geo, w.box_cnt, w.box_start, nl);
     k_box_scatter<<<pbl, 256, 0, s>>>(w.geo, nl, w.box, w.rank, w.box_start, w.perm);
     const int rbk = (int)std::max<int64_t>(1, std::min<int64_t>((nl + 8 * 32 * kRunPts - 1) / (8 * 32 * kRunPts),
-                                                                  (int64_t)kNumSMs * 3));
+                                                                  (int64_t)kNumSMs * RUNS_MINB));
     k_spread_runs<<<rbk, 256, 0, s>>>(Yl, nl, w.geo, w.perm, w.wgrid, w.tw);
     return cudaGetLastError();
 }
