@@ -54,7 +54,7 @@ constexpr int kRow = 16;        // bytes per row
 // Each issuer streams `per` gather4s of 4 hashed random rows.
 __global__ void __launch_bounds__(32 * kIssuers) k_tma_g4(const __grid_constant__ CUtensorMap tm, int rows, int per,
                                                           float* out) {
-    __shared__ __align__(128) uint8_t ring[kIssuers][kDepth][4 * kRow];
+    __shared__ __align__(128) uint8_t ring[kIssuers][kDepth][128];   // TMA destinations: 128-byte aligned
     __shared__ __align__(8) uint64_t bar[kIssuers][kDepth];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0)
