@@ -143,8 +143,7 @@ __global__ void k_x_reduce(const Geo* __restrict__ g, unsigned long long* const*
     const unsigned long long t = own_flags[1];
     if (threadIdx.x == 0) {
         for (int r = 0; r < world; ++r)
-            while (ld_acquire_sys(flags[r]) < t) {
-            }
+            wait_peer_counter(flags[r], t);
     }
     __syncthreads();
     float4* const* gr = grids + (t & 1) * world;
@@ -194,8 +193,7 @@ __global__ void k_y_enter(unsigned long long* const* __restrict__ flags, int wor
                           const unsigned long long* __restrict__ own) {
     const unsigned long long t = own[kFIter];
     for (int r = threadIdx.x; r < world; r += blockDim.x)
-        while (ld_acquire_sys(flags[r] + kFMoved) < t) {
-        }
+        wait_peer_counter(flags[r] + kFMoved, t);
 }
 
 // after the field chain and the SpMV of iteration t: this rank no longer reads Y(t)

@@ -187,6 +187,23 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Wait until *p >= v (a peer's counter, system scope).  A peer that never
+// arrives (its process died) would hang the device forever: after kPeerWaitNs
+// the kernel traps instead, so the host sees a CUDA error on its next call.
+constexpr unsigned long long kPeerWaitNs = 60ull * 1000000000ull;
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void wait_peer_counter(const unsigned long long* p, unsigned long long v) {
+    if (ld_acquire_sys(p) >= v) return;
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_sys(p) < v) {
+        __nanosleep(64);
+        if (global_ns() - t0 > kPeerWaitNs) __trap();
+    }
+}
 
 struct SellMoveArgs {
     Geo* geo;

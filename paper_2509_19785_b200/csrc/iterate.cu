@@ -315,8 +315,7 @@ __global__ void __launch_bounds__(SMEM ? kUpdateThreads : kUpdateThreadsG, SMEM 
         // finished reading Y for this iteration (its field + SpMV)
         iter = push.own[kFIter];
         if (threadIdx.x < push.world)
-            while (ld_acquire_sys(push.flags[threadIdx.x] + kFRead) < iter + 1) {
-            }
+            wait_peer_counter(push.flags[threadIdx.x] + kFRead, iter + 1);
         __syncthreads();
     }
     const float4* fg = fgrid;
