@@ -443,7 +443,10 @@ static constexpr auto update_kernel_g = k_update<2, true, false>;
 cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel, float2* gains,
                           const tsnet_step_params& sp, cudaStream_t s, const PeerPush& push) {
     const int64_t nl = a.re - a.rb;
-    const int cap = (int)std::min<int64_t>((int64_t)w.N_max * w.N_max, kGridSmemCells);
+#ifndef MOVE_SMEM_MAX_CELLS   // probe builds: the largest grid the move stages in shared memory
+#define MOVE_SMEM_MAX_CELLS kGridSmemCells
+#endif
+    const int cap = (int)std::min<int64_t>((int64_t)w.N_max * w.N_max, MOVE_SMEM_MAX_CELLS);
     const size_t smem = sizeof(float4) * (size_t)cap;
     cudaError_t ea = cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)(sizeof(float4) * kGridSmemCells));
