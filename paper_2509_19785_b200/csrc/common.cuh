@@ -91,7 +91,7 @@ struct Ws {
     float2* tw;          // M_max twiddles exp(-2 pi i k / M)
     float2* spec;        // 10 * (M_max/2+1) * M_max : forward row spectra, [a][kx][y]
     float2* colout;      // 6 * (M_max/2+1) * N_max  : after column pass, [b][kx][y]
-    float4* fgrid;       // N_max^2 fields (P0, Qx, Qy, 0), row-major [gy][gx]
+    float4* fgrid;       // I_max^2 box records of kBoxRec float4 (P0, R_x, R_y of the 9 nodes; move.cuh)
     float2* state;       // 4 n : host-facing step staging (Y, vel, gains, next Y)
     float2* ynext;       // n   : new positions of the fused SpMV + move (sliced-ELL plan)
     double* cost;        // scratch for tsnet_cost (4 doubles)

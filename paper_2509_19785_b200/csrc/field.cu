@@ -13,9 +13,9 @@
 //   a3/a4 k_row_fwd, k_col, k_row_inv   kernel tabulation + 2-D FFT convolution
 //                             (rows -> columns with products -> inverse rows)
 //   a5 Z by Parseval inside k_col (fp64 accumulation)
-// Output: fgrid = (P0, Qx, Qy) per node, box-major (node (gx, gy) at
-// ((gy / 3) I + gx / 3) 9 + (gy % 3) 3 + gx % 3: the 9 nodes a point gathers are
-// one 144-byte run), with the combined kernel
+// Output: fgrid = one 112-byte record per box, box-major (box (gx / 3, gy / 3)
+// at (gy / 3) I + gx / 3; node k = 3 (gy % 3) + gx % 3 holds P0, R_x = Qx - s_a h P0
+// and R_y = Qy - s_c h P0 at floats k, 9 + k, 18 + k: move.cuh), with the combined kernel
 //   C = alpha K2 + beta K_e,  alpha = -4 lambda_kl / Z,  beta = -lambda_r / n^2,
 //   P0 = C * W1,  Qx = (D_x C) * W1 + C * M_x,  Qy = (D_y C) * W1 + C * M_y,
 // so that for a point in box (bx, by) with in-box coordinates (u_x, u_y):
@@ -770,6 +770,7 @@ __global__ void __launch_bounds__(kInvThreads) k_row_inv(Geo* __restrict__ gp, c
     const float beta = (float)(-(double)lambda_r / ((double)n * (double)n));
     if (blockIdx.x == 0 && threadIdx.x == 0) gp->Z = Z;
     const float sc = (float)(1.0 / M2);
+    const float hb = (float)gp->h_b;
     for (int k = threadIdx.x; k < M; k += blockDim.x) tw[k] = twg[k];
     for (int y = blockIdx.x; y < N; y += gridDim.x) {
         for (int t0 = 0; t0 < 2; t0 += B) {               // transform 0: P0 + i Qx, 1: Qy
@@ -792,16 +793,23 @@ __global__ void __launch_bounds__(kInvThreads) k_row_inv(Geo* __restrict__ gp, c
             __syncthreads();
             fft_block(buf, scr, M, nb, M, plan, nrad, tw, true);
             for (int x = threadIdx.x; x < N; x += blockDim.x) {
-                // box-major: the 9 nodes of box (x / 3, y / 3) are contiguous (144 B per box)
-                float* f = reinterpret_cast<float*>(fgrid + ((int64_t)(y / 3) * I + x / 3) * 9 + (y % 3) * 3 + x % 3);
+                // box record (kBoxRec float4 = 112 B per box, box-major): node
+                // k = 3 (y % 3) + x % 3 of box (x / 3, y / 3) puts P0 at float k,
+                // R_x = Q_x - s_a h P0 at 9 + k and R_y = Q_y - s_c h P0 at 18 + k
+                float* f = reinterpret_cast<float*>(fgrid + ((int64_t)(y / 3) * I + x / 3) * kBoxRec);
+                const int k = (y % 3) * 3 + x % 3;
+                const float sh_x = node_s(x % 3) * hb, sh_y = node_s(y % 3) * hb;
                 for (int q = 0; q < nb; ++q) {
                     const float2 a = buf[q * M + x];
                     if (t0 + q == 0) {
-                        f[0] = a.x * sc;
-                        f[1] = a.y * sc;
+                        const float p0 = a.x * sc;
+                        f[k] = p0;
+                        f[9 + k] = fmaf(-sh_x, p0, a.y * sc);
                     } else {
-                        f[2] = a.x * sc;
-                        f[3] = 0.f;
+                        // P0: this pass's transform 0, else the value this thread stored in the first pass
+                        const float p0 = nb == 2 ? buf[x].x * sc : f[k];
+                        f[18 + k] = fmaf(-sh_y, p0, a.x * sc);
+                        if (k == 0) f[27] = 0.f;
                     }
                 }
             }

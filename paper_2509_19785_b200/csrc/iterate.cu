@@ -285,9 +285,9 @@ __global__ void __launch_bounds__(256) k_grad_out(int64_t n, const Geo* __restri
 
 // n = rows of this call (local; Y, vel, gains point at the first own row); cn = lambda_c / n_global.
 // SMEM: the field grid (N^2 float4) fits the launch's dynamic shared memory
-// (grid_cap cells) and each CTA stages it first -- the 9 node gathers per point
-// then cost no L2 requests; else (large grids, N > 113) the 144-byte box runs
-// of the box-major grid are read through L1 by a launch without shared memory
+// (grid_cap float4) and each CTA stages it first -- the 7 record loads per point
+// then cost no L2 requests; else (large grids, I > 42, N > 126) the 112-byte box
+// records are read through L1 by a launch without shared memory
 // (the whole L1 caches the grid).  Both variants are launched each iteration
 // (N is only known on the device); the one that does not apply exits at once.
 constexpr int kUpdateThreads = 1024;
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(SMEM ? kUpdateThreads : kUpdateThreadsG, SMEM 
                                                               int grid_cap, PeerPush push, int64_t row0) {
     extern __shared__ float4 fsm[];
     const Geo g = *gp;
-    const int cells = g.N * g.N;
+    const int cells = g.I * g.I * kBoxRec;     // float4 of the box records (move.cuh)
     if (SMEM != (cells <= grid_cap)) return;   // the other variant handles this grid size
     unsigned long long iter = 0;
     if (push.y) {
@@ -446,7 +446,7 @@ cudaError_t launch_update(const Ws& w, const GradArgs& a, float2* Y, float2* vel
 #ifndef MOVE_SMEM_MAX_CELLS   // probe builds: the largest grid the move stages in shared memory
 #define MOVE_SMEM_MAX_CELLS kGridSmemCells
 #endif
-    const int cap = (int)std::min<int64_t>((int64_t)w.N_max * w.N_max, MOVE_SMEM_MAX_CELLS);
+    const int cap = (int)std::min<int64_t>((int64_t)w.I_max * w.I_max * kBoxRec, MOVE_SMEM_MAX_CELLS);
     const size_t smem = sizeof(float4) * (size_t)cap;
     cudaError_t ea = cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)(sizeof(float4) * kGridSmemCells));

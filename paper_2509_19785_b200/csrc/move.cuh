@@ -49,34 +49,46 @@ __device__ __forceinline__ void lagrange3u(float u, float (&L)[3]) {
     L[2] = 4.5f * (u - s0) * (u - s1);
 }
 
-// f_field_i = sum_{a,b} L_a(u_x) L_b(u_y) [ (X_i - t_ab) P0 + Q ],  X_i - t_ab = (u - s) h_b
-// The field grid is box-major (field.cu, k_row_inv): the 9 nodes of box b
-// are fgrid[9 b .. 9 b + 8], node (a, bb) at 9 b + 3 bb + a.
+// f_field_i = sum_{a,c} L_a(u_x) L_c(u_y) [ (X_i - t_ac) P0 + Q ],  X_i - t_ac = (u - s) h_b,
+// evaluated as  u h_b sum w P0 + sum w R  with R_x = Q_x - s_a h_b P0,
+// R_y = Q_y - s_c h_b P0 per node (formed once per node by k_row_inv).
+// The field grid is one record of kBoxRec float4 per box, box-major
+// (field.cu, k_row_inv): node k = 3 c + a of box b has P0 at float k, R_x at
+// 9 + k, R_y at 18 + k of record b (27 floats + 1 pad: 7 vector loads per
+// point instead of 9 (P0, Q_x, Q_y, pad) nodes; random box gathers are
+// shared-memory wavefront bound in the move).
+constexpr int kBoxRec = 7;
+// the node offsets s_t = (t + 1/2) / 3 of an interval
+__device__ __forceinline__ float node_s(int t) { return t == 0 ? 1.0f / 6.0f : (t == 1 ? 0.5f : 5.0f / 6.0f); }
 template <bool GLOBAL = false>
 __device__ __forceinline__ float2 gather_field(const Geo& g, const float4* __restrict__ fgrid, int b, float2 u) {
     const float h_b = (float)g.h_b;
     float Lx[3], Ly[3];
     lagrange3u(u.x, Lx);
     lagrange3u(u.y, Ly);
-    const float s[3] = {1.0f / 6.0f, 0.5f, 5.0f / 6.0f};
-    const float4* box = fgrid + (int64_t)b * 9;   // generic loads: fgrid may be the shared-memory copy
-    float4 f[9];
+    const float4* box = fgrid + (int64_t)b * kBoxRec;   // generic loads: fgrid may be the shared-memory copy
+    float f[4 * kBoxRec];
 #pragma unroll
-    for (int q = 0; q < 9; ++q) f[q] = GLOBAL ? __ldg(box + q) : box[q];
-    float fx = 0.f, fy = 0.f;
+    for (int q = 0; q < kBoxRec; ++q) {
+        const float4 v = GLOBAL ? __ldg(box + q) : box[q];
+        f[4 * q] = v.x;
+        f[4 * q + 1] = v.y;
+        f[4 * q + 2] = v.z;
+        f[4 * q + 3] = v.w;
+    }
+    float sp = 0.f, sx = 0.f, sy = 0.f;
 #pragma unroll
-    for (int bb = 0; bb < 3; ++bb) {
-        const float ey = (u.y - s[bb]) * h_b;
+    for (int c = 0; c < 3; ++c) {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            const float4 v = f[3 * bb + a];
-            const float wgt = Lx[a] * Ly[bb];
-            const float ex = (u.x - s[a]) * h_b;
-            fx = fmaf(wgt, fmaf(ex, v.x, v.y), fx);
-            fy = fmaf(wgt, fmaf(ey, v.x, v.z), fy);
+            const int k = 3 * c + a;
+            const float wgt = Lx[a] * Ly[c];
+            sp = fmaf(wgt, f[k], sp);
+            sx = fmaf(wgt, f[9 + k], sx);
+            sy = fmaf(wgt, f[18 + k], sy);
         }
     }
-    return make_float2(fx, fy);
+    return make_float2(fmaf(u.x * h_b, sp, sx), fmaf(u.y * h_b, sp, sy));
 }
 
 __device__ __forceinline__ float sgnf(float x) { return (float)((x > 0.f) - (x < 0.f)); }
