@@ -406,6 +406,20 @@ constexpr int kStrayCap = 2048;   // per CTA (16 B each)
 #ifndef RUNS_MINB
 #define RUNS_MINB 3
 #endif
+#ifndef RUNS_PIPE         // probe builds: the next chunk's order entries / positions loaded under this chunk's work
+#define RUNS_PIPE 0
+#endif
+// the order entries (or indices) of a lane's kRunPts positions from base
+__device__ __forceinline__ void runs_idx(const int* __restrict__ perm, bool ordered, int64_t base, int64_t n,
+                                         int (&idx)[kRunPts]) {
+    if (ordered) {
+#pragma unroll
+        for (int v = 0; v < kRunPts; ++v) idx[v] = __ldg(perm + min(base + v, n - 1));
+    } else {
+#pragma unroll
+        for (int v = 0; v < kRunPts; ++v) idx[v] = (int)min(base + v, n - 1);
+    }
+}
 __global__ void __launch_bounds__(256, RUNS_MINB) k_spread_runs(const float2* __restrict__ Y, int64_t n, Geo* __restrict__ g,
                                                      const int* __restrict__ perm, float4* __restrict__ wgrid,
                                                      float2* __restrict__ tw) {
@@ -427,22 +441,34 @@ __global__ void __launch_bounds__(256, RUNS_MINB) k_spread_runs(const float2* __
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     unsigned flushes = 0u;
-    for (int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); c * (32 * kRunPts) < n;
-         c += warps) {
+    const int64_t cfirst = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+#if RUNS_PIPE
+    float2 y[kRunPts];
+    if (cfirst * (32 * kRunPts) < n) {
+        int idx[kRunPts];
+        runs_idx(perm, ordered, cfirst * (32 * kRunPts) + (int64_t)lane * kRunPts, n, idx);
+#pragma unroll
+        for (int v = 0; v < kRunPts; ++v) y[v] = __ldg(Y + idx[v]);
+    }
+#endif
+    for (int64_t c = cfirst; c * (32 * kRunPts) < n; c += warps) {
         const int64_t base = c * (32 * kRunPts) + (int64_t)lane * kRunPts;
+#if RUNS_PIPE
+        // the next chunk's order entries now (they land under this chunk's
+        // accumulation), its positions after the accumulation (under the reduction)
+        const int64_t c1 = c + warps;
+        const bool more = c1 * (32 * kRunPts) < n;
+        int idx1[kRunPts];
+        if (more) runs_idx(perm, ordered, c1 * (32 * kRunPts) + (int64_t)lane * kRunPts, n, idx1);
+#else
         // all kRunPts order entries, then all kRunPts gathers, in flight together
         // (branch-free: positions past n read the last point and are masked below)
         int idx[kRunPts];
-        if (ordered) {
-#pragma unroll
-            for (int v = 0; v < kRunPts; ++v) idx[v] = __ldg(perm + min(base + v, n - 1));
-        } else {
-#pragma unroll
-            for (int v = 0; v < kRunPts; ++v) idx[v] = (int)min(base + v, n - 1);
-        }
+        runs_idx(perm, ordered, base, n, idx);
         float2 y[kRunPts];
 #pragma unroll
         for (int v = 0; v < kRunPts; ++v) y[v] = __ldg(Y + idx[v]);
+#endif
         float acc[27];
 #pragma unroll
         for (int q = 0; q < 27; ++q) acc[q] = 0.f;
@@ -486,6 +512,12 @@ __global__ void __launch_bounds__(256, RUNS_MINB) k_spread_runs(const float2* __
                     }
             }
         }
+#if RUNS_PIPE
+        if (more) {
+#pragma unroll
+            for (int v = 0; v < kRunPts; ++v) y[v] = __ldg(Y + idx1[v]);
+        }
+#endif
         __syncwarp();
         // segmented inclusive scan over the lanes, segments = equal boxes
         // (lanes without points: key -1 - lane, a segment of their own)

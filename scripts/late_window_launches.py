@@ -10,6 +10,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
+from paper_2509_19785_b200 import tsnet as T  # noqa: E402
+if os.environ.get("PROBE_LIB"):      # a probe build (scripts/tile_variants.sh): build/variants/libtsnet_<name>.so
+    T.LIB_PATH = os.path.join(ROOT, "paper_2509_19785_b200", "build", "variants", f"libtsnet_{os.environ['PROBE_LIB']}.so")
 from paper_2509_19785_b200 import Layout, tsnet_build_P, tsnet_read_stats  # noqa: E402
 from workloads import config_graph, init_layout  # noqa: E402
 
