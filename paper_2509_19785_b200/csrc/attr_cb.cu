@@ -155,12 +155,28 @@ static TileHeader tile_layout(int64_t n, int64_t rb, int64_t re, int64_t nnz, in
 
 // Host cut (pure).  ipr[q] = indptr[rb + q], q = 0 .. nr.  Panels:
 // P = G ceil(nr / (G R_cap)) (at most nr, at least 1), rows dealt by LPT on
-// weight (entries + 8): rows in decreasing weight (ties: smaller row), each to
+// weight (entries + 8, plus the hub penalty of tile_row_weight below): rows in decreasing entries (ties: smaller row), each to
 // the panel with the least weight so far (ties: smaller panel) among those
 // with < R_cap rows.  Inside a panel rows are in ascending order.  Outputs:
 // row_panel[q], row_local[q], panel_off[P + 1] (exclusive scan of the panel
 // sizes), panel_rows[panel_off[p] + l] = the row q with local index l.
 // Returns P, or -1.
+// Rows with >= TILE_HUB_MIN entries weigh TILE_HUB_PM per mille more in the
+// deal: a hub row's runs are split between warps in every block (shared rows,
+// atomic flushes), so its panel ran ~3 % longer than the others at equal
+// entries (cfg 4: the 7 panels holding the 74k-200k-entry rows were the 7
+// slowest CTAs, 946k vs 918k cycles mean); measured on cfg 4, the kernel takes
+// 0.4946 ms without the penalty, 0.4848-0.4861 ms for thresholds 8k-64k and
+// 400-900 per mille (profiles/r2s4gh_tile_hub_weight_cfg4.jsonl).
+#ifndef TILE_HUB_MIN
+#define TILE_HUB_MIN 32768
+#endif
+#ifndef TILE_HUB_PM
+#define TILE_HUB_PM 600
+#endif
+static inline int64_t tile_row_weight(int64_t e) {
+    return e + 8 + ((TILE_HUB_MIN > 0 && e >= TILE_HUB_MIN) ? e * TILE_HUB_PM / 1000 : 0);
+}
 static int32_t tile_partition(const int64_t* ipr, int64_t nr, int32_t G, int32_t R_cap, std::vector<int32_t>& row_panel,
                               std::vector<int32_t>& row_local, std::vector<int32_t>& panel_off,
                               std::vector<int32_t>& panel_rows) {
@@ -189,7 +205,7 @@ static int32_t tile_partition(const int64_t* ipr, int64_t nr, int32_t G, int32_t
         heap.pop();
         row_panel[q] = it.second;
         ++cnt[it.second];
-        if (cnt[it.second] < R_cap) heap.push({it.first + (ipr[q + 1] - ipr[q]) + 8, it.second});
+        if (cnt[it.second] < R_cap) heap.push({it.first + tile_row_weight(ipr[q + 1] - ipr[q]), it.second});
     }
     for (int32_t p = 0; p < P; ++p) panel_off[p + 1] = panel_off[p] + cnt[p];
     std::vector<int32_t> fill(panel_off.begin(), panel_off.end() - 1);

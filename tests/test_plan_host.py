@@ -15,6 +15,15 @@ def T():
     return tsnet
 
 
+# the deal's row weight (attr_cb.cu, tile_row_weight): entries + 8, and rows of
+# >= HUB_MIN entries weigh HUB_PM per mille more
+HUB_MIN, HUB_PM = 32768, 600
+
+
+def row_weight(L):
+    return L + 8 + np.where(L >= HUB_MIN, L * HUB_PM // 1000, 0)
+
+
 def check_cut(ip, rb, re, G, cap, cut):
     P, row_panel, row_local, panel_off, panel_rows = cut
     nr = re - rb
@@ -32,14 +41,15 @@ def check_cut(ip, rb, re, G, cap, cut):
         assert np.all(np.diff(rows) > 0)
         assert np.all(row_panel[rows] == p)
         assert np.array_equal(row_local[rows], np.arange(len(rows)))
-    # LPT balance on weight = entries + 8: no panel exceeds the mean by more than the
+    # LPT balance on the row weight: no panel exceeds the mean by more than the
     # largest single row weight (the textbook LPT bound); with a cap that binds,
     # only panels below the cap are compared
     if nr:
-        wts = np.bincount(row_panel, weights=L + 8, minlength=P)
+        w = row_weight(L)
+        wts = np.bincount(row_panel, weights=w, minlength=P)
         open_ = sizes < cap
         if open_.any():
-            assert wts[open_].max() <= wts.sum() / P + (L.max() + 8) + 1e-9
+            assert wts[open_].max() <= wts.sum() / P + w.max() + 1e-9
     return P
 
 
@@ -87,3 +97,20 @@ def test_empty_rows_and_bad_args(T):
     check_cut(ip2, 0, 1000, 3, 2000, T.tsnet_plan_partition(ip2, 0, 1000, 3, 2000))
     with pytest.raises(Exception):
         T.tsnet_plan_partition(ip, 5, 3, 16, 704)
+
+
+def test_hub_rows_weigh_more(T):
+    """Rows of >= HUB_MIN entries carry the hub penalty in the deal: the panels
+    holding them get fewer entries than the others (their runs are split between
+    warps in every block: DESIGN §5.1), and the LPT bound holds on the weight."""
+    rng = np.random.default_rng(3)
+    L = np.concatenate([[100000, 70000, 50000, 40000], rng.integers(5, 50, 20000)]).astype(np.int64)
+    rng.shuffle(L)
+    ip = np.concatenate([[0], np.cumsum(L)]).astype(np.int64)
+    G = 8
+    P, row_panel, _, _, _ = cut = T.tsnet_plan_partition(ip, 0, len(L), G, 8192)
+    check_cut(ip, 0, len(L), G, 8192, cut)
+    ent = np.bincount(row_panel, weights=L, minlength=P)
+    hubp = np.unique(row_panel[L >= HUB_MIN])
+    rest = np.setdiff1d(np.arange(P), hubp)
+    assert len(rest) > 0 and ent[hubp].max() < ent[rest].min(), (ent[hubp], ent[rest])
