@@ -48,6 +48,36 @@ __device__ __forceinline__ bool is5smooth(int m) {
 __device__ __forceinline__ unsigned bb_key(float x) { return (unsigned)f2o(x) ^ 0x80000000u; }
 __device__ __forceinline__ float bb_val(unsigned u) { return o2f((int)(u ^ 0x80000000u)); }
 
+// The field chain's kernels are launched with programmatic stream serialization
+// (FIELD_PDL, on; 0 = plain launches, the probe baseline): a kernel's CTAs may become resident while its
+// predecessor still runs; each waits here for the predecessor to complete (and
+// its writes to be visible) before it touches memory, then lets its own
+// successor's CTAs in.  Every kernel of the chain calls it first, also on the
+// paths that exit at once, so completion stays transitive along the chain.
+#ifndef FIELD_PDL
+#define FIELD_PDL 1
+#endif
+__device__ __forceinline__ void chain_wait() {
+#if FIELD_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_chain(void (*k)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = FIELD_PDL ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, KArgs(args)...);
+}
+
 // a0: bounding box of Y and, in the last block, the grid geometry (R9).
 constexpr int kBBoxPts = 8;
 #ifndef RUNS_RESORT       // probe builds (scripts/tile_variants.sh SRC=field): the re-sort threshold
@@ -245,6 +275,7 @@ __device__ __forceinline__ void write_twiddles(const Geo* __restrict__ g, float2
 __global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__ Y, int64_t n, Geo* __restrict__ g,
                                                    int* __restrict__ box_cnt, int* __restrict__ box,
                                                    int* __restrict__ rank) {
+    chain_wait();
     __shared__ int hist[kBoxSmem];
     if (g->smode != kSpreadSort) return;
     const double lo_x = g->lo_x, lo_y = g->lo_y, h_b = g->h_b, inv_h = g->inv_h;
@@ -296,6 +327,7 @@ __global__ void __launch_bounds__(256, 4) k_box_count(const float2* __restrict__
 // a1: exclusive scan of box counts -> box_start.  Single CTA of 1024 threads.
 __global__ void __launch_bounds__(1024) k_box_scan(Geo* g, int* __restrict__ box_cnt, int* __restrict__ box_start,
                                                    int64_t n) {
+    chain_wait();
     if (g->smode != kSpreadSort) return;
     const int nb = g->I * g->I;
     const int T = blockDim.x;
@@ -328,6 +360,7 @@ __global__ void __launch_bounds__(1024) k_box_scan(Geo* g, int* __restrict__ box
 __global__ void __launch_bounds__(256) k_box_scatter(Geo* __restrict__ g, int64_t n, const int* __restrict__ box,
                                                      const int* __restrict__ rank, const int* __restrict__ box_start,
                                                      int* __restrict__ perm) {
+    chain_wait();
     constexpr int V = 4;
     if (g->smode != kSpreadSort) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) g->perm_n = n;   // the box order of these n points
@@ -423,6 +456,7 @@ __device__ __forceinline__ void runs_idx(const int* __restrict__ perm, bool orde
 __global__ void __launch_bounds__(256, RUNS_MINB) k_spread_runs(const float2* __restrict__ Y, int64_t n, Geo* __restrict__ g,
                                                      const int* __restrict__ perm, float4* __restrict__ wgrid,
                                                      float2* __restrict__ tw) {
+    chain_wait();
     __shared__ unsigned s_flush;
     __shared__ int s_nstray;
     __shared__ int4 s_stray[kStrayCap];    // (box, u_x, u_y) of points outside their lane's run
@@ -599,6 +633,7 @@ __device__ __forceinline__ int fft_batch(int cap, int M, int want) {
 __global__ void __launch_bounds__(kRowThreads, 1) k_row_fwd(const Geo* __restrict__ gp, const float4* __restrict__ wgrid,
                                                          const float2* __restrict__ twg, float2* __restrict__ spec,
                                                          int M_max, float eps, int cap) {
+    chain_wait();
     extern __shared__ float2 sm[];
     const int M = gp->M, N = gp->N, half = M / 2 + 1, nrad = gp->nrad;
     const int B = fft_batch(cap, M, 5);
@@ -689,6 +724,7 @@ __device__ __forceinline__ double col_products(const float2 (&v)[10], float2 (&o
 __global__ void __launch_bounds__(kColThreads, 1) k_col(Geo* __restrict__ gp, float2* __restrict__ spec,
                                                         const float2* __restrict__ twg, float2* __restrict__ colout,
                                                         int M_max, int N_max, int cap) {
+    chain_wait();
     extern __shared__ float2 sm[];
     __shared__ double zred[kColThreads / 32];
     const int M = gp->M, N = gp->N, half = M / 2 + 1, nrad = gp->nrad;
@@ -787,6 +823,7 @@ __global__ void __launch_bounds__(kInvThreads) k_row_inv(Geo* __restrict__ gp, c
                                                          const float2* __restrict__ twg, float4* __restrict__ fgrid,
                                                          int M_max, int N_max, int64_t n, float lambda_kl,
                                                          float lambda_r, int cap) {
+    chain_wait();
     extern __shared__ float2 sm[];
     const int M = gp->M, N = gp->N, nrad = gp->nrad, I = gp->I;
     const int B = fft_batch(cap, M, 2);
@@ -979,12 +1016,12 @@ cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, b
     // on the device, and the iteration is one CUDA graph) and exit at once on
     // the runs path
     const int cb = (int)std::max<int64_t>(kNumSMs, (nl + kBoxChunk - 1) / kBoxChunk);
-    k_box_count<<<cb, 256, 0, s>>>(Yl, nl, w.geo, w.box_cnt, w.box, w.rank);
-    k_box_scan<<<1, 1024, 0, s>>>(w.geo, w.box_cnt, w.box_start, nl);
-    k_box_scatter<<<pbl, 256, 0, s>>>(w.geo, nl, w.box, w.rank, w.box_start, w.perm);
+    if ((e = launch_chain(k_box_count, cb, 256, 0, s, Yl, nl, w.geo, w.box_cnt, w.box, w.rank)) != cudaSuccess) return e;
+    if ((e = launch_chain(k_box_scan, 1, 1024, 0, s, w.geo, w.box_cnt, w.box_start, nl)) != cudaSuccess) return e;
+    if ((e = launch_chain(k_box_scatter, pbl, 256, 0, s, w.geo, nl, w.box, w.rank, w.box_start, w.perm)) != cudaSuccess) return e;
     const int rbk = (int)std::max<int64_t>(1, std::min<int64_t>((nl + 8 * 32 * kRunPts - 1) / (8 * 32 * kRunPts),
                                                                   (int64_t)kNumSMs * RUNS_MINB));
-    k_spread_runs<<<rbk, 256, 0, s>>>(Yl, nl, w.geo, w.perm, w.wgrid, w.tw);
+    if ((e = launch_chain(k_spread_runs, rbk, 256, 0, s, Yl, nl, w.geo, w.perm, w.wgrid, w.tw)) != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -993,13 +1030,15 @@ cudaError_t launch_field_local(const Ws& w, const GradArgs& a, cudaStream_t s, b
 cudaError_t launch_field_conv(const Ws& w, const GradArgs& a, cudaStream_t s) {
     cudaError_t e;
     if ((e = field_set_attrs(w.M_max)) != cudaSuccess) return e;
-    k_row_fwd<<<kNumSMs * 2, kRowThreads, field_smem_row(w.M_max), s>>>(w.geo, w.wgrid, w.tw, w.spec, w.M_max, a.eps,
-                                                                         smem_cap_row(w.M_max));
-    k_col<<<kNumSMs, kColThreads, field_smem_col(w.M_max), s>>>(w.geo, w.spec, w.tw, w.colout, w.M_max, w.N_max,
-                                                                smem_cap_col(w.M_max));
-    k_row_inv<<<kNumSMs * 2, kInvThreads, field_smem_inv(w.M_max), s>>>(w.geo, w.colout, w.tw, w.fgrid, w.M_max,
-                                                                        w.N_max, a.n, a.lambda_kl, a.lambda_r,
-                                                                        smem_cap_inv(w.M_max));
+    if ((e = launch_chain(k_row_fwd, kNumSMs * 2, kRowThreads, field_smem_row(w.M_max), s, w.geo, w.wgrid, w.tw, w.spec,
+                          w.M_max, a.eps, smem_cap_row(w.M_max))) != cudaSuccess)
+        return e;
+    if ((e = launch_chain(k_col, kNumSMs, kColThreads, field_smem_col(w.M_max), s, w.geo, w.spec, w.tw, w.colout, w.M_max,
+                          w.N_max, smem_cap_col(w.M_max))) != cudaSuccess)
+        return e;
+    if ((e = launch_chain(k_row_inv, kNumSMs * 2, kInvThreads, field_smem_inv(w.M_max), s, w.geo, w.colout, w.tw, w.fgrid,
+                          w.M_max, w.N_max, a.n, a.lambda_kl, a.lambda_r, smem_cap_inv(w.M_max))) != cudaSuccess)
+        return e;
     return cudaGetLastError();
 }
 
